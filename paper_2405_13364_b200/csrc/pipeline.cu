@@ -1,0 +1,2080 @@
+// libveil device pipeline: sort-middle exact-OIT frame render on sm_100a.
+//
+// Stage map (reference -> kernel):
+//   setup phase 1 + compaction   setup.cpp:255-302   k_setup_count, k_scan_blocks
+//   setup phase 2 (records)      setup.cpp:305-349   k_setup_write
+//   binning count / offsets      binning.cpp:124-145 k_bin_count, k_bin_scan
+//   binning write                binning.cpp:147-186 k_bin_scatter, k_bin_sort
+//   bin rasterization low/high   raster.cpp:41-335,  k_raster<kGlobal>
+//                                renderer.cpp:117-165
+//   stats merge                  renderer.cpp:170-212 k_finalize
+//
+// Design notes (DESIGN.md has the full version):
+//  * Setup is two passes over the quad stream (count, then recompute+write)
+//    with a block-offset scan in between, so visible quads land in ascending
+//    input order without a per-quad intermediate array.
+//  * Per-bin lists are filled with warp-aggregated atomics and then sorted
+//    per bin, giving the reference's order (small quads ascending, then large
+//    triangles ascending, binning.cpp:147-166).
+//  * The rasterizer is a persistent kernel over (bin, block-row) work items.
+//    A CTA of 4 warps builds the block-row's tri-block-rows in shared
+//    memory; warp w then owns block w of the row: it sorts the block's
+//    tri-blocks by (quantized centroid depth, is_large, triangle) -- the
+//    same order as the reference's (depth, selection index) key because
+//    selection index is monotone in (is_large, triangle) -- splits them into
+//    tri-half-blocks and shades both half-blocks with lane == pixel, keeping
+//    the depth filter in registers.
+//  * Items that do not fit the shared-memory capacities but are within the
+//    rasterizer limits are re-run by the same kernel with global scratch.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "device_math.cuh"
+#include "veil_internal.hpp"
+
+namespace veil {
+
+// ============================================================ device side
+namespace dev {
+
+constexpr int kSetupBlock = 256;
+constexpr uint64_t kHashSeed = 0xcbf29ce484222325ull;
+constexpr uint64_t kHashPrime = 0x100000001b3ull;
+constexpr float kAlphaThreshold = 1.0f - 1.0f / 128.0f;  // raster.hpp:51
+
+struct Limits {
+  uint32_t tbr, tb, thb, frags;
+};
+
+struct MatDev {
+  float base[4];
+  float opacity;
+  uint32_t flags;  // bit0 colors, bit1 normals (already AND-ed with scene flags)
+  uint32_t pad[2];
+};
+
+struct FrameConst {
+  double m[16];
+  double eye[3];
+  double fwd[3];
+  int has_eye;
+  int width, height, bins_x, bins_y, nbins;
+  int backface, extended;
+  uint32_t nquads;
+  float light[3];
+  float ambient;
+  float bg[4];  // premultiplied background
+  int df;
+  int threshold, visualize, force_high;
+  Limits low, high;
+  uint32_t items_cap;
+  uint32_t tri_cap;  // visible-triangle capacity (2^24 standard)
+  int rank, world;
+  int dump;
+};
+
+// Device counters; one instance per scene workspace, zeroed per frame.
+struct Counters {
+  unsigned long long cull[5];  // visible, degenerate, backfacing, frustum, between
+  unsigned long long pairs;
+  unsigned long long small_quads, large_tris;
+  unsigned long long bin_error;  // min(bin * 64 + code)
+  unsigned int nvis;
+  unsigned int error;  // bit0 visible capacity, bit1 item capacity
+  unsigned int work_next[4];
+  unsigned int spill_count[2];
+  unsigned long long samples, fragments, thb, segments, invalid;
+  unsigned long long bins_empty, bins_low, bins_high, bins_propagated;
+  unsigned int hi_items;
+  unsigned int pad;
+};
+
+struct Buffers {
+  // scene
+  const float4* pos;
+  const uint32_t* vcol;
+  const uint32_t* vnrm;
+  const uint4* quads;
+  const uint32_t* qmat;
+  const MatDev* mats;
+  // setup
+  uint32_t* block_cnt;
+  uint32_t* block_off;
+  uint32_t* vq_src;
+  uint2* vq_box;  // (x0 | x1 << 16, y0 | y1 << 16)
+  uint32_t* vq_flags;  // bit0 large, 1 colors, 2 normals, 3 uvs, 4-5 cull flags
+  uint32_t* vq_mat;
+  uint4* vq_col;
+  uint4* vq_nrm;
+  TriRec* tri;
+  uint4* tri_meta;  // flat normal, material, quad index, tri | valid << 8
+  // bins
+  uint32_t* qcnt;
+  uint32_t* tcnt;
+  uint32_t* off;
+  uint32_t* qcur;
+  uint32_t* tcur;
+  uint8_t* cat;
+  uint8_t* prop;
+  uint32_t* items;
+  // raster
+  unsigned long long* slots;  // per (bin, row): samples, frags, thb, segments, invalid
+  uint32_t* spill[2];
+  uint8_t* scratch;
+  uint64_t scratch_per_cta;
+  uint32_t* fb;
+  uint8_t* mask;
+  uint64_t* hash;
+  uint32_t* emit;
+  uint32_t* thb_cnt;  // dump: per (bin, half-block)
+  uint64_t* thb_off;  // dump: offsets (second pass)
+  uint64_t* thb_out;  // dump
+  uint32_t* thb_tri;  // dump
+  uint32_t* thb_pre;  // dump
+  Counters* ctr;
+};
+
+// ------------------------------------------------------------ setup
+
+__device__ __forceinline__ void load_quad(const Buffers& B, uint32_t q, uint4* idx,
+                                          float4 p[4]) {
+  *idx = B.quads[q];
+  p[0] = __ldg(&B.pos[idx->x]);
+  p[1] = __ldg(&B.pos[idx->y]);
+  p[2] = __ldg(&B.pos[idx->z]);
+  p[3] = __ldg(&B.pos[idx->w]);
+}
+
+// triangle_front_facing, setup.cpp:104-110
+__device__ __forceinline__ bool front_facing(const FrameConst& fc, const double* p0,
+                                             const double* p1, const double* p2) {
+  double a[3] = {__dsub_rn(p1[0], p0[0]), __dsub_rn(p1[1], p0[1]), __dsub_rn(p1[2], p0[2])};
+  double b[3] = {__dsub_rn(p2[0], p0[0]), __dsub_rn(p2[1], p0[1]), __dsub_rn(p2[2], p0[2])};
+  double n[3];
+  cross3(a, b, n);
+  if (fc.has_eye) {
+    double v[3] = {__dsub_rn(fc.eye[0], p0[0]), __dsub_rn(fc.eye[1], p0[1]),
+                   __dsub_rn(fc.eye[2], p0[2])};
+    return dot3(n, v) > 0.0;
+  }
+  return dot3(n, fc.fwd) < 0.0;
+}
+
+__device__ __forceinline__ uint32_t outside_mask(const double* c) {
+  uint32_t m = 0;
+  if (c[0] < -c[3]) m |= 1u;
+  if (c[0] > c[3]) m |= 2u;
+  if (c[1] < -c[3]) m |= 4u;
+  if (c[1] > c[3]) m |= 8u;
+  if (c[2] < 0.0) m |= 16u;
+  if (c[2] > c[3]) m |= 32u;
+  return m;
+}
+
+__constant__ int c_quad_edges[5][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 0}, {0, 2}};
+__constant__ int c_tri_edges[3][2] = {{0, 1}, {1, 2}, {2, 0}};
+
+struct CullOut {
+  int reason;  // 0 visible, 1 degenerate, 2 backfacing, 3 frustum, 4 between samples
+  uint32_t flags;
+  int x0, y0, x1, y1;
+  bool large;
+};
+
+// project_quad + cull_projected, setup.cpp:119-186
+__device__ void cull_quad(const FrameConst& fc, const uint4& idx, const float4 p[4],
+                          double clip[4][4], CullOut* o) {
+  o->flags = 0;
+  o->large = false;
+  bool d0 = idx.x == idx.y || idx.y == idx.z || idx.x == idx.z;
+  bool d1 = idx.x == idx.z || idx.z == idx.w || idx.x == idx.w;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) to_clip(fc.m, p[i].x, p[i].y, p[i].z, clip[i]);
+  if (d0) o->flags |= 1u;
+  if (d1) o->flags |= 2u;
+  if (d0 && d1) {
+    o->reason = 1;
+    return;
+  }
+  if (fc.backface) {
+    double w[4][3];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) w[i][0] = p[i].x, w[i][1] = p[i].y, w[i][2] = p[i].z;
+    bool b0 = d0 ? true : !front_facing(fc, w[0], w[1], w[2]);
+    bool b1 = d1 ? true : !front_facing(fc, w[0], w[2], w[3]);
+    if (!d0 && b0) o->flags |= 1u;
+    if (!d1 && b1) o->flags |= 2u;
+    if (b0 && b1) {
+      o->reason = 2;
+      return;
+    }
+  }
+  if ((outside_mask(clip[0]) & outside_mask(clip[1]) & outside_mask(clip[2]) &
+       outside_mask(clip[3])) != 0) {
+    o->reason = 3;
+    return;
+  }
+  double px[4], py[4], pw[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    double h[3];
+    hpixel(clip[i], fc.width, fc.height, h);
+    px[i] = h[0], py[i] = h[1], pw[i] = h[2];
+  }
+  double bx0, bx1, by0, by1;
+  extend_axis<4, 5>(px, pw, c_quad_edges, (double)fc.width, &bx0, &bx1);
+  extend_axis<4, 5>(py, pw, c_quad_edges, (double)fc.height, &by0, &by1);
+  int xf, xl, yf, yl;
+  pixel_range(bx0, bx1, fc.width, &xf, &xl);
+  pixel_range(by0, by1, fc.height, &yf, &yl);
+  if (bx0 > bx1 || by0 > by1 || xf > xl || yf > yl) {
+    o->reason = 4;
+    return;
+  }
+  o->reason = 0;
+  o->x0 = xf / kBin;
+  o->y0 = yf / kBin;
+  o->x1 = xl / kBin;
+  o->y1 = yl / kBin;
+  o->large = (o->x1 - o->x0 + 1) * (o->y1 - o->y0 + 1) > 4;
+}
+
+__global__ void __launch_bounds__(kSetupBlock) k_setup_count(FrameConst fc, Buffers B) {
+  uint32_t q = blockIdx.x * kSetupBlock + threadIdx.x;
+  int reason = -1;
+  if (q < fc.nquads) {
+    uint4 idx;
+    float4 p[4];
+    load_quad(B, q, &idx, p);
+    double clip[4][4];
+    CullOut o;
+    cull_quad(fc, idx, p, clip, &o);
+    reason = o.reason;
+  }
+  int vis = __syncthreads_count(reason == 0);
+  int deg = __syncthreads_count(reason == 1);
+  int back = __syncthreads_count(reason == 2);
+  int fru = __syncthreads_count(reason == 3);
+  int bet = __syncthreads_count(reason == 4);
+  if (threadIdx.x == 0) {
+    B.block_cnt[blockIdx.x] = (uint32_t)vis;
+    if (vis) atomicAdd(&B.ctr->cull[0], (unsigned long long)vis);
+    if (deg) atomicAdd(&B.ctr->cull[1], (unsigned long long)deg);
+    if (back) atomicAdd(&B.ctr->cull[2], (unsigned long long)back);
+    if (fru) atomicAdd(&B.ctr->cull[3], (unsigned long long)fru);
+    if (bet) atomicAdd(&B.ctr->cull[4], (unsigned long long)bet);
+  }
+}
+
+// Exclusive scan of up to 1024*kPer values with one CTA.
+template <int kThreads>
+__device__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* total) {
+  __shared__ uint32_t warp_sums[kThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_sums[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t s = lane < kThreads / 32 ? warp_sums[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    if (lane < kThreads / 32) warp_sums[lane] = s;
+  }
+  __syncthreads();
+  uint32_t warp_prefix = warp ? warp_sums[warp - 1] : 0;
+  *total = warp_sums[kThreads / 32 - 1];
+  __syncthreads();
+  return warp_prefix + x - v;
+}
+
+__global__ void __launch_bounds__(1024) k_scan_blocks(FrameConst fc, Buffers B, uint32_t nblocks) {
+  __shared__ uint32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (uint32_t base = 0; base < nblocks; base += 1024) {
+    uint32_t i = base + threadIdx.x;
+    uint32_t v = i < nblocks ? B.block_cnt[i] : 0;
+    uint32_t total;
+    uint32_t ex = block_exclusive_scan<1024>(v, &total);
+    if (i < nblocks) B.block_off[i] = carry + ex;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    B.ctr->nvis = carry;
+    // setup.cpp:298-299: 2 * visible > 2^24 is a capacity error
+    if ((unsigned long long)carry * 2ull > (unsigned long long)fc.tri_cap) atomicOr(&B.ctr->error, 1u);
+  }
+}
+
+// triangle setup, setup.cpp:209-239 (+ flat normal, setup.cpp:342-343)
+__device__ void triangle_setup(const FrameConst& fc, const double c0[4], const double c1[4],
+                               const double c2[4], TriRec* out, bool* valid) {
+  double v0[3], v1[3], v2[3], e0[3], e1[3], e2[3];
+  hpixel(c0, fc.width, fc.height, v0);
+  hpixel(c1, fc.width, fc.height, v1);
+  hpixel(c2, fc.width, fc.height, v2);
+  cross3(v1, v2, e0);
+  cross3(v2, v0, e1);
+  cross3(v0, v1, e2);
+  double det = dot3(e0, v0);
+  TriRec r;
+  memset(&r, 0, sizeof r);
+  r.y_min = 0;
+  r.y_max = -1;
+  *valid = false;
+  if (!(det == 0.0 || !isfinite(det))) {
+    double s = det > 0.0 ? 1.0 : -1.0;
+    const double* es[3] = {e0, e1, e2};
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      r.e[i].a = __dmul_rn(es[i][0], s);
+      r.e[i].b = __dmul_rn(es[i][1], s);
+      r.e[i].c = __dmul_rn(es[i][2], s);
+    }
+    double inv_det = __ddiv_rn(1.0, det);
+    double z0 = c0[2], z1 = c1[2], z2 = c2[2];
+    double* dz[3] = {&r.dz.a, &r.dz.b, &r.dz.c};
+    double* iw[3] = {&r.iw.a, &r.iw.b, &r.iw.c};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      *dz[k] = __dmul_rn(
+          __dadd_rn(__dadd_rn(__dmul_rn(e0[k], z0), __dmul_rn(e1[k], z1)), __dmul_rn(e2[k], z2)),
+          inv_det);
+      *iw[k] = __dmul_rn(__dadd_rn(__dadd_rn(e0[k], e1[k]), e2[k]), inv_det);
+    }
+    double py[3] = {v0[1], v1[1], v2[1]}, pw[3] = {v0[2], v1[2], v2[2]};
+    double lo, hi;
+    extend_axis<3, 3>(py, pw, c_tri_edges, (double)fc.height, &lo, &hi);
+    int f, l;
+    pixel_range(lo, hi, fc.height, &f, &l);
+    r.y_min = f;
+    r.y_max = l;
+    *valid = true;
+  }
+  *out = r;
+}
+
+__device__ __forceinline__ uint32_t flat_normal(const float4& a, const float4& b,
+                                                const float4& c) {
+  double w0[3] = {a.x, a.y, a.z}, w1[3] = {b.x, b.y, b.z}, w2[3] = {c.x, c.y, c.z};
+  double u[3] = {__dsub_rn(w1[0], w0[0]), __dsub_rn(w1[1], w0[1]), __dsub_rn(w1[2], w0[2])};
+  double v[3] = {__dsub_rn(w2[0], w0[0]), __dsub_rn(w2[1], w0[1]), __dsub_rn(w2[2], w0[2])};
+  double n[3];
+  cross3(u, v, n);
+  double l2 = dot3(n, n);
+  if (l2 <= 0.0) {
+    n[0] = n[1] = n[2] = 0.0;
+  } else {
+    double inv = __ddiv_rn(1.0, __dsqrt_rn(l2));
+    n[0] = __dmul_rn(n[0], inv);
+    n[1] = __dmul_rn(n[1], inv);
+    n[2] = __dmul_rn(n[2], inv);
+  }
+  return encode_normal((float)n[0], (float)n[1], (float)n[2]);
+}
+
+__global__ void __launch_bounds__(kSetupBlock) k_setup_write(FrameConst fc, Buffers B) {
+  if (B.ctr->error & 1u) return;
+  uint32_t q = blockIdx.x * kSetupBlock + threadIdx.x;
+  uint4 idx = make_uint4(0, 0, 0, 0);
+  float4 p[4];
+  double clip[4][4];
+  CullOut o;
+  o.reason = -1;
+  if (q < fc.nquads) {
+    load_quad(B, q, &idx, p);
+    cull_quad(fc, idx, p, clip, &o);
+  }
+  uint32_t total;
+  uint32_t rank = block_exclusive_scan<kSetupBlock>(o.reason == 0 ? 1u : 0u, &total);
+  if (o.reason != 0) return;
+  uint32_t slot = B.block_off[blockIdx.x] + rank;
+  uint32_t mat = B.qmat[q];
+  MatDev md = B.mats[mat];
+  bool has_c = md.flags & 1u, has_n = md.flags & 2u;
+  B.vq_src[slot] = q;
+  B.vq_box[slot] = make_uint2((uint32_t)o.x0 | ((uint32_t)o.x1 << 16),
+                              (uint32_t)o.y0 | ((uint32_t)o.y1 << 16));
+  B.vq_flags[slot] = (o.large ? 1u : 0u) | (has_c ? 2u : 0u) | (has_n ? 4u : 0u) | (o.flags << 4);
+  B.vq_mat[slot] = mat;
+  uint4 col = make_uint4(0, 0, 0, 0), nrm = make_uint4(0, 0, 0, 0);
+  if (has_c) col = make_uint4(B.vcol[idx.x], B.vcol[idx.y], B.vcol[idx.z], B.vcol[idx.w]);
+  if (has_n) nrm = make_uint4(B.vnrm[idx.x], B.vnrm[idx.y], B.vnrm[idx.z], B.vnrm[idx.w]);
+  B.vq_col[slot] = col;
+  B.vq_nrm[slot] = nrm;
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    TriRec rec;
+    uint4 meta = make_uint4(0, 0, 0, 0);
+    bool valid = false;
+    if (o.flags & (1u << t)) {
+      memset(&rec, 0, sizeof rec);
+      rec.y_min = 0;
+      rec.y_max = -1;
+    } else {
+      const int k1 = t == 0 ? 1 : 2, k2 = t == 0 ? 2 : 3;
+      triangle_setup(fc, clip[0], clip[k1], clip[k2], &rec, &valid);
+      meta.x = flat_normal(p[0], p[k1], p[k2]);
+      meta.y = mat;
+      meta.z = slot;
+      meta.w = (uint32_t)t | (valid ? 0x100u : 0u);
+    }
+    B.tri[slot * 2 + t] = rec;
+    B.tri_meta[slot * 2 + t] = meta;
+  }
+}
+
+// ------------------------------------------------------------ binning
+
+__device__ __forceinline__ void warp_agg_add(uint32_t* base, uint32_t bin, bool active,
+                                             uint32_t* slot_out) {
+  // Warp-aggregated atomic: lanes with the same bin share one atomicAdd.
+  unsigned mask = __ballot_sync(0xffffffffu, active);
+  if (!active) return;
+  unsigned peers = __match_any_sync(mask, bin);
+  int leader = __ffs(peers) - 1;
+  int lane = threadIdx.x & 31;
+  uint32_t base_slot = 0;
+  if (lane == leader) base_slot = atomicAdd(&base[bin], (uint32_t)__popc(peers));
+  base_slot = __shfl_sync(peers, base_slot, leader);
+  if (slot_out) *slot_out = base_slot + __popc(peers & ((1u << lane) - 1u));
+}
+
+// rasterize_triangle_bins, binning.hpp:89-117: calls fn(bin) per covered bin
+template <typename Fn>
+__device__ void tri_bins(const FrameConst& fc, const TriRec& t, Fn&& fn) {
+  int y = t.y_min;
+  while (y <= t.y_max) {
+    int bin_row = y / kBin;
+    int row_end = min(t.y_max, (bin_row + 1) * kBin - 1);
+    uint64_t mask[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (; y <= row_end; ++y) {
+      int b, l;
+      if (!row_span(t, y, 0, fc.width - 1, &b, &l)) continue;
+      int b0 = b / kBin, b1 = l / kBin;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) {
+        int lo = max(b0, w * 64), hi = min(b1, w * 64 + 63);
+        if (lo > hi) continue;
+        int n = hi - lo + 1;
+        uint64_t bits = n == 64 ? ~0ull : (((1ull << n) - 1ull) << (lo - w * 64));
+        mask[w] |= bits;
+      }
+    }
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      uint64_t bits = mask[w];
+      while (bits) {
+        int b = w * 64 + __ffsll((long long)bits) - 1;
+        bits &= bits - 1;
+        if (b < fc.bins_x) fn(bin_row * fc.bins_x + b);
+      }
+    }
+  }
+}
+
+template <bool kWrite>
+__global__ void __launch_bounds__(256) k_bin_pass(FrameConst fc, Buffers B) {
+  if (B.ctr->error) return;
+  const uint32_t nvis = B.ctr->nvis;
+  for (uint32_t base = blockIdx.x * 256; base < nvis; base += gridDim.x * 256) {
+    uint32_t q = base + threadIdx.x;
+    bool in = q < nvis;
+    uint32_t flags = in ? B.vq_flags[q] : 0u;
+    bool small = in && !(flags & 1u);
+    uint2 box = in ? B.vq_box[q] : make_uint2(0, 0);
+    uint32_t x0 = box.x & 0xffffu, x1 = box.x >> 16, y0 = box.y & 0xffffu, y1 = box.y >> 16;
+    // small quads: every bin of the AABB (binning.hpp:76-81), 1..4 bins
+    uint32_t nb = small ? (x1 - x0 + 1) * (y1 - y0 + 1) : 0u;
+    if (!kWrite) {
+      unsigned sm = __ballot_sync(0xffffffffu, small);
+      if ((threadIdx.x & 31) == 0 && sm) atomicAdd(&B.ctr->small_quads, (unsigned long long)__popc(sm));
+    }
+    for (uint32_t k = 0; k < 4; ++k) {
+      bool act = k < nb;
+      uint32_t bx = x0 + (k % (x1 - x0 + 1 > 0 ? x1 - x0 + 1 : 1));
+      uint32_t by = y0 + (k / (x1 - x0 + 1 > 0 ? x1 - x0 + 1 : 1));
+      uint32_t bin = act ? by * (uint32_t)fc.bins_x + bx : 0u;
+      if (__any_sync(0xffffffffu, act)) {
+        if (kWrite) {
+          uint32_t slot = 0;
+          warp_agg_add(B.qcur, bin, act, &slot);
+          if (act && slot < fc.items_cap) B.items[slot] = q;
+        } else {
+          warp_agg_add(B.qcnt, bin, act, nullptr);
+        }
+      }
+    }
+    if (in && (flags & 1u)) {
+      for (uint32_t t = 0; t < 2; ++t) {
+        uint32_t ti = q * 2 + t;
+        if (!(B.tri_meta[ti].w & 0x100u)) continue;
+        TriRec tr = B.tri[ti];
+        if (!kWrite) atomicAdd(&B.ctr->large_tris, 1ull);
+        tri_bins(fc, tr, [&](int bin) {
+          if (kWrite) {
+            uint32_t slot = atomicAdd(&B.tcur[bin], 1u);
+            if (slot < fc.items_cap) B.items[slot] = ti;
+          } else {
+            atomicAdd(&B.tcnt[bin], 1u);
+          }
+        });
+      }
+    }
+  }
+}
+
+// offsets (binning.cpp:24-32) + categories (34-37) + write cursors
+__global__ void __launch_bounds__(1024) k_bin_scan(FrameConst fc, Buffers B) {
+  if (B.ctr->error) return;
+  __shared__ unsigned long long carry;
+  __shared__ unsigned int cnt[3];
+  if (threadIdx.x == 0) carry = 0, cnt[0] = cnt[1] = cnt[2] = 0;
+  __syncthreads();
+  for (int base = 0; base < fc.nbins; base += 1024) {
+    int b = base + threadIdx.x;
+    uint32_t qc = b < fc.nbins ? B.qcnt[b] : 0, tc = b < fc.nbins ? B.tcnt[b] : 0;
+    uint32_t total;
+    uint32_t ex = block_exclusive_scan<1024>(qc + tc, &total);
+    if (b < fc.nbins) {
+      unsigned long long o = carry + ex;
+      B.off[b] = (uint32_t)o;
+      B.qcur[b] = (uint32_t)o;
+      B.tcur[b] = (uint32_t)(o + qc);
+      uint32_t eq = 2u * qc + tc;
+      uint8_t c = eq == 0 ? 0 : (eq < 1024u ? 1 : 2);
+      B.cat[b] = c;
+      B.prop[b] = 0;
+      atomicAdd(&cnt[c], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) carry += total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    B.ctr->pairs = carry;
+    B.ctr->bins_empty = cnt[0];
+    B.ctr->bins_low = cnt[1];
+    B.ctr->bins_high = cnt[2];
+    if (carry > fc.items_cap) atomicOr(&B.ctr->error, 2u);
+  }
+}
+
+// Sort one segment of u32 ascending in place (bitonic; SMEM when it fits).
+__device__ void cta_sort_segment(uint32_t* g, uint32_t n, uint32_t* sm, uint32_t sm_cap) {
+  if (n < 2) return;
+  uint32_t N = 1;
+  while (N < n) N <<= 1;
+  uint32_t* a = N <= sm_cap ? sm : g;
+  if (N > sm_cap) {
+    // Global-memory path for very long lists: pad is impossible in place, so
+    // run an odd-even transposition merge on the real length instead.
+    for (uint32_t phase = 0; phase < n; ++phase) {
+      for (uint32_t i = 2 * threadIdx.x + (phase & 1); i + 1 < n; i += 2 * blockDim.x) {
+        uint32_t x = g[i], y = g[i + 1];
+        if (x > y) g[i] = y, g[i + 1] = x;
+      }
+      __syncthreads();
+    }
+    return;
+  }
+  for (uint32_t i = threadIdx.x; i < N; i += blockDim.x) a[i] = i < n ? g[i] : 0xffffffffu;
+  __syncthreads();
+  for (uint32_t k = 2; k <= N; k <<= 1)
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = threadIdx.x; i < N; i += blockDim.x) {
+        uint32_t ixj = i ^ j;
+        if (ixj > i) {
+          uint32_t x = a[i], y = a[ixj];
+          bool up = (i & k) == 0;
+          if ((x > y) == up) a[i] = y, a[ixj] = x;
+        }
+      }
+      __syncthreads();
+    }
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) g[i] = a[i];
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) k_bin_sort(FrameConst fc, Buffers B) {
+  if (B.ctr->error) return;
+  __shared__ uint32_t sm[4096];
+  for (int b = blockIdx.x; b < fc.nbins; b += gridDim.x) {
+    uint32_t qc = B.qcnt[b], tc = B.tcnt[b], o = B.off[b];
+    cta_sort_segment(B.items + o, qc, sm, 4096);
+    cta_sort_segment(B.items + o + qc, tc, sm, 4096);
+  }
+}
+
+// ------------------------------------------------------------ raster
+
+struct Tbr {  // one triangle's coverage of a 32x8 block-row (packing.hpp:108-149)
+  uint32_t tri;
+  uint32_t meta;   // bits 0-3 block-column mask, bit 4 large
+  uint32_t b[2];   // 8 row begins, one byte each
+  uint32_t l[2];   // 8 row lasts, one byte each; empty row = (31, 0)
+};
+
+__device__ __forceinline__ uint32_t byte_of(const uint32_t* w, int i) {
+  return (w[i >> 2] >> ((i & 3) * 8)) & 0xffu;
+}
+
+// Register depth filter (depth_filter.hpp:31-92) with compile-time maximum
+// capacity KM and runtime capacity cap <= KM; entries ascending by key.
+template <int KM>
+struct RegFilter {
+  uint64_t key[KM + 1];
+  float4 col[KM + 1];
+  int n;
+  uint64_t max_key;
+  bool any;
+
+  __device__ __forceinline__ void reset() {
+    n = 0;
+    max_key = 0;
+    any = false;
+  }
+  // Inserts (k, c); returns true and the popped minimum when over capacity.
+  __device__ __forceinline__ bool push(int cap, uint64_t k, float4 c, uint64_t* pk, float4* pc,
+                                       bool* ooo) {
+    // bubble the new entry into place (keys are unique per pixel)
+    uint64_t ck = k;
+    float4 cc = c;
+#pragma unroll
+    for (int i = 0; i <= KM; ++i) {
+      if (i < n) {
+        if (key[i] > ck) {
+          uint64_t tk = key[i];
+          float4 tc = col[i];
+          key[i] = ck;
+          col[i] = cc;
+          ck = tk;
+          cc = tc;
+        }
+      } else if (i == n) {
+        key[i] = ck;
+        col[i] = cc;
+      }
+    }
+    ++n;
+    if (n <= cap) return false;
+    pop(pk, pc, ooo);
+    return true;
+  }
+  __device__ __forceinline__ void pop(uint64_t* pk, float4* pc, bool* ooo) {
+    *pk = key[0];
+    *pc = col[0];
+#pragma unroll
+    for (int i = 0; i < KM; ++i) {
+      if (i + 1 < n) {
+        key[i] = key[i + 1];
+        col[i] = col[i + 1];
+      }
+    }
+    --n;
+    *ooo = any && *pk < max_key;
+    if (!any || *pk > max_key) max_key = *pk;
+    any = true;
+  }
+  // Peek at what push(k) would pop, without modifying the filter.
+  __device__ __forceinline__ bool peek(int cap, uint64_t k, float4 c, float4* pc) const {
+    if (n + 1 <= cap) return false;
+    if (n == 0 || k < key[0]) {
+      *pc = c;
+    } else {
+      *pc = col[0];
+    }
+    return true;
+  }
+};
+
+__device__ __forceinline__ float4 blend(float4 acc, float4 s) {
+  float t = __fsub_rn(1.0f, acc.w);
+  return make_float4(__fadd_rn(acc.x, __fmul_rn(t, s.x)), __fadd_rn(acc.y, __fmul_rn(t, s.y)),
+                     __fadd_rn(acc.z, __fmul_rn(t, s.z)), __fadd_rn(acc.w, __fmul_rn(t, s.w)));
+}
+
+// make_sample_context (shading.cpp:24-77) + shade_sample (123-139), no
+// textures. Returns the premultiplied colour and the sample depth.
+__device__ __forceinline__ float4 shade_sample(const FrameConst& fc, const Buffers& B,
+                                               uint32_t tri, int px, int py, double* depth) {
+  const TriRec& t = B.tri[tri];
+  const uint4 meta = B.tri_meta[tri];
+  const double x = (double)px + 0.5, y = (double)py + 0.5;
+  const double e0 = eval(t.e[0], x, y), e1 = eval(t.e[1], x, y), e2 = eval(t.e[2], x, y);
+  const double sum = __dadd_rn(__dadd_rn(e0, e1), e2);
+  const double inv = __ddiv_rn(1.0, sum);
+  const float b0 = (float)__dmul_rn(e0, inv), b1 = (float)__dmul_rn(e1, inv),
+              b2 = (float)__dmul_rn(e2, inv);
+  *depth = eval(t.dz, x, y);
+  const uint32_t q = tri >> 1;
+  const uint32_t qf = B.vq_flags[q];
+  const int ltri = (int)(meta.w & 0xffu);
+  float4 color = make_float4(1.0f, 1.0f, 1.0f, 1.0f);
+  if (qf & 2u) {
+    const uint4 c = B.vq_col[q];
+    const uint32_t w0 = c.x, w1 = ltri == 0 ? c.y : c.z, w2 = ltri == 0 ? c.z : c.w;
+    float r[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      r[k] = __fadd_rn(__fadd_rn(__fmul_rn(unpack_c(w0, 8 * k), b0), __fmul_rn(unpack_c(w1, 8 * k), b1)),
+                       __fmul_rn(unpack_c(w2, 8 * k), b2));
+    color = make_float4(r[0], r[1], r[2], r[3]);
+  }
+  float n[3];
+  if (qf & 4u) {
+    const uint4 c = B.vq_nrm[q];
+    const uint32_t w0 = c.x, w1 = ltri == 0 ? c.y : c.z, w2 = ltri == 0 ? c.z : c.w;
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      n[k] = __fadd_rn(__fadd_rn(__fmul_rn(dec_normal_c((w0 >> (10 * k)) & 0x3ffu), b0),
+                                 __fmul_rn(dec_normal_c((w1 >> (10 * k)) & 0x3ffu), b1)),
+                       __fmul_rn(dec_normal_c((w2 >> (10 * k)) & 0x3ffu), b2));
+  } else {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) n[k] = dec_normal_c((meta.x >> (10 * k)) & 0x3ffu);
+  }
+  // normalize (float), math.hpp:80-85
+  float len2 = __fadd_rn(__fadd_rn(__fmul_rn(n[0], n[0]), __fmul_rn(n[1], n[1])), __fmul_rn(n[2], n[2]));
+  if (len2 <= 0.0f) {
+    n[0] = n[1] = n[2] = 0.0f;
+  } else {
+    float il = __fdiv_rn(1.0f, __fsqrt_rn(len2));
+    n[0] = __fmul_rn(n[0], il);
+    n[1] = __fmul_rn(n[1], il);
+    n[2] = __fmul_rn(n[2], il);
+  }
+  const MatDev& m = B.mats[meta.y];
+  float d = __fadd_rn(__fadd_rn(__fmul_rn(n[0], fc.light[0]), __fmul_rn(n[1], fc.light[1])),
+                      __fmul_rn(n[2], fc.light[2]));
+  float lam = smaxf(0.0f, -d);
+  float light = sminf(1.0f, __fadd_rn(fc.ambient, lam));
+  float r = __fmul_rn(__fmul_rn(__fmul_rn(m.base[0], color.x), 1.0f), light);
+  float g = __fmul_rn(__fmul_rn(__fmul_rn(m.base[1], color.y), 1.0f), light);
+  float b = __fmul_rn(__fmul_rn(__fmul_rn(m.base[2], color.z), 1.0f), light);
+  float a = __fmul_rn(__fmul_rn(m.opacity, color.w), 1.0f);
+  return make_float4(__fmul_rn(r, a), __fmul_rn(g, a), __fmul_rn(b, a), a);
+}
+
+struct RasterShared {
+  // Shared-memory capacities: the reference's low-path limits (raster.hpp:46).
+  static constexpr int kTbr = 1024, kTb = 256, kThb = 256;
+  Tbr tbr[kTbr];
+  uint64_t keys[4][kTb];
+  uint16_t refs[4][kTb];
+  uint64_t thb[4][2][kThb];
+};
+
+struct ItemState {
+  int ntbr;
+  int status;  // 0 ok, 1 overflow (soft), 2 spill, 3 hard error
+  int err_code;
+  uint32_t nthb[4][2];
+  uint64_t frags[4][2];
+};
+
+enum { kPassLow = 0, kPassHigh = 1 };
+
+__device__ __forceinline__ void set_status(ItemState* st, int s, int code) {
+  atomicMax(&st->status, s);
+  if (s == 3) atomicMin(&st->err_code, code);
+}
+
+template <int KM>
+__device__ void shade_half_blocks(const FrameConst& fc, const Buffers& B, int bin, int row,
+                                  int warp, const uint64_t* thb0, const uint64_t* thb1,
+                                  uint32_t n0, uint32_t n1, unsigned long long* acc_stats) {
+  const int lane = threadIdx.x & 31;
+  const int bxi = bin % fc.bins_x, byi = bin / fc.bins_x;
+  const int ly = lane >> 3, cx = lane & 7;
+  unsigned long long samples = 0, segments = 0, invalid_px = 0;
+#pragma unroll 1
+  for (int half = 0; half < 2; ++half) {
+    const uint64_t* list = half ? thb1 : thb0;
+    const uint32_t n = half ? n1 : n0;
+    const int px = bxi * kBin + warp * 8 + cx;
+    const int py = byi * kBin + row * 8 + half * 4 + ly;
+    RegFilter<KM> f;
+    f.reset();
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    bool invalid = false, saturated = false, stopped = false;
+    uint64_t hash = kHashSeed;
+    uint32_t emitted = 0;
+    unsigned sat_mask = 0;
+    unsigned long long enumerated = 0;
+    for (uint32_t r = 0; r < n; ++r) {
+      const uint64_t rec = list[r];
+      const uint32_t tri = (uint32_t)(rec >> 32);
+      const uint32_t sp = (uint32_t)rec & 0xffffffu;
+      const uint32_t b = (sp >> (6 * ly)) & 7u, l = (sp >> (6 * ly + 3)) & 7u;
+      const bool covered = b <= (uint32_t)cx && (uint32_t)cx <= l;
+      const unsigned cov_mask = __ballot_sync(0xffffffffu, covered);
+      float4 col;
+      uint64_t key = 0;
+      if (covered) {
+        double depth;
+        col = shade_sample(fc, B, tri, px, py, &depth);
+        uint32_t qd = quantize_depth(depth);
+        key = fc.extended ? (((uint64_t)qd << 32) | tri) : (((uint64_t)qd << 24) | (tri & 0xffffffu));
+      }
+      int commit_until = 32;  // lanes >= this do not commit (alpha-threshold stop)
+      if (fc.threshold) {
+        bool newly = false;
+        if (covered && !saturated) {
+          float4 pc;
+          if (f.peek(fc.df, key, col, &pc)) newly = blend(acc, pc).w >= kAlphaThreshold;
+        }
+        unsigned new_mask = __ballot_sync(0xffffffffu, newly);
+        if (new_mask && (sat_mask | new_mask) == 0xffffffffu) {
+          int L = 31 - __clz(new_mask);
+          commit_until = L + 1;
+          stopped = true;
+        }
+      }
+      enumerated += __popc(cov_mask & (commit_until == 32 ? 0xffffffffu : ((1u << commit_until) - 1u)));
+      if (covered && lane < commit_until) {
+        uint64_t pk;
+        float4 pc;
+        bool ooo;
+        if (f.push(fc.df, key, col, &pk, &pc, &ooo)) {
+          acc = blend(acc, pc);
+          ++samples;
+          ++emitted;
+          hash = (hash ^ pk) * kHashPrime;
+          if (ooo) invalid = true;
+          if (fc.threshold && !saturated && acc.w >= kAlphaThreshold) saturated = true;
+        }
+      }
+      sat_mask = __ballot_sync(0xffffffffu, saturated);
+      if (stopped) break;
+    }
+    if (!stopped) {
+      bool done = fc.threshold && acc.w >= kAlphaThreshold;
+      while (f.n > 0) {
+        uint64_t pk;
+        float4 pc;
+        bool ooo;
+        f.pop(&pk, &pc, &ooo);
+        if (done) continue;
+        acc = blend(acc, pc);
+        ++samples;
+        ++emitted;
+        hash = (hash ^ pk) * kHashPrime;
+        if (ooo) invalid = true;
+        if (fc.threshold && acc.w >= kAlphaThreshold) done = true;
+      }
+    }
+    segments += (enumerated + 255ull) / 256ull;
+    if (px < fc.width && py < fc.height) {
+      const size_t pix = (size_t)py * fc.width + px;
+      uint32_t word;
+      if (invalid && fc.visualize) {
+        word = 0xffff00ffu;  // magenta overlay, renderer.cpp:56-65
+      } else {
+        float4 o = blend(acc, make_float4(fc.bg[0], fc.bg[1], fc.bg[2], fc.bg[3]));
+        word = quantize_channel(o.x) | (quantize_channel(o.y) << 8) |
+               (quantize_channel(o.z) << 16) | (quantize_channel(o.w) << 24);
+      }
+      B.fb[pix] = word;
+      B.mask[pix] = invalid ? 1 : 0;
+      if (fc.dump) {
+        B.hash[pix] = hash;
+        B.emit[pix] = emitted;
+      }
+      if (invalid) ++invalid_px;
+    }
+  }
+  // warp-reduce the per-lane counts
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    samples += __shfl_xor_sync(0xffffffffu, samples, o);
+    invalid_px += __shfl_xor_sync(0xffffffffu, invalid_px, o);
+  }
+  if (lane == 0) {
+    atomicAdd(&acc_stats[0], samples);
+    atomicAdd(&acc_stats[3], segments);  // warp-uniform: lane 0's count is the total
+    atomicAdd(&acc_stats[4], invalid_px);
+  }
+}
+
+__device__ void write_background(const FrameConst& fc, const Buffers& B, int bin, int row) {
+  const int bxi = bin % fc.bins_x, byi = bin / fc.bins_x;
+  uint32_t word = quantize_channel(fc.bg[0]) | (quantize_channel(fc.bg[1]) << 8) |
+                  (quantize_channel(fc.bg[2]) << 16) | (quantize_channel(fc.bg[3]) << 24);
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    int px = bxi * kBin + (i & 31), py = byi * kBin + row * 8 + (i >> 5);
+    if (px < fc.width && py < fc.height) {
+      size_t pix = (size_t)py * fc.width + px;
+      B.fb[pix] = word;
+      B.mask[pix] = 0;
+      if (fc.dump) {
+        B.hash[pix] = kHashSeed;
+        B.emit[pix] = 0;
+      }
+    }
+  }
+}
+
+// One (bin, block-row) work item. kGlobal selects global-memory scratch
+// (capacities = the active limits) instead of shared memory.
+template <bool kGlobal, int KM>
+__device__ void raster_item(const FrameConst& fc, const Buffers& B, int pass, int bin, int row,
+                            RasterShared* sh, ItemState* st, uint8_t* gscratch,
+                            uint32_t cap_tbr, uint32_t cap_tb) {
+  const Limits lim = pass == kPassLow ? fc.low : fc.high;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int bxi = bin % fc.bins_x, byi = bin / fc.bins_x;
+  const int px0 = bxi * kBin, py0 = byi * kBin;
+  const int px_last = min(px0 + kBin - 1, fc.width - 1);
+  const int py_last = min(py0 + kBin - 1, fc.height - 1);
+  const int ry0 = py0 + row * 8, ry1 = min(ry0 + 7, py_last);
+
+  Tbr* tbr;
+  uint64_t* keys;
+  uint16_t* refs;
+  uint64_t* thb0;
+  uint64_t* thb1;
+  if (kGlobal) {
+    tbr = reinterpret_cast<Tbr*>(gscratch);
+    uint8_t* w = gscratch + (size_t)cap_tbr * sizeof(Tbr) +
+                 (size_t)warp * cap_tb * (sizeof(uint64_t) * 3 + sizeof(uint16_t));
+    keys = reinterpret_cast<uint64_t*>(w);
+    thb0 = keys + cap_tb;
+    thb1 = thb0 + cap_tb;
+    refs = reinterpret_cast<uint16_t*>(thb1 + cap_tb);
+  } else {
+    tbr = sh->tbr;
+    keys = sh->keys[warp];
+    refs = sh->refs[warp];
+    thb0 = sh->thb[warp][0];
+    thb1 = sh->thb[warp][1];
+  }
+
+  if (threadIdx.x == 0) {
+    st->ntbr = 0;
+    st->status = 0;
+    st->err_code = 0x7fffffff;
+  }
+  __syncthreads();
+
+  // ---- phase A: tri-block-rows of this block-row (raster.cpp:41-98)
+  const uint32_t nq = B.qcnt[bin], nt = B.tcnt[bin], o = B.off[bin];
+  const uint32_t T = 2 * nq + nt;
+  for (uint32_t i = threadIdx.x; i < T; i += blockDim.x) {
+    uint32_t ti, large;
+    if (i < 2 * nq) {
+      ti = B.items[o + (i >> 1)] * 2 + (i & 1);
+      large = 0;
+    } else {
+      ti = B.items[o + nq + (i - 2 * nq)];
+      large = 1;
+    }
+    const uint4 meta = B.tri_meta[ti];
+    if (!(meta.w & 0x100u)) continue;
+    const TriRec& t = B.tri[ti];
+    int yb = max(max(t.y_min, py0), ry0), ye = min(min(t.y_max, py_last), ry1);
+    if (yb > ye) continue;
+    Tbr rec;
+    rec.tri = ti;
+    rec.b[0] = rec.b[1] = 0x1f1f1f1fu;
+    rec.l[0] = rec.l[1] = 0u;
+    uint32_t cols = 0;
+    for (int py = yb; py <= ye; ++py) {
+      int b, l;
+      if (!row_span(t, py, px0, px_last, &b, &l)) continue;
+      int ly = py - ry0;
+      uint32_t bb = (uint32_t)(b - px0), ll = (uint32_t)(l - px0);
+      int sh8 = (ly & 3) * 8;
+      rec.b[ly >> 2] = (rec.b[ly >> 2] & ~(0xffu << sh8)) | (bb << sh8);
+      rec.l[ly >> 2] = (rec.l[ly >> 2] & ~(0xffu << sh8)) | (ll << sh8);
+      cols |= ((2u << (ll >> 3)) - 1u) & ~((1u << (bb >> 3)) - 1u);
+    }
+    if (!cols) continue;
+    rec.meta = cols | (large << 4);
+    int slot = atomicAdd(&st->ntbr, 1);
+    if ((uint32_t)slot < cap_tbr) tbr[slot] = rec;
+  }
+  __syncthreads();
+  const uint32_t ntbr = (uint32_t)st->ntbr;
+  if (ntbr > lim.tbr) {
+    if (threadIdx.x == 0) set_status(st, pass == kPassLow ? 1 : 3, 0);
+  } else if (ntbr > cap_tbr) {
+    if (threadIdx.x == 0) set_status(st, 2, 0);
+  }
+  __syncthreads();
+  if (st->status) return;
+
+  // ---- phase B: warp w extracts block (row, w) (raster.cpp:100-199)
+  const int block = row * 4 + warp;
+  const uint32_t c0 = (uint32_t)warp * 8u, c1 = c0 + 7u;
+  const double bpx0 = (double)(px0 + warp * 8), bpy0 = (double)(py0 + row * 8);
+  uint32_t n = 0;
+  for (uint32_t base = 0; base < ntbr; base += 32) {
+    uint32_t i = base + lane;
+    bool sel = i < ntbr && ((tbr[i].meta >> warp) & 1u);
+    unsigned m = __ballot_sync(0xffffffffu, sel);
+    if (sel) {
+      uint32_t pos = n + __popc(m & ((1u << lane) - 1u));
+      if (pos < cap_tb) {
+        const Tbr& rw = tbr[i];
+        uint32_t count = 0, sx = 0, sy = 0;
+#pragma unroll
+        for (int y = 0; y < 8; ++y) {
+          uint32_t b = byte_of(rw.b, y), l = byte_of(rw.l, y);
+          if (b > l) continue;
+          b = max(b, c0);
+          l = min(l, c1);
+          if (b > l) continue;
+          uint32_t k = l - b + 1;
+          count += k;
+          sx += (b + l) * k / 2 - c0 * k;
+          sy += (uint32_t)y * k;
+        }
+        uint32_t qd = 0x3fffffu;
+        if (count) {
+          double cx = __dadd_rn(__dadd_rn(bpx0, __ddiv_rn((double)sx, (double)count)), 0.5);
+          double cy = __dadd_rn(__dadd_rn(bpy0, __ddiv_rn((double)sy, (double)count)), 0.5);
+          qd = quantize_depth(eval(B.tri[rw.tri].dz, cx, cy));
+        }
+        keys[pos] = ((uint64_t)qd << 33) | ((uint64_t)((rw.meta >> 4) & 1u) << 32) | rw.tri;
+        refs[pos] = (uint16_t)i;
+      }
+    }
+    n += __popc(m);
+  }
+  if (n > lim.tb) {
+    if (lane == 0) set_status(st, pass == kPassLow ? 1 : 3, 1 + 3 * block);
+  } else if (n > cap_tb) {
+    if (lane == 0) set_status(st, 2, 0);
+  }
+  __syncwarp();
+  bool ok = n <= lim.tb && n <= cap_tb;
+  uint32_t nthb[2] = {0, 0};
+  uint64_t frags[2] = {0, 0};
+  if (ok && n > 1) {
+    // bitonic sort of (key, ref) ascending
+    uint32_t N = 1;
+    while (N < n) N <<= 1;
+    for (uint32_t i = n + lane; i < N; i += 32) keys[i] = ~0ull, refs[i] = 0;
+    __syncwarp();
+    for (uint32_t k = 2; k <= N; k <<= 1)
+      for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+        for (uint32_t i = lane; i < N; i += 32) {
+          uint32_t ixj = i ^ j;
+          if (ixj > i) {
+            uint64_t x = keys[i], y = keys[ixj];
+            bool up = (i & k) == 0;
+            if ((x > y) == up) {
+              keys[i] = y;
+              keys[ixj] = x;
+              uint16_t t = refs[i];
+              refs[i] = refs[ixj];
+              refs[ixj] = t;
+            }
+          }
+        }
+        __syncwarp();
+      }
+  }
+  if (ok) {
+    // split into upper/lower tri-half-blocks with fragment prefix sums
+    for (uint32_t base = 0; base < n; base += 32) {
+      uint32_t k = base + lane;
+      uint32_t sp[2] = {0, 0}, fr[2] = {0, 0};
+      uint32_t tri = 0;
+      if (k < n) {
+        const Tbr& rw = tbr[refs[k]];
+        tri = rw.tri;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          uint32_t s = 0, f = 0;
+#pragma unroll
+          for (int y = 0; y < 4; ++y) {
+            uint32_t b = byte_of(rw.b, h * 4 + y), l = byte_of(rw.l, h * 4 + y);
+            uint32_t lb = 7, ll = 0;
+            if (b <= l) {
+              b = max(b, c0);
+              l = min(l, c1);
+              if (b <= l) {
+                lb = b - c0;
+                ll = l - c0;
+                f += l - b + 1;
+              }
+            }
+            s |= (lb | (ll << 3)) << (6 * y);
+          }
+          sp[h] = s;
+          fr[h] = f;
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        bool ne = fr[h] > 0;
+        unsigned m = __ballot_sync(0xffffffffu, ne);
+        uint32_t pos = nthb[h] + __popc(m & ((1u << lane) - 1u));
+        uint64_t* out = h ? thb1 : thb0;
+        if (ne && pos < cap_tb) out[pos] = ((uint64_t)tri << 32) | sp[h] | ((uint64_t)fr[h] << 24);
+        uint32_t f = fr[h];
+#pragma unroll
+        for (int s = 16; s > 0; s >>= 1) f += __shfl_xor_sync(0xffffffffu, f, s);
+        nthb[h] += __popc(m);
+        frags[h] += f;
+      }
+    }
+    for (int h = 0; h < 2; ++h) {
+      if (nthb[h] > lim.thb) {
+        if (lane == 0) set_status(st, pass == kPassLow ? 1 : 3, 2 + 3 * block);
+      } else if (frags[h] > lim.frags) {
+        if (lane == 0) set_status(st, pass == kPassLow ? 1 : 3, 3 + 3 * block);
+      }
+    }
+  }
+  if (lane == 0) {
+    st->nthb[warp][0] = nthb[0];
+    st->nthb[warp][1] = nthb[1];
+    st->frags[warp][0] = frags[0];
+    st->frags[warp][1] = frags[1];
+  }
+  __syncthreads();
+  if (st->status) return;
+
+  // ---- phase C: shade + blend both half-blocks of block (row, warp)
+  unsigned long long* slot = B.slots + ((size_t)bin * 4 + row) * 5;
+  if (threadIdx.x < 5) slot[threadIdx.x] = 0;
+  __syncthreads();
+  if (lane == 0) {
+    atomicAdd(&slot[1], (unsigned long long)(frags[0] + frags[1]));
+    atomicAdd(&slot[2], (unsigned long long)(nthb[0] + nthb[1]));
+  }
+  if (fc.dump && lane < 2) {
+    int hb = block * 2 + lane;
+    B.thb_cnt[(size_t)bin * 32 + hb] = nthb[lane];
+    if (B.thb_off) {
+      uint64_t base = B.thb_off[(size_t)bin * 32 + hb];
+      const uint64_t* list = lane ? thb1 : thb0;
+      uint32_t prefix = 0;
+      for (uint32_t i = 0; i < nthb[lane]; ++i) {
+        uint64_t r = list[i];
+        uint32_t tri = (uint32_t)(r >> 32);
+        prefix += (uint32_t)(r >> 24) & 0x3fu;
+        // TriHalfBlock::make, packing.hpp:154-176
+        B.thb_out[base + i] = (r & 0xffffffull) | ((uint64_t)(tri & 0xffffffu) << 24) |
+                              ((uint64_t)(prefix & 0xfffu) << 48);
+        B.thb_tri[base + i] = tri;
+        B.thb_pre[base + i] = prefix;
+      }
+    }
+  }
+  shade_half_blocks<KM>(fc, B, bin, row, warp, thb0, thb1, nthb[0], nthb[1], slot);
+}
+
+template <bool kGlobal, int KM>
+__global__ void __launch_bounds__(128) k_raster(FrameConst fc, Buffers B, int pass,
+                                                uint32_t cap_tbr, uint32_t cap_tb) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  RasterShared* sh = kGlobal ? nullptr : reinterpret_cast<RasterShared*>(smem_raw);
+  __shared__ ItemState st;
+  __shared__ uint32_t item_s;
+  if (B.ctr->error) return;
+  uint8_t* gscratch = kGlobal ? B.scratch + (size_t)blockIdx.x * B.scratch_per_cta : nullptr;
+  const uint32_t nitems = kGlobal ? B.ctr->spill_count[pass] : (uint32_t)fc.nbins * 4u;
+  unsigned int* counter = &B.ctr->work_next[pass * 2 + (kGlobal ? 1 : 0)];
+  for (;;) {
+    if (threadIdx.x == 0) item_s = atomicAdd(counter, 1u);
+    __syncthreads();
+    const uint32_t item = item_s;
+    __syncthreads();
+    if (item >= nitems) break;
+    const uint32_t code = kGlobal ? B.spill[pass][item] : item;
+    const int bin = (int)(code >> 2), row = (int)(code & 3u);
+    const int bxi = bin % fc.bins_x, byi = bin / fc.bins_x;
+    const uint8_t cat = B.cat[bin];
+    const bool owned = fc.world <= 1 || ((bxi + 3 * byi) % fc.world) == fc.rank;
+    if (!owned) continue;
+    bool run;
+    if (pass == kPassLow) {
+      if (cat == 0) {
+        if (!kGlobal) {
+          write_background(fc, B, bin, row);
+          if (threadIdx.x < 5) B.slots[((size_t)bin * 4 + row) * 5 + threadIdx.x] = 0;
+        }
+        continue;
+      }
+      run = cat == 1 && !fc.force_high;
+    } else {
+      run = cat == 2 || (cat == 1 && fc.force_high) || B.prop[bin];
+    }
+    if (!run) continue;
+    if (!kGlobal && pass == kPassLow && B.prop[bin]) continue;  // sibling already overflowed
+    raster_item<kGlobal, KM>(fc, B, pass, bin, row, sh, &st, gscratch, cap_tbr, cap_tb);
+    __syncthreads();
+    if (threadIdx.x == 0 && st.status) {
+      if (st.status == 1) {
+        B.prop[bin] = 1;
+      } else if (st.status == 2) {
+        uint32_t s = atomicAdd(&B.ctr->spill_count[pass], 1u);
+        B.spill[pass][s] = code;
+      } else {
+        atomicMin(&B.ctr->bin_error, (unsigned long long)bin * 64ull +
+                                         (unsigned long long)min(st.err_code, 63));
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_finalize(FrameConst fc, Buffers B) {
+  if (B.ctr->error) return;
+  __shared__ unsigned long long acc[6];
+  if (threadIdx.x < 6) acc[threadIdx.x] = 0;
+  __syncthreads();
+  unsigned long long s[5] = {0, 0, 0, 0, 0}, prop = 0;
+  for (int b = threadIdx.x; b < fc.nbins; b += blockDim.x) {
+    const int bxi = b % fc.bins_x, byi = b / fc.bins_x;
+    const bool owned = fc.world <= 1 || ((bxi + 3 * byi) % fc.world) == fc.rank;
+    if (!owned) continue;
+    for (int r = 0; r < 4; ++r)
+      for (int k = 0; k < 5; ++k) s[k] += B.slots[((size_t)b * 4 + r) * 5 + k];
+    prop += B.prop[b];
+  }
+  for (int k = 0; k < 5; ++k) atomicAdd(&acc[k], s[k]);
+  atomicAdd(&acc[5], prop);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    B.ctr->samples = acc[0];
+    B.ctr->fragments = acc[1];
+    B.ctr->thb = acc[2];
+    B.ctr->segments = acc[3];
+    B.ctr->invalid = acc[4];
+    B.ctr->bins_propagated = acc[5];
+  }
+}
+
+// a-buffer reference renderer (oracle.cpp:28-117) on the bin lists: every
+// triangle covering a pixel is in that pixel's bin list. Fragments are
+// blended in exact key order by repeated selection of the next key, so no
+// per-pixel list storage is needed (an oracle mode, not a fast path).
+__global__ void __launch_bounds__(128) k_abuffer(FrameConst fc, Buffers B) {
+  if (B.ctr->error) return;
+  const int px = blockIdx.x * 16 + (threadIdx.x & 15);
+  const int py = blockIdx.y * 8 + (threadIdx.x >> 4);
+  if (px >= fc.width || py >= fc.height) return;
+  const size_t pix = (size_t)py * fc.width + px;
+  const int bin = (py / kBin) * fc.bins_x + px / kBin;
+  const uint32_t nq = B.qcnt[bin], nt = B.tcnt[bin], o = B.off[bin];
+  const uint32_t T = 2 * nq + nt;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  uint64_t hash = kHashSeed;
+  uint32_t n = 0;
+  uint64_t last = 0;
+  bool first = true;
+  for (;;) {
+    uint64_t best = ~0ull;
+    uint32_t best_t = 0;
+    bool found = false;
+    for (uint32_t i = 0; i < T; ++i) {
+      uint32_t ti = i < 2 * nq ? B.items[o + (i >> 1)] * 2 + (i & 1) : B.items[o + nq + (i - 2 * nq)];
+      if (!(B.tri_meta[ti].w & 0x100u)) continue;
+      const TriRec& t = B.tri[ti];
+      if (py < t.y_min || py > t.y_max || !covers(t, px, py)) continue;
+      uint32_t qd = quantize_depth(eval(t.dz, (double)px + 0.5, (double)py + 0.5));
+      uint64_t k = fc.extended ? (((uint64_t)qd << 32) | ti) : (((uint64_t)qd << 24) | (ti & 0xffffffu));
+      if ((first || k > last) && k < best) {
+        best = k;
+        best_t = ti;
+        found = true;
+      }
+    }
+    if (!found) break;
+    double depth;
+    float4 c = shade_sample(fc, B, best_t, px, py, &depth);
+    acc = blend(acc, c);
+    hash = (hash ^ best) * kHashPrime;
+    ++n;
+    last = best;
+    first = false;
+  }
+  float4 out = blend(acc, make_float4(fc.bg[0], fc.bg[1], fc.bg[2], fc.bg[3]));
+  B.fb[pix] = quantize_channel(out.x) | (quantize_channel(out.y) << 8) |
+              (quantize_channel(out.z) << 16) | (quantize_channel(out.w) << 24);
+  B.mask[pix] = 0;
+  if (fc.dump) {
+    B.hash[pix] = hash;
+    B.emit[pix] = n;
+  }
+  atomicAdd(&B.ctr->samples, (unsigned long long)n);
+}
+
+}  // namespace dev
+
+// ============================================================ host side
+
+namespace {
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw Error(VEIL_ERR_INTERNAL, std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+thread_local int t_device = 0;
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void ensure(size_t n) {
+    if (n <= bytes) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    size_t alloc = std::max<size_t>(n, 256);
+    ck(cudaMalloc(&p, alloc), "cudaMalloc");
+    bytes = alloc;
+  }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  template <typename T>
+  T* as() const {
+    return reinterpret_cast<T*>(p);
+  }
+};
+
+}  // namespace
+
+struct DeviceScene {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  uint64_t uploaded_version = 0;
+  uint32_t nverts = 0, nquads = 0;
+  DevBuf pos, vcol, vnrm, quads, qmat, mats;
+  DevBuf block_cnt, block_off, vq_src, vq_box, vq_flags, vq_mat, vq_col, vq_nrm, tri, tri_meta;
+  DevBuf qcnt, tcnt, off, qcur, tcur, cat, prop, items, slots, spill0, spill1, scratch, fb, mask,
+      hash, emit, thb_cnt, thb_off, thb_out, thb_tri, thb_pre, ctr;
+  uint32_t items_cap = 0;
+  cudaEvent_t ev[6] = {};
+  veil_frame_stats last{};
+  int fb_w = 0, fb_h = 0;
+  int sm_count = 148;
+  int raster_ctas_smem = 0;
+  int raster_ctas_global = 0;
+
+  ~DeviceScene() {
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+void release_device_scene(DeviceScene* d) {
+  if (!d) return;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(d->device);
+  delete d;
+  cudaSetDevice(prev);
+}
+
+void set_current_device(int device) {
+  int n = 0;
+  ck(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
+  if (device < 0 || device >= n) throw Error(VEIL_ERR_INVALID_ARG, "no such CUDA device");
+  t_device = device;
+  ck(cudaSetDevice(device), "cudaSetDevice");
+}
+
+bool bin_owned(int bx, int by, int rank, int world) {
+  return world <= 1 || ((bx + 3 * by) % world) == rank;
+}
+
+uint64_t shard_tile_count(int bins_x, int bins_y, int rank, int world) {
+  uint64_t n = 0;
+  for (int y = 0; y < bins_y; ++y)
+    for (int x = 0; x < bins_x; ++x)
+      if (bin_owned(x, y, rank, world)) ++n;
+  return n;
+}
+
+namespace {
+
+DeviceScene* device_scene(const Scene& s) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+    throw Error(VEIL_ERR_INTERNAL, "no CUDA device available (libveil has no CPU fallback)");
+  ck(cudaSetDevice(t_device), "cudaSetDevice");
+  if (s.device && s.device->device != t_device) {
+    release_device_scene(s.device);
+    s.device = nullptr;
+  }
+  if (!s.device) {
+    DeviceScene* d = new DeviceScene();
+    d->device = t_device;
+    ck(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    for (auto& e : d->ev) ck(cudaEventCreate(&e), "cudaEventCreate");
+    cudaDeviceGetAttribute(&d->sm_count, cudaDevAttrMultiProcessorCount, t_device);
+    s.device = d;
+  }
+  DeviceScene* d = s.device;
+  if (d->uploaded_version != s.geometry_version) {
+    const size_t V = s.vertices.size(), Q = s.quads.size();
+    std::vector<float4> pos(V);
+    std::vector<uint32_t> vcol(V), vnrm(V), qmat(Q);
+    std::vector<uint4> quads(Q);
+    for (size_t i = 0; i < V; ++i) {
+      const veil_vertex& v = s.vertices[i];
+      pos[i] = make_float4(v.position[0], v.position[1], v.position[2], 0.0f);
+      // pack_color / encode_normal of the vertex (packing.hpp:33-61); the
+      // setup kernel gathers these per visible quad (setup.cpp:329-333).
+      auto enc = [](float c, double s, long lo, long hi) {
+        long q = std::lround(double(c) * s);
+        return q < lo ? lo : (q > hi ? hi : q);
+      };
+      vcol[i] = uint32_t(enc(v.color[0], 255.0, 0, 255)) |
+                (uint32_t(enc(v.color[1], 255.0, 0, 255)) << 8) |
+                (uint32_t(enc(v.color[2], 255.0, 0, 255)) << 16) |
+                (uint32_t(enc(v.color[3], 255.0, 0, 255)) << 24);
+      vnrm[i] = (uint32_t(enc(v.normal[0], 511.0, -511, 511)) & 0x3ffu) |
+                ((uint32_t(enc(v.normal[1], 511.0, -511, 511)) & 0x3ffu) << 10) |
+                ((uint32_t(enc(v.normal[2], 511.0, -511, 511)) & 0x3ffu) << 20);
+    }
+    for (size_t i = 0; i < Q; ++i) {
+      const veil_quad& q = s.quads[i];
+      quads[i] = make_uint4(q.v[0], q.v[1], q.v[2], q.v[3]);
+      qmat[i] = q.material;
+    }
+    std::vector<dev::MatDev> mats(s.materials.size());
+    for (size_t i = 0; i < mats.size(); ++i) {
+      const veil_material& m = s.materials[i];
+      dev::MatDev md{};
+      for (int k = 0; k < 4; ++k) md.base[k] = m.base_color[k];
+      md.opacity = m.opacity;
+      bool hc = (m.flags & VEIL_MATERIAL_VERTEX_COLORS) && (s.flags & VEIL_SCENE_HAS_COLORS);
+      bool hn = (m.flags & VEIL_MATERIAL_VERTEX_NORMALS) && (s.flags & VEIL_SCENE_HAS_NORMALS);
+      md.flags = (hc ? 1u : 0u) | (hn ? 2u : 0u);
+      mats[i] = md;
+    }
+    d->pos.ensure(V * sizeof(float4));
+    d->vcol.ensure(V * 4);
+    d->vnrm.ensure(V * 4);
+    d->quads.ensure(Q * sizeof(uint4));
+    d->qmat.ensure(Q * 4);
+    d->mats.ensure(mats.size() * sizeof(dev::MatDev));
+    if (V) {
+      ck(cudaMemcpy(d->pos.p, pos.data(), V * sizeof(float4), cudaMemcpyHostToDevice), "upload");
+      ck(cudaMemcpy(d->vcol.p, vcol.data(), V * 4, cudaMemcpyHostToDevice), "upload");
+      ck(cudaMemcpy(d->vnrm.p, vnrm.data(), V * 4, cudaMemcpyHostToDevice), "upload");
+    }
+    if (Q) {
+      ck(cudaMemcpy(d->quads.p, quads.data(), Q * sizeof(uint4), cudaMemcpyHostToDevice), "upload");
+      ck(cudaMemcpy(d->qmat.p, qmat.data(), Q * 4, cudaMemcpyHostToDevice), "upload");
+    }
+    if (!mats.empty())
+      ck(cudaMemcpy(d->mats.p, mats.data(), mats.size() * sizeof(dev::MatDev),
+                    cudaMemcpyHostToDevice),
+         "upload");
+    d->nverts = uint32_t(V);
+    d->nquads = uint32_t(Q);
+    d->uploaded_version = s.geometry_version;
+    d->items_cap = 0;
+  }
+  return d;
+}
+
+void camera_vectors(const Camera& c, dev::FrameConst* fc) {
+  // camera_eye / camera_forward, scene.cpp:67-84
+  fc->has_eye = 0;
+  if (c.has_eye) {
+    fc->has_eye = 1;
+    for (int i = 0; i < 3; ++i) fc->eye[i] = c.eye[i];
+  } else {
+    double inv[16];
+    if (mat4_inverse(c.m, inv)) {
+      double v[4] = {0.0, 0.0, 1.0, 0.0}, h[4];
+      for (int r = 0; r < 4; ++r)
+        h[r] = inv[r * 4] * v[0] + inv[r * 4 + 1] * v[1] + inv[r * 4 + 2] * v[2] + inv[r * 4 + 3] * v[3];
+      if (!(std::abs(h[3]) < 1e-12)) {
+        double s = 1.0 / h[3];
+        fc->eye[0] = h[0] * s;
+        fc->eye[1] = h[1] * s;
+        fc->eye[2] = h[2] * s;
+        fc->has_eye = 1;
+      }
+    }
+  }
+  double g[3] = {c.m[8], c.m[9], c.m[10]};
+  double len = std::sqrt(g[0] * g[0] + g[1] * g[1] + g[2] * g[2]);
+  if (len <= 0.0) {
+    fc->fwd[0] = 0.0, fc->fwd[1] = 0.0, fc->fwd[2] = 1.0;
+  } else {
+    double inv = 1.0 / len;
+    for (int i = 0; i < 3; ++i) fc->fwd[i] = g[i] * inv;
+  }
+}
+
+template <int KM>
+void launch_raster_pair(DeviceScene* d, const dev::FrameConst& fc, const dev::Buffers& B, int pass,
+                        uint32_t gcap_tbr, uint32_t gcap_tb, int* launches) {
+  const size_t smem = sizeof(dev::RasterShared);
+  static thread_local bool configured[2] = {false, false};
+  (void)configured;
+  ck(cudaFuncSetAttribute(dev::k_raster<false, KM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          int(smem)),
+     "cudaFuncSetAttribute");
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_raster<false, KM>, 128, smem);
+  int grid = std::max(1, per_sm) * d->sm_count;
+  grid = std::min<long long>(grid, (long long)fc.nbins * 4);
+  dev::k_raster<false, KM><<<grid, 128, smem, d->stream>>>(fc, B, pass, dev::RasterShared::kTbr,
+                                                             dev::RasterShared::kTb);
+  ++*launches;
+  dev::k_raster<true, KM><<<d->raster_ctas_global, 128, 0, d->stream>>>(fc, B, pass, gcap_tbr, gcap_tb);
+  ++*launches;
+}
+
+template <int KM>
+void launch_raster_km(DeviceScene* d, const dev::FrameConst& fc, const dev::Buffers& B, int pass,
+                      uint32_t gcap_tbr, uint32_t gcap_tb, int* launches) {
+  launch_raster_pair<KM>(d, fc, B, pass, gcap_tbr, gcap_tb, launches);
+}
+
+void launch_raster(DeviceScene* d, const dev::FrameConst& fc, const dev::Buffers& B, int pass,
+                   uint32_t gcap_tbr, uint32_t gcap_tb, int* launches) {
+  int df = fc.df;
+  if (df <= 1) launch_raster_km<1>(d, fc, B, pass, gcap_tbr, gcap_tb, launches);
+  else if (df <= 2) launch_raster_km<2>(d, fc, B, pass, gcap_tbr, gcap_tb, launches);
+  else if (df <= 3) launch_raster_km<3>(d, fc, B, pass, gcap_tbr, gcap_tb, launches);
+  else if (df <= 4) launch_raster_km<4>(d, fc, B, pass, gcap_tbr, gcap_tb, launches);
+  else if (df <= 8) launch_raster_km<8>(d, fc, B, pass, gcap_tbr, gcap_tb, launches);
+  else if (df <= 16) launch_raster_km<16>(d, fc, B, pass, gcap_tbr, gcap_tb, launches);
+  else if (df <= 32) launch_raster_km<32>(d, fc, B, pass, gcap_tbr, gcap_tb, launches);
+  else throw Error(VEIL_ERR_INVALID_ARG, "depth_filter_size above 32 is not supported on the device path");
+}
+
+template <typename T>
+void dump_put(RenderOutput* out, const char* name, const T* dptr, size_t count,
+              cudaStream_t stream) {
+  DumpArray a;
+  a.count = count;
+  a.bytes.resize(count * sizeof(T));
+  if (count)
+    ck(cudaMemcpyAsync(a.bytes.data(), dptr, count * sizeof(T), cudaMemcpyDeviceToHost, stream),
+       "dump copy");
+  out->dumps[name] = std::move(a);
+}
+
+template <typename T>
+void dump_put_host(RenderOutput* out, const char* name, const std::vector<T>& v) {
+  DumpArray a;
+  a.count = v.size();
+  a.bytes.resize(v.size() * sizeof(T));
+  if (!v.empty()) std::memcpy(a.bytes.data(), v.data(), a.bytes.size());
+  out->dumps[name] = std::move(a);
+}
+
+struct Prepared {
+  dev::FrameConst fc;
+  dev::Buffers B;
+  uint32_t nblocks;
+  uint32_t gcap_tbr, gcap_tb;
+};
+
+Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
+  const veil_render_params& p = opt.params;
+  const Camera& cam = s.camera;
+  Prepared P;
+  dev::FrameConst& fc = P.fc;
+  std::memset(&fc, 0, sizeof fc);
+  for (int i = 0; i < 16; ++i) fc.m[i] = cam.m[i];
+  camera_vectors(cam, &fc);
+  fc.width = cam.width;
+  fc.height = cam.height;
+  fc.bins_x = (cam.width + kBinSize - 1) / kBinSize;
+  fc.bins_y = (cam.height + kBinSize - 1) / kBinSize;
+  fc.nbins = fc.bins_x * fc.bins_y;
+  fc.backface = (p.flags & VEIL_RENDER_BACKFACE_CULLING) ? 1 : 0;
+  fc.extended = s.extended ? 1 : 0;
+  fc.nquads = d->nquads;
+  {
+    // normalize(light_dir) in float, math.hpp:80-85
+    float l[3] = {p.light_dir[0], p.light_dir[1], p.light_dir[2]};
+    float l2 = l[0] * l[0] + l[1] * l[1] + l[2] * l[2];
+    if (l2 <= 0.0f) {
+      fc.light[0] = fc.light[1] = fc.light[2] = 0.0f;
+    } else {
+      float inv = 1.0f / std::sqrt(l2);
+      for (int i = 0; i < 3; ++i) fc.light[i] = l[i] * inv;
+    }
+  }
+  fc.ambient = p.ambient;
+  float a = p.background[3];
+  fc.bg[0] = p.background[0] * a;
+  fc.bg[1] = p.background[1] * a;
+  fc.bg[2] = p.background[2] * a;
+  fc.bg[3] = a;
+  fc.df = std::max(1, p.depth_filter_size);
+  fc.threshold = (p.flags & VEIL_RENDER_ALPHA_THRESHOLD) ? 1 : 0;
+  fc.visualize = (p.flags & VEIL_RENDER_VISUALIZE_ERRORS) ? 1 : 0;
+  fc.force_high = (p.flags & VEIL_RENDER_FORCE_HIGH_PATH) ? 1 : 0;
+  // limits, renderer.cpp:130-142
+  fc.low = {1024, 256, 256, 4095};
+  fc.high = {16384, 4096, 4096, 0xffffffffu};
+  if (p.limit_low_tbr) fc.low.tbr = p.limit_low_tbr;
+  if (p.limit_low_tri_blocks) fc.low.tb = fc.low.thb = p.limit_low_tri_blocks;
+  if (p.limit_low_frags) fc.low.frags = p.limit_low_frags;
+  if (p.limit_high_tbr) fc.high.tbr = p.limit_high_tbr;
+  if (p.limit_high_thb) fc.high.thb = p.limit_high_thb;
+  fc.tri_cap = s.extended ? 0x80000000u : (1u << 24);
+  fc.rank = opt.rank;
+  fc.world = opt.world_size;
+  fc.dump = opt.dump ? 1 : 0;
+
+  const uint32_t Q = d->nquads;
+  const size_t nb = size_t(fc.nbins);
+  P.nblocks = (Q + dev::kSetupBlock - 1) / dev::kSetupBlock;
+  d->block_cnt.ensure(std::max<size_t>(1, P.nblocks) * 4);
+  d->block_off.ensure(std::max<size_t>(1, P.nblocks) * 4);
+  d->vq_src.ensure(size_t(Q) * 4);
+  d->vq_box.ensure(size_t(Q) * 8);
+  d->vq_flags.ensure(size_t(Q) * 4);
+  d->vq_mat.ensure(size_t(Q) * 4);
+  d->vq_col.ensure(size_t(Q) * 16);
+  d->vq_nrm.ensure(size_t(Q) * 16);
+  d->tri.ensure(size_t(Q) * 2 * sizeof(dev::TriRec));
+  d->tri_meta.ensure(size_t(Q) * 2 * 16);
+  d->qcnt.ensure(nb * 4);
+  d->tcnt.ensure(nb * 4);
+  d->off.ensure(nb * 4);
+  d->qcur.ensure(nb * 4);
+  d->tcur.ensure(nb * 4);
+  d->cat.ensure(nb);
+  d->prop.ensure(nb);
+  d->slots.ensure(nb * 4 * 5 * 8);
+  d->spill0.ensure(nb * 4 * 4);
+  d->spill1.ensure(nb * 4 * 4);
+  if (d->items_cap == 0) d->items_cap = std::max<uint32_t>(1u << 20, Q * 6u);
+  d->items.ensure(size_t(d->items_cap) * 4);
+  fc.items_cap = d->items_cap;
+  const size_t npx = size_t(cam.width) * cam.height;
+  d->fb.ensure(npx * 4);
+  d->mask.ensure(npx);
+  if (opt.dump) {
+    d->hash.ensure(npx * 8);
+    d->emit.ensure(npx * 4);
+    d->thb_cnt.ensure(nb * 32 * 4);
+  }
+  d->ctr.ensure(sizeof(dev::Counters));
+  // global scratch for spilled items: capacities follow the active limits
+  P.gcap_tbr = std::min<uint32_t>(std::max(fc.low.tbr, fc.high.tbr), 1u << 16);
+  P.gcap_tb = std::min<uint32_t>(std::max(std::max(fc.low.tb, fc.high.tb), fc.high.thb), P.gcap_tbr);
+  {  // the per-warp bitonic sort pads to a power of two
+    uint32_t p2 = 1;
+    while (p2 < P.gcap_tb) p2 <<= 1;
+    P.gcap_tb = p2;
+  }
+  size_t per_cta = size_t(P.gcap_tbr) * sizeof(dev::Tbr) +
+                   4 * size_t(P.gcap_tb) * (sizeof(uint64_t) * 3 + sizeof(uint16_t));
+  per_cta = (per_cta + 255) & ~size_t(255);
+  d->raster_ctas_global = d->sm_count * 2;
+  d->scratch.ensure(per_cta * d->raster_ctas_global);
+  d->fb_w = cam.width;
+  d->fb_h = cam.height;
+
+  dev::Buffers& B = P.B;
+  std::memset(&B, 0, sizeof B);
+  B.pos = d->pos.as<float4>();
+  B.vcol = d->vcol.as<uint32_t>();
+  B.vnrm = d->vnrm.as<uint32_t>();
+  B.quads = d->quads.as<uint4>();
+  B.qmat = d->qmat.as<uint32_t>();
+  B.mats = d->mats.as<dev::MatDev>();
+  B.block_cnt = d->block_cnt.as<uint32_t>();
+  B.block_off = d->block_off.as<uint32_t>();
+  B.vq_src = d->vq_src.as<uint32_t>();
+  B.vq_box = d->vq_box.as<uint2>();
+  B.vq_flags = d->vq_flags.as<uint32_t>();
+  B.vq_mat = d->vq_mat.as<uint32_t>();
+  B.vq_col = d->vq_col.as<uint4>();
+  B.vq_nrm = d->vq_nrm.as<uint4>();
+  B.tri = d->tri.as<dev::TriRec>();
+  B.tri_meta = d->tri_meta.as<uint4>();
+  B.qcnt = d->qcnt.as<uint32_t>();
+  B.tcnt = d->tcnt.as<uint32_t>();
+  B.off = d->off.as<uint32_t>();
+  B.qcur = d->qcur.as<uint32_t>();
+  B.tcur = d->tcur.as<uint32_t>();
+  B.cat = d->cat.as<uint8_t>();
+  B.prop = d->prop.as<uint8_t>();
+  B.items = d->items.as<uint32_t>();
+  B.slots = d->slots.as<unsigned long long>();
+  B.spill[0] = d->spill0.as<uint32_t>();
+  B.spill[1] = d->spill1.as<uint32_t>();
+  B.scratch = d->scratch.as<uint8_t>();
+  B.scratch_per_cta = per_cta;
+  B.fb = d->fb.as<uint32_t>();
+  B.mask = d->mask.as<uint8_t>();
+  B.hash = opt.dump ? d->hash.as<uint64_t>() : nullptr;
+  B.emit = opt.dump ? d->emit.as<uint32_t>() : nullptr;
+  B.thb_cnt = opt.dump ? d->thb_cnt.as<uint32_t>() : nullptr;
+  B.ctr = d->ctr.as<dev::Counters>();
+  return P;
+}
+
+// Enqueues setup + binning; returns kernel launches.
+int enqueue_front(DeviceScene* d, Prepared& P) {
+  const dev::FrameConst& fc = P.fc;
+  const dev::Buffers& B = P.B;
+  cudaStream_t st = d->stream;
+  int launches = 0;
+  ck(cudaMemsetAsync(B.ctr, 0, sizeof(dev::Counters), st), "memset");
+  ck(cudaMemsetAsync(&B.ctr->bin_error, 0xff, sizeof(unsigned long long), st), "memset");
+  ck(cudaMemsetAsync(B.qcnt, 0, size_t(fc.nbins) * 4, st), "memset");
+  ck(cudaMemsetAsync(B.tcnt, 0, size_t(fc.nbins) * 4, st), "memset");
+  if (B.thb_cnt) ck(cudaMemsetAsync(B.thb_cnt, 0, size_t(fc.nbins) * 32 * 4, st), "memset");
+  cudaEventRecord(d->ev[0], st);
+  if (P.nblocks) {
+    dev::k_setup_count<<<P.nblocks, dev::kSetupBlock, 0, st>>>(fc, B);
+    dev::k_scan_blocks<<<1, 1024, 0, st>>>(fc, B, P.nblocks);
+    dev::k_setup_write<<<P.nblocks, dev::kSetupBlock, 0, st>>>(fc, B);
+    launches += 3;
+  }
+  cudaEventRecord(d->ev[1], st);
+  int grid = std::max(1, std::min<int>(d->sm_count * 8, int((fc.nquads + 255) / 256)));
+  dev::k_bin_pass<false><<<grid, 256, 0, st>>>(fc, B);
+  dev::k_bin_scan<<<1, 1024, 0, st>>>(fc, B);
+  dev::k_bin_pass<true><<<grid, 256, 0, st>>>(fc, B);
+  dev::k_bin_sort<<<std::min(fc.nbins, d->sm_count * 8), 256, 0, st>>>(fc, B);
+  launches += 4;
+  cudaEventRecord(d->ev[2], st);
+  return launches;
+}
+
+void read_stats(DeviceScene* d, const dev::Counters& c, const Scene& s, veil_frame_stats* st) {
+  float ms[4] = {0, 0, 0, 0};
+  cudaEventElapsedTime(&ms[0], d->ev[0], d->ev[1]);
+  cudaEventElapsedTime(&ms[1], d->ev[1], d->ev[2]);
+  cudaEventElapsedTime(&ms[2], d->ev[2], d->ev[3]);
+  cudaEventElapsedTime(&ms[3], d->ev[3], d->ev[4]);
+  float total = 0;
+  cudaEventElapsedTime(&total, d->ev[0], d->ev[4]);
+  st->setup_ms = ms[0];
+  st->binning_ms = ms[1];
+  st->low_raster_ms = ms[2];
+  st->hi_raster_ms = ms[3];
+  st->total_ms = total;
+  st->samples = c.samples;
+  st->fragments = c.fragments;
+  st->tri_half_blocks = c.thb;
+  st->segments = c.segments;
+  st->input_quads = s.quads.size();
+  st->visible_quads = c.cull[0];
+  st->culled_degenerate = c.cull[1];
+  st->culled_backfacing = c.cull[2];
+  st->culled_frustum = c.cull[3];
+  st->culled_between_samples = c.cull[4];
+  st->bins_empty = c.bins_empty;
+  st->bins_low = c.bins_low;
+  st->bins_high = c.bins_high;
+  st->bins_propagated = c.bins_propagated;
+  st->invalid_pixels = c.invalid;
+  st->bin_pairs = c.pairs;
+  st->large_tris = c.large_tris;
+  st->small_quads = c.small_quads;
+}
+
+const char* limit_name(int code) {
+  if (code == 0) return "tri-block-rows per block-row";
+  switch ((code - 1) % 3) {
+    case 0: return "tri-blocks per block";
+    case 1: return "tri-half-blocks per half-block";
+    default: return "fragments per half-block";
+  }
+}
+
+void check_frame_errors(const dev::Counters& c, const dev::FrameConst& fc) {
+  if (c.error & 1u)
+    throw Error(VEIL_ERR_CAPACITY, "visible primitive count exceeds 24-bit index space");
+  if (c.error & 4u) throw Error(VEIL_ERR_CAPACITY, "a-buffer fragment list capacity exceeded");
+  if (c.bin_error != ~0ull) {
+    int bin = int(c.bin_error / 64), code = int(c.bin_error % 64);
+    throw Error(VEIL_ERR_CAPACITY, "bin (" + std::to_string(bin % fc.bins_x) + "," +
+                                       std::to_string(bin / fc.bins_x) +
+                                       ") exceeds high-rasterizer limit: " + limit_name(code));
+  }
+}
+
+void validate_frame(const Scene& s, const RenderOptions& opt) {
+  validate_scene(s);
+  const veil_render_params& p = opt.params;
+  bool reference = p.flags & VEIL_RENDER_REFERENCE;
+  if (!reference && p.depth_filter_size < 1)
+    throw Error(VEIL_ERR_INVALID_ARG, "depth_filter_size must be >= 1");
+  int bx = (s.camera.width + kBinSize - 1) / kBinSize, by = (s.camera.height + kBinSize - 1) / kBinSize;
+  if (!reference && !s.extended && bx * by > kMaxBins)
+    throw Error(VEIL_ERR_CAPACITY, "bin grid exceeds 5120 bins");
+  if (!reference) {
+    uint32_t lt = p.limit_low_tbr ? p.limit_low_tbr : 1024;
+    uint32_t ht = p.limit_high_tbr ? p.limit_high_tbr : 16384;
+    uint32_t lb = p.limit_low_tri_blocks ? p.limit_low_tri_blocks : 256;
+    uint32_t hb = p.limit_high_thb ? p.limit_high_thb : 4096;
+    if (lt > ht || lb > hb)
+      throw Error(VEIL_ERR_INVALID_ARG, "low rasterizer limits exceed high limits");
+  }
+}
+
+void collect_dumps(DeviceScene* d, Prepared& P, const dev::Counters& c, RenderOutput* out) {
+  cudaStream_t st = d->stream;
+  const uint32_t nv = c.nvis;
+  const dev::Buffers& B = P.B;
+  const dev::FrameConst& fc = P.fc;
+  std::vector<uint32_t> src(nv), flags(nv), mat(nv);
+  std::vector<uint2> box(nv);
+  std::vector<uint4> col(nv), nrm(nv), meta(size_t(nv) * 2);
+  std::vector<dev::TriRec> tri(size_t(nv) * 2);
+  if (nv) {
+    ck(cudaMemcpyAsync(src.data(), B.vq_src, nv * 4, cudaMemcpyDeviceToHost, st), "dump");
+    ck(cudaMemcpyAsync(flags.data(), B.vq_flags, nv * 4, cudaMemcpyDeviceToHost, st), "dump");
+    ck(cudaMemcpyAsync(mat.data(), B.vq_mat, nv * 4, cudaMemcpyDeviceToHost, st), "dump");
+    ck(cudaMemcpyAsync(box.data(), B.vq_box, nv * 8, cudaMemcpyDeviceToHost, st), "dump");
+    ck(cudaMemcpyAsync(col.data(), B.vq_col, nv * 16, cudaMemcpyDeviceToHost, st), "dump");
+    ck(cudaMemcpyAsync(nrm.data(), B.vq_nrm, nv * 16, cudaMemcpyDeviceToHost, st), "dump");
+    ck(cudaMemcpyAsync(meta.data(), B.tri_meta, size_t(nv) * 32, cudaMemcpyDeviceToHost, st), "dump");
+    ck(cudaMemcpyAsync(tri.data(), B.tri, size_t(nv) * 2 * sizeof(dev::TriRec),
+                       cudaMemcpyDeviceToHost, st),
+       "dump");
+  }
+  ck(cudaStreamSynchronize(st), "dump sync");
+  std::vector<uint64_t> aabb(nv);
+  std::vector<uint8_t> cls(nv), valid(size_t(nv) * 2);
+  std::vector<uint32_t> attr(size_t(nv) * 9), tmeta(size_t(nv) * 8);
+  std::vector<int32_t> yr(size_t(nv) * 4);
+  std::vector<double> fn(size_t(nv) * 30);
+  for (uint32_t i = 0; i < nv; ++i) {
+    uint32_t x0 = box[i].x & 0xffff, x1 = box[i].x >> 16, y0 = box[i].y & 0xffff, y1 = box[i].y >> 16;
+    uint32_t cf = (flags[i] >> 4) & 3u;
+    aabb[i] = fc.extended ? (uint64_t(x0) | (uint64_t(y0) << 16) | (uint64_t(x1) << 32) | (uint64_t(y1) << 48))
+                          : uint64_t(x0 | (y0 << 7) | (x1 << 14) | (y1 << 21) | (cf << 28));
+    cls[i] = uint8_t((flags[i] & 1u) | (flags[i] & 2u) | (flags[i] & 4u) | (cf << 4));
+    const uint32_t cc[4] = {col[i].x, col[i].y, col[i].z, col[i].w};
+    const uint32_t nn[4] = {nrm[i].x, nrm[i].y, nrm[i].z, nrm[i].w};
+    for (int k = 0; k < 4; ++k) attr[i * 9 + k] = cc[k], attr[i * 9 + 4 + k] = nn[k];
+    attr[i * 9 + 8] = mat[i];
+  }
+  for (size_t t = 0; t < size_t(nv) * 2; ++t) {
+    const dev::TriRec& r = tri[t];
+    bool v = meta[t].w & 0x100u;
+    valid[t] = v;
+    yr[t * 2] = v ? r.y_min : 0;
+    yr[t * 2 + 1] = v ? r.y_max : -1;
+    const dev::Fn3* fs[5] = {&r.e[0], &r.e[1], &r.e[2], &r.iw, &r.dz};
+    for (int k = 0; k < 5; ++k) {
+      fn[t * 15 + k * 3] = fs[k]->a;
+      fn[t * 15 + k * 3 + 1] = fs[k]->b;
+      fn[t * 15 + k * 3 + 2] = fs[k]->c;
+    }
+    tmeta[t * 4] = meta[t].x;
+    tmeta[t * 4 + 1] = meta[t].y;
+    tmeta[t * 4 + 2] = meta[t].z;
+    tmeta[t * 4 + 3] = meta[t].w & 0xffu;
+  }
+  fn.resize(size_t(nv) * 30);
+  yr.resize(size_t(nv) * 4);
+  tmeta.resize(size_t(nv) * 8);
+  dump_put_host(out, "quad_source", src);
+  dump_put_host(out, "quad_aabb", aabb);
+  dump_put_host(out, "quad_class", cls);
+  dump_put_host(out, "quad_attr", attr);
+  dump_put_host(out, "tri_valid", valid);
+  dump_put_host(out, "tri_yrange", yr);
+  dump_put_host(out, "tri_fn", fn);
+  dump_put_host(out, "tri_meta", tmeta);
+  dump_put_host(out, "setup_stats",
+                std::vector<uint64_t>{uint64_t(d->nquads), c.cull[0], c.cull[1], c.cull[2], c.cull[3], c.cull[4]});
+  dump_put_host(out, "bin_dims", std::vector<int32_t>{fc.bins_x, fc.bins_y});
+  const size_t nb = size_t(fc.nbins);
+  dump_put(out, "bin_quad_counts", B.qcnt, nb, st);
+  dump_put(out, "bin_tri_counts", B.tcnt, nb, st);
+  dump_put(out, "bin_offsets", B.off, nb, st);
+  dump_put(out, "bin_categories", B.cat, nb, st);
+  dump_put(out, "bin_items", B.items, size_t(c.pairs), st);
+  std::vector<uint8_t> prop(nb), cat(nb);
+  ck(cudaMemcpyAsync(prop.data(), B.prop, nb, cudaMemcpyDeviceToHost, st), "dump");
+  ck(cudaMemcpyAsync(cat.data(), B.cat, nb, cudaMemcpyDeviceToHost, st), "dump");
+  ck(cudaStreamSynchronize(st), "dump sync");
+  std::vector<uint8_t> path(nb);
+  bool force_high = fc.force_high;
+  for (size_t b = 0; b < nb; ++b) {
+    if (cat[b] == 0) path[b] = 0;
+    else if (cat[b] == 2 || force_high) path[b] = 2;
+    else path[b] = prop[b] ? 3 : 1;
+  }
+  dump_put_host(out, "bin_path", path);
+}
+
+}  // namespace
+
+static void enqueue_raster(DeviceScene* d, Prepared& P, int* launches) {
+  launch_raster(d, P.fc, P.B, dev::kPassLow, P.gcap_tbr, P.gcap_tb, launches);
+  cudaEventRecord(d->ev[3], d->stream);
+  launch_raster(d, P.fc, P.B, dev::kPassHigh, P.gcap_tbr, P.gcap_tb, launches);
+  dev::k_finalize<<<1, 1024, 0, d->stream>>>(P.fc, P.B);
+  ++*launches;
+  cudaEventRecord(d->ev[4], d->stream);
+}
+
+void render_frame(const Scene& s, const RenderOptions& opt, RenderOutput* out) {
+  validate_frame(s, opt);
+  DeviceScene* d = device_scene(s);
+  for (int attempt = 0; attempt < 3; ++attempt) {
+    Prepared P = prepare(d, s, opt);
+    int launches = enqueue_front(d, P);
+    enqueue_raster(d, P, &launches);
+    dev::Counters c;
+    ck(cudaMemcpyAsync(&c, P.B.ctr, sizeof c, cudaMemcpyDeviceToHost, d->stream), "counters");
+    ck(cudaStreamSynchronize(d->stream), "frame");
+    if (c.error & 2u) {  // bin item capacity: grow and re-run (first frames only)
+      d->items_cap = uint32_t(std::min<unsigned long long>(c.pairs + c.pairs / 4 + 1024, 0xffffffffull));
+      continue;
+    }
+    check_frame_errors(c, P.fc);
+    out->width = s.camera.width;
+    out->height = s.camera.height;
+    read_stats(d, c, s, &out->stats);
+    out->stats.kernel_launches = launches;
+    d->last = out->stats;
+    if (opt.dump) {
+      // second pass with THB offsets (deterministic: identical lists)
+      const size_t nb = size_t(P.fc.nbins);
+      std::vector<uint32_t> cnt(nb * 32);
+      ck(cudaMemcpy(cnt.data(), P.B.thb_cnt, nb * 32 * 4, cudaMemcpyDeviceToHost), "dump");
+      std::vector<uint8_t> cat(nb);
+      ck(cudaMemcpy(cat.data(), P.B.cat, nb, cudaMemcpyDeviceToHost), "dump");
+      std::vector<uint64_t> offs(nb * 32 + 1, 0);
+      for (size_t i = 0; i < nb * 32; ++i) offs[i + 1] = offs[i] + (cat[i / 32] ? cnt[i] : 0);
+      d->thb_off.ensure(offs.size() * 8);
+      d->thb_out.ensure(std::max<uint64_t>(1, offs.back()) * 8);
+      d->thb_tri.ensure(std::max<uint64_t>(1, offs.back()) * 4);
+      d->thb_pre.ensure(std::max<uint64_t>(1, offs.back()) * 4);
+      ck(cudaMemcpy(d->thb_off.p, offs.data(), offs.size() * 8, cudaMemcpyHostToDevice), "dump");
+      P.B.thb_off = d->thb_off.as<uint64_t>();
+      P.B.thb_out = d->thb_out.as<uint64_t>();
+      P.B.thb_tri = d->thb_tri.as<uint32_t>();
+      P.B.thb_pre = d->thb_pre.as<uint32_t>();
+      int l2 = enqueue_front(d, P);
+      (void)l2;
+      enqueue_raster(d, P, &l2);
+      dev::Counters c2;
+      ck(cudaMemcpyAsync(&c2, P.B.ctr, sizeof c2, cudaMemcpyDeviceToHost, d->stream), "counters");
+      ck(cudaStreamSynchronize(d->stream), "frame");
+      collect_dumps(d, P, c2, out);
+      dump_put_host(out, "thb_offsets", offs);
+      dump_put(out, "thb", P.B.thb_out, offs.back(), d->stream);
+      dump_put(out, "thb_tri", P.B.thb_tri, offs.back(), d->stream);
+      dump_put(out, "thb_prefix", P.B.thb_pre, offs.back(), d->stream);
+      const size_t npx = size_t(s.camera.width) * s.camera.height;
+      dump_put(out, "emit_hash", P.B.hash, npx, d->stream);
+      dump_put(out, "emit_count", P.B.emit, npx, d->stream);
+      ck(cudaStreamSynchronize(d->stream), "dump");
+    }
+    if (opt.host_readback) {
+      const size_t npx = size_t(s.camera.width) * s.camera.height;
+      out->rgba.resize(npx * 4);
+      out->mask.resize(npx);
+      ck(cudaMemcpyAsync(out->rgba.data(), P.B.fb, npx * 4, cudaMemcpyDeviceToHost, d->stream), "readback");
+      ck(cudaMemcpyAsync(out->mask.data(), P.B.mask, npx, cudaMemcpyDeviceToHost, d->stream), "readback");
+      ck(cudaStreamSynchronize(d->stream), "readback");
+    }
+    if (opt.dump) {
+      DumpArray img, msk;
+      img.count = out->rgba.size();
+      img.bytes = out->rgba;
+      msk.count = out->mask.size();
+      msk.bytes = out->mask;
+      out->dumps["image"] = std::move(img);
+      out->dumps["mask"] = std::move(msk);
+      const veil_frame_stats& t = out->stats;
+      dump_put_host(out, "counters",
+                    std::vector<uint64_t>{t.samples, t.fragments, t.tri_half_blocks, t.segments,
+                                          t.bins_empty, t.bins_low, t.bins_high, t.bins_propagated,
+                                          t.invalid_pixels});
+    }
+    return;
+  }
+  throw Error(VEIL_ERR_INTERNAL, "bin item buffer could not be sized");
+}
+
+void render_reference_frame(const Scene& s, const RenderOptions& opt, RenderOutput* out) {
+  validate_scene(s);
+  DeviceScene* d = device_scene(s);
+  Prepared P = prepare(d, s, opt);
+  for (int attempt = 0; attempt < 3; ++attempt) {
+    int launches = enqueue_front(d, P);
+    dim3 grid((s.camera.width + 15) / 16, (s.camera.height + 7) / 8);
+    dev::k_abuffer<<<grid, 128, 0, d->stream>>>(P.fc, P.B);
+    ++launches;
+    cudaEventRecord(d->ev[3], d->stream);
+    cudaEventRecord(d->ev[4], d->stream);
+    dev::Counters c;
+    ck(cudaMemcpyAsync(&c, P.B.ctr, sizeof c, cudaMemcpyDeviceToHost, d->stream), "counters");
+    ck(cudaStreamSynchronize(d->stream), "frame");
+    if (c.error & 2u) {
+      d->items_cap = uint32_t(std::min<unsigned long long>(c.pairs + c.pairs / 4 + 1024, 0xffffffffull));
+      P = prepare(d, s, opt);
+      continue;
+    }
+    check_frame_errors(c, P.fc);
+    out->width = s.camera.width;
+    out->height = s.camera.height;
+    out->reference = true;
+    read_stats(d, c, s, &out->stats);
+    out->stats.fragments = c.samples;
+    out->stats.tri_half_blocks = 0;
+    out->stats.segments = 0;
+    out->stats.bins_empty = out->stats.bins_low = out->stats.bins_high = 0;
+    out->stats.setup_ms = out->stats.binning_ms = out->stats.low_raster_ms = out->stats.hi_raster_ms = 0;
+    out->stats.kernel_launches = launches;
+    const size_t npx = size_t(s.camera.width) * s.camera.height;
+    out->rgba.resize(npx * 4);
+    out->mask.assign(npx, 0);
+    ck(cudaMemcpy(out->rgba.data(), P.B.fb, npx * 4, cudaMemcpyDeviceToHost), "readback");
+    if (opt.dump) {
+      dump_put(out, "emit_hash", P.B.hash, npx, d->stream);
+      dump_put(out, "emit_count", P.B.emit, npx, d->stream);
+      ck(cudaStreamSynchronize(d->stream), "dump");
+    }
+    return;
+  }
+  throw Error(VEIL_ERR_INTERNAL, "bin item buffer could not be sized");
+}
+
+void device_framebuffer(const Scene& s, void** rgba, void** mask) {
+  if (!s.device) throw Error(VEIL_ERR_INVALID_ARG, "scene has not been rendered on a device");
+  if (rgba) *rgba = s.device->fb.p;
+  if (mask) *mask = s.device->mask.p;
+}
+
+void* device_stream(const Scene& s) {
+  DeviceScene* d = device_scene(s);
+  return d->stream;
+}
+
+const veil_frame_stats& device_last_stats(const Scene& s) {
+  if (!s.device) throw Error(VEIL_ERR_INVALID_ARG, "scene has not been rendered on a device");
+  return s.device->last;
+}
+
+}  // namespace veil

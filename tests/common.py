@@ -1,0 +1,116 @@
+"""Shared test helpers: golden fixtures, scene builders, dump comparison."""
+import glob
+import json
+import os
+
+import numpy as np
+
+from paper_2405_13364_b200.abi import (
+    MATERIAL_DTYPE,
+    MATERIAL_VERTEX_COLORS,
+    MATERIAL_VERTEX_NORMALS,
+    QUAD_DTYPE,
+    SCENE_HAS_COLORS,
+    SCENE_HAS_NORMALS,
+    VERTEX_DTYPE,
+    SceneArrays,
+    default_params,
+)
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLDEN = os.path.join(HERE, "golden")
+REF_SCENES = "/root/reference/proj/scenes"
+
+# Every array both the reference dump and the restatement/libveil produce.
+PARITY_ARRAYS = [
+    "quad_source", "quad_aabb", "quad_class", "quad_attr", "tri_valid", "tri_yrange", "tri_fn",
+    "tri_meta", "setup_stats", "bin_dims", "bin_quad_counts", "bin_tri_counts", "bin_offsets",
+    "bin_categories", "bin_items", "bin_path", "thb_offsets", "thb", "thb_prefix", "emit_hash",
+    "emit_count", "image", "mask", "counters",
+]
+
+
+def golden_names():
+    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz")))
+
+
+def load_golden(name):
+    z = np.load(os.path.join(GOLDEN, name + ".npz"))
+    eye = z["scene_eye"]
+    scene = SceneArrays(z["scene_vertices"], z["scene_quads"], z["scene_materials"],
+                        int(z["scene_flags"][0]), z["scene_matrix"], int(z["scene_size"][0]),
+                        int(z["scene_size"][1]), eye if len(eye) else None)
+    p = json.loads(bytes(z["params"]).decode())
+    params = default_params(**p)
+    expect = {k: z[k] for k in PARITY_ARRAYS if k in z}
+    return scene, params, expect
+
+
+def compare(got, expect, names=None, label=""):
+    """Returns the list of arrays that differ (empty = bit-exact)."""
+    bad = []
+    for k in names or expect:
+        if k not in expect:
+            continue
+        if k not in got:
+            bad.append(f"{k}: missing")
+            continue
+        a, b = np.asarray(got[k]), np.asarray(expect[k])
+        if k == "quad_aabb":
+            a, b = a.astype(np.uint64), b.astype(np.uint64)
+        if a.shape != b.shape:
+            bad.append(f"{k}: shape {a.shape} != {b.shape}")
+        elif not np.array_equal(a, b):
+            idx = np.flatnonzero(a.reshape(-1) != b.reshape(-1))
+            bad.append(f"{k}: {len(idx)} differ, first at {idx[0]}: {a.reshape(-1)[idx[0]]} vs {b.reshape(-1)[idx[0]]}")
+    return bad
+
+
+def clip_scene(width, height, flags=SCENE_HAS_COLORS | SCENE_HAS_NORMALS):
+    """ClipSceneBuilder of the reference tests (test_util.hpp:51-90)."""
+
+    class B:
+        def __init__(self):
+            self.v = []
+            self.q = []
+            self.w, self.h = width, height
+
+        def vertex(self, x, y, z, color=(1, 1, 1, 1)):
+            self.v.append(((x, y, z), (0, 0, -1), tuple(color), (0, 0)))
+            return len(self.v) - 1
+
+        def ndc(self, px, py):
+            return 2.0 * px / self.w - 1.0, 1.0 - 2.0 * py / self.h
+
+        def pixel_rect(self, px0, py0, px1, py1, z, color=(1, 1, 1, 1)):
+            c = [self.ndc(px0, py0), self.ndc(px1, py0), self.ndc(px1, py1), self.ndc(px0, py1)]
+            ids = [self.vertex(x, y, z, color) for x, y in c]
+            self.q.append((ids, 0))
+
+        def pixel_triangle(self, p0, p1, p2, z, color=(1, 1, 1, 1)):
+            ids = [self.vertex(*self.ndc(*p), z, color) for p in (p0, p1, p2)]
+            self.q.append((ids + [ids[2]], 0))
+
+        def quad_ids(self, ids):
+            self.q.append((list(ids), 0))
+
+        def build(self):
+            v = np.zeros(len(self.v), dtype=VERTEX_DTYPE)
+            for i, (p, n, c, uv) in enumerate(self.v):
+                v[i] = (p, n, c, uv)
+            q = np.zeros(len(self.q), dtype=QUAD_DTYPE)
+            for i, (ids, m) in enumerate(self.q):
+                q[i] = (ids, m)
+            m = np.zeros(1, dtype=MATERIAL_DTYPE)
+            m[0] = ((1, 1, 1, 1), 1.0, -1, MATERIAL_VERTEX_COLORS | MATERIAL_VERTEX_NORMALS)
+            return SceneArrays(v, q, m, flags, np.eye(4).reshape(16), self.w, self.h)
+
+    return B()
+
+
+def boxes_arrays(width=256, height=256):
+    """The bundled boxes scene (reference proj/scenes/boxes.obj + camera), as
+    captured from the reference loader into the C1 golden fixture."""
+    scene, _, _ = load_golden("c1_boxes_256")
+    scene.width, scene.height = width, height
+    return scene

@@ -1,0 +1,240 @@
+"""libveil (sm_100a) vs the reference: bit-exact parity through the C ABI.
+
+Oracle: the committed reference fixtures (tests/golden, produced by the
+unmodified reference via oracle/make_golden.py) and the C restatement
+(oracle/liboracle.so) on the same seeded scenes. Bar: every setup record,
+bin list, tri-half-block list, per-pixel blend-order hash, image byte, mask
+byte and counter identical.
+"""
+import numpy as np
+import pytest
+
+import bindings
+from common import PARITY_ARRAYS, boxes_arrays, clip_scene, compare, golden_names, load_golden
+from paper_2405_13364_b200 import veil
+from paper_2405_13364_b200.abi import (
+    RENDER_ALPHA_THRESHOLD,
+    RENDER_BACKFACE_CULLING,
+    RENDER_FORCE_HIGH_PATH,
+    RENDER_REFERENCE,
+    RENDER_VISUALIZE_ERRORS,
+    VEIL_ERR_CAPACITY,
+    VEIL_ERR_INVALID_ARG,
+    default_params,
+)
+
+pytestmark = pytest.mark.gpu
+
+
+def gpu_dump(arrays, params):
+    return veil.render_dump(veil.Scene.from_arrays(arrays), params)
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_golden_fixture(name):
+    scene, params, expect = load_golden(name)
+    bad = compare(gpu_dump(scene, params), expect)
+    assert not bad, bad
+
+
+FLAG_SETS = [0, RENDER_ALPHA_THRESHOLD, RENDER_FORCE_HIGH_PATH,
+             RENDER_BACKFACE_CULLING | RENDER_VISUALIZE_ERRORS]
+
+
+@pytest.mark.parametrize("kind,size", [("layered_quads", (128, 128)),
+                                       ("intersecting_shells", (128, 96)),
+                                       ("random_soup", (160, 128)),
+                                       ("dense_bin", (256, 256))])
+@pytest.mark.parametrize("flags", FLAG_SETS)
+@pytest.mark.parametrize("df", [1, 3, 8])
+def test_synthetic_vs_restatement(kind, size, flags, df):
+    arr = veil.Scene.synthetic(kind, 11, *size).arrays()
+    p = default_params(flags=flags, depth_filter_size=df)
+    expect = bindings.oracle_render(arr, p)
+    bad = compare(gpu_dump(arr, p), expect, PARITY_ARRAYS)
+    assert not bad, bad
+
+
+@pytest.mark.parametrize("frame", [0, 9, 21, 40])
+@pytest.mark.parametrize("backface", [False, True])
+def test_boxes_orbit_vs_restatement(frame, backface):
+    """C3 camera path at 320x180: perspective, large quads."""
+    arr = boxes_arrays(320, 180)
+    R = np.hypot(5.5, 9.0)
+    th = np.arctan2(5.5, 9.0) + 2 * np.pi * frame / 64
+    eye = [R * np.sin(th), 4.5, R * np.cos(th)]
+    m = veil.look_at(eye, [0, 0, 0], [0, 1, 0], 55.0, 0.5, 40.0, 320, 180)
+    arr = arr.with_camera(m, eye)
+    p = default_params(flags=RENDER_BACKFACE_CULLING if backface else 0)
+    bad = compare(gpu_dump(arr, p), bindings.oracle_render(arr, p), PARITY_ARRAYS)
+    assert not bad, bad
+
+
+def test_camera_inside_scene_w_crossing():
+    """Eye inside the boxes: edges cross w = 0 (Blinn AABB extension)."""
+    arr = boxes_arrays(200, 150)
+    eye = [0.2, 0.1, 0.3]
+    m = veil.look_at(eye, [3, -1, -2], [0, 1, 0], 90.0, 0.05, 40.0, 200, 150)
+    for e in (eye, None):
+        a = arr.with_camera(m, e)
+        p = default_params(flags=RENDER_BACKFACE_CULLING)
+        bad = compare(gpu_dump(a, p), bindings.oracle_render(a, p), PARITY_ARRAYS)
+        assert not bad, bad
+
+
+def test_stack_workload_small_vs_restatement():
+    """The C2 generator at a reduced viewport (every stage exercised)."""
+    s = veil.Scene.workload("stack64k", 2, 320, 180)
+    arr = s.arrays()
+    keep = 3000
+    arr.quads = arr.quads[:keep].copy()
+    p = default_params()
+    bad = compare(gpu_dump(arr, p), bindings.oracle_render(arr, p), PARITY_ARRAYS)
+    assert not bad, bad
+
+
+def test_tiny_grid_extended_vs_restatement():
+    """C4-style jittered grid mesh with extended limits, reduced size."""
+    s = veil.Scene.workload("tiny4m", 4, 3840, 2160)
+    arr = s.arrays()
+    # keep the first 64 grid rows (2048 quads per row), at a 2600x300 viewport
+    arr.quads = arr.quads[: 2048 * 64].copy()
+    arr.width, arr.height = 2600, 300
+    p = default_params()
+    exp = bindings.oracle_render(arr, p, extended=True)
+    sc = veil.Scene.from_arrays(arr)
+    got = veil.render_dump(sc, p)
+    bad = compare(got, exp, PARITY_ARRAYS)
+    assert not bad, bad
+
+
+def test_reference_abuffer_mode_matches_restatement():
+    arr = veil.Scene.synthetic("random_soup", 4, 128, 128).arrays()
+    p = default_params(flags=RENDER_REFERENCE)
+    exp = bindings.oracle_render(arr, p)
+    got = gpu_dump(arr, p)
+    for k in ("image", "emit_hash", "emit_count"):
+        assert np.array_equal(got[k], exp[k]), k
+
+
+def test_pipeline_equals_abuffer_when_disorder_within_df():
+    """test_oracle.cpp:45-53 / acceptance criterion 1 analogue."""
+    sc = veil.Scene.synthetic("layered_quads", 3, 160, 120)
+    a = veil.render(sc, default_params()).pixels()
+    b = veil.render(sc, default_params(flags=RENDER_REFERENCE)).pixels()
+    assert np.array_equal(a, b)
+
+
+def test_capacity_error_names_the_bin():
+    """test_raster.cpp:279-295: 4100 stacked tiny triangles -> high limit."""
+    b = clip_scene(32, 32)
+    for i in range(4100):
+        z = 0.1 + 0.0001 * (i % 1000)
+        b.pixel_triangle((-2, -2), (10, -2), (-2, 6), z, (1, 1, 1, 0.2))
+    sc = veil.Scene.from_arrays(b.build())
+    with pytest.raises(veil.VeilError) as e:
+        veil.render(sc)
+    assert e.value.status == VEIL_ERR_CAPACITY
+    assert "bin (0,0)" in e.value.message
+    with pytest.raises(bindings.CheckerError) as e2:
+        bindings.oracle_render(b.build())
+    assert e2.value.message == e.value.message
+
+
+def test_invalid_limits_rejected():
+    sc = veil.Scene.synthetic("layered_quads", 6, 128, 128)
+    with pytest.raises(veil.VeilError) as e:
+        veil.render(sc, default_params(limit_low_tbr=1 << 20))
+    assert e.value.status == VEIL_ERR_INVALID_ARG
+
+
+def test_segment_arithmetic_300_layers():
+    """test_raster.cpp:158-177: 300 full-coverage layers on 64x64."""
+    b = clip_scene(64, 64)
+    for i in range(300):
+        b.pixel_triangle((-80, -80), (200, -10), (-10, 200), 0.1 + 0.6 * (i / 300.0),
+                         (1, 1, 1, 0.01))
+    r = veil.render(veil.Scene.from_arrays(b.build()))
+    rep = r.report()
+    assert rep["segments"] == 4 * 32 * 38
+    assert rep["samples"] == 300 * 64 * 64
+    assert rep["fragments"] == rep["samples"]
+    assert rep["tri_half_blocks"] == 4 * 32 * 300
+    assert rep["bins"]["low"] == 4 and rep["bins"]["propagated"] == 4
+
+
+def test_alpha_threshold_opaque_front():
+    """test_raster.cpp:197-214: exactly one blended sample per pixel."""
+    b = clip_scene(64, 64)
+    for i in range(6):
+        b.pixel_triangle((-200, -200), (400, -20), (-20, 400), 0.2 + 0.1 * i,
+                         (0.8, 0.6, 0.4, 1.0 if i == 0 else 0.5))
+    sc = veil.Scene.from_arrays(b.build())
+    base = veil.render(sc)
+    fast = veil.render(sc, default_params(flags=RENDER_ALPHA_THRESHOLD))
+    assert base.report()["samples"] == 6 * 64 * 64
+    assert fast.report()["samples"] == 64 * 64
+    assert np.array_equal(base.pixels(), fast.pixels())
+
+
+def test_low_path_1023_vs_1025():
+    """test_raster.cpp:216-239: 1023 triangle-equivalents stay low."""
+    b = clip_scene(192, 64)
+    for i in range(511):
+        x0, y0 = 1 + (i % 5) * 6, 1 + ((i // 5) % 5) * 6
+        b.pixel_rect(x0, y0, x0 + 5, y0 + 5, 0.1 + 0.001 * i, (1, 1, 1, 0.1))
+    b.pixel_triangle((-5, 24), (200, 24), (-5, 30), 0.05)
+    rep = veil.render(veil.Scene.from_arrays(b.build())).report()
+    assert rep["bins"]["high"] == 0 and rep["bins"]["propagated"] == 0 and rep["bins"]["low"] == 6
+    b.pixel_rect(5, 5, 11, 11, 0.5, (1, 1, 1, 0.1))
+    assert veil.render(veil.Scene.from_arrays(b.build())).report()["bins"]["high"] == 1
+
+
+def test_deterministic_across_runs():
+    arr = veil.Scene.workload("stack64k", 2, 640, 360).arrays()
+    arr.quads = arr.quads[:8000].copy()
+    sc = veil.Scene.from_arrays(arr)
+    a = veil.render_dump(sc)
+    b = veil.render_dump(sc)
+    assert not compare(a, b, PARITY_ARRAYS)
+
+
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
+def test_sharded_render_reassembles_full_frame(world):
+    """Bin-interleaved shards (8(e)) combine to the single-GPU frame."""
+    sc = veil.Scene.synthetic("random_soup", 8, 256, 192)
+    full = veil.render(sc)
+    img = np.zeros_like(full.pixels())
+    mask = np.zeros_like(full.invalid_mask())
+    total_samples = 0
+    bx, by = (256 + 31) // 32, (192 + 31) // 32
+    for r in range(world):
+        part = veil.render(sc, shard=(r, world))
+        px, m = part.pixels(), part.invalid_mask()
+        for y in range(by):
+            for x in range(bx):
+                if (x + 3 * y) % world == r:
+                    img[y * 32:(y + 1) * 32, x * 32:(x + 1) * 32] = px[y * 32:(y + 1) * 32, x * 32:(x + 1) * 32]
+                    mask[y * 32:(y + 1) * 32, x * 32:(x + 1) * 32] = m[y * 32:(y + 1) * 32, x * 32:(x + 1) * 32]
+        total_samples += part.report()["samples"]
+    assert np.array_equal(img, full.pixels())
+    assert np.array_equal(mask, full.invalid_mask())
+    assert total_samples == full.report()["samples"]
+
+
+def test_report_schema():
+    rep = veil.render(veil.Scene.synthetic("layered_quads", 1, 64, 64)).report()
+    for key in ("config", "timings_us", "samples", "tri_half_blocks", "s_per_thb", "fragments",
+                "segments", "setup_stats", "bins", "invalid_pixels"):
+        assert key in rep
+    for key in ("setup", "binning", "low_raster", "hi_raster", "total"):
+        assert key in rep["timings_us"]
+
+
+def test_png_roundtrip(tmp_path):
+    r = veil.render(veil.Scene.synthetic("intersecting_shells", 2, 96, 64))
+    a, b = str(tmp_path / "a.png"), str(tmp_path / "b.png")
+    r.write_png(a)
+    r.write_png(b)
+    d = veil.compare_png(a, b)
+    assert d.differing_pixels == 0 and d.width == 96 and d.height == 64
