@@ -1,0 +1,469 @@
+"""bench.py -- LucidRaster frame benchmark on B200 (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload stack64k|boxes1080|tiny4m|mixed16m]
+
+A "step" is one frame of the workload through the full sort-middle pipeline
+(setup -> binning -> low/high bin rasterization -> framebuffer). The default
+workload is BASELINE.json configs[1] ("stack64k": 65,536 overlapping
+translucent quads at 1920x1080, depth complexity ~32). N > 1 (torchrun, one
+rank per GPU over NCCL) splits the frame's bins across ranks
+(owner = (bx + 3*by) mod N, setup replicated) and gathers the finished 32x32
+tiles to rank 0 over NVLink with NCCL; the frame time is the max over ranks.
+
+value      = fragments per second of whole frames, all ranks (Gfragments/s)
+ms_per_step = ms per frame (device time, CUDA events on the renderer's stream)
+e2e        = the same metric through the reference-facing C ABI
+             (veil_scene_set_camera + veil_render_scene + pixel readback into
+             host memory) -- the headline number against the reference arm
+roofline   = the dominant kernel (bin rasterizer) vs measured HBM bandwidth
+cpu_baseline = the unmodified reference (oracle/_ref) on this host's cores
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ms/frame & Gfragments/s at 1920x1080 vs HBM roofline; at 1/2/4/8 B200"
+L2_BYTES = 126 * 1024 * 1024
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="stack64k",
+                    choices=["stack64k", "boxes1080", "tiny4m", "mixed16m"])
+    ap.add_argument("--cpu-seconds", type=float, default=12.0,
+                    help="bound on the CPU-baseline sample (rank 0, N=1)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ----------------------------------------------------------------- workloads
+
+def boxes_orbit_camera(frame, w, h):
+    import numpy as np
+    from paper_2405_13364_b200 import veil
+
+    R = float(np.hypot(5.5, 9.0))
+    th = float(np.arctan2(5.5, 9.0)) + 2.0 * np.pi * frame / 64.0
+    eye = [R * np.sin(th), 4.5, R * np.cos(th)]
+    return veil.look_at(eye, [0, 0, 0], [0, 1, 0], 55.0, 0.5, 40.0, w, h), eye
+
+
+def make_scene(workload):
+    """Returns (veil.Scene, description dict, camera_fn or None)."""
+    from paper_2405_13364_b200 import veil
+
+    if workload == "stack64k":
+        s = veil.Scene.workload("stack64k", 2)
+        return s, {"workload": "stack64k", "quads": 65536, "width": 1920, "height": 1080,
+                   "seed": 2, "depth_complexity": "~32"}, None
+    if workload == "tiny4m":
+        s = veil.Scene.workload("tiny4m", 4)
+        return s, {"workload": "tiny4m", "quads": 4194304, "width": 3840, "height": 2160,
+                   "seed": 4}, None
+    if workload == "mixed16m":
+        s = veil.Scene.workload("mixed16m", 5)
+        return s, {"workload": "mixed16m", "quads": 16777216, "width": 7680, "height": 4320,
+                   "seed": 5}, None
+    # boxes1080: the bundled boxes scene (captured from the reference loader
+    # into tests/golden/c1_boxes_256.npz) on the 64-frame orbit at 1080p
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from common import boxes_arrays
+
+    arr = boxes_arrays(1920, 1080)
+    s = veil.Scene.from_arrays(arr)
+    return s, {"workload": "boxes1080", "quads": len(arr.quads), "width": 1920, "height": 1080,
+               "camera_path": "64-frame orbit"}, (lambda i: boxes_orbit_camera(i % 64, 1920, 1080))
+
+
+def bytes_model(stats, width, height, a_q=32, a_v=8):
+    """SURVEY.md 8(d) algorithmic bytes (per frame, and the raster kernel's)."""
+    Q, V = stats["input_quads"], stats["vertices"]
+    Qv, Tv = stats["visible_quads"], 2 * stats["visible_quads"]
+    Qs, Tl = stats["small_quads"], stats["large_tris"]
+    P = stats["bin_pairs"]
+    # split pairs into small-quad pairs and large-triangle pairs
+    Ps, Pl = stats["pairs_small"], stats["pairs_large"]
+    frame = (20 * Q + 12 * V + a_v * V + (4 + a_q) * Qv + 84 * Tv + 8 * Qs + 64 * Tl + 8 * P
+             + (168 + a_q) * Ps + (84 + a_q) * Pl + 4 * width * height)
+    raster = (168 + a_q) * Ps + (84 + a_q) * Pl + 4 * P + 5 * width * height
+    b_min = 20 * Q + 12 * V + a_v * V + 8 * P + 4 * width * height
+    return frame, raster, b_min
+
+
+# ------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for i, n in enumerate(names):
+                if len(r) > 5 + i and r[5 + i].lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------- CPU baseline
+
+def cpu_reference_run(arrays, frames_max, seconds, threads, camera_fn=None):
+    """The unmodified reference (oracle/_ref) through its own C API."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import bindings  # test/baseline infrastructure only
+    from paper_2405_13364_b200.abi import default_params
+
+    if not bindings.ref_available():
+        return None
+    fits = arrays.width <= 2560 and arrays.height <= 2048
+    if not fits:
+        return None
+    rs = bindings.RefScene.from_arrays(arrays)
+    p = default_params(thread_count=threads)
+    times, frags = [], []
+    t_end = time.perf_counter() + seconds
+    i = 0
+    while i < frames_max and (i == 0 or time.perf_counter() < t_end):
+        if camera_fn:
+            m, eye = camera_fn(i)
+            rs.set_camera(m, eye)
+        t0 = time.perf_counter()
+        _, _, rep = rs.render(p)
+        times.append(time.perf_counter() - t0)
+        frags.append(rep["fragments"])
+        i += 1
+    return {"frames": len(times), "seconds": sum(times), "fragments": sum(frags),
+            "gfrag_s": sum(frags) / sum(times) / 1e9, "ms_per_frame": 1e3 * sum(times) / len(times)}
+
+
+# ------------------------------------------------------------------ our arm
+
+def device_bytes(ptr, n):
+    """A torch uint8 view of n bytes of libveil device memory."""
+    import torch
+
+    class _View:
+        __cuda_array_interface__ = {"shape": (n,), "typestr": "|u1", "data": (ptr, False),
+                                    "version": 3, "strides": None}
+
+    return torch.as_tensor(_View(), device="cuda")
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2405_13364_b200 import veil
+    from paper_2405_13364_b200.abi import default_params
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    torch.cuda.set_device(local)
+    veil.set_device(local)
+
+    scene, cfg, camera_fn = make_scene(args.workload)
+    arrays = scene.arrays() if rank == 0 else None
+    W, H = cfg["width"], cfg["height"]
+    params = default_params()
+    shard = (rank, world)
+    stream = torch.cuda.ExternalStream(scene.stream())
+    flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device="cuda")
+    bx, by = (W + 31) // 32, (H + 31) // 32
+    counts = [veil.shard_tile_count(bx, by, r, world) for r in range(world)]
+    max_tiles = max(counts)
+    tiles = torch.empty(max_tiles * 5120, dtype=torch.uint8, device="cuda")
+    gathered = [torch.empty_like(tiles) for _ in range(world)] if (world > 1 and rank == 0) else None
+
+    def frame(i, timed_events=None):
+        if camera_fn:
+            m, eye = camera_fn(i)
+            scene.set_camera(m, eye)
+        if timed_events:
+            timed_events[0].record(stream)
+        st = veil.render_device(scene, params, shard)
+        if world > 1:
+            veil.pack_tiles_device(scene, rank, world, tiles.data_ptr(), tiles.numel())
+            with torch.cuda.stream(stream):
+                if rank == 0:
+                    dist.gather(tiles, gathered, dst=0)
+                    for r in range(1, world):
+                        veil.unpack_tiles_device(scene, r, world, gathered[r].data_ptr(),
+                                                 gathered[r].numel())
+                else:
+                    dist.gather(tiles, None, dst=0)
+        if timed_events:
+            timed_events[1].record(stream)
+        return st
+
+    for i in range(args.warmup):
+        frame(i)
+    torch.cuda.synchronize()
+
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    stats = []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        for i in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()  # L2 flush between timed frames (outside the events)
+            stats.append(frame(args.warmup + i, evs[i]))
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ms = [a.elapsed_time(b) for a, b in evs]
+    ms_sum = torch.tensor([sum(ms)], dtype=torch.float64, device="cuda")
+    frag_local = torch.tensor([sum(int(s.fragments) for s in stats)], dtype=torch.float64,
+                              device="cuda")
+    if world > 1:
+        dist.all_reduce(ms_sum, op=dist.ReduceOp.MAX)
+        dist.all_reduce(frag_local, op=dist.ReduceOp.SUM)
+    ms_per_frame = float(ms_sum.item()) / args.steps
+    fragments_per_frame = float(frag_local.item()) / args.steps
+    value = fragments_per_frame / (ms_per_frame * 1e-3) / 1e9
+
+    # --- e2e through the C ABI with host buffers (rank 0 owns the output)
+    e2e = None
+    if not args.no_e2e:
+        if world == 1:
+            e2e_ms = []
+            for i in range(max(3, args.steps // 2)):
+                if camera_fn:
+                    m, eye = camera_fn(i)
+                t0 = time.perf_counter()
+                if camera_fn:
+                    scene.set_camera(m, eye)
+                r = veil.render(scene, params)
+                px = r.pixels()
+                mk = r.invalid_mask()
+                e2e_ms.append((time.perf_counter() - t0) * 1e3)
+                del r
+            e2e_ms = statistics.median(e2e_ms)
+            e2e = {"value": fragments_per_frame / (e2e_ms * 1e-3) / 1e9, "unit": "Gfragments/s",
+                   "ms_per_step": e2e_ms, "h2d_bytes_per_step": 128 + 64,
+                   "d2h_bytes_per_step": int(px.nbytes + mk.nbytes),
+                   "path": "veil_scene_set_camera + veil_render_scene + veil_render_pixels/"
+                           "veil_render_invalid_mask (host RGBA8 + mask)"}
+        else:
+            host = torch.empty(W * H * 5, dtype=torch.uint8, pin_memory=True) if rank == 0 else None
+            e2e_ms = []
+            for i in range(max(3, args.steps // 2)):
+                torch.cuda.synchronize()
+                dist.barrier()
+                t0 = time.perf_counter()
+                frame(i)
+                if rank == 0:  # D2H of the assembled framebuffer + mask
+                    rgba, msk = scene.device_framebuffer()
+                    host[: W * H * 4].copy_(device_bytes(rgba, W * H * 4))
+                    host[W * H * 4:].copy_(device_bytes(msk, W * H))
+                torch.cuda.synchronize()
+                dt = torch.tensor([(time.perf_counter() - t0) * 1e3], dtype=torch.float64,
+                                  device="cuda")
+                dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+                e2e_ms.append(float(dt.item()))
+            e2e_ms = statistics.median(e2e_ms)
+            e2e = {"value": fragments_per_frame / (e2e_ms * 1e-3) / 1e9, "unit": "Gfragments/s",
+                   "ms_per_step": e2e_ms, "h2d_bytes_per_step": 128 + 64,
+                   "d2h_bytes_per_step": W * H * 5,
+                   "path": "sharded device frame + NCCL tile gather + rank-0 readback"}
+
+    s0 = stats[-1]
+    info = {
+        "input_quads": int(s0.input_quads), "visible_quads": int(s0.visible_quads),
+        "vertices": int(len(arrays.vertices)) if arrays is not None else 0,
+        "small_quads": int(s0.small_quads), "large_tris": int(s0.large_tris),
+        "bin_pairs": int(s0.bin_pairs),
+    }
+    result = None
+    if rank == 0:
+        # pairs split: small-quad pairs vs large-triangle pairs from the bin counts
+        info["pairs_large"] = int(s0.bin_pairs) - 0
+        info["pairs_small"] = 0
+        try:
+            d = veil.render_dump(scene, params, names={"bin_quad_counts", "bin_tri_counts"})
+            info["pairs_small"] = int(d["bin_quad_counts"].sum())
+            info["pairs_large"] = int(d["bin_tri_counts"].sum())
+        except Exception:
+            pass
+        b_frame, b_raster, b_min = bytes_model(info, W, H)
+        peak, peak_kind = peaks()
+        raster_ms = statistics.median([float(s.low_raster_ms + s.hi_raster_ms) for s in stats])
+        achieved = b_raster / (raster_ms * 1e-3) / 1e9
+        launches = sum(int(s.kernel_launches) for s in stats)
+        if world > 1:
+            launches += 2 * args.steps
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cores = os.cpu_count() or 1
+            ref = cpu_reference_run(arrays, 1000, args.cpu_seconds, cores, camera_fn)
+            if ref:
+                cpu = {"value": ref["gfrag_s"], "unit": "Gfragments/s", "cores": cores,
+                       "kind": "reference",
+                       "sample": f"{ref['frames']} full frame(s) of {cfg['workload']} via the "
+                                 f"reference's veil_render_scene (oracle/_ref), "
+                                 f"{ref['ms_per_frame']:.1f} ms/frame"}
+        clk = clocks.summary()
+        result = {
+            "metric": METRIC,
+            "value": value,
+            "unit": "Gfragments/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_per_frame,
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "f64+f32",
+            "data": "synthetic",
+            "config": dict(cfg, parallelism=f"bins interleaved over {world} GPU(s), setup replicated",
+                           fragments_per_frame=int(fragments_per_frame),
+                           l2="flushed between timed frames (256 MiB write, outside the events)"),
+            "e2e": e2e,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "kernel": "k_raster (bin rasterizer, low+high passes)",
+                         "algorithmic_bytes_per_launch": b_raster,
+                         "peak_source": peak_kind,
+                         "frame_bytes": b_frame, "frame_bytes_min": b_min,
+                         "frame_frac": b_frame / (ms_per_frame * 1e-3) / 1e9 / peak},
+            "cpu_baseline": cpu,
+            "clocks": clk,
+            "gpu_launches": launches,
+            "stages_ms": {"setup": float(s0.setup_ms), "binning": float(s0.binning_ms),
+                          "low_raster": float(s0.low_raster_ms), "hi_raster": float(s0.hi_raster_ms),
+                          "total": float(s0.total_ms)},
+        }
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return result
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    from paper_2405_13364_b200 import veil
+
+    scene, cfg, camera_fn = make_scene(args.workload)
+    arrays = scene.arrays()
+    cores = os.cpu_count() or 1
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import bindings
+
+    fits = arrays.width <= 2560 and arrays.height <= 2048
+    if not bindings.ref_available() or not fits:
+        why = ("oracle/_ref missing" if not bindings.ref_available()
+               else "viewport exceeds the reference's 2560x2048 limit")
+        return {"impl": "reference", "unavailable": why, "metric": METRIC}
+    from paper_2405_13364_b200.abi import default_params
+
+    rs = bindings.RefScene.from_arrays(arrays)
+    p = default_params(thread_count=cores)
+    for i in range(args.warmup):
+        if camera_fn:
+            rs.set_camera(*camera_fn(i))
+        rs.render(p)
+    times, frags = [], 0
+    for i in range(args.steps):
+        if camera_fn:
+            rs.set_camera(*camera_fn(args.warmup + i))
+        t0 = time.perf_counter()
+        _, _, rep = rs.render(p)
+        times.append(time.perf_counter() - t0)
+        frags += rep["fragments"]
+    ms = 1e3 * sum(times) / len(times)
+    value = frags / sum(times) / 1e9
+    return {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "Gfragments/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64+f32",
+        "data": "synthetic", "config": dict(cfg, parallelism=f"{cores} host threads"),
+        "cpu_baseline": {"value": value, "unit": "Gfragments/s", "cores": cores,
+                         "kind": "reference",
+                         "sample": f"{args.steps} full frame(s) of {cfg['workload']} through the "
+                                   f"reference's veil_render_scene (oracle/_ref)"},
+        "e2e": {"value": value, "unit": "Gfragments/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    args = parse()
+    res = run_reference(args) if args.impl == "reference" else run_ours(args)
+    if res is not None:
+        print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -121,6 +121,14 @@ veil_status veil_shard_pack_tiles(const veil_render* render, const veil_shard* s
 veil_status veil_shard_unpack_tiles(veil_render* render, const veil_shard* shard,
                                     const uint8_t* tiles, uint64_t bytes);
 
+/* Device-memory variants on the scene's last device frame (the NCCL gather
+ * path): pack this rank's owned tiles into dev_tiles / write tiles received
+ * for `shard` into the scene's device framebuffer. Synchronous. */
+veil_status veil_shard_pack_tiles_device(const veil_scene* scene, const veil_shard* shard,
+                                         void* dev_tiles, uint64_t bytes);
+veil_status veil_shard_unpack_tiles_device(const veil_scene* scene, const veil_shard* shard,
+                                           const void* dev_tiles, uint64_t bytes);
+
 /* ---- device-resident frame loop ------------------------------------------- */
 
 /* Renders into device memory only (no host copies); for benchmarks that time

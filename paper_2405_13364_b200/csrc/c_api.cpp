@@ -374,6 +374,23 @@ veil_status veil_render_device(const veil_scene* scene, const veil_render_params
   });
 }
 
+veil_status veil_shard_pack_tiles_device(const veil_scene* scene, const veil_shard* shard,
+                                         void* dev_tiles, uint64_t bytes) {
+  if (!scene || !shard || !dev_tiles) return bad_arg("scene, shard and dev_tiles are required");
+  return guard([&] {
+    veil::shard_tiles_device(scene->s, shard->rank, shard->world_size, dev_tiles, bytes, false);
+  });
+}
+
+veil_status veil_shard_unpack_tiles_device(const veil_scene* scene, const veil_shard* shard,
+                                           const void* dev_tiles, uint64_t bytes) {
+  if (!scene || !shard || !dev_tiles) return bad_arg("scene, shard and dev_tiles are required");
+  return guard([&] {
+    veil::shard_tiles_device(scene->s, shard->rank, shard->world_size,
+                             const_cast<void*>(dev_tiles), bytes, true);
+  });
+}
+
 veil_status veil_device_framebuffer(const veil_scene* scene, void** rgba, void** mask) {
   if (!scene) return bad_arg("scene is required");
   return guard([&] { veil::device_framebuffer(scene->s, rgba, mask); });

@@ -1321,6 +1321,33 @@ __global__ void __launch_bounds__(128) k_abuffer(FrameConst fc, Buffers B) {
   atomicAdd(&B.ctr->samples, (unsigned long long)n);
 }
 
+// Owned 32x32 tiles <-> dense tile buffer (RGBA8 4096 B, then mask 1024 B per
+// tile), tile i of a rank = its i-th owned bin in row-major bin order. One
+// CTA per tile; 16-byte loads/stores along tile rows.
+__global__ void __launch_bounds__(256) k_tile_copy(FrameConst fc, uint32_t* fb, uint8_t* mask,
+                                                   uint8_t* tiles, const uint32_t* bins,
+                                                   uint32_t ntiles, int unpack) {
+  for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int bin = (int)bins[t];
+    const int bx = bin % fc.bins_x, by = bin / fc.bins_x;
+    uint8_t* tile = tiles + (size_t)t * 5120;
+    for (int i = threadIdx.x; i < 32 * 32; i += blockDim.x) {
+      const int lx = i & 31, ly = i >> 5;
+      const int px = bx * kBin + lx, py = by * kBin + ly;
+      if (px >= fc.width || py >= fc.height) continue;
+      const size_t pix = (size_t)py * fc.width + px;
+      uint32_t* tw = reinterpret_cast<uint32_t*>(tile) + i;
+      if (unpack) {
+        fb[pix] = *tw;
+        mask[pix] = tile[4096 + i];
+      } else {
+        *tw = fb[pix];
+        tile[4096 + i] = mask[pix];
+      }
+    }
+  }
+}
+
 }  // namespace dev
 
 // ============================================================ host side
@@ -1365,7 +1392,7 @@ struct DeviceScene {
   DevBuf pos, vcol, vnrm, quads, qmat, mats;
   DevBuf block_cnt, block_off, vq_src, vq_box, vq_flags, vq_mat, vq_col, vq_nrm, tri, tri_meta;
   DevBuf qcnt, tcnt, off, qcur, tcur, cat, prop, items, slots, spill0, spill1, scratch, fb, mask,
-      hash, emit, thb_cnt, thb_off, thb_out, thb_tri, thb_pre, ctr;
+      hash, emit, thb_cnt, thb_off, thb_out, thb_tri, thb_pre, ctr, tile_ids;
   uint32_t items_cap = 0;
   cudaEvent_t ev[6] = {};
   veil_frame_stats last{};
@@ -2055,10 +2082,42 @@ void render_reference_frame(const Scene& s, const RenderOptions& opt, RenderOutp
       dump_put(out, "emit_hash", P.B.hash, npx, d->stream);
       dump_put(out, "emit_count", P.B.emit, npx, d->stream);
       ck(cudaStreamSynchronize(d->stream), "dump");
+      dump_put_host(out, "image", out->rgba);
+      dump_put_host(out, "mask", out->mask);
     }
     return;
   }
   throw Error(VEIL_ERR_INTERNAL, "bin item buffer could not be sized");
+}
+
+void shard_tiles_device(const Scene& s, int rank, int world, void* tiles, uint64_t bytes,
+                        bool unpack) {
+  DeviceScene* d = s.device;
+  if (!d || d->fb_w != s.camera.width || d->fb_h != s.camera.height)
+    throw Error(VEIL_ERR_INVALID_ARG, "scene has no device frame of its current viewport");
+  ck(cudaSetDevice(d->device), "cudaSetDevice");
+  const int bx = (s.camera.width + kBinSize - 1) / kBinSize, by = (s.camera.height + kBinSize - 1) / kBinSize;
+  std::vector<uint32_t> bins;
+  for (int y = 0; y < by; ++y)
+    for (int x = 0; x < bx; ++x)
+      if (bin_owned(x, y, rank, world)) bins.push_back(uint32_t(y * bx + x));
+  if (bytes < bins.size() * 5120ull) throw Error(VEIL_ERR_INVALID_ARG, "tile buffer too small");
+  if (bins.empty()) return;
+  DevBuf& ids = d->tile_ids;
+  ids.ensure(bins.size() * 4);
+  ck(cudaMemcpyAsync(ids.p, bins.data(), bins.size() * 4, cudaMemcpyHostToDevice, d->stream), "tiles");
+  dev::FrameConst fc;
+  std::memset(&fc, 0, sizeof fc);
+  fc.width = s.camera.width;
+  fc.height = s.camera.height;
+  fc.bins_x = bx;
+  fc.bins_y = by;
+  int grid = std::min<int>(int(bins.size()), d->sm_count * 8);
+  dev::k_tile_copy<<<grid, 256, 0, d->stream>>>(fc, d->fb.as<uint32_t>(), d->mask.as<uint8_t>(),
+                                                 reinterpret_cast<uint8_t*>(tiles), ids.as<uint32_t>(),
+                                                 uint32_t(bins.size()), unpack ? 1 : 0);
+  ck(cudaGetLastError(), "k_tile_copy");
+  ck(cudaStreamSynchronize(d->stream), "tiles");
 }
 
 void device_framebuffer(const Scene& s, void** rgba, void** mask) {

@@ -85,6 +85,8 @@ def lib():
         "veil_shard_tile_count": ([C.c_int, C.c_int, C.POINTER(Shard)], C.c_uint64),
         "veil_shard_pack_tiles": ([_P, C.POINTER(Shard), _P, C.c_uint64], C.c_int),
         "veil_shard_unpack_tiles": ([_P, C.POINTER(Shard), _P, C.c_uint64], C.c_int),
+        "veil_shard_pack_tiles_device": ([_P, C.POINTER(Shard), _P, C.c_uint64], C.c_int),
+        "veil_shard_unpack_tiles_device": ([_P, C.POINTER(Shard), _P, C.c_uint64], C.c_int),
         "veil_render_device": ([_P, C.POINTER(RenderParams), C.POINTER(Shard)], C.c_int),
         "veil_device_framebuffer": ([_P, _PP, _PP], C.c_int),
         "veil_scene_stream": ([_P], C.c_void_p),
@@ -288,6 +290,16 @@ def render_device(scene: Scene, params=None, shard=None):
     sh = None if shard is None else C.byref(Shard(*shard))
     _check(lib().veil_render_device(scene.h, C.byref(params), sh))
     return scene.last_stats()
+
+
+def pack_tiles_device(scene: Scene, rank, world, dev_ptr, nbytes):
+    sh = Shard(rank, world)
+    _check(lib().veil_shard_pack_tiles_device(scene.h, C.byref(sh), C.c_void_p(dev_ptr), nbytes))
+
+
+def unpack_tiles_device(scene: Scene, rank, world, dev_ptr, nbytes):
+    sh = Shard(rank, world)
+    _check(lib().veil_shard_unpack_tiles_device(scene.h, C.byref(sh), C.c_void_p(dev_ptr), nbytes))
 
 
 def compare_png(a, b):
