@@ -710,12 +710,26 @@ __device__ __forceinline__ float4 blend(float4 acc, float4 s) {
                      __fadd_rn(acc.z, __fmul_rn(t, s.z)), __fadd_rn(acc.w, __fmul_rn(t, s.w)));
 }
 
+// Exact unpack tables: g_lut_c[q] = float(q) / 255.0f (unpack_color,
+// packing.hpp:63-66) and g_lut_n[q + 512] = float(q) / 511.0f
+// (decode_normal, packing.hpp:43-49), filled by the host with IEEE division.
+__device__ float g_lut_c[256];
+__device__ float g_lut_n[1024];
+
+__device__ __forceinline__ float lut_c(uint32_t w, int shift) {
+  return __ldg(&g_lut_c[(w >> shift) & 0xffu]);
+}
+__device__ __forceinline__ float lut_n(uint32_t w, int shift) {
+  int32_t q = (int32_t)(((w >> shift) & 0x3ffu) << 22) >> 22;
+  return __ldg(&g_lut_n[q + 512]);
+}
+
 // make_sample_context (shading.cpp:24-77) + shade_sample (123-139), no
 // textures. Returns the premultiplied colour and the sample depth.
 __device__ __forceinline__ float4 shade_sample(const FrameConst& fc, const Buffers& B,
                                                uint32_t tri, int px, int py, double* depth) {
   const TriRec& t = B.tri[tri];
-  const uint4 meta = B.tri_meta[tri];
+  const uint4 meta = __ldg(&B.tri_meta[tri]);
   const double x = (double)px + 0.5, y = (double)py + 0.5;
   const double e0 = eval(t.e[0], x, y), e1 = eval(t.e[1], x, y), e2 = eval(t.e[2], x, y);
   const double sum = __dadd_rn(__dadd_rn(e0, e1), e2);
@@ -724,31 +738,30 @@ __device__ __forceinline__ float4 shade_sample(const FrameConst& fc, const Buffe
               b2 = (float)__dmul_rn(e2, inv);
   *depth = eval(t.dz, x, y);
   const uint32_t q = tri >> 1;
-  const uint32_t qf = B.vq_flags[q];
+  const uint32_t qf = __ldg(&B.vq_flags[q]);
   const int ltri = (int)(meta.w & 0xffu);
   float4 color = make_float4(1.0f, 1.0f, 1.0f, 1.0f);
   if (qf & 2u) {
-    const uint4 c = B.vq_col[q];
+    const uint4 c = __ldg(&B.vq_col[q]);
     const uint32_t w0 = c.x, w1 = ltri == 0 ? c.y : c.z, w2 = ltri == 0 ? c.z : c.w;
     float r[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k)
-      r[k] = __fadd_rn(__fadd_rn(__fmul_rn(unpack_c(w0, 8 * k), b0), __fmul_rn(unpack_c(w1, 8 * k), b1)),
-                       __fmul_rn(unpack_c(w2, 8 * k), b2));
+      r[k] = __fadd_rn(__fadd_rn(__fmul_rn(lut_c(w0, 8 * k), b0), __fmul_rn(lut_c(w1, 8 * k), b1)),
+                       __fmul_rn(lut_c(w2, 8 * k), b2));
     color = make_float4(r[0], r[1], r[2], r[3]);
   }
   float n[3];
   if (qf & 4u) {
-    const uint4 c = B.vq_nrm[q];
+    const uint4 c = __ldg(&B.vq_nrm[q]);
     const uint32_t w0 = c.x, w1 = ltri == 0 ? c.y : c.z, w2 = ltri == 0 ? c.z : c.w;
 #pragma unroll
     for (int k = 0; k < 3; ++k)
-      n[k] = __fadd_rn(__fadd_rn(__fmul_rn(dec_normal_c((w0 >> (10 * k)) & 0x3ffu), b0),
-                                 __fmul_rn(dec_normal_c((w1 >> (10 * k)) & 0x3ffu), b1)),
-                       __fmul_rn(dec_normal_c((w2 >> (10 * k)) & 0x3ffu), b2));
+      n[k] = __fadd_rn(__fadd_rn(__fmul_rn(lut_n(w0, 10 * k), b0), __fmul_rn(lut_n(w1, 10 * k), b1)),
+                       __fmul_rn(lut_n(w2, 10 * k), b2));
   } else {
 #pragma unroll
-    for (int k = 0; k < 3; ++k) n[k] = dec_normal_c((meta.x >> (10 * k)) & 0x3ffu);
+    for (int k = 0; k < 3; ++k) n[k] = lut_n(meta.x, 10 * k);
   }
   // normalize (float), math.hpp:80-85
   float len2 = __fadd_rn(__fadd_rn(__fmul_rn(n[0], n[0]), __fmul_rn(n[1], n[1])), __fmul_rn(n[2], n[2]));
@@ -765,28 +778,54 @@ __device__ __forceinline__ float4 shade_sample(const FrameConst& fc, const Buffe
                       __fmul_rn(n[2], fc.light[2]));
   float lam = smaxf(0.0f, -d);
   float light = sminf(1.0f, __fadd_rn(fc.ambient, lam));
-  float r = __fmul_rn(__fmul_rn(__fmul_rn(m.base[0], color.x), 1.0f), light);
-  float g = __fmul_rn(__fmul_rn(__fmul_rn(m.base[1], color.y), 1.0f), light);
-  float b = __fmul_rn(__fmul_rn(__fmul_rn(m.base[2], color.z), 1.0f), light);
-  float a = __fmul_rn(__fmul_rn(m.opacity, color.w), 1.0f);
+  float r = __fmul_rn(__fmul_rn(__fmul_rn(__ldg(&m.base[0]), color.x), 1.0f), light);
+  float g = __fmul_rn(__fmul_rn(__fmul_rn(__ldg(&m.base[1]), color.y), 1.0f), light);
+  float b = __fmul_rn(__fmul_rn(__fmul_rn(__ldg(&m.base[2]), color.z), 1.0f), light);
+  float a = __fmul_rn(__fmul_rn(__ldg(&m.opacity), color.w), 1.0f);
   return make_float4(__fmul_rn(r, a), __fmul_rn(g, a), __fmul_rn(b, a), a);
 }
 
-struct RasterShared {
-  // Shared-memory capacities: the reference's low-path limits (raster.hpp:46).
-  static constexpr int kTbr = 1024, kTb = 256, kThb = 256;
-  Tbr tbr[kTbr];
-  uint64_t keys[4][kTb];
-  uint16_t refs[4][kTb];
-  uint64_t thb[4][2][kThb];
+__device__ __forceinline__ uint64_t sample_key(const FrameConst& fc, uint32_t qd, uint32_t tri) {
+  // sample_sort_key, raster.hpp:95-97 (32-bit triangle field when extended)
+  return fc.extended ? (((uint64_t)qd << 32) | tri) : (((uint64_t)qd << 24) | (tri & 0xffffffu));
+}
+
+// Scratch of one (bin, block-row) work item, in shared or global memory.
+struct RasterView {
+  Tbr* tbr;
+  uint64_t* keys;     // [4][cap_tb]
+  uint16_t* refs;     // [4][cap_tb]
+  uint32_t* thb_tri;  // [8][cap_tb]  tri-half-block lists, half-block hb = block*2 + half
+  uint32_t* thb_mask; // [8][cap_tb]  32-bit coverage (bit = ly*8 + lx)
+  uint32_t* thb_pre;  // [8][cap_tb]  exclusive fragment prefix
+  uint32_t* route;    // [4][32]
 };
+
+struct RasterShared {
+  // Shared-memory capacities; larger items (within the active limits) run
+  // again with global scratch.
+  static constexpr int kTbr = 512, kTb = 256;
+  Tbr tbr[kTbr];
+  uint64_t keys[4 * kTb];
+  uint16_t refs[4 * kTb];
+  uint32_t thb_tri[8 * kTb];
+  uint32_t thb_mask[8 * kTb];
+  uint32_t thb_pre[8 * kTb];
+  uint32_t route[4 * 32];
+};
+
+__host__ __device__ inline size_t global_scratch_bytes(uint32_t cap_tbr, uint32_t cap_tb) {
+  return (size_t)cap_tbr * sizeof(Tbr) + (size_t)4 * cap_tb * (8 + 2) +
+         (size_t)8 * cap_tb * 12 + 4 * 32 * 4 + 64;
+}
 
 struct ItemState {
   int ntbr;
   int status;  // 0 ok, 1 overflow (soft), 2 spill, 3 hard error
   int err_code;
-  uint32_t nthb[4][2];
-  uint64_t frags[4][2];
+  int next_hb;
+  uint32_t nthb[8];
+  uint32_t frags[8];
 };
 
 enum { kPassLow = 0, kPassHigh = 1 };
@@ -796,121 +835,155 @@ __device__ __forceinline__ void set_status(ItemState* st, int s, int code) {
   if (s == 3) atomicMin(&st->err_code, code);
 }
 
+struct PixelOut {
+  float4 acc;
+  bool invalid;
+  uint64_t hash;
+  uint32_t emitted;
+};
+
+// Blend one popped sample into the pixel state (shade_half_block,
+// raster.cpp:248-255).
+__device__ __forceinline__ void commit(PixelOut& o, uint64_t pk, float4 pc, bool ooo) {
+  o.acc = blend(o.acc, pc);
+  o.hash = (o.hash ^ pk) * kHashPrime;
+  ++o.emitted;
+  if (ooo) o.invalid = true;
+}
+
+// Canonical-order shading of one half-block without the alpha threshold:
+// the sample stream (THBs in sorted order, then row-major) is cut into
+// 32-sample segments; lane s shades sample base+s, then each pixel's lane
+// takes its samples of the segment in stream order through a per-warp
+// routing table and pushes them into its register depth filter. Every
+// pixel therefore sees exactly the reference's per-pixel sequence.
 template <int KM>
-__device__ void shade_half_blocks(const FrameConst& fc, const Buffers& B, int bin, int row,
-                                  int warp, const uint64_t* thb0, const uint64_t* thb1,
-                                  uint32_t n0, uint32_t n1, unsigned long long* acc_stats) {
+__device__ void shade_segments(const FrameConst& fc, const Buffers& B, int px0, int py0,
+                               const uint32_t* tri_l, const uint32_t* mask_l,
+                               const uint32_t* pre_l, uint32_t n, uint32_t total,
+                               uint32_t* route, PixelOut& o) {
   const int lane = threadIdx.x & 31;
-  const int bxi = bin % fc.bins_x, byi = bin / fc.bins_x;
-  const int ly = lane >> 3, cx = lane & 7;
-  unsigned long long samples = 0, segments = 0, invalid_px = 0;
-#pragma unroll 1
-  for (int half = 0; half < 2; ++half) {
-    const uint64_t* list = half ? thb1 : thb0;
-    const uint32_t n = half ? n1 : n0;
-    const int px = bxi * kBin + warp * 8 + cx;
-    const int py = byi * kBin + row * 8 + half * 4 + ly;
-    RegFilter<KM> f;
-    f.reset();
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    bool invalid = false, saturated = false, stopped = false;
-    uint64_t hash = kHashSeed;
-    uint32_t emitted = 0;
-    unsigned sat_mask = 0;
-    unsigned long long enumerated = 0;
-    for (uint32_t r = 0; r < n; ++r) {
-      const uint64_t rec = list[r];
-      const uint32_t tri = (uint32_t)(rec >> 32);
-      const uint32_t sp = (uint32_t)rec & 0xffffffu;
-      const uint32_t b = (sp >> (6 * ly)) & 7u, l = (sp >> (6 * ly + 3)) & 7u;
-      const bool covered = b <= (uint32_t)cx && (uint32_t)cx <= l;
-      const unsigned cov_mask = __ballot_sync(0xffffffffu, covered);
-      float4 col;
-      uint64_t key = 0;
-      if (covered) {
-        double depth;
-        col = shade_sample(fc, B, tri, px, py, &depth);
-        uint32_t qd = quantize_depth(depth);
-        key = fc.extended ? (((uint64_t)qd << 32) | tri) : (((uint64_t)qd << 24) | (tri & 0xffffffu));
+  RegFilter<KM> f;
+  f.reset();
+  uint32_t r_lo = 0;
+  for (uint32_t base = 0; base < total; base += 32) {
+    const uint32_t s = base + lane;
+    const bool valid = s < total;
+    uint32_t pix = 32u + lane;
+    uint32_t r = r_lo;
+    float4 col = make_float4(0.f, 0.f, 0.f, 0.f);
+    uint64_t key = 0;
+    if (valid) {
+      // THB holding sample s: THB r_lo holds a sample < base and every THB
+      // holds >= 1 sample, so r <= r_lo + lane + 1
+      uint32_t lo = r_lo, hi = min(n - 1, r_lo + (uint32_t)lane + 1u);
+      while (lo < hi) {
+        uint32_t mid = (lo + hi + 1) >> 1;
+        if (pre_l[mid] <= s) lo = mid; else hi = mid - 1;
       }
-      int commit_until = 32;  // lanes >= this do not commit (alpha-threshold stop)
-      if (fc.threshold) {
-        bool newly = false;
-        if (covered && !saturated) {
-          float4 pc;
-          if (f.peek(fc.df, key, col, &pc)) newly = blend(acc, pc).w >= kAlphaThreshold;
-        }
-        unsigned new_mask = __ballot_sync(0xffffffffu, newly);
-        if (new_mask && (sat_mask | new_mask) == 0xffffffffu) {
-          int L = 31 - __clz(new_mask);
-          commit_until = L + 1;
-          stopped = true;
-        }
-      }
-      enumerated += __popc(cov_mask & (commit_until == 32 ? 0xffffffffu : ((1u << commit_until) - 1u)));
-      if (covered && lane < commit_until) {
+      r = lo;
+      pix = __fns(mask_l[r], 0, (int)(s - pre_l[r]) + 1);
+      const uint32_t tri = tri_l[r];
+      double depth;
+      col = shade_sample(fc, B, tri, px0 + (int)(pix & 7u), py0 + (int)(pix >> 3), &depth);
+      key = sample_key(fc, quantize_depth(depth), tri);
+    }
+    r_lo = __shfl_sync(0xffffffffu, r, 31);
+    // routing: route[p] = lanes (= stream positions) whose sample is pixel p
+    route[lane] = 0u;
+    __syncwarp();
+    const unsigned peers = __match_any_sync(0xffffffffu, pix);
+    if (valid && lane == __ffs(peers) - 1) route[pix] = peers;
+    __syncwarp();
+    uint32_t mine = route[lane];
+    __syncwarp();
+    while (__any_sync(0xffffffffu, mine != 0u)) {
+      const int src = mine ? __ffs(mine) - 1 : lane;
+      const uint64_t k2 = __shfl_sync(0xffffffffu, key, src);
+      float4 c2;
+      c2.x = __shfl_sync(0xffffffffu, col.x, src);
+      c2.y = __shfl_sync(0xffffffffu, col.y, src);
+      c2.z = __shfl_sync(0xffffffffu, col.z, src);
+      c2.w = __shfl_sync(0xffffffffu, col.w, src);
+      if (mine) {
+        mine &= mine - 1u;
         uint64_t pk;
         float4 pc;
         bool ooo;
-        if (f.push(fc.df, key, col, &pk, &pc, &ooo)) {
-          acc = blend(acc, pc);
-          ++samples;
-          ++emitted;
-          hash = (hash ^ pk) * kHashPrime;
-          if (ooo) invalid = true;
-          if (fc.threshold && !saturated && acc.w >= kAlphaThreshold) saturated = true;
-        }
-      }
-      sat_mask = __ballot_sync(0xffffffffu, saturated);
-      if (stopped) break;
-    }
-    if (!stopped) {
-      bool done = fc.threshold && acc.w >= kAlphaThreshold;
-      while (f.n > 0) {
-        uint64_t pk;
-        float4 pc;
-        bool ooo;
-        f.pop(&pk, &pc, &ooo);
-        if (done) continue;
-        acc = blend(acc, pc);
-        ++samples;
-        ++emitted;
-        hash = (hash ^ pk) * kHashPrime;
-        if (ooo) invalid = true;
-        if (fc.threshold && acc.w >= kAlphaThreshold) done = true;
+        if (f.push(fc.df, k2, c2, &pk, &pc, &ooo)) commit(o, pk, pc, ooo);
       }
     }
-    segments += (enumerated + 255ull) / 256ull;
-    if (px < fc.width && py < fc.height) {
-      const size_t pix = (size_t)py * fc.width + px;
-      uint32_t word;
-      if (invalid && fc.visualize) {
-        word = 0xffff00ffu;  // magenta overlay, renderer.cpp:56-65
-      } else {
-        float4 o = blend(acc, make_float4(fc.bg[0], fc.bg[1], fc.bg[2], fc.bg[3]));
-        word = quantize_channel(o.x) | (quantize_channel(o.y) << 8) |
-               (quantize_channel(o.z) << 16) | (quantize_channel(o.w) << 24);
+  }
+  while (f.n > 0) {
+    uint64_t pk;
+    float4 pc;
+    bool ooo;
+    f.pop(&pk, &pc, &ooo);
+    commit(o, pk, pc, ooo);
+  }
+}
+
+// Alpha-threshold variant (raster.cpp:232-284): THB-by-THB walk with lane ==
+// pixel so the 32nd saturation can be located at its exact stream position.
+template <int KM>
+__device__ void shade_threshold(const FrameConst& fc, const Buffers& B, int px0, int py0,
+                                const uint32_t* tri_l, const uint32_t* mask_l, uint32_t n,
+                                PixelOut& o, unsigned long long* enumerated_out) {
+  const int lane = threadIdx.x & 31;
+  const int px = px0 + (lane & 7), py = py0 + (lane >> 3);
+  RegFilter<KM> f;
+  f.reset();
+  bool saturated = false, stopped = false;
+  unsigned sat_mask = 0;
+  unsigned long long enumerated = 0;
+  for (uint32_t r = 0; r < n; ++r) {
+    const uint32_t m = mask_l[r];
+    const uint32_t tri = tri_l[r];
+    const bool covered = (m >> lane) & 1u;
+    float4 col;
+    uint64_t key = 0;
+    if (covered) {
+      double depth;
+      col = shade_sample(fc, B, tri, px, py, &depth);
+      key = sample_key(fc, quantize_depth(depth), tri);
+    }
+    int commit_until = 32;
+    bool newly = false;
+    if (covered && !saturated) {
+      float4 pc;
+      if (f.peek(fc.df, key, col, &pc)) newly = blend(o.acc, pc).w >= kAlphaThreshold;
+    }
+    const unsigned new_mask = __ballot_sync(0xffffffffu, newly);
+    if (new_mask && (sat_mask | new_mask) == 0xffffffffu) {
+      commit_until = 32 - __clz(new_mask);
+      stopped = true;
+    }
+    enumerated += __popc(m & (commit_until == 32 ? 0xffffffffu : ((1u << commit_until) - 1u)));
+    if (covered && lane < commit_until) {
+      uint64_t pk;
+      float4 pc;
+      bool ooo;
+      if (f.push(fc.df, key, col, &pk, &pc, &ooo)) {
+        commit(o, pk, pc, ooo);
+        if (!saturated && o.acc.w >= kAlphaThreshold) saturated = true;
       }
-      B.fb[pix] = word;
-      B.mask[pix] = invalid ? 1 : 0;
-      if (fc.dump) {
-        B.hash[pix] = hash;
-        B.emit[pix] = emitted;
-      }
-      if (invalid) ++invalid_px;
+    }
+    sat_mask = __ballot_sync(0xffffffffu, saturated);
+    if (stopped) break;
+  }
+  if (!stopped) {
+    bool done = o.acc.w >= kAlphaThreshold;
+    while (f.n > 0) {
+      uint64_t pk;
+      float4 pc;
+      bool ooo;
+      f.pop(&pk, &pc, &ooo);
+      if (done) continue;
+      commit(o, pk, pc, ooo);
+      if (o.acc.w >= kAlphaThreshold) done = true;
     }
   }
-  // warp-reduce the per-lane counts
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    samples += __shfl_xor_sync(0xffffffffu, samples, o);
-    invalid_px += __shfl_xor_sync(0xffffffffu, invalid_px, o);
-  }
-  if (lane == 0) {
-    atomicAdd(&acc_stats[0], samples);
-    atomicAdd(&acc_stats[3], segments);  // warp-uniform: lane 0's count is the total
-    atomicAdd(&acc_stats[4], invalid_px);
-  }
+  *enumerated_out = enumerated;
 }
 
 __device__ void write_background(const FrameConst& fc, const Buffers& B, int bin, int row) {
@@ -931,12 +1004,20 @@ __device__ void write_background(const FrameConst& fc, const Buffers& B, int bin
   }
 }
 
-// One (bin, block-row) work item. kGlobal selects global-memory scratch
-// (capacities = the active limits) instead of shared memory.
+__device__ __forceinline__ uint32_t span_mask(uint32_t b, uint32_t l, uint32_t c0, uint32_t c1) {
+  // row span [b, l] (bin-local) clipped to block columns [c0, c1] as 8 bits
+  if (b > l) return 0u;
+  b = max(b, c0);
+  l = min(l, c1);
+  if (b > l) return 0u;
+  return ((2u << (l - b)) - 1u) << (b - c0);
+}
+
+// One (bin, block-row) work item. kGlobal selects global-memory scratch.
 template <bool kGlobal, int KM>
 __device__ void raster_item(const FrameConst& fc, const Buffers& B, int pass, int bin, int row,
-                            RasterShared* sh, ItemState* st, uint8_t* gscratch,
-                            uint32_t cap_tbr, uint32_t cap_tb) {
+                            const RasterView& V, ItemState* st, uint32_t cap_tbr,
+                            uint32_t cap_tb) {
   const Limits lim = pass == kPassLow ? fc.low : fc.high;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int bxi = bin % fc.bins_x, byi = bin / fc.bins_x;
@@ -945,31 +1026,11 @@ __device__ void raster_item(const FrameConst& fc, const Buffers& B, int pass, in
   const int py_last = min(py0 + kBin - 1, fc.height - 1);
   const int ry0 = py0 + row * 8, ry1 = min(ry0 + 7, py_last);
 
-  Tbr* tbr;
-  uint64_t* keys;
-  uint16_t* refs;
-  uint64_t* thb0;
-  uint64_t* thb1;
-  if (kGlobal) {
-    tbr = reinterpret_cast<Tbr*>(gscratch);
-    uint8_t* w = gscratch + (size_t)cap_tbr * sizeof(Tbr) +
-                 (size_t)warp * cap_tb * (sizeof(uint64_t) * 3 + sizeof(uint16_t));
-    keys = reinterpret_cast<uint64_t*>(w);
-    thb0 = keys + cap_tb;
-    thb1 = thb0 + cap_tb;
-    refs = reinterpret_cast<uint16_t*>(thb1 + cap_tb);
-  } else {
-    tbr = sh->tbr;
-    keys = sh->keys[warp];
-    refs = sh->refs[warp];
-    thb0 = sh->thb[warp][0];
-    thb1 = sh->thb[warp][1];
-  }
-
   if (threadIdx.x == 0) {
     st->ntbr = 0;
     st->status = 0;
     st->err_code = 0x7fffffff;
+    st->next_hb = 0;
   }
   __syncthreads();
 
@@ -1008,7 +1069,7 @@ __device__ void raster_item(const FrameConst& fc, const Buffers& B, int pass, in
     if (!cols) continue;
     rec.meta = cols | (large << 4);
     int slot = atomicAdd(&st->ntbr, 1);
-    if ((uint32_t)slot < cap_tbr) tbr[slot] = rec;
+    if ((uint32_t)slot < cap_tbr) V.tbr[slot] = rec;
   }
   __syncthreads();
   const uint32_t ntbr = (uint32_t)st->ntbr;
@@ -1024,15 +1085,17 @@ __device__ void raster_item(const FrameConst& fc, const Buffers& B, int pass, in
   const int block = row * 4 + warp;
   const uint32_t c0 = (uint32_t)warp * 8u, c1 = c0 + 7u;
   const double bpx0 = (double)(px0 + warp * 8), bpy0 = (double)(py0 + row * 8);
+  uint64_t* keys = V.keys + (size_t)warp * cap_tb;
+  uint16_t* refs = V.refs + (size_t)warp * cap_tb;
   uint32_t n = 0;
   for (uint32_t base = 0; base < ntbr; base += 32) {
     uint32_t i = base + lane;
-    bool sel = i < ntbr && ((tbr[i].meta >> warp) & 1u);
+    bool sel = i < ntbr && ((V.tbr[i].meta >> warp) & 1u);
     unsigned m = __ballot_sync(0xffffffffu, sel);
     if (sel) {
       uint32_t pos = n + __popc(m & ((1u << lane) - 1u));
       if (pos < cap_tb) {
-        const Tbr& rw = tbr[i];
+        const Tbr& rw = V.tbr[i];
         uint32_t count = 0, sx = 0, sy = 0;
 #pragma unroll
         for (int y = 0; y < 8; ++y) {
@@ -1052,6 +1115,8 @@ __device__ void raster_item(const FrameConst& fc, const Buffers& B, int pass, in
           double cy = __dadd_rn(__dadd_rn(bpy0, __ddiv_rn((double)sy, (double)count)), 0.5);
           qd = quantize_depth(eval(B.tri[rw.tri].dz, cx, cy));
         }
+        // (depth, is_large, triangle) orders exactly like the reference's
+        // (depth, selection index): selection order is bin-list order.
         keys[pos] = ((uint64_t)qd << 33) | ((uint64_t)((rw.meta >> 4) & 1u) << 32) | rw.tri;
         refs[pos] = (uint16_t)i;
       }
@@ -1064,11 +1129,8 @@ __device__ void raster_item(const FrameConst& fc, const Buffers& B, int pass, in
     if (lane == 0) set_status(st, 2, 0);
   }
   __syncwarp();
-  bool ok = n <= lim.tb && n <= cap_tb;
-  uint32_t nthb[2] = {0, 0};
-  uint64_t frags[2] = {0, 0};
+  const bool ok = n <= lim.tb && n <= cap_tb;
   if (ok && n > 1) {
-    // bitonic sort of (key, ref) ascending
     uint32_t N = 1;
     while (N < n) N <<= 1;
     for (uint32_t i = n + lane; i < N; i += 32) keys[i] = ~0ull, refs[i] = 0;
@@ -1092,49 +1154,43 @@ __device__ void raster_item(const FrameConst& fc, const Buffers& B, int pass, in
         __syncwarp();
       }
   }
+  uint32_t nthb[2] = {0, 0}, frags[2] = {0, 0};
   if (ok) {
-    // split into upper/lower tri-half-blocks with fragment prefix sums
+    uint32_t* tl[2] = {V.thb_tri + (size_t)(warp * 2) * cap_tb, V.thb_tri + (size_t)(warp * 2 + 1) * cap_tb};
+    uint32_t* ml[2] = {V.thb_mask + (size_t)(warp * 2) * cap_tb, V.thb_mask + (size_t)(warp * 2 + 1) * cap_tb};
+    uint32_t* pl[2] = {V.thb_pre + (size_t)(warp * 2) * cap_tb, V.thb_pre + (size_t)(warp * 2 + 1) * cap_tb};
     for (uint32_t base = 0; base < n; base += 32) {
       uint32_t k = base + lane;
-      uint32_t sp[2] = {0, 0}, fr[2] = {0, 0};
+      uint32_t hm[2] = {0u, 0u};
       uint32_t tri = 0;
       if (k < n) {
-        const Tbr& rw = tbr[refs[k]];
+        const Tbr& rw = V.tbr[refs[k]];
         tri = rw.tri;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          uint32_t s = 0, f = 0;
+        for (int h = 0; h < 2; ++h)
 #pragma unroll
-          for (int y = 0; y < 4; ++y) {
-            uint32_t b = byte_of(rw.b, h * 4 + y), l = byte_of(rw.l, h * 4 + y);
-            uint32_t lb = 7, ll = 0;
-            if (b <= l) {
-              b = max(b, c0);
-              l = min(l, c1);
-              if (b <= l) {
-                lb = b - c0;
-                ll = l - c0;
-                f += l - b + 1;
-              }
-            }
-            s |= (lb | (ll << 3)) << (6 * y);
-          }
-          sp[h] = s;
-          fr[h] = f;
-        }
+          for (int y = 0; y < 4; ++y)
+            hm[h] |= span_mask(byte_of(rw.b, h * 4 + y), byte_of(rw.l, h * 4 + y), c0, c1) << (8 * y);
       }
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        bool ne = fr[h] > 0;
-        unsigned m = __ballot_sync(0xffffffffu, ne);
-        uint32_t pos = nthb[h] + __popc(m & ((1u << lane) - 1u));
-        uint64_t* out = h ? thb1 : thb0;
-        if (ne && pos < cap_tb) out[pos] = ((uint64_t)tri << 32) | sp[h] | ((uint64_t)fr[h] << 24);
-        uint32_t f = fr[h];
+        const uint32_t fr = __popc(hm[h]);
+        const bool ne = fr > 0;
+        const unsigned m = __ballot_sync(0xffffffffu, ne);
+        const uint32_t pos = nthb[h] + __popc(m & ((1u << lane) - 1u));
+        uint32_t incl = fr;  // inclusive scan of fragment counts
 #pragma unroll
-        for (int s = 16; s > 0; s >>= 1) f += __shfl_xor_sync(0xffffffffu, f, s);
+        for (int s = 1; s < 32; s <<= 1) {
+          uint32_t y = __shfl_up_sync(0xffffffffu, incl, s);
+          if (lane >= s) incl += y;
+        }
+        if (ne && pos < cap_tb) {
+          tl[h][pos] = tri;
+          ml[h][pos] = hm[h];
+          pl[h][pos] = frags[h] + incl - fr;
+        }
         nthb[h] += __popc(m);
-        frags[h] += f;
+        frags[h] += __shfl_sync(0xffffffffu, incl, 31);
       }
     }
     for (int h = 0; h < 2; ++h) {
@@ -1146,53 +1202,136 @@ __device__ void raster_item(const FrameConst& fc, const Buffers& B, int pass, in
     }
   }
   if (lane == 0) {
-    st->nthb[warp][0] = nthb[0];
-    st->nthb[warp][1] = nthb[1];
-    st->frags[warp][0] = frags[0];
-    st->frags[warp][1] = frags[1];
+    st->nthb[warp * 2] = nthb[0];
+    st->nthb[warp * 2 + 1] = nthb[1];
+    st->frags[warp * 2] = frags[0];
+    st->frags[warp * 2 + 1] = frags[1];
   }
   __syncthreads();
   if (st->status) return;
 
-  // ---- phase C: shade + blend both half-blocks of block (row, warp)
+  // ---- phase C: shade + blend; warps take half-blocks dynamically
   unsigned long long* slot = B.slots + ((size_t)bin * 4 + row) * 5;
   if (threadIdx.x < 5) slot[threadIdx.x] = 0;
   __syncthreads();
-  if (lane == 0) {
-    atomicAdd(&slot[1], (unsigned long long)(frags[0] + frags[1]));
-    atomicAdd(&slot[2], (unsigned long long)(nthb[0] + nthb[1]));
-  }
-  if (fc.dump && lane < 2) {
-    int hb = block * 2 + lane;
-    B.thb_cnt[(size_t)bin * 32 + hb] = nthb[lane];
-    if (B.thb_off) {
-      uint64_t base = B.thb_off[(size_t)bin * 32 + hb];
-      const uint64_t* list = lane ? thb1 : thb0;
-      uint32_t prefix = 0;
-      for (uint32_t i = 0; i < nthb[lane]; ++i) {
-        uint64_t r = list[i];
-        uint32_t tri = (uint32_t)(r >> 32);
-        prefix += (uint32_t)(r >> 24) & 0x3fu;
-        // TriHalfBlock::make, packing.hpp:154-176
-        B.thb_out[base + i] = (r & 0xffffffull) | ((uint64_t)(tri & 0xffffffu) << 24) |
-                              ((uint64_t)(prefix & 0xfffu) << 48);
-        B.thb_tri[base + i] = tri;
-        B.thb_pre[base + i] = prefix;
+  unsigned long long w_samples = 0, w_segments = 0, w_invalid = 0, w_frags = 0, w_thb = 0;
+  uint32_t* route = V.route + warp * 32;
+  for (;;) {
+    int hb = 0;
+    if (lane == 0) hb = atomicAdd(&st->next_hb, 1);
+    hb = __shfl_sync(0xffffffffu, hb, 0);
+    if (hb >= 8) break;
+    const uint32_t cnt = st->nthb[hb], total = st->frags[hb];
+    const uint32_t* tri_l = V.thb_tri + (size_t)hb * cap_tb;
+    const uint32_t* mask_l = V.thb_mask + (size_t)hb * cap_tb;
+    const uint32_t* pre_l = V.thb_pre + (size_t)hb * cap_tb;
+    const int hpx0 = px0 + (hb >> 1) * 8, hpy0 = ry0 + (hb & 1) * 4;
+    PixelOut po;
+    po.acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    po.invalid = false;
+    po.hash = kHashSeed;
+    po.emitted = 0;
+    unsigned long long enumerated = total;
+    if (fc.threshold)
+      shade_threshold<KM>(fc, B, hpx0, hpy0, tri_l, mask_l, cnt, po, &enumerated);
+    else if (total)
+      shade_segments<KM>(fc, B, hpx0, hpy0, tri_l, mask_l, pre_l, cnt, total, route, po);
+    w_segments += (enumerated + 255ull) / 256ull;
+    w_frags += total;
+    w_thb += cnt;
+    const int px = hpx0 + (lane & 7), py = hpy0 + (lane >> 3);
+    if (px < fc.width && py < fc.height) {
+      const size_t pix = (size_t)py * fc.width + px;
+      uint32_t word;
+      if (po.invalid && fc.visualize) {
+        word = 0xffff00ffu;  // magenta overlay, renderer.cpp:56-65
+      } else {
+        float4 out = blend(po.acc, make_float4(fc.bg[0], fc.bg[1], fc.bg[2], fc.bg[3]));
+        word = quantize_channel(out.x) | (quantize_channel(out.y) << 8) |
+               (quantize_channel(out.z) << 16) | (quantize_channel(out.w) << 24);
+      }
+      B.fb[pix] = word;
+      B.mask[pix] = po.invalid ? 1 : 0;
+      if (fc.dump) {
+        B.hash[pix] = po.hash;
+        B.emit[pix] = po.emitted;
+      }
+      if (po.invalid) ++w_invalid;
+    }
+    w_samples += po.emitted;
+    if (fc.dump) {
+      B.thb_cnt[(size_t)bin * 32 + row * 8 + hb] = cnt;
+      if (B.thb_off) {
+        const uint64_t obase = B.thb_off[(size_t)bin * 32 + row * 8 + hb];
+        for (uint32_t i = lane; i < cnt; i += 32) {
+          const uint32_t m = mask_l[i], tri = tri_l[i];
+          uint64_t bits = 0;  // TriHalfBlock::make, packing.hpp:154-176
+          for (int y = 0; y < 4; ++y) {
+            const uint32_t rb = (m >> (8 * y)) & 0xffu;
+            uint32_t b = 7, l = 0;
+            if (rb) {
+              b = __ffs(rb) - 1;
+              l = 31 - __clz(rb);
+            }
+            bits |= (uint64_t)(b | (l << 3)) << (6 * y);
+          }
+          const uint32_t prefix = pre_l[i] + __popc(m);
+          B.thb_out[obase + i] = bits | ((uint64_t)(tri & 0xffffffu) << 24) |
+                                 ((uint64_t)(prefix & 0xfffu) << 48);
+          B.thb_tri[obase + i] = tri;
+          B.thb_pre[obase + i] = prefix;
+        }
       }
     }
   }
-  shade_half_blocks<KM>(fc, B, bin, row, warp, thb0, thb1, nthb[0], nthb[1], slot);
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) {
+    w_samples += __shfl_xor_sync(0xffffffffu, w_samples, s);
+    w_invalid += __shfl_xor_sync(0xffffffffu, w_invalid, s);
+  }
+  if (lane == 0) {
+    atomicAdd(&slot[0], w_samples);
+    atomicAdd(&slot[1], w_frags);
+    atomicAdd(&slot[2], w_thb);
+    atomicAdd(&slot[3], w_segments);
+    atomicAdd(&slot[4], w_invalid);
+  }
 }
 
 template <bool kGlobal, int KM>
 __global__ void __launch_bounds__(128) k_raster(FrameConst fc, Buffers B, int pass,
                                                 uint32_t cap_tbr, uint32_t cap_tb) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
-  RasterShared* sh = kGlobal ? nullptr : reinterpret_cast<RasterShared*>(smem_raw);
   __shared__ ItemState st;
   __shared__ uint32_t item_s;
   if (B.ctr->error) return;
-  uint8_t* gscratch = kGlobal ? B.scratch + (size_t)blockIdx.x * B.scratch_per_cta : nullptr;
+  RasterView V;
+  if (kGlobal) {
+    uint8_t* g = B.scratch + (size_t)blockIdx.x * B.scratch_per_cta;
+    V.tbr = reinterpret_cast<Tbr*>(g);
+    g += (size_t)cap_tbr * sizeof(Tbr);
+    g = reinterpret_cast<uint8_t*>(((uintptr_t)g + 15) & ~(uintptr_t)15);
+    V.keys = reinterpret_cast<uint64_t*>(g);
+    g += (size_t)4 * cap_tb * 8;
+    V.thb_tri = reinterpret_cast<uint32_t*>(g);
+    g += (size_t)8 * cap_tb * 4;
+    V.thb_mask = reinterpret_cast<uint32_t*>(g);
+    g += (size_t)8 * cap_tb * 4;
+    V.thb_pre = reinterpret_cast<uint32_t*>(g);
+    g += (size_t)8 * cap_tb * 4;
+    V.route = reinterpret_cast<uint32_t*>(g);
+    g += 4 * 32 * 4;
+    V.refs = reinterpret_cast<uint16_t*>(g);
+  } else {
+    RasterShared* sh = reinterpret_cast<RasterShared*>(smem_raw);
+    V.tbr = sh->tbr;
+    V.keys = sh->keys;
+    V.refs = sh->refs;
+    V.thb_tri = sh->thb_tri;
+    V.thb_mask = sh->thb_mask;
+    V.thb_pre = sh->thb_pre;
+    V.route = sh->route;
+  }
   const uint32_t nitems = kGlobal ? B.ctr->spill_count[pass] : (uint32_t)fc.nbins * 4u;
   unsigned int* counter = &B.ctr->work_next[pass * 2 + (kGlobal ? 1 : 0)];
   for (;;) {
@@ -1222,7 +1361,7 @@ __global__ void __launch_bounds__(128) k_raster(FrameConst fc, Buffers B, int pa
     }
     if (!run) continue;
     if (!kGlobal && pass == kPassLow && B.prop[bin]) continue;  // sibling already overflowed
-    raster_item<kGlobal, KM>(fc, B, pass, bin, row, sh, &st, gscratch, cap_tbr, cap_tb);
+    raster_item<kGlobal, KM>(fc, B, pass, bin, row, V, &st, cap_tbr, cap_tb);
     __syncthreads();
     if (threadIdx.x == 0 && st.status) {
       if (st.status == 1) {
@@ -1454,6 +1593,13 @@ DeviceScene* device_scene(const Scene& s) {
     ck(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking), "cudaStreamCreate");
     for (auto& e : d->ev) ck(cudaEventCreate(&e), "cudaEventCreate");
     cudaDeviceGetAttribute(&d->sm_count, cudaDevAttrMultiProcessorCount, t_device);
+    {  // exact unpack tables (IEEE float division on the host)
+      float lc[256], ln[1024];
+      for (int q = 0; q < 256; ++q) lc[q] = float(q) / 255.0f;
+      for (int q = -512; q < 512; ++q) ln[q + 512] = float(q) / 511.0f;
+      ck(cudaMemcpyToSymbol(dev::g_lut_c, lc, sizeof lc), "lut");
+      ck(cudaMemcpyToSymbol(dev::g_lut_n, ln, sizeof ln), "lut");
+    }
     s.device = d;
   }
   DeviceScene* d = s.device;
@@ -1568,6 +1714,7 @@ void launch_raster_pair(DeviceScene* d, const dev::FrameConst& fc, const dev::Bu
   grid = std::min<long long>(grid, (long long)fc.nbins * 4);
   dev::k_raster<false, KM><<<grid, 128, smem, d->stream>>>(fc, B, pass, dev::RasterShared::kTbr,
                                                              dev::RasterShared::kTb);
+  ck(cudaGetLastError(), "k_raster launch");
   ++*launches;
   dev::k_raster<true, KM><<<d->raster_ctas_global, 128, 0, d->stream>>>(fc, B, pass, gcap_tbr, gcap_tb);
   ++*launches;
@@ -1713,8 +1860,7 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
     while (p2 < P.gcap_tb) p2 <<= 1;
     P.gcap_tb = p2;
   }
-  size_t per_cta = size_t(P.gcap_tbr) * sizeof(dev::Tbr) +
-                   4 * size_t(P.gcap_tb) * (sizeof(uint64_t) * 3 + sizeof(uint16_t));
+  size_t per_cta = dev::global_scratch_bytes(P.gcap_tbr, P.gcap_tb);
   per_cta = (per_cta + 255) & ~size_t(255);
   d->raster_ctas_global = d->sm_count * 2;
   d->scratch.ensure(per_cta * d->raster_ctas_global);
