@@ -636,11 +636,14 @@ __device__ __forceinline__ uint32_t byte_of(const uint32_t* w, int i) {
 }
 
 // Register depth filter (depth_filter.hpp:31-92) with compile-time maximum
-// capacity KM and runtime capacity cap <= KM; entries ascending by key.
+// capacity KM and runtime capacity cap <= KM; entries ascending by key
+// (keys are unique per pixel). push() returns the entry the reference's
+// insert-then-pop_min would emit: when full, that is min(new, oldest
+// minimum), and the survivor set is merged back with one select pass.
 template <int KM>
 struct RegFilter {
-  uint64_t key[KM + 1];
-  float4 col[KM + 1];
+  uint64_t key[KM];
+  float4 col[KM];
   int n;
   uint64_t max_key;
   bool any;
@@ -650,56 +653,75 @@ struct RegFilter {
     max_key = 0;
     any = false;
   }
-  // Inserts (k, c); returns true and the popped minimum when over capacity.
+  __device__ __forceinline__ void note(uint64_t pk, bool* ooo) {
+    *ooo = any && pk < max_key;
+    if (!any || pk > max_key) max_key = pk;
+    any = true;
+  }
   __device__ __forceinline__ bool push(int cap, uint64_t k, float4 c, uint64_t* pk, float4* pc,
                                        bool* ooo) {
-    // bubble the new entry into place (keys are unique per pixel)
-    uint64_t ck = k;
-    float4 cc = c;
+    if (n < cap) {  // not full: bubble into [0, n]
+      uint64_t ck = k;
+      float4 cc = c;
 #pragma unroll
-    for (int i = 0; i <= KM; ++i) {
-      if (i < n) {
-        if (key[i] > ck) {
-          uint64_t tk = key[i];
-          float4 tc = col[i];
+      for (int i = 0; i < KM; ++i) {
+        if (i < n) {
+          const bool sw = key[i] > ck;
+          const uint64_t tk = key[i];
+          const float4 tc = col[i];
+          key[i] = sw ? ck : tk;
+          col[i] = sw ? cc : tc;
+          ck = sw ? tk : ck;
+          cc = sw ? tc : cc;
+        } else if (i == n) {
           key[i] = ck;
           col[i] = cc;
-          ck = tk;
-          cc = tc;
         }
-      } else if (i == n) {
+      }
+      ++n;
+      return false;
+    }
+    if (k < key[0]) {  // the new sample is the minimum: it falls straight out
+      *pk = k;
+      *pc = c;
+      note(k, ooo);
+      return true;
+    }
+    *pk = key[0];
+    *pc = col[0];
+    note(key[0], ooo);
+    uint64_t ck = k;  // slots <- sorted(key[1..cap-1] + {k})
+    float4 cc = c;
+#pragma unroll
+    for (int i = 0; i < KM; ++i) {
+      if (i + 1 < cap) {
+        const uint64_t x = key[i + 1];
+        const float4 xc = col[i + 1];
+        const bool lt = x < ck;
+        key[i] = lt ? x : ck;
+        col[i] = lt ? xc : cc;
+        ck = lt ? ck : x;
+        cc = lt ? cc : xc;
+      } else if (i + 1 == cap) {
         key[i] = ck;
         col[i] = cc;
       }
     }
-    ++n;
-    if (n <= cap) return false;
-    pop(pk, pc, ooo);
     return true;
   }
   __device__ __forceinline__ void pop(uint64_t* pk, float4* pc, bool* ooo) {
     *pk = key[0];
     *pc = col[0];
 #pragma unroll
-    for (int i = 0; i < KM; ++i) {
-      if (i + 1 < n) {
-        key[i] = key[i + 1];
-        col[i] = col[i + 1];
-      }
-    }
+    for (int i = 0; i + 1 < KM; ++i)
+      if (i + 1 < n) key[i] = key[i + 1], col[i] = col[i + 1];
     --n;
-    *ooo = any && *pk < max_key;
-    if (!any || *pk > max_key) max_key = *pk;
-    any = true;
+    note(*pk, ooo);
   }
-  // Peek at what push(k) would pop, without modifying the filter.
+  // Colour push(k) would pop (if any), without modifying the filter.
   __device__ __forceinline__ bool peek(int cap, uint64_t k, float4 c, float4* pc) const {
-    if (n + 1 <= cap) return false;
-    if (n == 0 || k < key[0]) {
-      *pc = c;
-    } else {
-      *pc = col[0];
-    }
+    if (n < cap) return false;
+    *pc = (k < key[0]) ? c : col[0];
     return true;
   }
 };
@@ -851,6 +873,19 @@ __device__ __forceinline__ void commit(PixelOut& o, uint64_t pk, float4 pc, bool
   if (ooo) o.invalid = true;
 }
 
+// k-th covered pixel (row-major) of a tri-half-block coverage mask; each of
+// the 4 rows is one contiguous run (packing.hpp:96-103), so row counts and
+// the run start locate it without a bit-by-bit scan.
+__device__ __forceinline__ uint32_t kth_pixel(uint32_t m, uint32_t k) {
+  const uint32_t c0 = __popc(m & 0xffu), c1 = __popc(m & 0xff00u), c2 = __popc(m & 0xff0000u);
+  uint32_t row = 0, before = 0;
+  if (k >= c0) row = 1, before = c0;
+  if (k >= c0 + c1) row = 2, before = c0 + c1;
+  if (k >= c0 + c1 + c2) row = 3, before = c0 + c1 + c2;
+  const uint32_t rb = (m >> (8 * row)) & 0xffu;
+  return row * 8 + (__ffs(rb) - 1) + (k - before);
+}
+
 // Canonical-order shading of one half-block without the alpha threshold:
 // the sample stream (THBs in sorted order, then row-major) is cut into
 // 32-sample segments; lane s shades sample base+s, then each pixel's lane
@@ -858,7 +893,7 @@ __device__ __forceinline__ void commit(PixelOut& o, uint64_t pk, float4 pc, bool
 // routing table and pushes them into its register depth filter. Every
 // pixel therefore sees exactly the reference's per-pixel sequence.
 template <int KM>
-__device__ void shade_segments(const FrameConst& fc, const Buffers& B, int px0, int py0,
+__device__ __forceinline__ void shade_segments(const FrameConst& fc, const Buffers& B, int px0, int py0,
                                const uint32_t* tri_l, const uint32_t* mask_l,
                                const uint32_t* pre_l, uint32_t n, uint32_t total,
                                uint32_t* route, PixelOut& o) {
@@ -882,7 +917,7 @@ __device__ void shade_segments(const FrameConst& fc, const Buffers& B, int px0, 
         if (pre_l[mid] <= s) lo = mid; else hi = mid - 1;
       }
       r = lo;
-      pix = __fns(mask_l[r], 0, (int)(s - pre_l[r]) + 1);
+      pix = kth_pixel(mask_l[r], s - pre_l[r]);
       const uint32_t tri = tri_l[r];
       double depth;
       col = shade_sample(fc, B, tri, px0 + (int)(pix & 7u), py0 + (int)(pix >> 3), &depth);
@@ -926,7 +961,7 @@ __device__ void shade_segments(const FrameConst& fc, const Buffers& B, int px0, 
 // Alpha-threshold variant (raster.cpp:232-284): THB-by-THB walk with lane ==
 // pixel so the 32nd saturation can be located at its exact stream position.
 template <int KM>
-__device__ void shade_threshold(const FrameConst& fc, const Buffers& B, int px0, int py0,
+__device__ __forceinline__ void shade_threshold(const FrameConst& fc, const Buffers& B, int px0, int py0,
                                 const uint32_t* tri_l, const uint32_t* mask_l, uint32_t n,
                                 PixelOut& o, unsigned long long* enumerated_out) {
   const int lane = threadIdx.x & 31;
@@ -1015,7 +1050,7 @@ __device__ __forceinline__ uint32_t span_mask(uint32_t b, uint32_t l, uint32_t c
 
 // One (bin, block-row) work item. kGlobal selects global-memory scratch.
 template <bool kGlobal, int KM>
-__device__ void raster_item(const FrameConst& fc, const Buffers& B, int pass, int bin, int row,
+__device__ __forceinline__ void raster_item(const FrameConst& fc, const Buffers& B, int pass, int bin, int row,
                             const RasterView& V, ItemState* st, uint32_t cap_tbr,
                             uint32_t cap_tb) {
   const Limits lim = pass == kPassLow ? fc.low : fc.high;
@@ -1051,23 +1086,31 @@ __device__ void raster_item(const FrameConst& fc, const Buffers& B, int pass, in
     const TriRec& t = B.tri[ti];
     int yb = max(max(t.y_min, py0), ry0), ye = min(min(t.y_max, py_last), ry1);
     if (yb > ye) continue;
-    Tbr rec;
-    rec.tri = ti;
-    rec.b[0] = rec.b[1] = 0x1f1f1f1fu;
-    rec.l[0] = rec.l[1] = 0u;
-    uint32_t cols = 0;
+    uint32_t rb0 = 0x1f1f1f1fu, rb1 = 0x1f1f1f1fu, rl0 = 0u, rl1 = 0u, cols = 0;
     for (int py = yb; py <= ye; ++py) {
       int b, l;
       if (!row_span(t, py, px0, px_last, &b, &l)) continue;
-      int ly = py - ry0;
-      uint32_t bb = (uint32_t)(b - px0), ll = (uint32_t)(l - px0);
-      int sh8 = (ly & 3) * 8;
-      rec.b[ly >> 2] = (rec.b[ly >> 2] & ~(0xffu << sh8)) | (bb << sh8);
-      rec.l[ly >> 2] = (rec.l[ly >> 2] & ~(0xffu << sh8)) | (ll << sh8);
+      const int ly = py - ry0;
+      const uint32_t bb = (uint32_t)(b - px0), ll = (uint32_t)(l - px0);
+      const int sh8 = (ly & 3) * 8;
+      const uint32_t keep = ~(0xffu << sh8);
+      if (ly < 4) {
+        rb0 = (rb0 & keep) | (bb << sh8);
+        rl0 = (rl0 & keep) | (ll << sh8);
+      } else {
+        rb1 = (rb1 & keep) | (bb << sh8);
+        rl1 = (rl1 & keep) | (ll << sh8);
+      }
       cols |= ((2u << (ll >> 3)) - 1u) & ~((1u << (bb >> 3)) - 1u);
     }
     if (!cols) continue;
+    Tbr rec;
+    rec.tri = ti;
     rec.meta = cols | (large << 4);
+    rec.b[0] = rb0;
+    rec.b[1] = rb1;
+    rec.l[0] = rl0;
+    rec.l[1] = rl1;
     int slot = atomicAdd(&st->ntbr, 1);
     if ((uint32_t)slot < cap_tbr) V.tbr[slot] = rec;
   }
@@ -1156,9 +1199,6 @@ __device__ void raster_item(const FrameConst& fc, const Buffers& B, int pass, in
   }
   uint32_t nthb[2] = {0, 0}, frags[2] = {0, 0};
   if (ok) {
-    uint32_t* tl[2] = {V.thb_tri + (size_t)(warp * 2) * cap_tb, V.thb_tri + (size_t)(warp * 2 + 1) * cap_tb};
-    uint32_t* ml[2] = {V.thb_mask + (size_t)(warp * 2) * cap_tb, V.thb_mask + (size_t)(warp * 2 + 1) * cap_tb};
-    uint32_t* pl[2] = {V.thb_pre + (size_t)(warp * 2) * cap_tb, V.thb_pre + (size_t)(warp * 2 + 1) * cap_tb};
     for (uint32_t base = 0; base < n; base += 32) {
       uint32_t k = base + lane;
       uint32_t hm[2] = {0u, 0u};
@@ -1185,14 +1225,16 @@ __device__ void raster_item(const FrameConst& fc, const Buffers& B, int pass, in
           if (lane >= s) incl += y;
         }
         if (ne && pos < cap_tb) {
-          tl[h][pos] = tri;
-          ml[h][pos] = hm[h];
-          pl[h][pos] = frags[h] + incl - fr;
+          const size_t at = (size_t)(warp * 2 + h) * cap_tb + pos;
+          V.thb_tri[at] = tri;
+          V.thb_mask[at] = hm[h];
+          V.thb_pre[at] = frags[h] + incl - fr;
         }
         nthb[h] += __popc(m);
         frags[h] += __shfl_sync(0xffffffffu, incl, 31);
       }
     }
+#pragma unroll
     for (int h = 0; h < 2; ++h) {
       if (nthb[h] > lim.thb) {
         if (lane == 0) set_status(st, pass == kPassLow ? 1 : 3, 2 + 3 * block);
@@ -1299,7 +1341,7 @@ __device__ void raster_item(const FrameConst& fc, const Buffers& B, int pass, in
 }
 
 template <bool kGlobal, int KM>
-__global__ void __launch_bounds__(128) k_raster(FrameConst fc, Buffers B, int pass,
+__global__ void __launch_bounds__(128, 4) k_raster(FrameConst fc, Buffers B, int pass,
                                                 uint32_t cap_tbr, uint32_t cap_tb) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   __shared__ ItemState st;
