@@ -77,6 +77,7 @@ struct FrameConst {
   uint32_t tri_cap;  // visible-triangle capacity (2^24 standard)
   int rank, world;
   int dump;
+  int decoded;  // setup writes per-triangle decoded shading records
 };
 
 // Device counters; one instance per scene workspace, zeroed per frame.
@@ -94,6 +95,18 @@ struct Counters {
   unsigned int hi_items;
   unsigned int pad;
 };
+
+// Decoded per-triangle shading inputs (unpack_color / decode_normal of the
+// three corners, material colour and opacity), written by setup when
+// triangles cover many pixels so the per-sample path skips the unpacking.
+struct __align__(16) ShadeRec {
+  float4 c[3];    // corner colours (valid when flags & 1)
+  float4 n[3];    // corner normals (flags & 2) or n[0] = flat normal
+  float4 mat;     // base rgb, opacity
+  uint32_t flags;
+  uint32_t pad[3];
+};
+static_assert(sizeof(ShadeRec) == 128, "ShadeRec is one cache line");
 
 struct Buffers {
   // scene
@@ -114,6 +127,7 @@ struct Buffers {
   uint4* vq_nrm;
   TriRec* tri;
   uint4* tri_meta;  // flat normal, material, quad index, tri | valid << 8
+  struct ShadeRec* shade;  // per triangle, when FrameConst::decoded
   // bins
   uint32_t* qcnt;
   uint32_t* tcnt;
@@ -139,6 +153,20 @@ struct Buffers {
   uint32_t* thb_pre;  // dump
   Counters* ctr;
 };
+
+// Exact unpack tables: g_lut_c[q] = float(q) / 255.0f (unpack_color,
+// packing.hpp:63-66) and g_lut_n[q + 512] = float(q) / 511.0f
+// (decode_normal, packing.hpp:43-49), filled by the host with IEEE division.
+__device__ float g_lut_c[256];
+__device__ float g_lut_n[1024];
+
+__device__ __forceinline__ float lut_c(uint32_t w, int shift) {
+  return __ldg(&g_lut_c[(w >> shift) & 0xffu]);
+}
+__device__ __forceinline__ float lut_n(uint32_t w, int shift) {
+  int32_t q = (int32_t)(((w >> shift) & 0x3ffu) << 22) >> 22;
+  return __ldg(&g_lut_n[q + 512]);
+}
 
 // ------------------------------------------------------------ setup
 
@@ -437,6 +465,22 @@ __global__ void __launch_bounds__(kSetupBlock) k_setup_write(FrameConst fc, Buff
     }
     B.tri[slot * 2 + t] = rec;
     B.tri_meta[slot * 2 + t] = meta;
+    if (fc.decoded && valid) {
+      // corner slots (0,1,2) / (0,2,3), shading.cpp:41-44
+      const uint32_t cw[3] = {col.x, t == 0 ? col.y : col.z, t == 0 ? col.z : col.w};
+      const uint32_t nw[3] = {nrm.x, t == 0 ? nrm.y : nrm.z, t == 0 ? nrm.z : nrm.w};
+      ShadeRec sr;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        sr.c[k] = make_float4(lut_c(cw[k], 0), lut_c(cw[k], 8), lut_c(cw[k], 16), lut_c(cw[k], 24));
+        const uint32_t w = has_n ? nw[k] : meta.x;
+        sr.n[k] = make_float4(lut_n(w, 0), lut_n(w, 10), lut_n(w, 20), 0.0f);
+      }
+      sr.mat = make_float4(md.base[0], md.base[1], md.base[2], md.opacity);
+      sr.flags = (has_c ? 1u : 0u) | (has_n ? 2u : 0u);
+      sr.pad[0] = sr.pad[1] = sr.pad[2] = 0;
+      B.shade[slot * 2 + t] = sr;
+    }
   }
 }
 
@@ -732,18 +776,29 @@ __device__ __forceinline__ float4 blend(float4 acc, float4 s) {
                      __fadd_rn(acc.z, __fmul_rn(t, s.z)), __fadd_rn(acc.w, __fmul_rn(t, s.w)));
 }
 
-// Exact unpack tables: g_lut_c[q] = float(q) / 255.0f (unpack_color,
-// packing.hpp:63-66) and g_lut_n[q + 512] = float(q) / 511.0f
-// (decode_normal, packing.hpp:43-49), filled by the host with IEEE division.
-__device__ float g_lut_c[256];
-__device__ float g_lut_n[1024];
-
-__device__ __forceinline__ float lut_c(uint32_t w, int shift) {
-  return __ldg(&g_lut_c[(w >> shift) & 0xffu]);
-}
-__device__ __forceinline__ float lut_n(uint32_t w, int shift) {
-  int32_t q = (int32_t)(((w >> shift) & 0x3ffu) << 22) >> 22;
-  return __ldg(&g_lut_n[q + 512]);
+// normalize + Lambert + premultiply (shade_sample, shading.cpp:123-139) with
+// texture factor 1; mat = (base rgb, opacity).
+__device__ __forceinline__ float4 light_and_premultiply(const FrameConst& fc, float n[3],
+                                                        float4 color, float4 mat) {
+  // normalize (float), math.hpp:80-85
+  float len2 = __fadd_rn(__fadd_rn(__fmul_rn(n[0], n[0]), __fmul_rn(n[1], n[1])), __fmul_rn(n[2], n[2]));
+  if (len2 <= 0.0f) {
+    n[0] = n[1] = n[2] = 0.0f;
+  } else {
+    float il = __fdiv_rn(1.0f, __fsqrt_rn(len2));
+    n[0] = __fmul_rn(n[0], il);
+    n[1] = __fmul_rn(n[1], il);
+    n[2] = __fmul_rn(n[2], il);
+  }
+  float d = __fadd_rn(__fadd_rn(__fmul_rn(n[0], fc.light[0]), __fmul_rn(n[1], fc.light[1])),
+                      __fmul_rn(n[2], fc.light[2]));
+  float lam = smaxf(0.0f, -d);
+  float light = sminf(1.0f, __fadd_rn(fc.ambient, lam));
+  float r = __fmul_rn(__fmul_rn(__fmul_rn(mat.x, color.x), 1.0f), light);
+  float g = __fmul_rn(__fmul_rn(__fmul_rn(mat.y, color.y), 1.0f), light);
+  float b = __fmul_rn(__fmul_rn(__fmul_rn(mat.z, color.z), 1.0f), light);
+  float a = __fmul_rn(__fmul_rn(mat.w, color.w), 1.0f);
+  return make_float4(__fmul_rn(r, a), __fmul_rn(g, a), __fmul_rn(b, a), a);
 }
 
 // make_sample_context (shading.cpp:24-77) + shade_sample (123-139), no
@@ -759,6 +814,29 @@ __device__ __forceinline__ float4 shade_sample(const FrameConst& fc, const Buffe
   const float b0 = (float)__dmul_rn(e0, inv), b1 = (float)__dmul_rn(e1, inv),
               b2 = (float)__dmul_rn(e2, inv);
   *depth = eval(t.dz, x, y);
+  if (fc.decoded) {
+    const ShadeRec& sr = B.shade[tri];
+    const uint32_t fl = sr.flags;
+    float4 color = make_float4(1.0f, 1.0f, 1.0f, 1.0f);
+    if (fl & 1u) {
+      const float4 c0 = sr.c[0], c1 = sr.c[1], c2 = sr.c[2];
+      color.x = __fadd_rn(__fadd_rn(__fmul_rn(c0.x, b0), __fmul_rn(c1.x, b1)), __fmul_rn(c2.x, b2));
+      color.y = __fadd_rn(__fadd_rn(__fmul_rn(c0.y, b0), __fmul_rn(c1.y, b1)), __fmul_rn(c2.y, b2));
+      color.z = __fadd_rn(__fadd_rn(__fmul_rn(c0.z, b0), __fmul_rn(c1.z, b1)), __fmul_rn(c2.z, b2));
+      color.w = __fadd_rn(__fadd_rn(__fmul_rn(c0.w, b0), __fmul_rn(c1.w, b1)), __fmul_rn(c2.w, b2));
+    }
+    float n[3];
+    const float4 n0 = sr.n[0];
+    if (fl & 2u) {
+      const float4 n1 = sr.n[1], n2 = sr.n[2];
+      n[0] = __fadd_rn(__fadd_rn(__fmul_rn(n0.x, b0), __fmul_rn(n1.x, b1)), __fmul_rn(n2.x, b2));
+      n[1] = __fadd_rn(__fadd_rn(__fmul_rn(n0.y, b0), __fmul_rn(n1.y, b1)), __fmul_rn(n2.y, b2));
+      n[2] = __fadd_rn(__fadd_rn(__fmul_rn(n0.z, b0), __fmul_rn(n1.z, b1)), __fmul_rn(n2.z, b2));
+    } else {
+      n[0] = n0.x, n[1] = n0.y, n[2] = n0.z;
+    }
+    return light_and_premultiply(fc, n, color, sr.mat);
+  }
   const uint32_t q = tri >> 1;
   const uint32_t qf = __ldg(&B.vq_flags[q]);
   const int ltri = (int)(meta.w & 0xffu);
@@ -785,25 +863,53 @@ __device__ __forceinline__ float4 shade_sample(const FrameConst& fc, const Buffe
 #pragma unroll
     for (int k = 0; k < 3; ++k) n[k] = lut_n(meta.x, 10 * k);
   }
-  // normalize (float), math.hpp:80-85
-  float len2 = __fadd_rn(__fadd_rn(__fmul_rn(n[0], n[0]), __fmul_rn(n[1], n[1])), __fmul_rn(n[2], n[2]));
-  if (len2 <= 0.0f) {
-    n[0] = n[1] = n[2] = 0.0f;
-  } else {
-    float il = __fdiv_rn(1.0f, __fsqrt_rn(len2));
-    n[0] = __fmul_rn(n[0], il);
-    n[1] = __fmul_rn(n[1], il);
-    n[2] = __fmul_rn(n[2], il);
-  }
   const MatDev& m = B.mats[meta.y];
+  return light_and_premultiply(
+      fc, n, color, make_float4(__ldg(&m.base[0]), __ldg(&m.base[1]), __ldg(&m.base[2]), __ldg(&m.opacity)));
+}
+
+// Branch-free variant of shade_sample for the decoded-record path (selects
+// instead of branches) so two independent samples per lane can be
+// interleaved by the scheduler. Bit-identical to shade_sample.
+__device__ __forceinline__ float4 shade_decoded_bf(const FrameConst& fc, const Buffers& B,
+                                                   uint32_t tri, int px, int py, uint32_t* qd) {
+  const TriRec& t = B.tri[tri];
+  const ShadeRec& sr = B.shade[tri];
+  const double x = (double)px + 0.5, y = (double)py + 0.5;
+  const double e0 = eval(t.e[0], x, y), e1 = eval(t.e[1], x, y), e2 = eval(t.e[2], x, y);
+  const double sum = __dadd_rn(__dadd_rn(e0, e1), e2);
+  const double inv = __ddiv_rn(1.0, sum);
+  const float b0 = (float)__dmul_rn(e0, inv), b1 = (float)__dmul_rn(e1, inv),
+              b2 = (float)__dmul_rn(e2, inv);
+  *qd = quantize_depth(eval(t.dz, x, y));
+  const uint32_t fl = sr.flags;
+  const float4 c0 = sr.c[0], c1 = sr.c[1], c2 = sr.c[2];
+  const float4 n0 = sr.n[0], n1 = sr.n[1], n2 = sr.n[2];
+  const bool hc = fl & 1u, hn = fl & 2u;
+  float4 color;
+  color.x = hc ? __fadd_rn(__fadd_rn(__fmul_rn(c0.x, b0), __fmul_rn(c1.x, b1)), __fmul_rn(c2.x, b2)) : 1.0f;
+  color.y = hc ? __fadd_rn(__fadd_rn(__fmul_rn(c0.y, b0), __fmul_rn(c1.y, b1)), __fmul_rn(c2.y, b2)) : 1.0f;
+  color.z = hc ? __fadd_rn(__fadd_rn(__fmul_rn(c0.z, b0), __fmul_rn(c1.z, b1)), __fmul_rn(c2.z, b2)) : 1.0f;
+  color.w = hc ? __fadd_rn(__fadd_rn(__fmul_rn(c0.w, b0), __fmul_rn(c1.w, b1)), __fmul_rn(c2.w, b2)) : 1.0f;
+  float n[3];
+  n[0] = hn ? __fadd_rn(__fadd_rn(__fmul_rn(n0.x, b0), __fmul_rn(n1.x, b1)), __fmul_rn(n2.x, b2)) : n0.x;
+  n[1] = hn ? __fadd_rn(__fadd_rn(__fmul_rn(n0.y, b0), __fmul_rn(n1.y, b1)), __fmul_rn(n2.y, b2)) : n0.y;
+  n[2] = hn ? __fadd_rn(__fadd_rn(__fmul_rn(n0.z, b0), __fmul_rn(n1.z, b1)), __fmul_rn(n2.z, b2)) : n0.z;
+  float len2 = __fadd_rn(__fadd_rn(__fmul_rn(n[0], n[0]), __fmul_rn(n[1], n[1])), __fmul_rn(n[2], n[2]));
+  const bool pos = len2 > 0.0f;
+  const float il = __fdiv_rn(1.0f, __fsqrt_rn(pos ? len2 : 1.0f));
+  n[0] = pos ? __fmul_rn(n[0], il) : 0.0f;
+  n[1] = pos ? __fmul_rn(n[1], il) : 0.0f;
+  n[2] = pos ? __fmul_rn(n[2], il) : 0.0f;
+  const float4 mat = sr.mat;
   float d = __fadd_rn(__fadd_rn(__fmul_rn(n[0], fc.light[0]), __fmul_rn(n[1], fc.light[1])),
                       __fmul_rn(n[2], fc.light[2]));
   float lam = smaxf(0.0f, -d);
   float light = sminf(1.0f, __fadd_rn(fc.ambient, lam));
-  float r = __fmul_rn(__fmul_rn(__fmul_rn(__ldg(&m.base[0]), color.x), 1.0f), light);
-  float g = __fmul_rn(__fmul_rn(__fmul_rn(__ldg(&m.base[1]), color.y), 1.0f), light);
-  float b = __fmul_rn(__fmul_rn(__fmul_rn(__ldg(&m.base[2]), color.z), 1.0f), light);
-  float a = __fmul_rn(__fmul_rn(__ldg(&m.opacity), color.w), 1.0f);
+  float r = __fmul_rn(__fmul_rn(__fmul_rn(mat.x, color.x), 1.0f), light);
+  float g = __fmul_rn(__fmul_rn(__fmul_rn(mat.y, color.y), 1.0f), light);
+  float b = __fmul_rn(__fmul_rn(__fmul_rn(mat.z, color.z), 1.0f), light);
+  float a = __fmul_rn(__fmul_rn(mat.w, color.w), 1.0f);
   return make_float4(__fmul_rn(r, a), __fmul_rn(g, a), __fmul_rn(b, a), a);
 }
 
@@ -888,65 +994,93 @@ __device__ __forceinline__ uint32_t kth_pixel(uint32_t m, uint32_t k) {
 
 // Canonical-order shading of one half-block without the alpha threshold:
 // the sample stream (THBs in sorted order, then row-major) is cut into
-// 32-sample segments; lane s shades sample base+s, then each pixel's lane
-// takes its samples of the segment in stream order through a per-warp
-// routing table and pushes them into its register depth filter. Every
-// pixel therefore sees exactly the reference's per-pixel sequence.
+// 64-sample segments; lane s shades samples base+s and base+32+s (two
+// independent chains for ILP), then each pixel's lane takes its samples of
+// the segment in stream order through per-warp routing masks and pushes them
+// into its register depth filter. Every pixel therefore sees exactly the
+// reference's per-pixel sequence.
+__device__ __forceinline__ uint32_t find_thb(const uint32_t* pre_l, uint32_t lo, uint32_t hi,
+                                             uint32_t s) {
+  while (lo < hi) {  // largest r in [lo, hi] with pre[r] <= s
+    const uint32_t mid = (lo + hi + 1) >> 1;
+    if (pre_l[mid] <= s) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
 template <int KM>
-__device__ __forceinline__ void shade_segments(const FrameConst& fc, const Buffers& B, int px0, int py0,
-                               const uint32_t* tri_l, const uint32_t* mask_l,
-                               const uint32_t* pre_l, uint32_t n, uint32_t total,
-                               uint32_t* route, PixelOut& o) {
+__device__ __forceinline__ void blend_routed(const FrameConst& fc, RegFilter<KM>& f, PixelOut& o,
+                                             uint32_t mine, uint64_t key, float4 col) {
+  while (__any_sync(0xffffffffu, mine != 0u)) {
+    const int src = mine ? __ffs(mine) - 1 : (threadIdx.x & 31);
+    const uint64_t k2 = __shfl_sync(0xffffffffu, key, src);
+    float4 c2;
+    c2.x = __shfl_sync(0xffffffffu, col.x, src);
+    c2.y = __shfl_sync(0xffffffffu, col.y, src);
+    c2.z = __shfl_sync(0xffffffffu, col.z, src);
+    c2.w = __shfl_sync(0xffffffffu, col.w, src);
+    if (mine) {
+      mine &= mine - 1u;
+      uint64_t pk;
+      float4 pc;
+      bool ooo;
+      if (f.push(fc.df, k2, c2, &pk, &pc, &ooo)) commit(o, pk, pc, ooo);
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t route_mask(uint32_t* route, uint32_t pix, bool valid) {
+  const int lane = threadIdx.x & 31;
+  route[lane] = 0u;
+  __syncwarp();
+  const unsigned peers = __match_any_sync(0xffffffffu, pix);
+  if (valid && lane == __ffs(peers) - 1) route[pix] = peers;
+  __syncwarp();
+  const uint32_t mine = route[lane];
+  __syncwarp();
+  return mine;
+}
+
+template <int KM>
+__device__ __forceinline__ void shade_segments(const FrameConst& fc, const Buffers& B, int px0,
+                                               int py0, const uint32_t* tri_l,
+                                               const uint32_t* mask_l, const uint32_t* pre_l,
+                                               uint32_t n, uint32_t total, uint32_t* route,
+                                               PixelOut& o) {
   const int lane = threadIdx.x & 31;
   RegFilter<KM> f;
   f.reset();
   uint32_t r_lo = 0;
-  for (uint32_t base = 0; base < total; base += 32) {
-    const uint32_t s = base + lane;
-    const bool valid = s < total;
-    uint32_t pix = 32u + lane;
-    uint32_t r = r_lo;
-    float4 col = make_float4(0.f, 0.f, 0.f, 0.f);
-    uint64_t key = 0;
-    if (valid) {
-      // THB holding sample s: THB r_lo holds a sample < base and every THB
-      // holds >= 1 sample, so r <= r_lo + lane + 1
-      uint32_t lo = r_lo, hi = min(n - 1, r_lo + (uint32_t)lane + 1u);
-      while (lo < hi) {
-        uint32_t mid = (lo + hi + 1) >> 1;
-        if (pre_l[mid] <= s) lo = mid; else hi = mid - 1;
-      }
-      r = lo;
-      pix = kth_pixel(mask_l[r], s - pre_l[r]);
-      const uint32_t tri = tri_l[r];
-      double depth;
-      col = shade_sample(fc, B, tri, px0 + (int)(pix & 7u), py0 + (int)(pix >> 3), &depth);
-      key = sample_key(fc, quantize_depth(depth), tri);
+  for (uint32_t base = 0; base < total; base += 64) {
+    // THB r_lo holds a sample < base and every THB holds >= 1 sample, so
+    // sample base+j lies in a THB <= r_lo + j + 1.
+    const uint32_t s0 = base + lane, s1 = base + 32 + lane;
+    const bool v0 = s0 < total, v1 = s1 < total;
+    const uint32_t c0 = v0 ? s0 : total - 1, c1 = v1 ? s1 : total - 1;
+    const uint32_t r0 = find_thb(pre_l, r_lo, min(n - 1, r_lo + (uint32_t)lane + 1u), c0);
+    const uint32_t r1 = find_thb(pre_l, r0, min(n - 1, r_lo + (uint32_t)lane + 33u), c1);
+    const uint32_t p0 = kth_pixel(mask_l[r0], c0 - pre_l[r0]);
+    const uint32_t p1 = kth_pixel(mask_l[r1], c1 - pre_l[r1]);
+    const uint32_t t0 = tri_l[r0], t1 = tri_l[r1];
+    float4 col0, col1;
+    uint32_t q0, q1;
+    if (fc.decoded) {
+      col0 = shade_decoded_bf(fc, B, t0, px0 + (int)(p0 & 7u), py0 + (int)(p0 >> 3), &q0);
+      col1 = shade_decoded_bf(fc, B, t1, px0 + (int)(p1 & 7u), py0 + (int)(p1 >> 3), &q1);
+    } else {
+      double d0, d1;
+      col0 = shade_sample(fc, B, t0, px0 + (int)(p0 & 7u), py0 + (int)(p0 >> 3), &d0);
+      col1 = shade_sample(fc, B, t1, px0 + (int)(p1 & 7u), py0 + (int)(p1 >> 3), &d1);
+      q0 = quantize_depth(d0);
+      q1 = quantize_depth(d1);
     }
-    r_lo = __shfl_sync(0xffffffffu, r, 31);
-    // routing: route[p] = lanes (= stream positions) whose sample is pixel p
-    route[lane] = 0u;
-    __syncwarp();
-    const unsigned peers = __match_any_sync(0xffffffffu, pix);
-    if (valid && lane == __ffs(peers) - 1) route[pix] = peers;
-    __syncwarp();
-    uint32_t mine = route[lane];
-    __syncwarp();
-    while (__any_sync(0xffffffffu, mine != 0u)) {
-      const int src = mine ? __ffs(mine) - 1 : lane;
-      const uint64_t k2 = __shfl_sync(0xffffffffu, key, src);
-      float4 c2;
-      c2.x = __shfl_sync(0xffffffffu, col.x, src);
-      c2.y = __shfl_sync(0xffffffffu, col.y, src);
-      c2.z = __shfl_sync(0xffffffffu, col.z, src);
-      c2.w = __shfl_sync(0xffffffffu, col.w, src);
-      if (mine) {
-        mine &= mine - 1u;
-        uint64_t pk;
-        float4 pc;
-        bool ooo;
-        if (f.push(fc.df, k2, c2, &pk, &pc, &ooo)) commit(o, pk, pc, ooo);
-      }
+    const uint64_t key0 = sample_key(fc, q0, t0), key1 = sample_key(fc, q1, t1);
+    r_lo = __shfl_sync(0xffffffffu, r1, 31);
+    const uint32_t m0 = route_mask(route, v0 ? p0 : 32u + lane, v0);
+    blend_routed<KM>(fc, f, o, m0, key0, col0);
+    if (__any_sync(0xffffffffu, v1)) {
+      const uint32_t m1 = route_mask(route, v1 ? p1 : 32u + lane, v1);
+      blend_routed<KM>(fc, f, o, m1, key1, col1);
     }
   }
   while (f.n > 0) {
@@ -1571,7 +1705,7 @@ struct DeviceScene {
   uint64_t uploaded_version = 0;
   uint32_t nverts = 0, nquads = 0;
   DevBuf pos, vcol, vnrm, quads, qmat, mats;
-  DevBuf block_cnt, block_off, vq_src, vq_box, vq_flags, vq_mat, vq_col, vq_nrm, tri, tri_meta;
+  DevBuf block_cnt, block_off, vq_src, vq_box, vq_flags, vq_mat, vq_col, vq_nrm, tri, tri_meta, shade;
   DevBuf qcnt, tcnt, off, qcur, tcur, cat, prop, items, slots, spill0, spill1, scratch, fb, mask,
       hash, emit, thb_cnt, thb_off, thb_out, thb_tri, thb_pre, ctr, tile_ids;
   uint32_t items_cap = 0;
@@ -1872,6 +2006,11 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   d->vq_nrm.ensure(size_t(Q) * 16);
   d->tri.ensure(size_t(Q) * 2 * sizeof(dev::TriRec));
   d->tri_meta.ensure(size_t(Q) * 2 * 16);
+  // Decoded shading records pay off when triangles cover many pixels (each
+  // record is read by every sample of its triangle): >= 8 px per quad at
+  // depth complexity 1.
+  fc.decoded = (double)cam.width * cam.height >= 8.0 * std::max<double>(1.0, Q) ? 1 : 0;
+  if (fc.decoded) d->shade.ensure(size_t(Q) * 2 * sizeof(dev::ShadeRec));
   d->qcnt.ensure(nb * 4);
   d->tcnt.ensure(nb * 4);
   d->off.ensure(nb * 4);
@@ -1927,6 +2066,7 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   B.vq_nrm = d->vq_nrm.as<uint4>();
   B.tri = d->tri.as<dev::TriRec>();
   B.tri_meta = d->tri_meta.as<uint4>();
+  B.shade = fc.decoded ? d->shade.as<dev::ShadeRec>() : nullptr;
   B.qcnt = d->qcnt.as<uint32_t>();
   B.tcnt = d->tcnt.as<uint32_t>();
   B.off = d->off.as<uint32_t>();
