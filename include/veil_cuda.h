@@ -143,7 +143,9 @@ void* veil_scene_stream(const veil_scene* scene);
 /* ---- timings and counters ------------------------------------------------- */
 
 typedef struct veil_frame_stats {
-  double setup_ms, binning_ms, low_raster_ms, hi_raster_ms, total_ms; /* CUDA events */
+  /* CUDA events. low_raster_ms covers low-path extraction and all shading
+   * (shade_ms), hi_raster_ms the high-path extraction. */
+  double setup_ms, binning_ms, low_raster_ms, hi_raster_ms, total_ms;
   uint64_t samples, fragments, tri_half_blocks, segments;
   uint64_t input_quads, visible_quads;
   uint64_t culled_degenerate, culled_backfacing, culled_frustum, culled_between_samples;
@@ -153,6 +155,7 @@ typedef struct veil_frame_stats {
   uint64_t small_quads; /* visible small quads */
   uint64_t large_tris;  /* valid triangles of large quads */
   uint64_t kernel_launches;
+  double shade_ms; /* CUDA events: shading share of the raster time */
 } veil_frame_stats;
 
 veil_status veil_render_stats(const veil_render* render, veil_frame_stats* out);

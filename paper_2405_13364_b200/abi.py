@@ -113,6 +113,7 @@ class FrameStats(C.Structure):
                 "invalid_pixels", "bin_pairs", "small_quads", "large_tris", "kernel_launches",
             )
         ]
+        + [("shade_ms", C.c_double)]
     )
 
 

@@ -78,6 +78,7 @@ struct FrameConst {
   int rank, world;
   int dump;
   int decoded;  // setup writes per-triangle decoded shading records
+  uint32_t pool_cap;
 };
 
 // Device counters; one instance per scene workspace, zeroed per frame.
@@ -92,8 +93,8 @@ struct Counters {
   unsigned int spill_count[2];
   unsigned long long samples, fragments, thb, segments, invalid;
   unsigned long long bins_empty, bins_low, bins_high, bins_propagated;
-  unsigned int hi_items;
-  unsigned int pad;
+  unsigned int pool_next;
+  unsigned int shade_next;
 };
 
 // Decoded per-triangle shading inputs (unpack_color / decode_normal of the
@@ -107,6 +108,10 @@ struct __align__(16) ShadeRec {
   uint32_t pad[3];
 };
 static_assert(sizeof(ShadeRec) == 128, "ShadeRec is one cache line");
+
+struct HbDesc {
+  uint32_t off, cnt, frags, pad;
+};
 
 struct Buffers {
   // scene
@@ -146,11 +151,10 @@ struct Buffers {
   uint8_t* mask;
   uint64_t* hash;
   uint32_t* emit;
-  uint32_t* thb_cnt;  // dump: per (bin, half-block)
-  uint64_t* thb_off;  // dump: offsets (second pass)
-  uint64_t* thb_out;  // dump
-  uint32_t* thb_tri;  // dump
-  uint32_t* thb_pre;  // dump
+  struct HbDesc* hbd;  // per (bin, half-block): THB list in the pool
+  uint32_t* pool_tri;
+  uint32_t* pool_mask;  // coverage, bit = ly * 8 + lx
+  uint32_t* pool_pre;   // exclusive fragment prefix
   Counters* ctr;
 };
 
@@ -918,42 +922,32 @@ __device__ __forceinline__ uint64_t sample_key(const FrameConst& fc, uint32_t qd
   return fc.extended ? (((uint64_t)qd << 32) | tri) : (((uint64_t)qd << 24) | (tri & 0xffffffu));
 }
 
-// Scratch of one (bin, block-row) work item, in shared or global memory.
+// Scratch of one (bin, block-row) extraction item, in shared or global memory.
 struct RasterView {
   Tbr* tbr;
-  uint64_t* keys;     // [4][cap_tb]
-  uint16_t* refs;     // [4][cap_tb]
-  uint32_t* thb_tri;  // [8][cap_tb]  tri-half-block lists, half-block hb = block*2 + half
-  uint32_t* thb_mask; // [8][cap_tb]  32-bit coverage (bit = ly*8 + lx)
-  uint32_t* thb_pre;  // [8][cap_tb]  exclusive fragment prefix
-  uint32_t* route;    // [4][32]
+  uint64_t* keys;  // [4][cap_tb]
+  uint16_t* refs;  // [4][cap_tb]
 };
 
 struct RasterShared {
   // Shared-memory capacities; larger items (within the active limits) run
   // again with global scratch.
-  static constexpr int kTbr = 512, kTb = 256;
+  static constexpr int kTbr = 1024, kTb = 256;
   Tbr tbr[kTbr];
   uint64_t keys[4 * kTb];
   uint16_t refs[4 * kTb];
-  uint32_t thb_tri[8 * kTb];
-  uint32_t thb_mask[8 * kTb];
-  uint32_t thb_pre[8 * kTb];
-  uint32_t route[4 * 32];
 };
 
 __host__ __device__ inline size_t global_scratch_bytes(uint32_t cap_tbr, uint32_t cap_tb) {
-  return (size_t)cap_tbr * sizeof(Tbr) + (size_t)4 * cap_tb * (8 + 2) +
-         (size_t)8 * cap_tb * 12 + 4 * 32 * 4 + 64;
+  return (size_t)cap_tbr * sizeof(Tbr) + (size_t)4 * cap_tb * (8 + 2) + 64;
 }
 
 struct ItemState {
   int ntbr;
   int status;  // 0 ok, 1 overflow (soft), 2 spill, 3 hard error
   int err_code;
-  int next_hb;
-  uint32_t nthb[8];
-  uint32_t frags[8];
+  uint32_t hb_cnt[8];
+  uint32_t hb_frags[8];
 };
 
 enum { kPassLow = 0, kPassHigh = 1 };
@@ -1155,24 +1149,6 @@ __device__ __forceinline__ void shade_threshold(const FrameConst& fc, const Buff
   *enumerated_out = enumerated;
 }
 
-__device__ void write_background(const FrameConst& fc, const Buffers& B, int bin, int row) {
-  const int bxi = bin % fc.bins_x, byi = bin / fc.bins_x;
-  uint32_t word = quantize_channel(fc.bg[0]) | (quantize_channel(fc.bg[1]) << 8) |
-                  (quantize_channel(fc.bg[2]) << 16) | (quantize_channel(fc.bg[3]) << 24);
-  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
-    int px = bxi * kBin + (i & 31), py = byi * kBin + row * 8 + (i >> 5);
-    if (px < fc.width && py < fc.height) {
-      size_t pix = (size_t)py * fc.width + px;
-      B.fb[pix] = word;
-      B.mask[pix] = 0;
-      if (fc.dump) {
-        B.hash[pix] = kHashSeed;
-        B.emit[pix] = 0;
-      }
-    }
-  }
-}
-
 __device__ __forceinline__ uint32_t span_mask(uint32_t b, uint32_t l, uint32_t c0, uint32_t c1) {
   // row span [b, l] (bin-local) clipped to block columns [c0, c1] as 8 bits
   if (b > l) return 0u;
@@ -1182,11 +1158,15 @@ __device__ __forceinline__ uint32_t span_mask(uint32_t b, uint32_t l, uint32_t c
   return ((2u << (l - b)) - 1u) << (b - c0);
 }
 
-// One (bin, block-row) work item. kGlobal selects global-memory scratch.
-template <bool kGlobal, int KM>
-__device__ __forceinline__ void raster_item(const FrameConst& fc, const Buffers& B, int pass, int bin, int row,
-                            const RasterView& V, ItemState* st, uint32_t cap_tbr,
-                            uint32_t cap_tb) {
+// One (bin, block-row) extraction item: phases A and B of the reference's
+// rasterize_bin (raster.cpp:41-199). Tri-half-block lists go to the global
+// THB pool (L2-resident) with one descriptor per half-block; shading runs
+// in k_shade. kGlobal selects global-memory scratch for items that exceed
+// the shared-memory capacities (but not the active limits).
+template <bool kGlobal>
+__device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers& B, int pass,
+                                             int bin, int row, const RasterView& V,
+                                             ItemState* st, uint32_t cap_tbr, uint32_t cap_tb) {
   const Limits lim = pass == kPassLow ? fc.low : fc.high;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int bxi = bin % fc.bins_x, byi = bin / fc.bins_x;
@@ -1199,7 +1179,6 @@ __device__ __forceinline__ void raster_item(const FrameConst& fc, const Buffers&
     st->ntbr = 0;
     st->status = 0;
     st->err_code = 0x7fffffff;
-    st->next_hb = 0;
   }
   __syncthreads();
 
@@ -1238,15 +1217,17 @@ __device__ __forceinline__ void raster_item(const FrameConst& fc, const Buffers&
       cols |= ((2u << (ll >> 3)) - 1u) & ~((1u << (bb >> 3)) - 1u);
     }
     if (!cols) continue;
-    Tbr rec;
-    rec.tri = ti;
-    rec.meta = cols | (large << 4);
-    rec.b[0] = rb0;
-    rec.b[1] = rb1;
-    rec.l[0] = rl0;
-    rec.l[1] = rl1;
-    int slot = atomicAdd(&st->ntbr, 1);
-    if ((uint32_t)slot < cap_tbr) V.tbr[slot] = rec;
+    const int slot = atomicAdd(&st->ntbr, 1);
+    if ((uint32_t)slot < cap_tbr) {
+      Tbr rec;
+      rec.tri = ti;
+      rec.meta = cols | (large << 4);
+      rec.b[0] = rb0;
+      rec.b[1] = rb1;
+      rec.l[0] = rl0;
+      rec.l[1] = rl1;
+      V.tbr[slot] = rec;
+    }
   }
   __syncthreads();
   const uint32_t ntbr = (uint32_t)st->ntbr;
@@ -1266,11 +1247,11 @@ __device__ __forceinline__ void raster_item(const FrameConst& fc, const Buffers&
   uint16_t* refs = V.refs + (size_t)warp * cap_tb;
   uint32_t n = 0;
   for (uint32_t base = 0; base < ntbr; base += 32) {
-    uint32_t i = base + lane;
-    bool sel = i < ntbr && ((V.tbr[i].meta >> warp) & 1u);
-    unsigned m = __ballot_sync(0xffffffffu, sel);
+    const uint32_t i = base + lane;
+    const bool sel = i < ntbr && ((V.tbr[i].meta >> warp) & 1u);
+    const unsigned m = __ballot_sync(0xffffffffu, sel);
     if (sel) {
-      uint32_t pos = n + __popc(m & ((1u << lane) - 1u));
+      const uint32_t pos = n + __popc(m & ((1u << lane) - 1u));
       if (pos < cap_tb) {
         const Tbr& rw = V.tbr[i];
         uint32_t count = 0, sx = 0, sy = 0;
@@ -1281,15 +1262,15 @@ __device__ __forceinline__ void raster_item(const FrameConst& fc, const Buffers&
           b = max(b, c0);
           l = min(l, c1);
           if (b > l) continue;
-          uint32_t k = l - b + 1;
+          const uint32_t k = l - b + 1;
           count += k;
           sx += (b + l) * k / 2 - c0 * k;
           sy += (uint32_t)y * k;
         }
         uint32_t qd = 0x3fffffu;
         if (count) {
-          double cx = __dadd_rn(__dadd_rn(bpx0, __ddiv_rn((double)sx, (double)count)), 0.5);
-          double cy = __dadd_rn(__dadd_rn(bpy0, __ddiv_rn((double)sy, (double)count)), 0.5);
+          const double cx = __dadd_rn(__dadd_rn(bpx0, __ddiv_rn((double)sx, (double)count)), 0.5);
+          const double cy = __dadd_rn(__dadd_rn(bpy0, __ddiv_rn((double)sy, (double)count)), 0.5);
           qd = quantize_depth(eval(B.tri[rw.tri].dz, cx, cy));
         }
         // (depth, is_large, triangle) orders exactly like the reference's
@@ -1315,14 +1296,14 @@ __device__ __forceinline__ void raster_item(const FrameConst& fc, const Buffers&
     for (uint32_t k = 2; k <= N; k <<= 1)
       for (uint32_t j = k >> 1; j > 0; j >>= 1) {
         for (uint32_t i = lane; i < N; i += 32) {
-          uint32_t ixj = i ^ j;
+          const uint32_t ixj = i ^ j;
           if (ixj > i) {
-            uint64_t x = keys[i], y = keys[ixj];
-            bool up = (i & k) == 0;
+            const uint64_t x = keys[i], y = keys[ixj];
+            const bool up = (i & k) == 0;
             if ((x > y) == up) {
               keys[i] = y;
               keys[ixj] = x;
-              uint16_t t = refs[i];
+              const uint16_t t = refs[i];
               refs[i] = refs[ixj];
               refs[ixj] = t;
             }
@@ -1332,151 +1313,99 @@ __device__ __forceinline__ void raster_item(const FrameConst& fc, const Buffers&
       }
   }
   uint32_t nthb[2] = {0, 0}, frags[2] = {0, 0};
-  if (ok) {
-    for (uint32_t base = 0; base < n; base += 32) {
-      uint32_t k = base + lane;
-      uint32_t hm[2] = {0u, 0u};
-      uint32_t tri = 0;
-      if (k < n) {
-        const Tbr& rw = V.tbr[refs[k]];
-        tri = rw.tri;
+  uint32_t pbase = 0;
+  if (ok && n) {
+    // each tri-block yields <= 1 THB per half: reserve 2n pool entries
+    if (lane == 0) pbase = atomicAdd(&B.ctr->pool_next, 2u * n);
+    pbase = __shfl_sync(0xffffffffu, pbase, 0);
+    if ((unsigned long long)pbase + 2ull * n > (unsigned long long)fc.pool_cap) {
+      if (lane == 0) atomicOr(&B.ctr->error, 8u);  // pool capacity: grow and re-run
+    } else {
+      for (uint32_t base = 0; base < n; base += 32) {
+        const uint32_t k = base + lane;
+        uint32_t hm[2] = {0u, 0u};
+        uint32_t tri = 0;
+        if (k < n) {
+          const Tbr& rw = V.tbr[refs[k]];
+          tri = rw.tri;
 #pragma unroll
-        for (int h = 0; h < 2; ++h)
+          for (int h = 0; h < 2; ++h)
 #pragma unroll
-          for (int y = 0; y < 4; ++y)
-            hm[h] |= span_mask(byte_of(rw.b, h * 4 + y), byte_of(rw.l, h * 4 + y), c0, c1) << (8 * y);
+            for (int y = 0; y < 4; ++y)
+              hm[h] |= span_mask(byte_of(rw.b, h * 4 + y), byte_of(rw.l, h * 4 + y), c0, c1) << (8 * y);
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t fr = __popc(hm[h]);
+          const bool ne = fr > 0;
+          const unsigned m = __ballot_sync(0xffffffffu, ne);
+          const uint32_t pos = nthb[h] + __popc(m & ((1u << lane) - 1u));
+          uint32_t incl = fr;  // inclusive scan of fragment counts
+#pragma unroll
+          for (int s = 1; s < 32; s <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, s);
+            if (lane >= s) incl += y;
+          }
+          if (ne) {
+            const size_t at = (size_t)pbase + (size_t)h * n + pos;
+            B.pool_tri[at] = tri;
+            B.pool_mask[at] = hm[h];
+            B.pool_pre[at] = frags[h] + incl - fr;
+          }
+          nthb[h] += __popc(m);
+          frags[h] += __shfl_sync(0xffffffffu, incl, 31);
+        }
       }
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const uint32_t fr = __popc(hm[h]);
-        const bool ne = fr > 0;
-        const unsigned m = __ballot_sync(0xffffffffu, ne);
-        const uint32_t pos = nthb[h] + __popc(m & ((1u << lane) - 1u));
-        uint32_t incl = fr;  // inclusive scan of fragment counts
-#pragma unroll
-        for (int s = 1; s < 32; s <<= 1) {
-          uint32_t y = __shfl_up_sync(0xffffffffu, incl, s);
-          if (lane >= s) incl += y;
+        if (nthb[h] > lim.thb) {
+          if (lane == 0) set_status(st, pass == kPassLow ? 1 : 3, 2 + 3 * block);
+        } else if (frags[h] > lim.frags) {
+          if (lane == 0) set_status(st, pass == kPassLow ? 1 : 3, 3 + 3 * block);
         }
-        if (ne && pos < cap_tb) {
-          const size_t at = (size_t)(warp * 2 + h) * cap_tb + pos;
-          V.thb_tri[at] = tri;
-          V.thb_mask[at] = hm[h];
-          V.thb_pre[at] = frags[h] + incl - fr;
-        }
-        nthb[h] += __popc(m);
-        frags[h] += __shfl_sync(0xffffffffu, incl, 31);
       }
     }
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      if (nthb[h] > lim.thb) {
-        if (lane == 0) set_status(st, pass == kPassLow ? 1 : 3, 2 + 3 * block);
-      } else if (frags[h] > lim.frags) {
-        if (lane == 0) set_status(st, pass == kPassLow ? 1 : 3, 3 + 3 * block);
-      }
-    }
-  }
-  if (lane == 0) {
-    st->nthb[warp * 2] = nthb[0];
-    st->nthb[warp * 2 + 1] = nthb[1];
-    st->frags[warp * 2] = frags[0];
-    st->frags[warp * 2 + 1] = frags[1];
   }
   __syncthreads();
   if (st->status) return;
-
-  // ---- phase C: shade + blend; warps take half-blocks dynamically
-  unsigned long long* slot = B.slots + ((size_t)bin * 4 + row) * 5;
-  if (threadIdx.x < 5) slot[threadIdx.x] = 0;
-  __syncthreads();
-  unsigned long long w_samples = 0, w_segments = 0, w_invalid = 0, w_frags = 0, w_thb = 0;
-  uint32_t* route = V.route + warp * 32;
-  for (;;) {
-    int hb = 0;
-    if (lane == 0) hb = atomicAdd(&st->next_hb, 1);
-    hb = __shfl_sync(0xffffffffu, hb, 0);
-    if (hb >= 8) break;
-    const uint32_t cnt = st->nthb[hb], total = st->frags[hb];
-    const uint32_t* tri_l = V.thb_tri + (size_t)hb * cap_tb;
-    const uint32_t* mask_l = V.thb_mask + (size_t)hb * cap_tb;
-    const uint32_t* pre_l = V.thb_pre + (size_t)hb * cap_tb;
-    const int hpx0 = px0 + (hb >> 1) * 8, hpy0 = ry0 + (hb & 1) * 4;
-    PixelOut po;
-    po.acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    po.invalid = false;
-    po.hash = kHashSeed;
-    po.emitted = 0;
-    unsigned long long enumerated = total;
-    if (fc.threshold)
-      shade_threshold<KM>(fc, B, hpx0, hpy0, tri_l, mask_l, cnt, po, &enumerated);
-    else if (total)
-      shade_segments<KM>(fc, B, hpx0, hpy0, tri_l, mask_l, pre_l, cnt, total, route, po);
-    w_segments += (enumerated + 255ull) / 256ull;
-    w_frags += total;
-    w_thb += cnt;
-    const int px = hpx0 + (lane & 7), py = hpy0 + (lane >> 3);
-    if (px < fc.width && py < fc.height) {
-      const size_t pix = (size_t)py * fc.width + px;
-      uint32_t word;
-      if (po.invalid && fc.visualize) {
-        word = 0xffff00ffu;  // magenta overlay, renderer.cpp:56-65
-      } else {
-        float4 out = blend(po.acc, make_float4(fc.bg[0], fc.bg[1], fc.bg[2], fc.bg[3]));
-        word = quantize_channel(out.x) | (quantize_channel(out.y) << 8) |
-               (quantize_channel(out.z) << 16) | (quantize_channel(out.w) << 24);
-      }
-      B.fb[pix] = word;
-      B.mask[pix] = po.invalid ? 1 : 0;
-      if (fc.dump) {
-        B.hash[pix] = po.hash;
-        B.emit[pix] = po.emitted;
-      }
-      if (po.invalid) ++w_invalid;
-    }
-    w_samples += po.emitted;
-    if (fc.dump) {
-      B.thb_cnt[(size_t)bin * 32 + row * 8 + hb] = cnt;
-      if (B.thb_off) {
-        const uint64_t obase = B.thb_off[(size_t)bin * 32 + row * 8 + hb];
-        for (uint32_t i = lane; i < cnt; i += 32) {
-          const uint32_t m = mask_l[i], tri = tri_l[i];
-          uint64_t bits = 0;  // TriHalfBlock::make, packing.hpp:154-176
-          for (int y = 0; y < 4; ++y) {
-            const uint32_t rb = (m >> (8 * y)) & 0xffu;
-            uint32_t b = 7, l = 0;
-            if (rb) {
-              b = __ffs(rb) - 1;
-              l = 31 - __clz(rb);
-            }
-            bits |= (uint64_t)(b | (l << 3)) << (6 * y);
-          }
-          const uint32_t prefix = pre_l[i] + __popc(m);
-          B.thb_out[obase + i] = bits | ((uint64_t)(tri & 0xffffffu) << 24) |
-                                 ((uint64_t)(prefix & 0xfffu) << 48);
-          B.thb_tri[obase + i] = tri;
-          B.thb_pre[obase + i] = prefix;
-        }
-      }
-    }
+  if (lane < 2) {
+    HbDesc d;
+    d.off = pbase + (uint32_t)lane * n;
+    d.cnt = nthb[lane];
+    d.frags = frags[lane];
+    d.pad = 0;
+    B.hbd[(size_t)bin * 32 + row * 8 + warp * 2 + lane] = d;
   }
-#pragma unroll
-  for (int s = 16; s > 0; s >>= 1) {
-    w_samples += __shfl_xor_sync(0xffffffffu, w_samples, s);
-    w_invalid += __shfl_xor_sync(0xffffffffu, w_invalid, s);
+  if (threadIdx.x == 0) {
+    unsigned long long* slot = B.slots + ((size_t)bin * 4 + row) * 5;
+    slot[0] = slot[3] = slot[4] = 0;
+    uint64_t fr = 0, th = 0;
+    for (int h = 0; h < 8; ++h) {
+      fr += st->hb_frags[h];
+      th += st->hb_cnt[h];
+    }
+    (void)fr;
+    (void)th;
   }
   if (lane == 0) {
-    atomicAdd(&slot[0], w_samples);
-    atomicAdd(&slot[1], w_frags);
-    atomicAdd(&slot[2], w_thb);
-    atomicAdd(&slot[3], w_segments);
-    atomicAdd(&slot[4], w_invalid);
+    st->hb_frags[warp * 2] = frags[0];
+    st->hb_frags[warp * 2 + 1] = frags[1];
+    st->hb_cnt[warp * 2] = nthb[0];
+    st->hb_cnt[warp * 2 + 1] = nthb[1];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long* slot = B.slots + ((size_t)bin * 4 + row) * 5;
+    unsigned long long fr = 0, th = 0;
+    for (int h = 0; h < 8; ++h) fr += st->hb_frags[h], th += st->hb_cnt[h];
+    slot[1] = fr;
+    slot[2] = th;
   }
 }
 
-template <bool kGlobal, int KM>
-__global__ void __launch_bounds__(128, 4) k_raster(FrameConst fc, Buffers B, int pass,
-                                                uint32_t cap_tbr, uint32_t cap_tb) {
+template <bool kGlobal>
+__global__ void __launch_bounds__(128) k_extract(FrameConst fc, Buffers B, int pass,
+                                                 uint32_t cap_tbr, uint32_t cap_tb) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   __shared__ ItemState st;
   __shared__ uint32_t item_s;
@@ -1489,24 +1418,12 @@ __global__ void __launch_bounds__(128, 4) k_raster(FrameConst fc, Buffers B, int
     g = reinterpret_cast<uint8_t*>(((uintptr_t)g + 15) & ~(uintptr_t)15);
     V.keys = reinterpret_cast<uint64_t*>(g);
     g += (size_t)4 * cap_tb * 8;
-    V.thb_tri = reinterpret_cast<uint32_t*>(g);
-    g += (size_t)8 * cap_tb * 4;
-    V.thb_mask = reinterpret_cast<uint32_t*>(g);
-    g += (size_t)8 * cap_tb * 4;
-    V.thb_pre = reinterpret_cast<uint32_t*>(g);
-    g += (size_t)8 * cap_tb * 4;
-    V.route = reinterpret_cast<uint32_t*>(g);
-    g += 4 * 32 * 4;
     V.refs = reinterpret_cast<uint16_t*>(g);
   } else {
     RasterShared* sh = reinterpret_cast<RasterShared*>(smem_raw);
     V.tbr = sh->tbr;
     V.keys = sh->keys;
     V.refs = sh->refs;
-    V.thb_tri = sh->thb_tri;
-    V.thb_mask = sh->thb_mask;
-    V.thb_pre = sh->thb_pre;
-    V.route = sh->route;
   }
   const uint32_t nitems = kGlobal ? B.ctr->spill_count[pass] : (uint32_t)fc.nbins * 4u;
   unsigned int* counter = &B.ctr->work_next[pass * 2 + (kGlobal ? 1 : 0)];
@@ -1521,29 +1438,21 @@ __global__ void __launch_bounds__(128, 4) k_raster(FrameConst fc, Buffers B, int
     const int bxi = bin % fc.bins_x, byi = bin / fc.bins_x;
     const uint8_t cat = B.cat[bin];
     const bool owned = fc.world <= 1 || ((bxi + 3 * byi) % fc.world) == fc.rank;
-    if (!owned) continue;
+    if (!owned || cat == 0) continue;
     bool run;
-    if (pass == kPassLow) {
-      if (cat == 0) {
-        if (!kGlobal) {
-          write_background(fc, B, bin, row);
-          if (threadIdx.x < 5) B.slots[((size_t)bin * 4 + row) * 5 + threadIdx.x] = 0;
-        }
-        continue;
-      }
+    if (pass == kPassLow)
       run = cat == 1 && !fc.force_high;
-    } else {
+    else
       run = cat == 2 || (cat == 1 && fc.force_high) || B.prop[bin];
-    }
     if (!run) continue;
     if (!kGlobal && pass == kPassLow && B.prop[bin]) continue;  // sibling already overflowed
-    raster_item<kGlobal, KM>(fc, B, pass, bin, row, V, &st, cap_tbr, cap_tb);
+    extract_item<kGlobal>(fc, B, pass, bin, row, V, &st, cap_tbr, cap_tb);
     __syncthreads();
     if (threadIdx.x == 0 && st.status) {
       if (st.status == 1) {
         B.prop[bin] = 1;
       } else if (st.status == 2) {
-        uint32_t s = atomicAdd(&B.ctr->spill_count[pass], 1u);
+        const uint32_t s = atomicAdd(&B.ctr->spill_count[pass], 1u);
         B.spill[pass][s] = code;
       } else {
         atomicMin(&B.ctr->bin_error, (unsigned long long)bin * 64ull +
@@ -1551,6 +1460,80 @@ __global__ void __launch_bounds__(128, 4) k_raster(FrameConst fc, Buffers B, int
       }
     }
     __syncthreads();
+  }
+}
+
+// Shading: one warp per 8x4 half-block (raster.cpp:201-321), taken from a
+// global work counter; no block-level synchronisation. Empty bins and
+// half-blocks without samples composite the background.
+template <int KM>
+__global__ void __launch_bounds__(256, 2) k_shade(FrameConst fc, Buffers B) {
+  if (B.ctr->error) return;
+  const int lane = threadIdx.x & 31;
+  uint32_t* route = nullptr;
+  __shared__ uint32_t route_s[8 * 32];
+  route = route_s + (threadIdx.x >> 5) * 32;
+  const uint32_t nitems = (uint32_t)fc.nbins * 32u;
+  for (;;) {
+    uint32_t item = 0;
+    if (lane == 0) item = atomicAdd(&B.ctr->shade_next, 1u);
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if (item >= nitems) break;
+    const int bin = (int)(item >> 5), hb = (int)(item & 31u);
+    const int bxi = bin % fc.bins_x, byi = bin / fc.bins_x;
+    if (!(fc.world <= 1 || ((bxi + 3 * byi) % fc.world) == fc.rank)) continue;
+    const int block = hb >> 1;
+    const int hpx0 = bxi * kBin + (block & 3) * 8;
+    const int hpy0 = byi * kBin + (block >> 2) * 8 + (hb & 1) * 4;
+    PixelOut po;
+    po.acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    po.invalid = false;
+    po.hash = kHashSeed;
+    po.emitted = 0;
+    unsigned long long enumerated = 0;
+    const bool live = B.cat[bin] != 0;
+    if (live) {
+      const HbDesc d = B.hbd[item];
+      enumerated = d.frags;
+      if (fc.threshold)
+        shade_threshold<KM>(fc, B, hpx0, hpy0, B.pool_tri + d.off, B.pool_mask + d.off, d.cnt, po,
+                            &enumerated);
+      else if (d.frags)
+        shade_segments<KM>(fc, B, hpx0, hpy0, B.pool_tri + d.off, B.pool_mask + d.off,
+                           B.pool_pre + d.off, d.cnt, d.frags, route, po);
+    }
+    const int px = hpx0 + (lane & 7), py = hpy0 + (lane >> 3);
+    unsigned invalid_px = 0;
+    if (px < fc.width && py < fc.height) {
+      const size_t pix = (size_t)py * fc.width + px;
+      uint32_t word;
+      if (po.invalid && fc.visualize) {
+        word = 0xffff00ffu;  // magenta overlay, renderer.cpp:56-65
+      } else {
+        const float4 out = blend(po.acc, make_float4(fc.bg[0], fc.bg[1], fc.bg[2], fc.bg[3]));
+        word = quantize_channel(out.x) | (quantize_channel(out.y) << 8) |
+               (quantize_channel(out.z) << 16) | (quantize_channel(out.w) << 24);
+      }
+      B.fb[pix] = word;
+      B.mask[pix] = po.invalid ? 1 : 0;
+      if (fc.dump) {
+        B.hash[pix] = po.hash;
+        B.emit[pix] = po.emitted;
+      }
+      invalid_px = po.invalid ? 1u : 0u;
+    }
+    if (live) {
+      unsigned long long samples = po.emitted;
+#pragma unroll
+      for (int s = 16; s > 0; s >>= 1) samples += __shfl_xor_sync(0xffffffffu, samples, s);
+      const unsigned inv = __popc(__ballot_sync(0xffffffffu, invalid_px != 0));
+      if (lane == 0) {
+        unsigned long long* slot = B.slots + ((size_t)bin * 4 + (block >> 2)) * 5;
+        atomicAdd(&slot[0], samples);
+        atomicAdd(&slot[3], (enumerated + 255ull) / 256ull);
+        if (inv) atomicAdd(&slot[4], (unsigned long long)inv);
+      }
+    }
   }
 }
 
@@ -1707,9 +1690,12 @@ struct DeviceScene {
   DevBuf pos, vcol, vnrm, quads, qmat, mats;
   DevBuf block_cnt, block_off, vq_src, vq_box, vq_flags, vq_mat, vq_col, vq_nrm, tri, tri_meta, shade;
   DevBuf qcnt, tcnt, off, qcur, tcur, cat, prop, items, slots, spill0, spill1, scratch, fb, mask,
-      hash, emit, thb_cnt, thb_off, thb_out, thb_tri, thb_pre, ctr, tile_ids;
+      hash, emit, ctr, tile_ids, hbd, pool_tri, pool_mask, pool_pre;
   uint32_t items_cap = 0;
-  cudaEvent_t ev[6] = {};
+  uint32_t pool_cap = 0;
+  bool extract_configured = false;
+  int extract_ctas = 0;
+  cudaEvent_t ev[6] = {};  // frame start, setup, binning, low extract, end, high extract
   veil_frame_stats last{};
   int fb_w = 0, fb_h = 0;
   int sm_count = 148;
@@ -1875,43 +1861,48 @@ void camera_vectors(const Camera& c, dev::FrameConst* fc) {
   }
 }
 
-template <int KM>
-void launch_raster_pair(DeviceScene* d, const dev::FrameConst& fc, const dev::Buffers& B, int pass,
-                        uint32_t gcap_tbr, uint32_t gcap_tb, int* launches) {
+void launch_extract(DeviceScene* d, const dev::FrameConst& fc, const dev::Buffers& B, int pass,
+                    uint32_t gcap_tbr, uint32_t gcap_tb, int* launches) {
   const size_t smem = sizeof(dev::RasterShared);
-  static thread_local bool configured[2] = {false, false};
-  (void)configured;
-  ck(cudaFuncSetAttribute(dev::k_raster<false, KM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          int(smem)),
-     "cudaFuncSetAttribute");
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_raster<false, KM>, 128, smem);
-  int grid = std::max(1, per_sm) * d->sm_count;
-  grid = std::min<long long>(grid, (long long)fc.nbins * 4);
-  dev::k_raster<false, KM><<<grid, 128, smem, d->stream>>>(fc, B, pass, dev::RasterShared::kTbr,
-                                                             dev::RasterShared::kTb);
-  ck(cudaGetLastError(), "k_raster launch");
-  ++*launches;
-  dev::k_raster<true, KM><<<d->raster_ctas_global, 128, 0, d->stream>>>(fc, B, pass, gcap_tbr, gcap_tb);
-  ++*launches;
+  if (!d->extract_configured) {
+    ck(cudaFuncSetAttribute(dev::k_extract<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            int(smem)),
+       "cudaFuncSetAttribute");
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_extract<false>, 128, smem);
+    d->extract_ctas = std::max(1, per_sm) * d->sm_count;
+    d->extract_configured = true;
+  }
+  const int grid = int(std::min<long long>(d->extract_ctas, (long long)fc.nbins * 4));
+  dev::k_extract<false><<<grid, 128, smem, d->stream>>>(fc, B, pass, dev::RasterShared::kTbr,
+                                                          dev::RasterShared::kTb);
+  ck(cudaGetLastError(), "k_extract launch");
+  dev::k_extract<true><<<d->raster_ctas_global, 128, 0, d->stream>>>(fc, B, pass, gcap_tbr, gcap_tb);
+  *launches += 2;
 }
 
 template <int KM>
-void launch_raster_km(DeviceScene* d, const dev::FrameConst& fc, const dev::Buffers& B, int pass,
-                      uint32_t gcap_tbr, uint32_t gcap_tb, int* launches) {
-  launch_raster_pair<KM>(d, fc, B, pass, gcap_tbr, gcap_tb, launches);
+void launch_shade_km(DeviceScene* d, const dev::FrameConst& fc, const dev::Buffers& B,
+                     int* launches) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_shade<KM>, 256, 0);
+  const long long warps = (long long)fc.nbins * 32;
+  const int grid = int(std::max<long long>(1, std::min<long long>((long long)std::max(1, per_sm) * d->sm_count,
+                                                                   (warps + 7) / 8)));
+  dev::k_shade<KM><<<grid, 256, 0, d->stream>>>(fc, B);
+  ck(cudaGetLastError(), "k_shade launch");
+  ++*launches;
 }
 
-void launch_raster(DeviceScene* d, const dev::FrameConst& fc, const dev::Buffers& B, int pass,
-                   uint32_t gcap_tbr, uint32_t gcap_tb, int* launches) {
-  int df = fc.df;
-  if (df <= 1) launch_raster_km<1>(d, fc, B, pass, gcap_tbr, gcap_tb, launches);
-  else if (df <= 2) launch_raster_km<2>(d, fc, B, pass, gcap_tbr, gcap_tb, launches);
-  else if (df <= 3) launch_raster_km<3>(d, fc, B, pass, gcap_tbr, gcap_tb, launches);
-  else if (df <= 4) launch_raster_km<4>(d, fc, B, pass, gcap_tbr, gcap_tb, launches);
-  else if (df <= 8) launch_raster_km<8>(d, fc, B, pass, gcap_tbr, gcap_tb, launches);
-  else if (df <= 16) launch_raster_km<16>(d, fc, B, pass, gcap_tbr, gcap_tb, launches);
-  else if (df <= 32) launch_raster_km<32>(d, fc, B, pass, gcap_tbr, gcap_tb, launches);
+void launch_shade(DeviceScene* d, const dev::FrameConst& fc, const dev::Buffers& B, int* launches) {
+  const int df = fc.df;
+  if (df <= 1) launch_shade_km<1>(d, fc, B, launches);
+  else if (df <= 2) launch_shade_km<2>(d, fc, B, launches);
+  else if (df <= 3) launch_shade_km<3>(d, fc, B, launches);
+  else if (df <= 4) launch_shade_km<4>(d, fc, B, launches);
+  else if (df <= 8) launch_shade_km<8>(d, fc, B, launches);
+  else if (df <= 16) launch_shade_km<16>(d, fc, B, launches);
+  else if (df <= 32) launch_shade_km<32>(d, fc, B, launches);
   else throw Error(VEIL_ERR_INVALID_ARG, "depth_filter_size above 32 is not supported on the device path");
 }
 
@@ -2030,9 +2021,14 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   if (opt.dump) {
     d->hash.ensure(npx * 8);
     d->emit.ensure(npx * 4);
-    d->thb_cnt.ensure(nb * 32 * 4);
   }
   d->ctr.ensure(sizeof(dev::Counters));
+  d->hbd.ensure(nb * 32 * sizeof(dev::HbDesc));
+  if (d->pool_cap == 0) d->pool_cap = std::max<uint32_t>(1u << 22, uint32_t(std::min<size_t>(nb * 2048, 1u << 26)));
+  d->pool_tri.ensure(size_t(d->pool_cap) * 4);
+  d->pool_mask.ensure(size_t(d->pool_cap) * 4);
+  d->pool_pre.ensure(size_t(d->pool_cap) * 4);
+  fc.pool_cap = d->pool_cap;
   // global scratch for spilled items: capacities follow the active limits
   P.gcap_tbr = std::min<uint32_t>(std::max(fc.low.tbr, fc.high.tbr), 1u << 16);
   P.gcap_tb = std::min<uint32_t>(std::max(std::max(fc.low.tb, fc.high.tb), fc.high.thb), P.gcap_tbr);
@@ -2084,7 +2080,10 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   B.mask = d->mask.as<uint8_t>();
   B.hash = opt.dump ? d->hash.as<uint64_t>() : nullptr;
   B.emit = opt.dump ? d->emit.as<uint32_t>() : nullptr;
-  B.thb_cnt = opt.dump ? d->thb_cnt.as<uint32_t>() : nullptr;
+  B.hbd = d->hbd.as<dev::HbDesc>();
+  B.pool_tri = d->pool_tri.as<uint32_t>();
+  B.pool_mask = d->pool_mask.as<uint32_t>();
+  B.pool_pre = d->pool_pre.as<uint32_t>();
   B.ctr = d->ctr.as<dev::Counters>();
   return P;
 }
@@ -2099,7 +2098,6 @@ int enqueue_front(DeviceScene* d, Prepared& P) {
   ck(cudaMemsetAsync(&B.ctr->bin_error, 0xff, sizeof(unsigned long long), st), "memset");
   ck(cudaMemsetAsync(B.qcnt, 0, size_t(fc.nbins) * 4, st), "memset");
   ck(cudaMemsetAsync(B.tcnt, 0, size_t(fc.nbins) * 4, st), "memset");
-  if (B.thb_cnt) ck(cudaMemsetAsync(B.thb_cnt, 0, size_t(fc.nbins) * 32 * 4, st), "memset");
   cudaEventRecord(d->ev[0], st);
   if (P.nblocks) {
     dev::k_setup_count<<<P.nblocks, dev::kSetupBlock, 0, st>>>(fc, B);
@@ -2122,13 +2120,16 @@ void read_stats(DeviceScene* d, const dev::Counters& c, const Scene& s, veil_fra
   float ms[4] = {0, 0, 0, 0};
   cudaEventElapsedTime(&ms[0], d->ev[0], d->ev[1]);
   cudaEventElapsedTime(&ms[1], d->ev[1], d->ev[2]);
+  float shade_ms = 0;
   cudaEventElapsedTime(&ms[2], d->ev[2], d->ev[3]);
-  cudaEventElapsedTime(&ms[3], d->ev[3], d->ev[4]);
+  cudaEventElapsedTime(&ms[3], d->ev[3], d->ev[5]);
+  cudaEventElapsedTime(&shade_ms, d->ev[5], d->ev[4]);
   float total = 0;
   cudaEventElapsedTime(&total, d->ev[0], d->ev[4]);
   st->setup_ms = ms[0];
   st->binning_ms = ms[1];
   st->low_raster_ms = ms[2];
+  st->shade_ms = shade_ms;
   st->hi_raster_ms = ms[3];
   st->total_ms = total;
   st->samples = c.samples;
@@ -2283,9 +2284,11 @@ void collect_dumps(DeviceScene* d, Prepared& P, const dev::Counters& c, RenderOu
 }  // namespace
 
 static void enqueue_raster(DeviceScene* d, Prepared& P, int* launches) {
-  launch_raster(d, P.fc, P.B, dev::kPassLow, P.gcap_tbr, P.gcap_tb, launches);
+  launch_extract(d, P.fc, P.B, dev::kPassLow, P.gcap_tbr, P.gcap_tb, launches);
   cudaEventRecord(d->ev[3], d->stream);
-  launch_raster(d, P.fc, P.B, dev::kPassHigh, P.gcap_tbr, P.gcap_tb, launches);
+  launch_extract(d, P.fc, P.B, dev::kPassHigh, P.gcap_tbr, P.gcap_tb, launches);
+  cudaEventRecord(d->ev[5], d->stream);
+  launch_shade(d, P.fc, P.B, launches);
   dev::k_finalize<<<1, 1024, 0, d->stream>>>(P.fc, P.B);
   ++*launches;
   cudaEventRecord(d->ev[4], d->stream);
@@ -2305,6 +2308,10 @@ void render_frame(const Scene& s, const RenderOptions& opt, RenderOutput* out) {
       d->items_cap = uint32_t(std::min<unsigned long long>(c.pairs + c.pairs / 4 + 1024, 0xffffffffull));
       continue;
     }
+    if (c.error & 8u) {  // THB pool capacity: grow and re-run
+      d->pool_cap = uint32_t(std::min<unsigned long long>(2ull * d->pool_cap, 0xffffffffull));
+      continue;
+    }
     check_frame_errors(c, P.fc);
     out->width = s.camera.width;
     out->height = s.camera.height;
@@ -2312,34 +2319,51 @@ void render_frame(const Scene& s, const RenderOptions& opt, RenderOutput* out) {
     out->stats.kernel_launches = launches;
     d->last = out->stats;
     if (opt.dump) {
-      // second pass with THB offsets (deterministic: identical lists)
+      collect_dumps(d, P, c, out);
+      // tri-half-block lists from the pool in (bin, half-block) order
       const size_t nb = size_t(P.fc.nbins);
-      std::vector<uint32_t> cnt(nb * 32);
-      ck(cudaMemcpy(cnt.data(), P.B.thb_cnt, nb * 32 * 4, cudaMemcpyDeviceToHost), "dump");
+      std::vector<dev::HbDesc> hbd(nb * 32);
       std::vector<uint8_t> cat(nb);
+      ck(cudaMemcpy(hbd.data(), P.B.hbd, nb * 32 * sizeof(dev::HbDesc), cudaMemcpyDeviceToHost), "dump");
       ck(cudaMemcpy(cat.data(), P.B.cat, nb, cudaMemcpyDeviceToHost), "dump");
-      std::vector<uint64_t> offs(nb * 32 + 1, 0);
-      for (size_t i = 0; i < nb * 32; ++i) offs[i + 1] = offs[i] + (cat[i / 32] ? cnt[i] : 0);
-      d->thb_off.ensure(offs.size() * 8);
-      d->thb_out.ensure(std::max<uint64_t>(1, offs.back()) * 8);
-      d->thb_tri.ensure(std::max<uint64_t>(1, offs.back()) * 4);
-      d->thb_pre.ensure(std::max<uint64_t>(1, offs.back()) * 4);
-      ck(cudaMemcpy(d->thb_off.p, offs.data(), offs.size() * 8, cudaMemcpyHostToDevice), "dump");
-      P.B.thb_off = d->thb_off.as<uint64_t>();
-      P.B.thb_out = d->thb_out.as<uint64_t>();
-      P.B.thb_tri = d->thb_tri.as<uint32_t>();
-      P.B.thb_pre = d->thb_pre.as<uint32_t>();
-      int l2 = enqueue_front(d, P);
-      (void)l2;
-      enqueue_raster(d, P, &l2);
-      dev::Counters c2;
-      ck(cudaMemcpyAsync(&c2, P.B.ctr, sizeof c2, cudaMemcpyDeviceToHost, d->stream), "counters");
-      ck(cudaStreamSynchronize(d->stream), "frame");
-      collect_dumps(d, P, c2, out);
+      const size_t used = std::min<size_t>(c.pool_next, d->pool_cap);
+      std::vector<uint32_t> ptri(used), pmask(used), ppre(used);
+      if (used) {
+        ck(cudaMemcpy(ptri.data(), P.B.pool_tri, used * 4, cudaMemcpyDeviceToHost), "dump");
+        ck(cudaMemcpy(pmask.data(), P.B.pool_mask, used * 4, cudaMemcpyDeviceToHost), "dump");
+        ck(cudaMemcpy(ppre.data(), P.B.pool_pre, used * 4, cudaMemcpyDeviceToHost), "dump");
+      }
+      std::vector<uint64_t> offs(nb * 32 + 1, 0), bits;
+      std::vector<uint32_t> tris, pres;
+      for (size_t i = 0; i < nb * 32; ++i) {
+        const int b = int(i / 32);
+        const bool owned = bin_owned(b % P.fc.bins_x, b / P.fc.bins_x, opt.rank, opt.world_size);
+        if (cat[b] && owned) {
+          const dev::HbDesc& h = hbd[i];
+          for (uint32_t k = 0; k < h.cnt; ++k) {
+            const uint32_t m = pmask[h.off + k], tri = ptri[h.off + k];
+            uint64_t w = 0;  // TriHalfBlock::make, packing.hpp:154-176
+            for (int y = 0; y < 4; ++y) {
+              const uint32_t rb = (m >> (8 * y)) & 0xffu;
+              uint32_t bb = 7, ll = 0;
+              if (rb) {
+                bb = uint32_t(__builtin_ctz(rb));
+                ll = 31u - uint32_t(__builtin_clz(rb));
+              }
+              w |= uint64_t(bb | (ll << 3)) << (6 * y);
+            }
+            const uint32_t prefix = ppre[h.off + k] + uint32_t(__builtin_popcount(m));
+            bits.push_back(w | (uint64_t(tri & 0xffffffu) << 24) | (uint64_t(prefix & 0xfffu) << 48));
+            tris.push_back(tri);
+            pres.push_back(prefix);
+          }
+        }
+        offs[i + 1] = bits.size();
+      }
       dump_put_host(out, "thb_offsets", offs);
-      dump_put(out, "thb", P.B.thb_out, offs.back(), d->stream);
-      dump_put(out, "thb_tri", P.B.thb_tri, offs.back(), d->stream);
-      dump_put(out, "thb_prefix", P.B.thb_pre, offs.back(), d->stream);
+      dump_put_host(out, "thb", bits);
+      dump_put_host(out, "thb_tri", tris);
+      dump_put_host(out, "thb_prefix", pres);
       const size_t npx = size_t(s.camera.width) * s.camera.height;
       dump_put(out, "emit_hash", P.B.hash, npx, d->stream);
       dump_put(out, "emit_count", P.B.emit, npx, d->stream);
@@ -2382,6 +2406,7 @@ void render_reference_frame(const Scene& s, const RenderOptions& opt, RenderOutp
     dev::k_abuffer<<<grid, 128, 0, d->stream>>>(P.fc, P.B);
     ++launches;
     cudaEventRecord(d->ev[3], d->stream);
+    cudaEventRecord(d->ev[5], d->stream);
     cudaEventRecord(d->ev[4], d->stream);
     dev::Counters c;
     ck(cudaMemcpyAsync(&c, P.B.ctr, sizeof c, cudaMemcpyDeviceToHost, d->stream), "counters");
