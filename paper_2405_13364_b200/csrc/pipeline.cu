@@ -30,6 +30,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -79,6 +80,7 @@ struct FrameConst {
   int dump;
   int decoded;  // setup writes per-triangle decoded shading records
   uint32_t pool_cap;
+  int debug;  // experiment switch (VEIL_DEBUG_SHADE), 0 in production
 };
 
 // Device counters; one instance per scene workspace, zeroed per frame.
@@ -94,7 +96,7 @@ struct Counters {
   unsigned long long samples, fragments, thb, segments, invalid;
   unsigned long long bins_empty, bins_low, bins_high, bins_propagated;
   unsigned int pool_next;
-  unsigned int shade_next;
+  unsigned int shade_next[2];
 };
 
 // Decoded per-triangle shading inputs (unpack_color / decode_normal of the
@@ -988,8 +990,8 @@ __device__ __forceinline__ uint32_t kth_pixel(uint32_t m, uint32_t k) {
 
 // Canonical-order shading of one half-block without the alpha threshold:
 // the sample stream (THBs in sorted order, then row-major) is cut into
-// 64-sample segments; lane s shades samples base+s and base+32+s (two
-// independent chains for ILP), then each pixel's lane takes its samples of
+// 32-sample segments; lane s shades sample base+s, then each pixel's lane
+// takes its samples of
 // the segment in stream order through per-warp routing masks and pushes them
 // into its register depth filter. Every pixel therefore sees exactly the
 // reference's per-pixel sequence.
@@ -1045,37 +1047,28 @@ __device__ __forceinline__ void shade_segments(const FrameConst& fc, const Buffe
   RegFilter<KM> f;
   f.reset();
   uint32_t r_lo = 0;
-  for (uint32_t base = 0; base < total; base += 64) {
+  for (uint32_t base = 0; base < total; base += 32) {
     // THB r_lo holds a sample < base and every THB holds >= 1 sample, so
-    // sample base+j lies in a THB <= r_lo + j + 1.
-    const uint32_t s0 = base + lane, s1 = base + 32 + lane;
-    const bool v0 = s0 < total, v1 = s1 < total;
-    const uint32_t c0 = v0 ? s0 : total - 1, c1 = v1 ? s1 : total - 1;
+    // sample base+lane lies in a THB <= r_lo + lane + 1.
+    const uint32_t s0 = base + lane;
+    const bool v0 = s0 < total;
+    const uint32_t c0 = v0 ? s0 : total - 1;
     const uint32_t r0 = find_thb(pre_l, r_lo, min(n - 1, r_lo + (uint32_t)lane + 1u), c0);
-    const uint32_t r1 = find_thb(pre_l, r0, min(n - 1, r_lo + (uint32_t)lane + 33u), c1);
     const uint32_t p0 = kth_pixel(mask_l[r0], c0 - pre_l[r0]);
-    const uint32_t p1 = kth_pixel(mask_l[r1], c1 - pre_l[r1]);
-    const uint32_t t0 = tri_l[r0], t1 = tri_l[r1];
-    float4 col0, col1;
-    uint32_t q0, q1;
+    const uint32_t t0 = tri_l[r0];
+    float4 col0;
+    uint32_t q0;
     if (fc.decoded) {
       col0 = shade_decoded_bf(fc, B, t0, px0 + (int)(p0 & 7u), py0 + (int)(p0 >> 3), &q0);
-      col1 = shade_decoded_bf(fc, B, t1, px0 + (int)(p1 & 7u), py0 + (int)(p1 >> 3), &q1);
     } else {
-      double d0, d1;
+      double d0;
       col0 = shade_sample(fc, B, t0, px0 + (int)(p0 & 7u), py0 + (int)(p0 >> 3), &d0);
-      col1 = shade_sample(fc, B, t1, px0 + (int)(p1 & 7u), py0 + (int)(p1 >> 3), &d1);
       q0 = quantize_depth(d0);
-      q1 = quantize_depth(d1);
     }
-    const uint64_t key0 = sample_key(fc, q0, t0), key1 = sample_key(fc, q1, t1);
-    r_lo = __shfl_sync(0xffffffffu, r1, 31);
+    const uint64_t key0 = sample_key(fc, q0, t0);
+    r_lo = __shfl_sync(0xffffffffu, r0, 31);
     const uint32_t m0 = route_mask(route, v0 ? p0 : 32u + lane, v0);
     blend_routed<KM>(fc, f, o, m0, key0, col0);
-    if (__any_sync(0xffffffffu, v1)) {
-      const uint32_t m1 = route_mask(route, v1 ? p1 : 32u + lane, v1);
-      blend_routed<KM>(fc, f, o, m1, key1, col1);
-    }
   }
   while (f.n > 0) {
     uint64_t pk;
@@ -1086,12 +1079,17 @@ __device__ __forceinline__ void shade_segments(const FrameConst& fc, const Buffe
   }
 }
 
-// Alpha-threshold variant (raster.cpp:232-284): THB-by-THB walk with lane ==
-// pixel so the 32nd saturation can be located at its exact stream position.
-template <int KM>
-__device__ __forceinline__ void shade_threshold(const FrameConst& fc, const Buffers& B, int px0, int py0,
-                                const uint32_t* tri_l, const uint32_t* mask_l, uint32_t n,
-                                PixelOut& o, unsigned long long* enumerated_out) {
+// THB-by-THB walk with lane == pixel (raster.cpp:232-284): every lane visits
+// the THBs in sorted order and shades the ones covering its pixel, so the
+// triangle data of each step is a warp-wide broadcast. Used when THBs cover
+// many pixels (samples/THB high) and, with kThreshold, for the alpha
+// threshold, where the 32nd saturation must be located at its exact stream
+// position.
+template <int KM, bool kThreshold>
+__device__ __forceinline__ void shade_walk(const FrameConst& fc, const Buffers& B, int px0,
+                                           int py0, const uint32_t* tri_l, const uint32_t* mask_l,
+                                           uint32_t n, PixelOut& o,
+                                           unsigned long long* enumerated_out) {
   const int lane = threadIdx.x & 31;
   const int px = px0 + (lane & 7), py = py0 + (lane >> 3);
   RegFilter<KM> f;
@@ -1103,39 +1101,54 @@ __device__ __forceinline__ void shade_threshold(const FrameConst& fc, const Buff
     const uint32_t m = mask_l[r];
     const uint32_t tri = tri_l[r];
     const bool covered = (m >> lane) & 1u;
-    float4 col;
+    float4 col = make_float4(0.f, 0.f, 0.f, 0.f);
     uint64_t key = 0;
-    if (covered) {
-      double depth;
-      col = shade_sample(fc, B, tri, px, py, &depth);
-      key = sample_key(fc, quantize_depth(depth), tri);
+    if (covered && fc.debug == 1) {
+      col = make_float4(0.01f, 0.01f, 0.01f, 0.01f);
+      key = ((uint64_t)r << 24) | tri;
+    } else if (covered) {
+      uint32_t qd;
+      if (fc.decoded) {
+        col = shade_decoded_bf(fc, B, tri, px, py, &qd);
+      } else {
+        double depth;
+        col = shade_sample(fc, B, tri, px, py, &depth);
+        qd = quantize_depth(depth);
+      }
+      key = sample_key(fc, qd, tri);
     }
     int commit_until = 32;
-    bool newly = false;
-    if (covered && !saturated) {
-      float4 pc;
-      if (f.peek(fc.df, key, col, &pc)) newly = blend(o.acc, pc).w >= kAlphaThreshold;
+    if (kThreshold) {
+      bool newly = false;
+      if (covered && !saturated) {
+        float4 pc;
+        if (f.peek(fc.df, key, col, &pc)) newly = blend(o.acc, pc).w >= kAlphaThreshold;
+      }
+      const unsigned new_mask = __ballot_sync(0xffffffffu, newly);
+      if (new_mask && (sat_mask | new_mask) == 0xffffffffu) {
+        commit_until = 32 - __clz(new_mask);
+        stopped = true;
+      }
+      enumerated += __popc(m & (commit_until == 32 ? 0xffffffffu : ((1u << commit_until) - 1u)));
     }
-    const unsigned new_mask = __ballot_sync(0xffffffffu, newly);
-    if (new_mask && (sat_mask | new_mask) == 0xffffffffu) {
-      commit_until = 32 - __clz(new_mask);
-      stopped = true;
-    }
-    enumerated += __popc(m & (commit_until == 32 ? 0xffffffffu : ((1u << commit_until) - 1u)));
-    if (covered && lane < commit_until) {
+    if (covered && fc.debug == 2) {
+      commit(o, key, col, false);
+    } else if (covered && lane < commit_until) {
       uint64_t pk;
       float4 pc;
       bool ooo;
       if (f.push(fc.df, key, col, &pk, &pc, &ooo)) {
         commit(o, pk, pc, ooo);
-        if (!saturated && o.acc.w >= kAlphaThreshold) saturated = true;
+        if (kThreshold && !saturated && o.acc.w >= kAlphaThreshold) saturated = true;
       }
     }
-    sat_mask = __ballot_sync(0xffffffffu, saturated);
-    if (stopped) break;
+    if (kThreshold) {
+      sat_mask = __ballot_sync(0xffffffffu, saturated);
+      if (stopped) break;
+    }
   }
   if (!stopped) {
-    bool done = o.acc.w >= kAlphaThreshold;
+    bool done = kThreshold && o.acc.w >= kAlphaThreshold;
     while (f.n > 0) {
       uint64_t pk;
       float4 pc;
@@ -1143,10 +1156,10 @@ __device__ __forceinline__ void shade_threshold(const FrameConst& fc, const Buff
       f.pop(&pk, &pc, &ooo);
       if (done) continue;
       commit(o, pk, pc, ooo);
-      if (o.acc.w >= kAlphaThreshold) done = true;
+      if (kThreshold && o.acc.w >= kAlphaThreshold) done = true;
     }
   }
-  *enumerated_out = enumerated;
+  if (kThreshold) *enumerated_out = enumerated;
 }
 
 __device__ __forceinline__ uint32_t span_mask(uint32_t b, uint32_t l, uint32_t c0, uint32_t c1) {
@@ -1463,25 +1476,39 @@ __global__ void __launch_bounds__(128) k_extract(FrameConst fc, Buffers B, int p
   }
 }
 
-// Shading: one warp per 8x4 half-block (raster.cpp:201-321), taken from a
-// global work counter; no block-level synchronisation. Empty bins and
-// half-blocks without samples composite the background.
-template <int KM>
+// Shading: a CTA of 8 warps takes one (bin, block-row) work item; warp w
+// shades half-block w of the row (raster.cpp:201-321), so the 8 warps touch
+// the same triangles (L1 reuse). Each warp first stages its tri-half-block
+// list from the pool into shared memory (coalesced), keeping the segment
+// mapping's dependent lookups on-chip. Empty bins and half-blocks without
+// samples composite the background.
+constexpr int kShadeStage = 256;  // THB entries staged per warp; longer lists stream
+constexpr uint32_t kWalkMinSamplesPerThb = 12;  // walk vs segments crossover
+
+// kMode: 0 = broadcast walk for half-blocks with big THBs (also writes every
+// half-block without samples), 1 = segment routing for the rest, 2 = alpha
+// threshold walk for all. Separate instantiations keep each path's register
+// allocation small.
+template <int KM, int kMode>
 __global__ void __launch_bounds__(256, 2) k_shade(FrameConst fc, Buffers B) {
+  __shared__ uint32_t stage_tri[8][kShadeStage];
+  __shared__ uint32_t stage_mask[8][kShadeStage];
+  __shared__ uint32_t stage_pre[8][kShadeStage];
+  __shared__ uint32_t route_s[8][32];
+  __shared__ uint32_t item_s;
   if (B.ctr->error) return;
-  const int lane = threadIdx.x & 31;
-  uint32_t* route = nullptr;
-  __shared__ uint32_t route_s[8 * 32];
-  route = route_s + (threadIdx.x >> 5) * 32;
-  const uint32_t nitems = (uint32_t)fc.nbins * 32u;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t nitems = (uint32_t)fc.nbins * 4u;
   for (;;) {
-    uint32_t item = 0;
-    if (lane == 0) item = atomicAdd(&B.ctr->shade_next, 1u);
-    item = __shfl_sync(0xffffffffu, item, 0);
+    if (threadIdx.x == 0) item_s = atomicAdd(&B.ctr->shade_next[kMode == 1 ? 1 : 0], 1u);
+    __syncthreads();
+    const uint32_t item = item_s;
+    __syncthreads();
     if (item >= nitems) break;
-    const int bin = (int)(item >> 5), hb = (int)(item & 31u);
+    const int bin = (int)(item >> 2), row = (int)(item & 3u);
     const int bxi = bin % fc.bins_x, byi = bin / fc.bins_x;
     if (!(fc.world <= 1 || ((bxi + 3 * byi) % fc.world) == fc.rank)) continue;
+    const int hb = row * 8 + warp;  // reference half-block index in the bin
     const int block = hb >> 1;
     const int hpx0 = bxi * kBin + (block & 3) * 8;
     const int hpy0 = byi * kBin + (block >> 2) * 8 + (hb & 1) * 4;
@@ -1491,16 +1518,34 @@ __global__ void __launch_bounds__(256, 2) k_shade(FrameConst fc, Buffers B) {
     po.hash = kHashSeed;
     po.emitted = 0;
     unsigned long long enumerated = 0;
-    const bool live = B.cat[bin] != 0;
+    bool live = B.cat[bin] != 0;
+    HbDesc d = {0, 0, 0, 0};
+    if (live) d = B.hbd[(size_t)bin * 32 + hb];
+    const bool walk = !live || d.frags >= kWalkMinSamplesPerThb * d.cnt;
+    const bool mine = kMode == 2 || (kMode == 0 ? walk : !walk);
+    if (!mine) continue;  // warp-level skip: the other path's kernel owns it
     if (live) {
-      const HbDesc d = B.hbd[item];
       enumerated = d.frags;
-      if (fc.threshold)
-        shade_threshold<KM>(fc, B, hpx0, hpy0, B.pool_tri + d.off, B.pool_mask + d.off, d.cnt, po,
-                            &enumerated);
-      else if (d.frags)
-        shade_segments<KM>(fc, B, hpx0, hpy0, B.pool_tri + d.off, B.pool_mask + d.off,
-                           B.pool_pre + d.off, d.cnt, d.frags, route, po);
+      const uint32_t* tri_l = B.pool_tri + d.off;
+      const uint32_t* mask_l = B.pool_mask + d.off;
+      const uint32_t* pre_l = B.pool_pre + d.off;
+      if (d.cnt <= (uint32_t)kShadeStage) {
+        for (uint32_t i = lane; i < d.cnt; i += 32) {
+          stage_tri[warp][i] = tri_l[i];
+          stage_mask[warp][i] = mask_l[i];
+          stage_pre[warp][i] = pre_l[i];
+        }
+        __syncwarp();
+        tri_l = stage_tri[warp];
+        mask_l = stage_mask[warp];
+        pre_l = stage_pre[warp];
+      }
+      if (kMode == 2)
+        shade_walk<KM, true>(fc, B, hpx0, hpy0, tri_l, mask_l, d.cnt, po, &enumerated);
+      else if (kMode == 0)  // big THBs: broadcast walk
+        shade_walk<KM, false>(fc, B, hpx0, hpy0, tri_l, mask_l, d.cnt, po, &enumerated);
+      else if (d.frags)  // small THBs: dense segments + routing
+        shade_segments<KM>(fc, B, hpx0, hpy0, tri_l, mask_l, pre_l, d.cnt, d.frags, route_s[warp], po);
     }
     const int px = hpx0 + (lane & 7), py = hpy0 + (lane >> 3);
     unsigned invalid_px = 0;
@@ -1528,7 +1573,7 @@ __global__ void __launch_bounds__(256, 2) k_shade(FrameConst fc, Buffers B) {
       for (int s = 16; s > 0; s >>= 1) samples += __shfl_xor_sync(0xffffffffu, samples, s);
       const unsigned inv = __popc(__ballot_sync(0xffffffffu, invalid_px != 0));
       if (lane == 0) {
-        unsigned long long* slot = B.slots + ((size_t)bin * 4 + (block >> 2)) * 5;
+        unsigned long long* slot = B.slots + ((size_t)bin * 4 + row) * 5;
         atomicAdd(&slot[0], samples);
         atomicAdd(&slot[3], (enumerated + 255ull) / 256ull);
         if (inv) atomicAdd(&slot[4], (unsigned long long)inv);
@@ -1881,17 +1926,27 @@ void launch_extract(DeviceScene* d, const dev::FrameConst& fc, const dev::Buffer
   *launches += 2;
 }
 
+template <int KM, int kMode>
+void launch_shade_mode(DeviceScene* d, const dev::FrameConst& fc, const dev::Buffers& B,
+                       int* launches) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_shade<KM, kMode>, 256, 0);
+  const int grid = int(std::max<long long>(1, std::min<long long>((long long)std::max(1, per_sm) * d->sm_count,
+                                                                   (long long)fc.nbins * 4)));
+  dev::k_shade<KM, kMode><<<grid, 256, 0, d->stream>>>(fc, B);
+  ck(cudaGetLastError(), "k_shade launch");
+  ++*launches;
+}
+
 template <int KM>
 void launch_shade_km(DeviceScene* d, const dev::FrameConst& fc, const dev::Buffers& B,
                      int* launches) {
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_shade<KM>, 256, 0);
-  const long long warps = (long long)fc.nbins * 32;
-  const int grid = int(std::max<long long>(1, std::min<long long>((long long)std::max(1, per_sm) * d->sm_count,
-                                                                   (warps + 7) / 8)));
-  dev::k_shade<KM><<<grid, 256, 0, d->stream>>>(fc, B);
-  ck(cudaGetLastError(), "k_shade launch");
-  ++*launches;
+  if (fc.threshold) {
+    launch_shade_mode<KM, 2>(d, fc, B, launches);
+  } else {
+    launch_shade_mode<KM, 0>(d, fc, B, launches);
+    launch_shade_mode<KM, 1>(d, fc, B, launches);
+  }
 }
 
 void launch_shade(DeviceScene* d, const dev::FrameConst& fc, const dev::Buffers& B, int* launches) {
@@ -1983,6 +2038,7 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   fc.rank = opt.rank;
   fc.world = opt.world_size;
   fc.dump = opt.dump ? 1 : 0;
+  if (const char* dbg = std::getenv("VEIL_DEBUG_SHADE")) fc.debug = std::atoi(dbg);
 
   const uint32_t Q = d->nquads;
   const size_t nb = size_t(fc.nbins);
