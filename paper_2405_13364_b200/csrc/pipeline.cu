@@ -97,6 +97,8 @@ struct Counters {
   unsigned long long bins_empty, bins_low, bins_high, bins_propagated;
   unsigned int pool_next;
   unsigned int shade_next[2];
+  unsigned int seg_count;  // half-blocks queued for the segment-routing kernel
+  unsigned int pad2;
 };
 
 // Decoded per-triangle shading inputs (unpack_color / decode_normal of the
@@ -157,6 +159,7 @@ struct Buffers {
   uint32_t* pool_tri;
   uint32_t* pool_mask;  // coverage, bit = ly * 8 + lx
   uint32_t* pool_pre;   // exclusive fragment prefix
+  uint32_t* seg_queue;  // (bin * 32 + hb) of half-blocks for k_shade<.., 1>
   Counters* ctr;
 };
 
@@ -571,20 +574,57 @@ __global__ void __launch_bounds__(256) k_bin_pass(FrameConst fc, Buffers B) {
         }
       }
     }
-    if (in && (flags & 1u)) {
+  }
+}
+
+// Large quads' valid triangles (rasterize_triangle_bins, binning.hpp:89-117):
+// one warp per triangle, lane = pixel row of the current bin row; the
+// per-row covered bin-column ranges are OR-reduced across the warp, then
+// each set bin is counted (kWrite = false) or receives the triangle index.
+template <bool kWrite>
+__global__ void __launch_bounds__(256) k_bin_large(FrameConst fc, Buffers B) {
+  if (B.ctr->error) return;
+  const uint32_t nvis = B.ctr->nvis;
+  const int lane = threadIdx.x & 31;
+  const uint32_t gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int nwords = (fc.bins_x + 31) / 32;
+  for (uint32_t base = gwarp * 32; base < nvis; base += nwarps * 32) {
+    const uint32_t q = base + lane;
+    const bool large = q < nvis && (B.vq_flags[q] & 1u);
+    unsigned m = __ballot_sync(0xffffffffu, large);
+    while (m) {
+      const uint32_t quad = base + (__ffs(m) - 1);
+      m &= m - 1;
       for (uint32_t t = 0; t < 2; ++t) {
-        uint32_t ti = q * 2 + t;
+        const uint32_t ti = quad * 2 + t;
         if (!(B.tri_meta[ti].w & 0x100u)) continue;
-        TriRec tr = B.tri[ti];
-        if (!kWrite) atomicAdd(&B.ctr->large_tris, 1ull);
-        tri_bins(fc, tr, [&](int bin) {
-          if (kWrite) {
-            uint32_t slot = atomicAdd(&B.tcur[bin], 1u);
-            if (slot < fc.items_cap) B.items[slot] = ti;
-          } else {
-            atomicAdd(&B.tcnt[bin], 1u);
+        const TriRec& tr = B.tri[ti];
+        const int y_min = tr.y_min, y_max = tr.y_max;
+        if (!kWrite && lane == 0) atomicAdd(&B.ctr->large_tris, 1ull);
+        for (int R = y_min / kBin; R <= y_max / kBin; ++R) {
+          const int y = R * kBin + lane;
+          int b0 = 1, b1 = 0;
+          if (y >= y_min && y <= y_max) {
+            int b, l;
+            if (row_span(tr, y, 0, fc.width - 1, &b, &l)) b0 = b / kBin, b1 = l / kBin;
           }
-        });
+          for (int w = 0; w < nwords; ++w) {
+            const int lo = max(b0, w * 32), hi = min(b1, w * 32 + 31);
+            uint32_t word = 0;
+            if (lo <= hi) word = (hi - lo == 31 ? 0xffffffffu : ((2u << (hi - lo)) - 1u)) << (lo - w * 32);
+            word = __reduce_or_sync(0xffffffffu, word);
+            if ((word >> lane) & 1u) {
+              const int bin = R * fc.bins_x + w * 32 + lane;
+              if (kWrite) {
+                const uint32_t slot = atomicAdd(&B.tcur[bin], 1u);
+                if (slot < fc.items_cap) B.items[slot] = ti;
+              } else {
+                atomicAdd(&B.tcnt[bin], 1u);
+              }
+            }
+          }
+        }
       }
     }
   }
@@ -1498,17 +1538,29 @@ __global__ void __launch_bounds__(256, 2) k_shade(FrameConst fc, Buffers B) {
   __shared__ uint32_t item_s;
   if (B.ctr->error) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t nitems = (uint32_t)fc.nbins * 4u;
+  // modes 0/2: CTA items = (bin, block-row), warp w = half-block w of the row
+  // mode 1: warp items from the queue mode 0 filled
+  const uint32_t nitems = kMode == 1 ? B.ctr->seg_count : (uint32_t)fc.nbins * 4u;
   for (;;) {
-    if (threadIdx.x == 0) item_s = atomicAdd(&B.ctr->shade_next[kMode == 1 ? 1 : 0], 1u);
-    __syncthreads();
-    const uint32_t item = item_s;
-    __syncthreads();
-    if (item >= nitems) break;
-    const int bin = (int)(item >> 2), row = (int)(item & 3u);
+    uint32_t item;
+    if (kMode == 1) {
+      item = 0;
+      if (lane == 0) item = atomicAdd(&B.ctr->shade_next[1], 1u);
+      item = __shfl_sync(0xffffffffu, item, 0);
+      if (item >= nitems) break;
+      item = B.seg_queue[item];
+    } else {
+      if (threadIdx.x == 0) item_s = atomicAdd(&B.ctr->shade_next[0], 1u);
+      __syncthreads();
+      item = item_s;
+      __syncthreads();
+      if (item >= nitems) break;
+      item = item * 8u + (uint32_t)warp;  // (bin * 32 + hb)
+    }
+    const int bin = (int)(item >> 5), row = (int)((item >> 3) & 3u);
     const int bxi = bin % fc.bins_x, byi = bin / fc.bins_x;
     if (!(fc.world <= 1 || ((bxi + 3 * byi) % fc.world) == fc.rank)) continue;
-    const int hb = row * 8 + warp;  // reference half-block index in the bin
+    const int hb = (int)(item & 31u);  // reference half-block index in the bin
     const int block = hb >> 1;
     const int hpx0 = bxi * kBin + (block & 3) * 8;
     const int hpy0 = byi * kBin + (block >> 2) * 8 + (hb & 1) * 4;
@@ -1522,8 +1574,10 @@ __global__ void __launch_bounds__(256, 2) k_shade(FrameConst fc, Buffers B) {
     HbDesc d = {0, 0, 0, 0};
     if (live) d = B.hbd[(size_t)bin * 32 + hb];
     const bool walk = !live || d.frags >= kWalkMinSamplesPerThb * d.cnt;
-    const bool mine = kMode == 2 || (kMode == 0 ? walk : !walk);
-    if (!mine) continue;  // warp-level skip: the other path's kernel owns it
+    if (kMode == 0 && !walk) {  // small THBs: hand over to the routing kernel
+      if (lane == 0) B.seg_queue[atomicAdd(&B.ctr->seg_count, 1u)] = item;
+      continue;
+    }
     if (live) {
       enumerated = d.frags;
       const uint32_t* tri_l = B.pool_tri + d.off;
@@ -1582,30 +1636,34 @@ __global__ void __launch_bounds__(256, 2) k_shade(FrameConst fc, Buffers B) {
   }
 }
 
-__global__ void __launch_bounds__(1024) k_finalize(FrameConst fc, Buffers B) {
+// Deterministic stat merge (renderer.cpp:170-212): integer sums over the
+// owned bins' (bin, block-row) slots; warp shuffles, then one atomic per
+// warp and counter.
+__global__ void __launch_bounds__(256) k_finalize(FrameConst fc, Buffers B) {
   if (B.ctr->error) return;
-  __shared__ unsigned long long acc[6];
-  if (threadIdx.x < 6) acc[threadIdx.x] = 0;
-  __syncthreads();
-  unsigned long long s[5] = {0, 0, 0, 0, 0}, prop = 0;
-  for (int b = threadIdx.x; b < fc.nbins; b += blockDim.x) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long v[6] = {0, 0, 0, 0, 0, 0};
+  if (b < fc.nbins) {
     const int bxi = b % fc.bins_x, byi = b / fc.bins_x;
     const bool owned = fc.world <= 1 || ((bxi + 3 * byi) % fc.world) == fc.rank;
-    if (!owned) continue;
-    for (int r = 0; r < 4; ++r)
-      for (int k = 0; k < 5; ++k) s[k] += B.slots[((size_t)b * 4 + r) * 5 + k];
-    prop += B.prop[b];
+    if (owned && B.cat[b]) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int k = 0; k < 5; ++k) v[k] += B.slots[((size_t)b * 4 + r) * 5 + k];
+      v[5] = B.prop[b];
+    }
   }
-  for (int k = 0; k < 5; ++k) atomicAdd(&acc[k], s[k]);
-  atomicAdd(&acc[5], prop);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    B.ctr->samples = acc[0];
-    B.ctr->fragments = acc[1];
-    B.ctr->thb = acc[2];
-    B.ctr->segments = acc[3];
-    B.ctr->invalid = acc[4];
-    B.ctr->bins_propagated = acc[5];
+#pragma unroll
+  for (int k = 0; k < 6; ++k)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+  if ((threadIdx.x & 31) == 0) {
+    unsigned long long* dst[6] = {&B.ctr->samples, &B.ctr->fragments, &B.ctr->thb,
+                                  &B.ctr->segments, &B.ctr->invalid, &B.ctr->bins_propagated};
+#pragma unroll
+    for (int k = 0; k < 6; ++k)
+      if (v[k]) atomicAdd(dst[k], v[k]);
   }
 }
 
@@ -1735,7 +1793,7 @@ struct DeviceScene {
   DevBuf pos, vcol, vnrm, quads, qmat, mats;
   DevBuf block_cnt, block_off, vq_src, vq_box, vq_flags, vq_mat, vq_col, vq_nrm, tri, tri_meta, shade;
   DevBuf qcnt, tcnt, off, qcur, tcur, cat, prop, items, slots, spill0, spill1, scratch, fb, mask,
-      hash, emit, ctr, tile_ids, hbd, pool_tri, pool_mask, pool_pre;
+      hash, emit, ctr, tile_ids, hbd, pool_tri, pool_mask, pool_pre, seg_queue;
   uint32_t items_cap = 0;
   uint32_t pool_cap = 0;
   bool extract_configured = false;
@@ -1931,8 +1989,9 @@ void launch_shade_mode(DeviceScene* d, const dev::FrameConst& fc, const dev::Buf
                        int* launches) {
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_shade<KM, kMode>, 256, 0);
+  const long long items = kMode == 1 ? ((long long)fc.nbins * 32 + 7) / 8 : (long long)fc.nbins * 4;
   const int grid = int(std::max<long long>(1, std::min<long long>((long long)std::max(1, per_sm) * d->sm_count,
-                                                                   (long long)fc.nbins * 4)));
+                                                                   items)));
   dev::k_shade<KM, kMode><<<grid, 256, 0, d->stream>>>(fc, B);
   ck(cudaGetLastError(), "k_shade launch");
   ++*launches;
@@ -2080,6 +2139,7 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   }
   d->ctr.ensure(sizeof(dev::Counters));
   d->hbd.ensure(nb * 32 * sizeof(dev::HbDesc));
+  d->seg_queue.ensure(nb * 32 * 4);
   if (d->pool_cap == 0) d->pool_cap = std::max<uint32_t>(1u << 22, uint32_t(std::min<size_t>(nb * 2048, 1u << 26)));
   d->pool_tri.ensure(size_t(d->pool_cap) * 4);
   d->pool_mask.ensure(size_t(d->pool_cap) * 4);
@@ -2140,6 +2200,7 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   B.pool_tri = d->pool_tri.as<uint32_t>();
   B.pool_mask = d->pool_mask.as<uint32_t>();
   B.pool_pre = d->pool_pre.as<uint32_t>();
+  B.seg_queue = d->seg_queue.as<uint32_t>();
   B.ctr = d->ctr.as<dev::Counters>();
   return P;
 }
@@ -2164,10 +2225,12 @@ int enqueue_front(DeviceScene* d, Prepared& P) {
   cudaEventRecord(d->ev[1], st);
   int grid = std::max(1, std::min<int>(d->sm_count * 8, int((fc.nquads + 255) / 256)));
   dev::k_bin_pass<false><<<grid, 256, 0, st>>>(fc, B);
+  dev::k_bin_large<false><<<grid, 256, 0, st>>>(fc, B);
   dev::k_bin_scan<<<1, 1024, 0, st>>>(fc, B);
   dev::k_bin_pass<true><<<grid, 256, 0, st>>>(fc, B);
+  dev::k_bin_large<true><<<grid, 256, 0, st>>>(fc, B);
   dev::k_bin_sort<<<std::min(fc.nbins, d->sm_count * 8), 256, 0, st>>>(fc, B);
-  launches += 4;
+  launches += 6;
   cudaEventRecord(d->ev[2], st);
   return launches;
 }
@@ -2345,7 +2408,7 @@ static void enqueue_raster(DeviceScene* d, Prepared& P, int* launches) {
   launch_extract(d, P.fc, P.B, dev::kPassHigh, P.gcap_tbr, P.gcap_tb, launches);
   cudaEventRecord(d->ev[5], d->stream);
   launch_shade(d, P.fc, P.B, launches);
-  dev::k_finalize<<<1, 1024, 0, d->stream>>>(P.fc, P.B);
+  dev::k_finalize<<<(P.fc.nbins + 255) / 256, 256, 0, d->stream>>>(P.fc, P.B);
   ++*launches;
   cudaEventRecord(d->ev[4], d->stream);
 }
