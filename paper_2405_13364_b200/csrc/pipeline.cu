@@ -2294,6 +2294,10 @@ void check_frame_errors(const dev::Counters& c, const dev::FrameConst& fc) {
 
 void validate_frame(const Scene& s, const RenderOptions& opt) {
   validate_scene(s);
+  for (const veil_material& m : s.materials)
+    if (m.texture >= 0)
+      throw Error(VEIL_ERR_INVALID_ARG,
+                  "textured materials are not supported by the device shading path");
   const veil_render_params& p = opt.params;
   bool reference = p.flags & VEIL_RENDER_REFERENCE;
   if (!reference && p.depth_filter_size < 1)
