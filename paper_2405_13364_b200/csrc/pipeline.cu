@@ -1202,6 +1202,56 @@ __device__ __forceinline__ void shade_walk(const FrameConst& fc, const Buffers& 
   if (kThreshold) *enumerated_out = enumerated;
 }
 
+// Wave walk (no alpha threshold): consecutive THBs whose coverage masks are
+// pairwise disjoint form a wave; each pixel receives at most one sample per
+// wave and waves follow the THB order, so every pixel still sees the
+// reference's per-pixel sequence (raster.cpp:232-267) while a warp step
+// shades up to 32 samples from several triangles (e.g. both triangles of a
+// quad, which are adjacent in the sort order and disjoint).
+template <int KM>
+__device__ __forceinline__ void shade_waves(const FrameConst& fc, const Buffers& B, int px0,
+                                            int py0, const uint32_t* tri_l,
+                                            const uint32_t* mask_l, uint32_t n, PixelOut& o) {
+  const int lane = threadIdx.x & 31;
+  const int px = px0 + (lane & 7), py = py0 + (lane >> 3);
+  RegFilter<KM> f;
+  f.reset();
+  uint32_t r = 0;
+  while (r < n) {
+    uint32_t acc_mask = 0, my_r = 0xffffffffu;
+    do {
+      const uint32_t m = mask_l[r];
+      if (acc_mask & m) break;
+      if ((m >> lane) & 1u) my_r = r;
+      acc_mask |= m;
+      ++r;
+    } while (r < n);
+    if (my_r != 0xffffffffu) {
+      const uint32_t tri = tri_l[my_r];
+      uint32_t qd;
+      float4 col;
+      if (fc.decoded) {
+        col = shade_decoded_bf(fc, B, tri, px, py, &qd);
+      } else {
+        double depth;
+        col = shade_sample(fc, B, tri, px, py, &depth);
+        qd = quantize_depth(depth);
+      }
+      uint64_t pk;
+      float4 pc;
+      bool ooo;
+      if (f.push(fc.df, sample_key(fc, qd, tri), col, &pk, &pc, &ooo)) commit(o, pk, pc, ooo);
+    }
+  }
+  while (f.n > 0) {
+    uint64_t pk;
+    float4 pc;
+    bool ooo;
+    f.pop(&pk, &pc, &ooo);
+    commit(o, pk, pc, ooo);
+  }
+}
+
 __device__ __forceinline__ uint32_t span_mask(uint32_t b, uint32_t l, uint32_t c0, uint32_t c1) {
   // row span [b, l] (bin-local) clipped to block columns [c0, c1] as 8 bits
   if (b > l) return 0u;
@@ -1596,8 +1646,8 @@ __global__ void __launch_bounds__(256, 2) k_shade(FrameConst fc, Buffers B) {
       }
       if (kMode == 2)
         shade_walk<KM, true>(fc, B, hpx0, hpy0, tri_l, mask_l, d.cnt, po, &enumerated);
-      else if (kMode == 0)  // big THBs: broadcast walk
-        shade_walk<KM, false>(fc, B, hpx0, hpy0, tri_l, mask_l, d.cnt, po, &enumerated);
+      else if (kMode == 0)  // big THBs: wave walk
+        shade_waves<KM>(fc, B, hpx0, hpy0, tri_l, mask_l, d.cnt, po);
       else if (d.frags)  // small THBs: dense segments + routing
         shade_segments<KM>(fc, B, hpx0, hpy0, tri_l, mask_l, pre_l, d.cnt, d.frags, route_s[warp], po);
     }
