@@ -95,10 +95,10 @@ struct Counters {
   unsigned int spill_count[2];
   unsigned long long samples, fragments, thb, segments, invalid;
   unsigned long long bins_empty, bins_low, bins_high, bins_propagated;
-  unsigned int pool_next;
+  unsigned long long pool_pair;  // low 32: THB pool entries, high 32: row-list entries
   unsigned int shade_next[2];
   unsigned int seg_count;  // half-blocks queued for the segment-routing kernel
-  unsigned int pad2;
+  unsigned int pad3;
 };
 
 // Decoded per-triangle shading inputs (unpack_color / decode_normal of the
@@ -160,6 +160,9 @@ struct Buffers {
   uint32_t* pool_mask;  // coverage, bit = ly * 8 + lx
   uint32_t* pool_pre;   // exclusive fragment prefix
   uint32_t* seg_queue;  // (bin * 32 + hb) of half-blocks for k_shade<.., 1>
+  uint16_t* pool_slot;  // per THB: row-local triangle slot (index into the row list)
+  uint2* rowd;          // per (bin, block-row): row triangle list (offset, count)
+  uint32_t* rowtri;     // row triangle lists (visible triangle indices)
   Counters* ctr;
 };
 
@@ -959,6 +962,77 @@ __device__ __forceinline__ float4 shade_decoded_bf(const FrameConst& fc, const B
   return make_float4(__fmul_rn(r, a), __fmul_rn(g, a), __fmul_rn(b, a), a);
 }
 
+// A bin-row's triangle, staged in shared memory by k_shade: edge and depth
+// planes plus the decoded shading record (one copy per bin-row instead of
+// one L1/L2 load per sample).
+struct __align__(16) StagedTri {
+  double e[9];
+  double dz[3];
+  float4 c[3];
+  float4 mat;
+  float n[9];
+  uint32_t flags;
+  uint32_t pad[2];
+};
+static_assert(sizeof(StagedTri) == 208, "StagedTri layout");
+constexpr int kStageTris = 224;
+
+__device__ __forceinline__ void stage_triangle(const Buffers& B, uint32_t tri, StagedTri* dst) {
+  const TriRec& t = B.tri[tri];
+  const ShadeRec& sr = B.shade[tri];
+  const double2* e2 = reinterpret_cast<const double2*>(&t.e[0]);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const double2 v = e2[k];
+    dst->e[2 * k] = v.x;
+    dst->e[2 * k + 1] = v.y;
+  }
+  dst->e[8] = t.e[2].c;
+  dst->dz[0] = t.dz.a;
+  dst->dz[1] = t.dz.b;
+  dst->dz[2] = t.dz.c;
+  dst->c[0] = sr.c[0];
+  dst->c[1] = sr.c[1];
+  dst->c[2] = sr.c[2];
+  dst->mat = sr.mat;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const float4 nn = sr.n[k];
+    dst->n[3 * k] = nn.x;
+    dst->n[3 * k + 1] = nn.y;
+    dst->n[3 * k + 2] = nn.z;
+  }
+  dst->flags = sr.flags;
+}
+
+// shade_decoded_bf on a staged triangle (bit-identical).
+__device__ __forceinline__ float4 shade_staged(const FrameConst& fc, const StagedTri& T, int px,
+                                               int py, uint32_t* qd) {
+  const double x = (double)px + 0.5, y = (double)py + 0.5;
+  const Fn3 f0 = {T.e[0], T.e[1], T.e[2]}, f1 = {T.e[3], T.e[4], T.e[5]}, f2 = {T.e[6], T.e[7], T.e[8]};
+  const Fn3 fz = {T.dz[0], T.dz[1], T.dz[2]};
+  const double e0 = eval(f0, x, y), e1 = eval(f1, x, y), e2 = eval(f2, x, y);
+  const double sum = __dadd_rn(__dadd_rn(e0, e1), e2);
+  const double inv = __ddiv_rn(1.0, sum);
+  const float b0 = (float)__dmul_rn(e0, inv), b1 = (float)__dmul_rn(e1, inv),
+              b2 = (float)__dmul_rn(e2, inv);
+  *qd = quantize_depth(eval(fz, x, y));
+  const uint32_t fl = T.flags;
+  const float4 c0 = T.c[0], c1 = T.c[1], c2 = T.c[2];
+  const bool hc = fl & 1u, hn = fl & 2u;
+  float4 color;
+  color.x = hc ? __fadd_rn(__fadd_rn(__fmul_rn(c0.x, b0), __fmul_rn(c1.x, b1)), __fmul_rn(c2.x, b2)) : 1.0f;
+  color.y = hc ? __fadd_rn(__fadd_rn(__fmul_rn(c0.y, b0), __fmul_rn(c1.y, b1)), __fmul_rn(c2.y, b2)) : 1.0f;
+  color.z = hc ? __fadd_rn(__fadd_rn(__fmul_rn(c0.z, b0), __fmul_rn(c1.z, b1)), __fmul_rn(c2.z, b2)) : 1.0f;
+  color.w = hc ? __fadd_rn(__fadd_rn(__fmul_rn(c0.w, b0), __fmul_rn(c1.w, b1)), __fmul_rn(c2.w, b2)) : 1.0f;
+  float n[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+    n[k] = hn ? __fadd_rn(__fadd_rn(__fmul_rn(T.n[k], b0), __fmul_rn(T.n[3 + k], b1)), __fmul_rn(T.n[6 + k], b2))
+              : T.n[k];
+  return light_and_premultiply(fc, n, color, T.mat);
+}
+
 __device__ __forceinline__ uint64_t sample_key(const FrameConst& fc, uint32_t qd, uint32_t tri) {
   // sample_sort_key, raster.hpp:95-97 (32-bit triangle field when extended)
   return fc.extended ? (((uint64_t)qd << 32) | tri) : (((uint64_t)qd << 24) | (tri & 0xffffffu));
@@ -988,6 +1062,9 @@ struct ItemState {
   int ntbr;
   int status;  // 0 ok, 1 overflow (soft), 2 spill, 3 hard error
   int err_code;
+  uint32_t warp_n[4];
+  uint32_t pool_base, row_base;
+  int alloc_ok;
   uint32_t hb_cnt[8];
   uint32_t hb_frags[8];
 };
@@ -1211,7 +1288,8 @@ __device__ __forceinline__ void shade_walk(const FrameConst& fc, const Buffers& 
 template <int KM>
 __device__ __forceinline__ void shade_waves(const FrameConst& fc, const Buffers& B, int px0,
                                             int py0, const uint32_t* tri_l,
-                                            const uint32_t* mask_l, uint32_t n, PixelOut& o) {
+                                            const uint32_t* mask_l, const uint16_t* slot_l,
+                                            const StagedTri* staged, uint32_t n, PixelOut& o) {
   const int lane = threadIdx.x & 31;
   const int px = px0 + (lane & 7), py = py0 + (lane >> 3);
   RegFilter<KM> f;
@@ -1230,7 +1308,9 @@ __device__ __forceinline__ void shade_waves(const FrameConst& fc, const Buffers&
       const uint32_t tri = tri_l[my_r];
       uint32_t qd;
       float4 col;
-      if (fc.decoded) {
+      if (staged) {
+        col = shade_staged(fc, staged[slot_l[my_r]], px, py, &qd);
+      } else if (fc.decoded) {
         col = shade_decoded_bf(fc, B, tri, px, py, &qd);
       } else {
         double depth;
@@ -1415,15 +1495,33 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
         __syncwarp();
       }
   }
+  // one pool allocation per item: the row's triangle list and 2n THB slots
+  // per warp (each tri-block yields <= 1 THB per half), a single 64-bit
+  // atomic for both regions
+  if (lane == 0) st->warp_n[warp] = ok ? n : 0u;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    st->alloc_ok = 0;
+    if (!st->status) {
+      const uint32_t tot = 2u * (st->warp_n[0] + st->warp_n[1] + st->warp_n[2] + st->warp_n[3]);
+      const unsigned long long old =
+          atomicAdd(&B.ctr->pool_pair, ((unsigned long long)ntbr << 32) | tot);
+      const uint32_t pb = (uint32_t)old, rb = (uint32_t)(old >> 32);
+      if ((unsigned long long)pb + tot > fc.pool_cap || (unsigned long long)rb + ntbr > fc.pool_cap) {
+        atomicOr(&B.ctr->error, 8u);  // pool capacity: grow and re-run
+      } else {
+        st->pool_base = pb;
+        st->row_base = rb;
+        st->alloc_ok = 1;
+      }
+    }
+  }
+  __syncthreads();
   uint32_t nthb[2] = {0, 0}, frags[2] = {0, 0};
-  uint32_t pbase = 0;
-  if (ok && n) {
-    // each tri-block yields <= 1 THB per half: reserve 2n pool entries
-    if (lane == 0) pbase = atomicAdd(&B.ctr->pool_next, 2u * n);
-    pbase = __shfl_sync(0xffffffffu, pbase, 0);
-    if ((unsigned long long)pbase + 2ull * n > (unsigned long long)fc.pool_cap) {
-      if (lane == 0) atomicOr(&B.ctr->error, 8u);  // pool capacity: grow and re-run
-    } else {
+  uint32_t pbase = st->pool_base;
+  for (int w = 0; w < warp; ++w) pbase += 2u * st->warp_n[w];
+  if (ok && n && st->alloc_ok) {
+    {
       for (uint32_t base = 0; base < n; base += 32) {
         const uint32_t k = base + lane;
         uint32_t hm[2] = {0u, 0u};
@@ -1454,6 +1552,7 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
             B.pool_tri[at] = tri;
             B.pool_mask[at] = hm[h];
             B.pool_pre[at] = frags[h] + incl - fr;
+            B.pool_slot[at] = k < n ? refs[k] : 0;
           }
           nthb[h] += __popc(m);
           frags[h] += __shfl_sync(0xffffffffu, incl, 31);
@@ -1470,7 +1569,10 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
     }
   }
   __syncthreads();
-  if (st->status) return;
+  if (st->status || !st->alloc_ok) return;
+  // the block-row's triangle list (TBR order): k_shade stages these records
+  if (threadIdx.x == 0) B.rowd[(size_t)bin * 4 + row] = make_uint2(st->row_base, ntbr);
+  for (uint32_t i = threadIdx.x; i < ntbr; i += blockDim.x) B.rowtri[st->row_base + i] = V.tbr[i].tri;
   if (lane < 2) {
     HbDesc d;
     d.off = pbase + (uint32_t)lane * n;
@@ -1584,6 +1686,9 @@ __global__ void __launch_bounds__(256, 2) k_shade(FrameConst fc, Buffers B) {
   __shared__ uint32_t stage_tri[8][kShadeStage];
   __shared__ uint32_t stage_mask[8][kShadeStage];
   __shared__ uint32_t stage_pre[8][kShadeStage];
+  __shared__ uint16_t stage_slot[8][kShadeStage];
+  extern __shared__ __align__(16) uint8_t shade_dyn[];  // mode 0: staged row triangles
+  StagedTri* row_tris = reinterpret_cast<StagedTri*>(shade_dyn);
   __shared__ uint32_t route_s[8][32];
   __shared__ uint32_t item_s;
   if (B.ctr->error) return;
@@ -1611,6 +1716,16 @@ __global__ void __launch_bounds__(256, 2) k_shade(FrameConst fc, Buffers B) {
     const int bxi = bin % fc.bins_x, byi = bin / fc.bins_x;
     if (!(fc.world <= 1 || ((bxi + 3 * byi) % fc.world) == fc.rank)) continue;
     const int hb = (int)(item & 31u);  // reference half-block index in the bin
+    // mode 0: stage the bin-row's triangle records (one copy per row)
+    bool staged_ok = false;
+    if (kMode == 0 && fc.decoded && B.cat[bin] != 0) {
+      const uint2 rd = B.rowd[(size_t)bin * 4 + row];
+      staged_ok = rd.y <= (uint32_t)kStageTris;
+      if (staged_ok)
+        for (uint32_t j = threadIdx.x; j < rd.y; j += blockDim.x)
+          stage_triangle(B, B.rowtri[rd.x + j], &row_tris[j]);
+      __syncthreads();
+    }
     const int block = hb >> 1;
     const int hpx0 = bxi * kBin + (block & 3) * 8;
     const int hpy0 = byi * kBin + (block >> 2) * 8 + (hb & 1) * 4;
@@ -1633,21 +1748,25 @@ __global__ void __launch_bounds__(256, 2) k_shade(FrameConst fc, Buffers B) {
       const uint32_t* tri_l = B.pool_tri + d.off;
       const uint32_t* mask_l = B.pool_mask + d.off;
       const uint32_t* pre_l = B.pool_pre + d.off;
+      const uint16_t* slot_l = B.pool_slot + d.off;
       if (d.cnt <= (uint32_t)kShadeStage) {
         for (uint32_t i = lane; i < d.cnt; i += 32) {
           stage_tri[warp][i] = tri_l[i];
           stage_mask[warp][i] = mask_l[i];
           stage_pre[warp][i] = pre_l[i];
+          stage_slot[warp][i] = slot_l[i];
         }
         __syncwarp();
         tri_l = stage_tri[warp];
         mask_l = stage_mask[warp];
         pre_l = stage_pre[warp];
+        slot_l = stage_slot[warp];
       }
       if (kMode == 2)
         shade_walk<KM, true>(fc, B, hpx0, hpy0, tri_l, mask_l, d.cnt, po, &enumerated);
       else if (kMode == 0)  // big THBs: wave walk
-        shade_waves<KM>(fc, B, hpx0, hpy0, tri_l, mask_l, d.cnt, po);
+        shade_waves<KM>(fc, B, hpx0, hpy0, tri_l, mask_l, slot_l, staged_ok ? row_tris : nullptr,
+                        d.cnt, po);
       else if (d.frags)  // small THBs: dense segments + routing
         shade_segments<KM>(fc, B, hpx0, hpy0, tri_l, mask_l, pre_l, d.cnt, d.frags, route_s[warp], po);
     }
@@ -1843,7 +1962,8 @@ struct DeviceScene {
   DevBuf pos, vcol, vnrm, quads, qmat, mats;
   DevBuf block_cnt, block_off, vq_src, vq_box, vq_flags, vq_mat, vq_col, vq_nrm, tri, tri_meta, shade;
   DevBuf qcnt, tcnt, off, qcur, tcur, cat, prop, items, slots, spill0, spill1, scratch, fb, mask,
-      hash, emit, ctr, tile_ids, hbd, pool_tri, pool_mask, pool_pre, seg_queue;
+      hash, emit, ctr, tile_ids, hbd, pool_tri, pool_mask, pool_pre, seg_queue, pool_slot, rowd,
+      rowtri;
   uint32_t items_cap = 0;
   uint32_t pool_cap = 0;
   bool extract_configured = false;
@@ -2037,12 +2157,20 @@ void launch_extract(DeviceScene* d, const dev::FrameConst& fc, const dev::Buffer
 template <int KM, int kMode>
 void launch_shade_mode(DeviceScene* d, const dev::FrameConst& fc, const dev::Buffers& B,
                        int* launches) {
+  const size_t dyn = kMode == 0 ? size_t(dev::kStageTris) * sizeof(dev::StagedTri) : 0;
+  static bool configured = false;  // per instantiation
+  if (!configured && dyn) {
+    ck(cudaFuncSetAttribute(dev::k_shade<KM, kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            int(dyn)),
+       "cudaFuncSetAttribute");
+    configured = true;
+  }
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_shade<KM, kMode>, 256, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_shade<KM, kMode>, 256, dyn);
   const long long items = kMode == 1 ? ((long long)fc.nbins * 32 + 7) / 8 : (long long)fc.nbins * 4;
   const int grid = int(std::max<long long>(1, std::min<long long>((long long)std::max(1, per_sm) * d->sm_count,
                                                                    items)));
-  dev::k_shade<KM, kMode><<<grid, 256, 0, d->stream>>>(fc, B);
+  dev::k_shade<KM, kMode><<<grid, 256, dyn, d->stream>>>(fc, B);
   ck(cudaGetLastError(), "k_shade launch");
   ++*launches;
 }
@@ -2190,10 +2318,13 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   d->ctr.ensure(sizeof(dev::Counters));
   d->hbd.ensure(nb * 32 * sizeof(dev::HbDesc));
   d->seg_queue.ensure(nb * 32 * 4);
+  d->rowd.ensure(nb * 4 * sizeof(uint2));
   if (d->pool_cap == 0) d->pool_cap = std::max<uint32_t>(1u << 22, uint32_t(std::min<size_t>(nb * 2048, 1u << 26)));
   d->pool_tri.ensure(size_t(d->pool_cap) * 4);
   d->pool_mask.ensure(size_t(d->pool_cap) * 4);
   d->pool_pre.ensure(size_t(d->pool_cap) * 4);
+  d->pool_slot.ensure(size_t(d->pool_cap) * 2);
+  d->rowtri.ensure(size_t(d->pool_cap) * 4);
   fc.pool_cap = d->pool_cap;
   // global scratch for spilled items: capacities follow the active limits
   P.gcap_tbr = std::min<uint32_t>(std::max(fc.low.tbr, fc.high.tbr), 1u << 16);
@@ -2251,6 +2382,9 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   B.pool_mask = d->pool_mask.as<uint32_t>();
   B.pool_pre = d->pool_pre.as<uint32_t>();
   B.seg_queue = d->seg_queue.as<uint32_t>();
+  B.pool_slot = d->pool_slot.as<uint16_t>();
+  B.rowd = d->rowd.as<uint2>();
+  B.rowtri = d->rowtri.as<uint32_t>();
   B.ctr = d->ctr.as<dev::Counters>();
   return P;
 }
@@ -2499,7 +2633,7 @@ void render_frame(const Scene& s, const RenderOptions& opt, RenderOutput* out) {
       std::vector<uint8_t> cat(nb);
       ck(cudaMemcpy(hbd.data(), P.B.hbd, nb * 32 * sizeof(dev::HbDesc), cudaMemcpyDeviceToHost), "dump");
       ck(cudaMemcpy(cat.data(), P.B.cat, nb, cudaMemcpyDeviceToHost), "dump");
-      const size_t used = std::min<size_t>(c.pool_next, d->pool_cap);
+      const size_t used = std::min<size_t>(uint32_t(c.pool_pair), d->pool_cap);
       std::vector<uint32_t> ptri(used), pmask(used), ppre(used);
       if (used) {
         ck(cudaMemcpy(ptri.data(), P.B.pool_tri, used * 4, cudaMemcpyDeviceToHost), "dump");
