@@ -136,6 +136,7 @@ struct Buffers {
   uint4* vq_nrm;
   TriRec* tri;
   uint4* tri_meta;  // flat normal, material, quad index, tri | valid << 8
+  uint32_t* tri_y;  // int16 y_min | int16 y_max << 16 (empty range when invalid)
   struct ShadeRec* shade;  // per triangle, when FrameConst::decoded
   // bins
   uint32_t* qcnt;
@@ -477,6 +478,9 @@ __global__ void __launch_bounds__(kSetupBlock) k_setup_write(FrameConst fc, Buff
     }
     B.tri[slot * 2 + t] = rec;
     B.tri_meta[slot * 2 + t] = meta;
+    B.tri_y[slot * 2 + t] = valid ? ((uint32_t)(uint16_t)(int16_t)rec.y_min |
+                                     ((uint32_t)(uint16_t)(int16_t)rec.y_max << 16))
+                                  : 0x00000001u;  // y_min 1 > y_max 0
     if (fc.decoded && valid) {
       // corner slots (0,1,2) / (0,2,3), shading.cpp:41-44
       const uint32_t cw[3] = {col.x, t == 0 ? col.y : col.z, t == 0 ? col.z : col.w};
@@ -1065,6 +1069,7 @@ struct ItemState {
   uint32_t warp_n[4];
   uint32_t pool_base, row_base;
   int alloc_ok;
+  uint32_t ncand;
   uint32_t hb_cnt[8];
   uint32_t hb_frags[8];
 };
@@ -1341,6 +1346,43 @@ __device__ __forceinline__ uint32_t span_mask(uint32_t b, uint32_t l, uint32_t c
   return ((2u << (l - b)) - 1u) << (b - c0);
 }
 
+// Warp bitonic sort of N = 32*J 64-bit keys held in registers, strided
+// layout (element i = j*32 + lane in v[j]); ascending.
+template <int J>
+__device__ __forceinline__ void warp_bitonic(uint64_t (&v)[4], int lane) {
+  constexpr int N = 32 * J;
+#pragma unroll
+  for (int k = 2; k <= N; k <<= 1) {
+#pragma unroll
+    for (int m = k >> 1; m > 0; m >>= 1) {
+      if (m >= 32) {
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+          const int jp = j ^ (m >> 5);
+          if (jp > j) {
+            const int i = j * 32 + lane;
+            const bool up = (i & k) == 0;
+            const uint64_t x = v[j], y = v[jp];
+            const bool sw = (x > y) == up;
+            v[j] = sw ? y : x;
+            v[jp] = sw ? x : y;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+          const int i = j * 32 + lane;
+          const uint64_t x = v[j];
+          const uint64_t y = __shfl_xor_sync(0xffffffffu, x, m);
+          const bool up = (i & k) == 0, lower = (lane & m) == 0;
+          const uint64_t lo = x < y ? x : y, hi = x < y ? y : x;
+          v[j] = (lower == up) ? lo : hi;
+        }
+      }
+    }
+  }
+}
+
 // One (bin, block-row) extraction item: phases A and B of the reference's
 // rasterize_bin (raster.cpp:41-199). Tri-half-block lists go to the global
 // THB pool (L2-resident) with one descriptor per half-block; shading runs
@@ -1365,52 +1407,79 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
   }
   __syncthreads();
 
-  // ---- phase A: tri-block-rows of this block-row (raster.cpp:41-98)
+  // ---- phase A: tri-block-rows of this block-row (raster.cpp:41-98).
+  // Candidates (valid triangles whose y range meets the block-row) are first
+  // compacted with warp ballots, so the FP64 row-span loop runs dense.
   const uint32_t nq = B.qcnt[bin], nt = B.tcnt[bin], o = B.off[bin];
   const uint32_t T = 2 * nq + nt;
-  for (uint32_t i = threadIdx.x; i < T; i += blockDim.x) {
-    uint32_t ti, large;
-    if (i < 2 * nq) {
-      ti = B.items[o + (i >> 1)] * 2 + (i & 1);
-      large = 0;
-    } else {
-      ti = B.items[o + nq + (i - 2 * nq)];
-      large = 1;
-    }
-    const uint4 meta = B.tri_meta[ti];
-    if (!(meta.w & 0x100u)) continue;
-    const TriRec& t = B.tri[ti];
-    int yb = max(max(t.y_min, py0), ry0), ye = min(min(t.y_max, py_last), ry1);
-    if (yb > ye) continue;
-    uint32_t rb0 = 0x1f1f1f1fu, rb1 = 0x1f1f1f1fu, rl0 = 0u, rl1 = 0u, cols = 0;
-    for (int py = yb; py <= ye; ++py) {
-      int b, l;
-      if (!row_span(t, py, px0, px_last, &b, &l)) continue;
-      const int ly = py - ry0;
-      const uint32_t bb = (uint32_t)(b - px0), ll = (uint32_t)(l - px0);
-      const int sh8 = (ly & 3) * 8;
-      const uint32_t keep = ~(0xffu << sh8);
-      if (ly < 4) {
-        rb0 = (rb0 & keep) | (bb << sh8);
-        rl0 = (rl0 & keep) | (ll << sh8);
-      } else {
-        rb1 = (rb1 & keep) | (bb << sh8);
-        rl1 = (rl1 & keep) | (ll << sh8);
+  uint32_t* cand = reinterpret_cast<uint32_t*>(V.keys);  // keys are free until phase B
+  const uint32_t cand_cap = 8u * cap_tb;
+  for (uint32_t round = 0; round < T; round += cand_cap) {
+    const uint32_t end = min(T, round + cand_cap);
+    if (threadIdx.x == 0) st->ncand = 0;
+    __syncthreads();
+    for (uint32_t i0 = round; i0 < end; i0 += blockDim.x) {
+      const uint32_t i = i0 + threadIdx.x;
+      bool keep = false;
+      uint32_t code = 0;
+      if (i < end) {
+        uint32_t ti, large;
+        if (i < 2 * nq) {
+          ti = B.items[o + (i >> 1)] * 2 + (i & 1);
+          large = 0;
+        } else {
+          ti = B.items[o + nq + (i - 2 * nq)];
+          large = 1;
+        }
+        const uint32_t yy = __ldg(&B.tri_y[ti]);
+        const int y_lo = (int)(int16_t)(yy & 0xffffu), y_hi = (int)(int16_t)(yy >> 16);
+        keep = max(y_lo, ry0) <= min(y_hi, ry1);
+        code = ti | (large << 31);
       }
-      cols |= ((2u << (ll >> 3)) - 1u) & ~((1u << (bb >> 3)) - 1u);
+      const unsigned m = __ballot_sync(0xffffffffu, keep);
+      uint32_t wbase = 0;
+      if (lane == 0 && m) wbase = atomicAdd(&st->ncand, (uint32_t)__popc(m));
+      wbase = __shfl_sync(0xffffffffu, wbase, 0);
+      if (keep) cand[wbase + __popc(m & ((1u << lane) - 1u))] = code;
     }
-    if (!cols) continue;
-    const int slot = atomicAdd(&st->ntbr, 1);
-    if ((uint32_t)slot < cap_tbr) {
-      Tbr rec;
-      rec.tri = ti;
-      rec.meta = cols | (large << 4);
-      rec.b[0] = rb0;
-      rec.b[1] = rb1;
-      rec.l[0] = rl0;
-      rec.l[1] = rl1;
-      V.tbr[slot] = rec;
+    __syncthreads();
+    const uint32_t nc = st->ncand;
+    for (uint32_t j = threadIdx.x; j < nc; j += blockDim.x) {
+      const uint32_t code = cand[j];
+      const uint32_t ti = code & 0x7fffffffu, large = code >> 31;
+      const TriRec& t = B.tri[ti];
+      const int yb = max(t.y_min, ry0), ye = min(t.y_max, ry1);
+      uint32_t rb0 = 0x1f1f1f1fu, rb1 = 0x1f1f1f1fu, rl0 = 0u, rl1 = 0u, cols = 0;
+      for (int py = yb; py <= ye; ++py) {
+        int b, l;
+        if (!row_span(t, py, px0, px_last, &b, &l)) continue;
+        const int ly = py - ry0;
+        const uint32_t bb = (uint32_t)(b - px0), ll = (uint32_t)(l - px0);
+        const int sh8 = (ly & 3) * 8;
+        const uint32_t keepm = ~(0xffu << sh8);
+        if (ly < 4) {
+          rb0 = (rb0 & keepm) | (bb << sh8);
+          rl0 = (rl0 & keepm) | (ll << sh8);
+        } else {
+          rb1 = (rb1 & keepm) | (bb << sh8);
+          rl1 = (rl1 & keepm) | (ll << sh8);
+        }
+        cols |= ((2u << (ll >> 3)) - 1u) & ~((1u << (bb >> 3)) - 1u);
+      }
+      if (!cols) continue;
+      const int slot = atomicAdd(&st->ntbr, 1);
+      if ((uint32_t)slot < cap_tbr) {
+        Tbr rec;
+        rec.tri = ti;
+        rec.meta = cols | (large << 4);
+        rec.b[0] = rb0;
+        rec.b[1] = rb1;
+        rec.l[0] = rl0;
+        rec.l[1] = rl1;
+        V.tbr[slot] = rec;
+      }
     }
+    __syncthreads();
   }
   __syncthreads();
   const uint32_t ntbr = (uint32_t)st->ntbr;
@@ -1428,6 +1497,7 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
   const double bpx0 = (double)(px0 + warp * 8), bpy0 = (double)(py0 + row * 8);
   uint64_t* keys = V.keys + (size_t)warp * cap_tb;
   uint16_t* refs = V.refs + (size_t)warp * cap_tb;
+  const bool packable = cap_tbr <= 16384u;  // TBR index fits the key's low 14 bits
   uint32_t n = 0;
   for (uint32_t base = 0; base < ntbr; base += 32) {
     const uint32_t i = base + lane;
@@ -1457,8 +1527,11 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
           qd = quantize_depth(eval(B.tri[rw.tri].dz, cx, cy));
         }
         // (depth, is_large, triangle) orders exactly like the reference's
-        // (depth, selection index): selection order is bin-list order.
-        keys[pos] = ((uint64_t)qd << 33) | ((uint64_t)((rw.meta >> 4) & 1u) << 32) | rw.tri;
+        // (depth, selection index): selection order is bin-list order. The
+        // packed form carries the TBR reference in the low 14 bits.
+        const uint64_t large = (rw.meta >> 4) & 1u;
+        keys[pos] = packable ? (((uint64_t)qd << 42) | (large << 41) | ((uint64_t)rw.tri << 14) | i)
+                             : (((uint64_t)qd << 33) | (large << 32) | rw.tri);
         refs[pos] = (uint16_t)i;
       }
     }
@@ -1471,7 +1544,16 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
   }
   __syncwarp();
   const bool ok = n <= lim.tb && n <= cap_tb;
-  if (ok && n > 1) {
+  const bool in_regs = ok && packable && n <= 128;
+  uint64_t v[4] = {~0ull, ~0ull, ~0ull, ~0ull};
+  if (in_regs) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if ((uint32_t)(j * 32 + lane) < n) v[j] = keys[j * 32 + lane];
+    if (n <= 32) warp_bitonic<1>(v, lane);
+    else if (n <= 64) warp_bitonic<2>(v, lane);
+    else warp_bitonic<4>(v, lane);
+  } else if (ok && n > 1) {
     uint32_t N = 1;
     while (N < n) N <<= 1;
     for (uint32_t i = n + lane; i < N; i += 32) keys[i] = ~0ull, refs[i] = 0;
@@ -1521,43 +1603,55 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
   uint32_t pbase = st->pool_base;
   for (int w = 0; w < warp; ++w) pbase += 2u * st->warp_n[w];
   if (ok && n && st->alloc_ok) {
-    {
+    auto chunk = [&](uint32_t k, uint32_t ref) {
+      uint32_t hm[2] = {0u, 0u};
+      uint32_t tri = 0;
+      if (k < n) {
+        const Tbr& rw = V.tbr[ref];
+        tri = rw.tri;
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int y = 0; y < 4; ++y)
+            hm[h] |= span_mask(byte_of(rw.b, h * 4 + y), byte_of(rw.l, h * 4 + y), c0, c1) << (8 * y);
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t fr = __popc(hm[h]);
+        const bool ne = fr > 0;
+        const unsigned m = __ballot_sync(0xffffffffu, ne);
+        const uint32_t pos = nthb[h] + __popc(m & ((1u << lane) - 1u));
+        uint32_t incl = fr;  // inclusive scan of fragment counts
+#pragma unroll
+        for (int s2 = 1; s2 < 32; s2 <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, incl, s2);
+          if (lane >= s2) incl += y;
+        }
+        if (ne) {
+          const size_t at = (size_t)pbase + (size_t)h * n + pos;
+          B.pool_tri[at] = tri;
+          B.pool_mask[at] = hm[h];
+          B.pool_pre[at] = frags[h] + incl - fr;
+          B.pool_slot[at] = (uint16_t)ref;
+        }
+        nthb[h] += __popc(m);
+        frags[h] += __shfl_sync(0xffffffffu, incl, 31);
+      }
+    };
+    if (in_regs) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if ((uint32_t)(j * 32) < n) {
+          const uint32_t k = j * 32 + lane;
+          chunk(k, k < n ? (uint32_t)(v[j] & 0x3fffu) : 0u);
+        }
+    } else {
       for (uint32_t base = 0; base < n; base += 32) {
         const uint32_t k = base + lane;
-        uint32_t hm[2] = {0u, 0u};
-        uint32_t tri = 0;
-        if (k < n) {
-          const Tbr& rw = V.tbr[refs[k]];
-          tri = rw.tri;
-#pragma unroll
-          for (int h = 0; h < 2; ++h)
-#pragma unroll
-            for (int y = 0; y < 4; ++y)
-              hm[h] |= span_mask(byte_of(rw.b, h * 4 + y), byte_of(rw.l, h * 4 + y), c0, c1) << (8 * y);
-        }
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const uint32_t fr = __popc(hm[h]);
-          const bool ne = fr > 0;
-          const unsigned m = __ballot_sync(0xffffffffu, ne);
-          const uint32_t pos = nthb[h] + __popc(m & ((1u << lane) - 1u));
-          uint32_t incl = fr;  // inclusive scan of fragment counts
-#pragma unroll
-          for (int s = 1; s < 32; s <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, s);
-            if (lane >= s) incl += y;
-          }
-          if (ne) {
-            const size_t at = (size_t)pbase + (size_t)h * n + pos;
-            B.pool_tri[at] = tri;
-            B.pool_mask[at] = hm[h];
-            B.pool_pre[at] = frags[h] + incl - fr;
-            B.pool_slot[at] = k < n ? refs[k] : 0;
-          }
-          nthb[h] += __popc(m);
-          frags[h] += __shfl_sync(0xffffffffu, incl, 31);
-        }
+        chunk(k, k < n ? (uint32_t)refs[k] : 0u);
       }
+    }
+    {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         if (nthb[h] > lim.thb) {
@@ -1960,7 +2054,8 @@ struct DeviceScene {
   uint64_t uploaded_version = 0;
   uint32_t nverts = 0, nquads = 0;
   DevBuf pos, vcol, vnrm, quads, qmat, mats;
-  DevBuf block_cnt, block_off, vq_src, vq_box, vq_flags, vq_mat, vq_col, vq_nrm, tri, tri_meta, shade;
+  DevBuf block_cnt, block_off, vq_src, vq_box, vq_flags, vq_mat, vq_col, vq_nrm, tri, tri_meta, shade,
+      tri_y;
   DevBuf qcnt, tcnt, off, qcur, tcur, cat, prop, items, slots, spill0, spill1, scratch, fb, mask,
       hash, emit, ctr, tile_ids, hbd, pool_tri, pool_mask, pool_pre, seg_queue, pool_slot, rowd,
       rowtri;
@@ -2271,7 +2366,9 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   if (p.limit_low_frags) fc.low.frags = p.limit_low_frags;
   if (p.limit_high_tbr) fc.high.tbr = p.limit_high_tbr;
   if (p.limit_high_thb) fc.high.thb = p.limit_high_thb;
-  fc.tri_cap = s.extended ? 0x80000000u : (1u << 24);
+  // visible-triangle index space: 24 bits like the reference (setup.hpp:32),
+  // 27 bits with extended limits (sort keys pack 22 depth + 1 + 27 + 14 bits)
+  fc.tri_cap = s.extended ? (1u << 27) : (1u << 24);
   fc.rank = opt.rank;
   fc.world = opt.world_size;
   fc.dump = opt.dump ? 1 : 0;
@@ -2290,6 +2387,7 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   d->vq_nrm.ensure(size_t(Q) * 16);
   d->tri.ensure(size_t(Q) * 2 * sizeof(dev::TriRec));
   d->tri_meta.ensure(size_t(Q) * 2 * 16);
+  d->tri_y.ensure(size_t(Q) * 2 * 4);
   // Decoded shading records pay off when triangles cover many pixels (each
   // record is read by every sample of its triangle): >= 8 px per quad at
   // depth complexity 1.
@@ -2359,6 +2457,7 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   B.vq_nrm = d->vq_nrm.as<uint4>();
   B.tri = d->tri.as<dev::TriRec>();
   B.tri_meta = d->tri_meta.as<uint4>();
+  B.tri_y = d->tri_y.as<uint32_t>();
   B.shade = fc.decoded ? d->shade.as<dev::ShadeRec>() : nullptr;
   B.qcnt = d->qcnt.as<uint32_t>();
   B.tcnt = d->tcnt.as<uint32_t>();
