@@ -459,43 +459,87 @@ __global__ void __launch_bounds__(kSetupBlock) k_setup_write(FrameConst fc, Buff
   if (has_n) nrm = make_uint4(B.vnrm[idx.x], B.vnrm[idx.y], B.vnrm[idx.z], B.vnrm[idx.w]);
   B.vq_col[slot] = col;
   B.vq_nrm[slot] = nrm;
-#pragma unroll
-  for (int t = 0; t < 2; ++t) {
+}
+
+// Triangle setups (setup.cpp:305-349, compute_triangle_setup 209-239): one
+// thread per visible triangle, re-projecting its quad's corners exactly as the
+// reference's phase 2 does. The warp's 128-byte records are staged in shared
+// memory and written back as 512-byte contiguous runs (coalesced stores).
+constexpr int kTriBlock = 128;
+
+__global__ void __launch_bounds__(kTriBlock) k_setup_tris(FrameConst fc, Buffers B) {
+  __shared__ __align__(16) TriRec stage[kTriBlock];
+  if (B.ctr->error & 1u) return;
+  const uint32_t nt = 2u * B.ctr->nvis;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint32_t base = blockIdx.x * kTriBlock; base < nt; base += gridDim.x * kTriBlock) {
+    const uint32_t ti = base + threadIdx.x;
     TriRec rec;
+    memset(&rec, 0, sizeof rec);
+    rec.y_min = 0;
+    rec.y_max = -1;
     uint4 meta = make_uint4(0, 0, 0, 0);
     bool valid = false;
-    if (o.flags & (1u << t)) {
-      memset(&rec, 0, sizeof rec);
-      rec.y_min = 0;
-      rec.y_max = -1;
-    } else {
-      const int k1 = t == 0 ? 1 : 2, k2 = t == 0 ? 2 : 3;
-      triangle_setup(fc, clip[0], clip[k1], clip[k2], &rec, &valid);
-      meta.x = flat_normal(p[0], p[k1], p[k2]);
-      meta.y = mat;
-      meta.z = slot;
-      meta.w = (uint32_t)t | (valid ? 0x100u : 0u);
-    }
-    B.tri[slot * 2 + t] = rec;
-    B.tri_meta[slot * 2 + t] = meta;
-    B.tri_y[slot * 2 + t] = valid ? ((uint32_t)(uint16_t)(int16_t)rec.y_min |
-                                     ((uint32_t)(uint16_t)(int16_t)rec.y_max << 16))
-                                  : 0x00000001u;  // y_min 1 > y_max 0
-    if (fc.decoded && valid) {
-      // corner slots (0,1,2) / (0,2,3), shading.cpp:41-44
-      const uint32_t cw[3] = {col.x, t == 0 ? col.y : col.z, t == 0 ? col.z : col.w};
-      const uint32_t nw[3] = {nrm.x, t == 0 ? nrm.y : nrm.z, t == 0 ? nrm.z : nrm.w};
-      ShadeRec sr;
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        sr.c[k] = make_float4(lut_c(cw[k], 0), lut_c(cw[k], 8), lut_c(cw[k], 16), lut_c(cw[k], 24));
-        const uint32_t w = has_n ? nw[k] : meta.x;
-        sr.n[k] = make_float4(lut_n(w, 0), lut_n(w, 10), lut_n(w, 20), 0.0f);
+    uint32_t slot = 0, t = 0, vf = 0, mat = 0;
+    if (ti < nt) {
+      slot = ti >> 1;
+      t = ti & 1u;
+      vf = B.vq_flags[slot];
+      if (!((vf >> 4) & (1u << t))) {  // not individually culled
+        const uint32_t q = B.vq_src[slot];
+        mat = B.vq_mat[slot];
+        const uint4 idx = B.quads[q];
+        const uint32_t i1 = t == 0 ? idx.y : idx.z, i2 = t == 0 ? idx.z : idx.w;
+        const float4 p0 = __ldg(&B.pos[idx.x]), p1 = __ldg(&B.pos[i1]), p2 = __ldg(&B.pos[i2]);
+        double c0[4], c1[4], c2[4];
+        to_clip(fc.m, p0.x, p0.y, p0.z, c0);
+        to_clip(fc.m, p1.x, p1.y, p1.z, c1);
+        to_clip(fc.m, p2.x, p2.y, p2.z, c2);
+        triangle_setup(fc, c0, c1, c2, &rec, &valid);
+        meta.x = flat_normal(p0, p1, p2);
+        meta.y = mat;
+        meta.z = slot;
+        meta.w = t | (valid ? 0x100u : 0u);
       }
-      sr.mat = make_float4(md.base[0], md.base[1], md.base[2], md.opacity);
-      sr.flags = (has_c ? 1u : 0u) | (has_n ? 2u : 0u);
-      sr.pad[0] = sr.pad[1] = sr.pad[2] = 0;
-      B.shade[slot * 2 + t] = sr;
+    }
+    stage[threadIdx.x] = rec;
+    __syncwarp();
+    {  // coalesced copy-out of this warp's 32 records (4 KB)
+      const uint32_t wbase = base + (uint32_t)warp * 32u;
+      const uint4* src = reinterpret_cast<const uint4*>(&stage[warp * 32]);
+      uint4* dst = reinterpret_cast<uint4*>(B.tri + wbase);
+      const uint32_t nrec = wbase < nt ? min(32u, nt - wbase) : 0u;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t e = (uint32_t)k * 32u + lane;  // 16-byte chunk index within the warp
+        if (e < nrec * 8u) dst[e] = src[e];
+      }
+    }
+    __syncwarp();
+    if (ti < nt) {
+      B.tri_meta[ti] = meta;
+      B.tri_y[ti] = valid ? ((uint32_t)(uint16_t)(int16_t)rec.y_min |
+                             ((uint32_t)(uint16_t)(int16_t)rec.y_max << 16))
+                          : 0x00000001u;  // y_min 1 > y_max 0
+      if (fc.decoded && valid) {
+        // corner slots (0,1,2) / (0,2,3), shading.cpp:41-44
+        const MatDev md = B.mats[mat];
+        const bool has_c = vf & 2u, has_n = vf & 4u;
+        const uint4 col = B.vq_col[slot], nrm = B.vq_nrm[slot];
+        const uint32_t cw[3] = {col.x, t == 0 ? col.y : col.z, t == 0 ? col.z : col.w};
+        const uint32_t nw[3] = {nrm.x, t == 0 ? nrm.y : nrm.z, t == 0 ? nrm.z : nrm.w};
+        ShadeRec sr;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          sr.c[k] = make_float4(lut_c(cw[k], 0), lut_c(cw[k], 8), lut_c(cw[k], 16), lut_c(cw[k], 24));
+          const uint32_t w = has_n ? nw[k] : meta.x;
+          sr.n[k] = make_float4(lut_n(w, 0), lut_n(w, 10), lut_n(w, 20), 0.0f);
+        }
+        sr.mat = make_float4(md.base[0], md.base[1], md.base[2], md.opacity);
+        sr.flags = (has_c ? 1u : 0u) | (has_n ? 2u : 0u);
+        sr.pad[0] = sr.pad[1] = sr.pad[2] = 0;
+        B.shade[ti] = sr;
+      }
     }
   }
 }
@@ -2503,7 +2547,10 @@ int enqueue_front(DeviceScene* d, Prepared& P) {
     dev::k_setup_count<<<P.nblocks, dev::kSetupBlock, 0, st>>>(fc, B);
     dev::k_scan_blocks<<<1, 1024, 0, st>>>(fc, B, P.nblocks);
     dev::k_setup_write<<<P.nblocks, dev::kSetupBlock, 0, st>>>(fc, B);
-    launches += 3;
+    const int tgrid = int(std::min<long long>(((long long)fc.nquads * 2 + dev::kTriBlock - 1) / dev::kTriBlock,
+                                              (long long)d->sm_count * 32));
+    dev::k_setup_tris<<<std::max(1, tgrid), dev::kTriBlock, 0, st>>>(fc, B);
+    launches += 4;
   }
   cudaEventRecord(d->ev[1], st);
   int grid = std::max(1, std::min<int>(d->sm_count * 8, int((fc.nquads + 255) / 256)));
