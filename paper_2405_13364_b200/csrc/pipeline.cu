@@ -80,6 +80,7 @@ struct FrameConst {
   int dump;
   int decoded;  // setup writes per-triangle decoded shading records
   uint32_t pool_cap;
+  uint32_t lpairs_cap;
   int debug;  // experiment switch (VEIL_DEBUG_SHADE), 0 in production
 };
 
@@ -98,7 +99,7 @@ struct Counters {
   unsigned long long pool_pair;  // low 32: THB pool entries, high 32: row-list entries
   unsigned int shade_next[2];
   unsigned int seg_count;  // half-blocks queued for the segment-routing kernel
-  unsigned int pad3;
+  unsigned int large_pairs;  // (large triangle, bin row) work pairs
 };
 
 // Decoded per-triangle shading inputs (unpack_color / decode_normal of the
@@ -164,6 +165,7 @@ struct Buffers {
   uint16_t* pool_slot;  // per THB: row-local triangle slot (index into the row list)
   uint2* rowd;          // per (bin, block-row): row triangle list (offset, count)
   uint32_t* rowtri;     // row triangle lists (visible triangle indices)
+  uint2* lpairs;        // (large triangle, bin row) pairs for k_bin_large
   Counters* ctr;
 };
 
@@ -610,6 +612,25 @@ __global__ void __launch_bounds__(256) k_bin_pass(FrameConst fc, Buffers B) {
       unsigned sm = __ballot_sync(0xffffffffu, small);
       if ((threadIdx.x & 31) == 0 && sm) atomicAdd(&B.ctr->small_quads, (unsigned long long)__popc(sm));
     }
+    if (!kWrite && in && (flags & 1u)) {
+      // large quad: one (triangle, bin row) pair per bin row of each valid
+      // triangle for k_bin_large (a warp per pair)
+      for (uint32_t t = 0; t < 2; ++t) {
+        const uint32_t ti = q * 2 + t;
+        if (!(B.tri_meta[ti].w & 0x100u)) continue;
+        const uint32_t yy = B.tri_y[ti];
+        const int y_lo = (int)(int16_t)(yy & 0xffffu), y_hi = (int)(int16_t)(yy >> 16);
+        atomicAdd(&B.ctr->large_tris, 1ull);
+        if (y_lo > y_hi) continue;
+        const uint32_t r0 = (uint32_t)y_lo / kBin, nr = (uint32_t)y_hi / kBin - r0 + 1u;
+        const uint32_t at = atomicAdd(&B.ctr->large_pairs, nr);
+        if ((unsigned long long)at + nr > fc.lpairs_cap) {
+          atomicOr(&B.ctr->error, 16u);  // pair list capacity: grow and re-run
+          continue;
+        }
+        for (uint32_t r = 0; r < nr; ++r) B.lpairs[at + r] = make_uint2(ti, r0 + r);
+      }
+    }
     for (uint32_t k = 0; k < 4; ++k) {
       bool act = k < nb;
       uint32_t bx = x0 + (k % (x1 - x0 + 1 > 0 ? x1 - x0 + 1 : 1));
@@ -629,52 +650,40 @@ __global__ void __launch_bounds__(256) k_bin_pass(FrameConst fc, Buffers B) {
 }
 
 // Large quads' valid triangles (rasterize_triangle_bins, binning.hpp:89-117):
-// one warp per triangle, lane = pixel row of the current bin row; the
-// per-row covered bin-column ranges are OR-reduced across the warp, then
-// each set bin is counted (kWrite = false) or receives the triangle index.
+// one warp per (triangle, bin row) pair, lane = pixel row; the per-row
+// covered bin-column ranges are OR-reduced across the warp, then each set bin
+// is counted (kWrite = false) or receives the triangle index.
 template <bool kWrite>
 __global__ void __launch_bounds__(256) k_bin_large(FrameConst fc, Buffers B) {
   if (B.ctr->error) return;
-  const uint32_t nvis = B.ctr->nvis;
+  const uint32_t npairs = min(B.ctr->large_pairs, fc.lpairs_cap);
   const int lane = threadIdx.x & 31;
   const uint32_t gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
   const int nwords = (fc.bins_x + 31) / 32;
-  for (uint32_t base = gwarp * 32; base < nvis; base += nwarps * 32) {
-    const uint32_t q = base + lane;
-    const bool large = q < nvis && (B.vq_flags[q] & 1u);
-    unsigned m = __ballot_sync(0xffffffffu, large);
-    while (m) {
-      const uint32_t quad = base + (__ffs(m) - 1);
-      m &= m - 1;
-      for (uint32_t t = 0; t < 2; ++t) {
-        const uint32_t ti = quad * 2 + t;
-        if (!(B.tri_meta[ti].w & 0x100u)) continue;
-        const TriRec& tr = B.tri[ti];
-        const int y_min = tr.y_min, y_max = tr.y_max;
-        if (!kWrite && lane == 0) atomicAdd(&B.ctr->large_tris, 1ull);
-        for (int R = y_min / kBin; R <= y_max / kBin; ++R) {
-          const int y = R * kBin + lane;
-          int b0 = 1, b1 = 0;
-          if (y >= y_min && y <= y_max) {
-            int b, l;
-            if (row_span(tr, y, 0, fc.width - 1, &b, &l)) b0 = b / kBin, b1 = l / kBin;
-          }
-          for (int w = 0; w < nwords; ++w) {
-            const int lo = max(b0, w * 32), hi = min(b1, w * 32 + 31);
-            uint32_t word = 0;
-            if (lo <= hi) word = (hi - lo == 31 ? 0xffffffffu : ((2u << (hi - lo)) - 1u)) << (lo - w * 32);
-            word = __reduce_or_sync(0xffffffffu, word);
-            if ((word >> lane) & 1u) {
-              const int bin = R * fc.bins_x + w * 32 + lane;
-              if (kWrite) {
-                const uint32_t slot = atomicAdd(&B.tcur[bin], 1u);
-                if (slot < fc.items_cap) B.items[slot] = ti;
-              } else {
-                atomicAdd(&B.tcnt[bin], 1u);
-              }
-            }
-          }
+  for (uint32_t w = gwarp; w < npairs; w += nwarps) {
+    const uint2 pr = B.lpairs[w];
+    const uint32_t ti = pr.x;
+    const int R = (int)pr.y;
+    const TriRec& tr = B.tri[ti];
+    const int y = R * kBin + lane;
+    int b0 = 1, b1 = 0;
+    if (y >= tr.y_min && y <= tr.y_max) {
+      int b, l;
+      if (row_span(tr, y, 0, fc.width - 1, &b, &l)) b0 = b / kBin, b1 = l / kBin;
+    }
+    for (int wd = 0; wd < nwords; ++wd) {
+      const int lo = max(b0, wd * 32), hi = min(b1, wd * 32 + 31);
+      uint32_t word = 0;
+      if (lo <= hi) word = (hi - lo == 31 ? 0xffffffffu : ((2u << (hi - lo)) - 1u)) << (lo - wd * 32);
+      word = __reduce_or_sync(0xffffffffu, word);
+      if ((word >> lane) & 1u) {
+        const int bin = R * fc.bins_x + wd * 32 + lane;
+        if (kWrite) {
+          const uint32_t slot = atomicAdd(&B.tcur[bin], 1u);
+          if (slot < fc.items_cap) B.items[slot] = ti;
+        } else {
+          atomicAdd(&B.tcnt[bin], 1u);
         }
       }
     }
@@ -2102,9 +2111,10 @@ struct DeviceScene {
       tri_y;
   DevBuf qcnt, tcnt, off, qcur, tcur, cat, prop, items, slots, spill0, spill1, scratch, fb, mask,
       hash, emit, ctr, tile_ids, hbd, pool_tri, pool_mask, pool_pre, seg_queue, pool_slot, rowd,
-      rowtri;
+      rowtri, lpairs;
   uint32_t items_cap = 0;
   uint32_t pool_cap = 0;
+  uint32_t lpairs_cap = 0;
   bool extract_configured = false;
   int extract_ctas = 0;
   cudaEvent_t ev[6] = {};  // frame start, setup, binning, low extract, end, high extract
@@ -2461,6 +2471,9 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   d->hbd.ensure(nb * 32 * sizeof(dev::HbDesc));
   d->seg_queue.ensure(nb * 32 * 4);
   d->rowd.ensure(nb * 4 * sizeof(uint2));
+  if (d->lpairs_cap == 0) d->lpairs_cap = std::max<uint32_t>(1u << 16, std::min<uint32_t>(Q * 2u, 1u << 26));
+  d->lpairs.ensure(size_t(d->lpairs_cap) * sizeof(uint2));
+  fc.lpairs_cap = d->lpairs_cap;
   if (d->pool_cap == 0) d->pool_cap = std::max<uint32_t>(1u << 22, uint32_t(std::min<size_t>(nb * 2048, 1u << 26)));
   d->pool_tri.ensure(size_t(d->pool_cap) * 4);
   d->pool_mask.ensure(size_t(d->pool_cap) * 4);
@@ -2528,6 +2541,7 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   B.pool_slot = d->pool_slot.as<uint16_t>();
   B.rowd = d->rowd.as<uint2>();
   B.rowtri = d->rowtri.as<uint32_t>();
+  B.lpairs = d->lpairs.as<uint2>();
   B.ctr = d->ctr.as<dev::Counters>();
   return P;
 }
@@ -2555,10 +2569,10 @@ int enqueue_front(DeviceScene* d, Prepared& P) {
   cudaEventRecord(d->ev[1], st);
   int grid = std::max(1, std::min<int>(d->sm_count * 8, int((fc.nquads + 255) / 256)));
   dev::k_bin_pass<false><<<grid, 256, 0, st>>>(fc, B);
-  dev::k_bin_large<false><<<grid, 256, 0, st>>>(fc, B);
+  dev::k_bin_large<false><<<d->sm_count * 8, 256, 0, st>>>(fc, B);
   dev::k_bin_scan<<<1, 1024, 0, st>>>(fc, B);
   dev::k_bin_pass<true><<<grid, 256, 0, st>>>(fc, B);
-  dev::k_bin_large<true><<<grid, 256, 0, st>>>(fc, B);
+  dev::k_bin_large<true><<<d->sm_count * 8, 256, 0, st>>>(fc, B);
   dev::k_bin_sort<<<std::min(fc.nbins, d->sm_count * 8), 256, 0, st>>>(fc, B);
   launches += 6;
   cudaEventRecord(d->ev[2], st);
@@ -2750,7 +2764,7 @@ static void enqueue_raster(DeviceScene* d, Prepared& P, int* launches) {
 void render_frame(const Scene& s, const RenderOptions& opt, RenderOutput* out) {
   validate_frame(s, opt);
   DeviceScene* d = device_scene(s);
-  for (int attempt = 0; attempt < 3; ++attempt) {
+  for (int attempt = 0; attempt < 8; ++attempt) {
     Prepared P = prepare(d, s, opt);
     int launches = enqueue_front(d, P);
     enqueue_raster(d, P, &launches);
@@ -2763,6 +2777,10 @@ void render_frame(const Scene& s, const RenderOptions& opt, RenderOutput* out) {
     }
     if (c.error & 8u) {  // THB pool capacity: grow and re-run
       d->pool_cap = uint32_t(std::min<unsigned long long>(2ull * d->pool_cap, 0xffffffffull));
+      continue;
+    }
+    if (c.error & 16u) {  // large-triangle pair list: grow and re-run
+      d->lpairs_cap = uint32_t(std::min<unsigned long long>(c.large_pairs + c.large_pairs / 4 + 1024, 0xffffffffull));
       continue;
     }
     check_frame_errors(c, P.fc);
@@ -2853,7 +2871,7 @@ void render_reference_frame(const Scene& s, const RenderOptions& opt, RenderOutp
   validate_scene(s);
   DeviceScene* d = device_scene(s);
   Prepared P = prepare(d, s, opt);
-  for (int attempt = 0; attempt < 3; ++attempt) {
+  for (int attempt = 0; attempt < 8; ++attempt) {
     int launches = enqueue_front(d, P);
     dim3 grid((s.camera.width + 15) / 16, (s.camera.height + 7) / 8);
     dev::k_abuffer<<<grid, 128, 0, d->stream>>>(P.fc, P.B);
@@ -2864,8 +2882,11 @@ void render_reference_frame(const Scene& s, const RenderOptions& opt, RenderOutp
     dev::Counters c;
     ck(cudaMemcpyAsync(&c, P.B.ctr, sizeof c, cudaMemcpyDeviceToHost, d->stream), "counters");
     ck(cudaStreamSynchronize(d->stream), "frame");
-    if (c.error & 2u) {
-      d->items_cap = uint32_t(std::min<unsigned long long>(c.pairs + c.pairs / 4 + 1024, 0xffffffffull));
+    if (c.error & (2u | 16u)) {  // capacity of the bin items / large-triangle pairs
+      if (c.error & 2u)
+        d->items_cap = uint32_t(std::min<unsigned long long>(c.pairs + c.pairs / 4 + 1024, 0xffffffffull));
+      if (c.error & 16u)
+        d->lpairs_cap = uint32_t(std::min<unsigned long long>(c.large_pairs + c.large_pairs / 4 + 1024, 0xffffffffull));
       P = prepare(d, s, opt);
       continue;
     }
