@@ -154,10 +154,10 @@ veil_status veil_render_scene(const veil_scene* scene, const veil_render_params*
 int veil_render_width(const veil_render* r) { return r ? r->out.width : 0; }
 int veil_render_height(const veil_render* r) { return r ? r->out.height : 0; }
 const uint8_t* veil_render_pixels(const veil_render* r) {
-  return r ? r->out.rgba.data() : nullptr;
+  return r ? r->out.rgba() : nullptr;
 }
 const uint8_t* veil_render_invalid_mask(const veil_render* r) {
-  return r ? r->out.mask.data() : nullptr;
+  return r ? r->out.mask() : nullptr;
 }
 const char* veil_render_report_json(const veil_render* r) { return r ? r->json.c_str() : ""; }
 
@@ -167,7 +167,7 @@ veil_status veil_render_write_png(const veil_render* r, const char* path) {
     veil::Image8 img;
     img.width = r->out.width;
     img.height = r->out.height;
-    img.rgba = r->out.rgba;
+    img.rgba.assign(r->out.rgba(), r->out.rgba() + size_t(img.width) * img.height * 4);
     veil::write_png(img, path);
   });
 }
@@ -325,8 +325,8 @@ veil_status veil_shard_pack_tiles(const veil_render* r, const veil_shard* shard,
           int py = y * K + ly;
           if (py >= H) break;
           int w = std::min(K, W - x * K);
-          std::memcpy(dst + ly * K * 4, r->out.rgba.data() + (size_t(py) * W + x * K) * 4, w * 4);
-          std::memcpy(dst + 4096 + ly * K, r->out.mask.data() + size_t(py) * W + x * K, w);
+          std::memcpy(dst + ly * K * 4, r->out.rgba() + (size_t(py) * W + x * K) * 4, w * 4);
+          std::memcpy(dst + 4096 + ly * K, r->out.mask() + size_t(py) * W + x * K, w);
         }
         ++t;
       }
@@ -350,8 +350,8 @@ veil_status veil_shard_unpack_tiles(veil_render* r, const veil_shard* shard, con
           int py = y * K + ly;
           if (py >= H) break;
           int w = std::min(K, W - x * K);
-          std::memcpy(r->out.rgba.data() + (size_t(py) * W + x * K) * 4, src + ly * K * 4, w * 4);
-          std::memcpy(r->out.mask.data() + size_t(py) * W + x * K, src + 4096 + ly * K, w);
+          std::memcpy(r->out.rgba() + (size_t(py) * W + x * K) * 4, src + ly * K * 4, w * 4);
+          std::memcpy(r->out.mask() + size_t(py) * W + x * K, src + 4096 + ly * K, w);
         }
         ++t;
       }

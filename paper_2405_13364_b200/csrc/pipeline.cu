@@ -32,6 +32,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
@@ -2131,6 +2133,33 @@ struct DeviceScene {
   }
 };
 
+namespace {
+std::mutex g_pinned_mu;
+std::multimap<size_t, uint8_t*> g_pinned_free;  // pooled pinned frames by size
+}  // namespace
+
+std::shared_ptr<uint8_t> acquire_host_frame(size_t bytes) {
+  uint8_t* p = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_pinned_mu);
+    auto it = g_pinned_free.lower_bound(bytes);
+    if (it != g_pinned_free.end() && it->first <= bytes * 2) {
+      p = it->second;
+      bytes = it->first;
+      g_pinned_free.erase(it);
+    }
+  }
+  if (!p) ck(cudaMallocHost(reinterpret_cast<void**>(&p), std::max<size_t>(bytes, 64)), "cudaMallocHost");
+  return std::shared_ptr<uint8_t>(p, [bytes](uint8_t* q) {
+    std::lock_guard<std::mutex> lk(g_pinned_mu);
+    if (g_pinned_free.size() < 8) {
+      g_pinned_free.emplace(bytes, q);
+    } else {
+      cudaFreeHost(q);
+    }
+  });
+}
+
 void release_device_scene(DeviceScene* d) {
   if (!d) return;
   int prev = 0;
@@ -2314,8 +2343,8 @@ void launch_shade_mode(DeviceScene* d, const dev::FrameConst& fc, const dev::Buf
        "cudaFuncSetAttribute");
     configured = true;
   }
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_shade<KM, kMode>, 256, dyn);
+  static int per_sm = -1;  // per instantiation (same on every B200)
+  if (per_sm < 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_shade<KM, kMode>, 256, dyn);
   const long long items = kMode == 1 ? ((long long)fc.nbins * 32 + 7) / 8 : (long long)fc.nbins * 4;
   const int grid = int(std::max<long long>(1, std::min<long long>((long long)std::max(1, per_sm) * d->sm_count,
                                                                    items)));
@@ -2840,20 +2869,20 @@ void render_frame(const Scene& s, const RenderOptions& opt, RenderOutput* out) {
       dump_put(out, "emit_count", P.B.emit, npx, d->stream);
       ck(cudaStreamSynchronize(d->stream), "dump");
     }
-    if (opt.host_readback) {
+    if (opt.host_readback || opt.dump) {
       const size_t npx = size_t(s.camera.width) * s.camera.height;
-      out->rgba.resize(npx * 4);
-      out->mask.resize(npx);
-      ck(cudaMemcpyAsync(out->rgba.data(), P.B.fb, npx * 4, cudaMemcpyDeviceToHost, d->stream), "readback");
-      ck(cudaMemcpyAsync(out->mask.data(), P.B.mask, npx, cudaMemcpyDeviceToHost, d->stream), "readback");
+      out->host = acquire_host_frame(npx * 5);
+      ck(cudaMemcpyAsync(out->rgba(), P.B.fb, npx * 4, cudaMemcpyDeviceToHost, d->stream), "readback");
+      ck(cudaMemcpyAsync(out->mask(), P.B.mask, npx, cudaMemcpyDeviceToHost, d->stream), "readback");
       ck(cudaStreamSynchronize(d->stream), "readback");
     }
     if (opt.dump) {
       DumpArray img, msk;
-      img.count = out->rgba.size();
-      img.bytes = out->rgba;
-      msk.count = out->mask.size();
-      msk.bytes = out->mask;
+      const size_t npx = size_t(s.camera.width) * s.camera.height;
+      img.count = npx * 4;
+      img.bytes.assign(out->rgba(), out->rgba() + npx * 4);
+      msk.count = npx;
+      msk.bytes.assign(out->mask(), out->mask() + npx);
       out->dumps["image"] = std::move(img);
       out->dumps["mask"] = std::move(msk);
       const veil_frame_stats& t = out->stats;
@@ -2902,15 +2931,15 @@ void render_reference_frame(const Scene& s, const RenderOptions& opt, RenderOutp
     out->stats.setup_ms = out->stats.binning_ms = out->stats.low_raster_ms = out->stats.hi_raster_ms = 0;
     out->stats.kernel_launches = launches;
     const size_t npx = size_t(s.camera.width) * s.camera.height;
-    out->rgba.resize(npx * 4);
-    out->mask.assign(npx, 0);
-    ck(cudaMemcpy(out->rgba.data(), P.B.fb, npx * 4, cudaMemcpyDeviceToHost), "readback");
+    out->host = acquire_host_frame(npx * 5);
+    std::memset(out->mask(), 0, npx);
+    ck(cudaMemcpy(out->rgba(), P.B.fb, npx * 4, cudaMemcpyDeviceToHost), "readback");
     if (opt.dump) {
       dump_put(out, "emit_hash", P.B.hash, npx, d->stream);
       dump_put(out, "emit_count", P.B.emit, npx, d->stream);
       ck(cudaStreamSynchronize(d->stream), "dump");
-      dump_put_host(out, "image", out->rgba);
-      dump_put_host(out, "mask", out->mask);
+      dump_put_host(out, "image", std::vector<uint8_t>(out->rgba(), out->rgba() + npx * 4));
+      dump_put_host(out, "mask", std::vector<uint8_t>(out->mask(), out->mask() + npx));
     }
     return;
   }

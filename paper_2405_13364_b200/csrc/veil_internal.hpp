@@ -106,10 +106,15 @@ struct DumpArray {
   uint64_t count = 0;
 };
 
+// Pinned, pooled host buffer for a frame: RGBA8 (4 B/px) then the invalid
+// mask (1 B/px). Returned to the pool when the last owner releases it.
+std::shared_ptr<uint8_t> acquire_host_frame(size_t bytes);
+
 struct RenderOutput {
   int width = 0, height = 0;
-  std::vector<uint8_t> rgba;
-  std::vector<uint8_t> mask;
+  std::shared_ptr<uint8_t> host;  // see acquire_host_frame
+  uint8_t* rgba() const { return host.get(); }
+  uint8_t* mask() const { return host ? host.get() + size_t(width) * height * 4 : nullptr; }
   veil_frame_stats stats{};
   bool reference = false;
   std::map<std::string, DumpArray> dumps;

@@ -226,15 +226,18 @@ class Render:
     def height(self):
         return lib().veil_render_height(self.h)
 
-    def pixels(self):
+    def pixels(self, copy=True):
+        """RGBA8 (H, W, 4). copy=False returns a view valid while this handle lives."""
         w, h = self.width, self.height
         p = lib().veil_render_pixels(self.h)
-        return np.ctypeslib.as_array(p, shape=(h * w * 4,)).copy().reshape(h, w, 4)
+        a = np.ctypeslib.as_array(p, shape=(h * w * 4,)).reshape(h, w, 4)
+        return a.copy() if copy else a
 
-    def invalid_mask(self):
+    def invalid_mask(self, copy=True):
         w, h = self.width, self.height
         p = lib().veil_render_invalid_mask(self.h)
-        return np.ctypeslib.as_array(p, shape=(h * w,)).copy().reshape(h, w)
+        a = np.ctypeslib.as_array(p, shape=(h * w,)).reshape(h, w)
+        return a.copy() if copy else a
 
     def report(self):
         return json.loads(lib().veil_render_report_json(self.h).decode())
