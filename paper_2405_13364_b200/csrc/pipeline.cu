@@ -792,7 +792,7 @@ __device__ __forceinline__ uint32_t byte_of(const uint32_t* w, int i) {
 // (keys are unique per pixel). push() returns the entry the reference's
 // insert-then-pop_min would emit: when full, that is min(new, oldest
 // minimum), and the survivor set is merged back with one select pass.
-template <int KM>
+template <int KM, bool kExact = false>
 struct RegFilter {
   uint64_t key[KM];
   float4 col[KM];
@@ -810,8 +810,9 @@ struct RegFilter {
     if (!any || pk > max_key) max_key = pk;
     any = true;
   }
-  __device__ __forceinline__ bool push(int cap, uint64_t k, float4 c, uint64_t* pk, float4* pc,
+  __device__ __forceinline__ bool push(int cap_rt, uint64_t k, float4 c, uint64_t* pk, float4* pc,
                                        bool* ooo) {
+    const int cap = kExact ? KM : cap_rt;
     if (n < cap) {  // not full: bubble into [0, n]
       uint64_t ck = k;
       float4 cc = c;
@@ -871,7 +872,8 @@ struct RegFilter {
     note(*pk, ooo);
   }
   // Colour push(k) would pop (if any), without modifying the filter.
-  __device__ __forceinline__ bool peek(int cap, uint64_t k, float4 c, float4* pc) const {
+  __device__ __forceinline__ bool peek(int cap_rt, uint64_t k, float4 c, float4* pc) const {
+    const int cap = kExact ? KM : cap_rt;
     if (n < cap) return false;
     *pc = (k < key[0]) ? c : col[0];
     return true;
@@ -1182,7 +1184,7 @@ __device__ __forceinline__ uint32_t find_thb(const uint32_t* pre_l, uint32_t lo,
 }
 
 template <int KM>
-__device__ __forceinline__ void blend_routed(const FrameConst& fc, RegFilter<KM>& f, PixelOut& o,
+__device__ __forceinline__ void blend_routed(const FrameConst& fc, RegFilter<KM, (KM <= 8)>& f, PixelOut& o,
                                              uint32_t mine, uint64_t key, float4 col) {
   while (__any_sync(0xffffffffu, mine != 0u)) {
     const int src = mine ? __ffs(mine) - 1 : (threadIdx.x & 31);
@@ -1221,7 +1223,7 @@ __device__ __forceinline__ void shade_segments(const FrameConst& fc, const Buffe
                                                uint32_t n, uint32_t total, uint32_t* route,
                                                PixelOut& o) {
   const int lane = threadIdx.x & 31;
-  RegFilter<KM> f;
+  RegFilter<KM, (KM <= 8)> f;
   f.reset();
   uint32_t r_lo = 0;
   for (uint32_t base = 0; base < total; base += 32) {
@@ -1269,7 +1271,7 @@ __device__ __forceinline__ void shade_walk(const FrameConst& fc, const Buffers& 
                                            unsigned long long* enumerated_out) {
   const int lane = threadIdx.x & 31;
   const int px = px0 + (lane & 7), py = py0 + (lane >> 3);
-  RegFilter<KM> f;
+  RegFilter<KM, (KM <= 8)> f;
   f.reset();
   bool saturated = false, stopped = false;
   unsigned sat_mask = 0;
@@ -1352,7 +1354,7 @@ __device__ __forceinline__ void shade_waves(const FrameConst& fc, const Buffers&
                                             const StagedTri* staged, uint32_t n, PixelOut& o) {
   const int lane = threadIdx.x & 31;
   const int px = px0 + (lane & 7), py = py0 + (lane >> 3);
-  RegFilter<KM> f;
+  RegFilter<KM, (KM <= 8)> f;
   f.reset();
   uint32_t r = 0;
   while (r < n) {
@@ -2366,11 +2368,15 @@ void launch_shade_km(DeviceScene* d, const dev::FrameConst& fc, const dev::Buffe
 
 void launch_shade(DeviceScene* d, const dev::FrameConst& fc, const dev::Buffers& B, int* launches) {
   const int df = fc.df;
-  if (df <= 1) launch_shade_km<1>(d, fc, B, launches);
-  else if (df <= 2) launch_shade_km<2>(d, fc, B, launches);
-  else if (df <= 3) launch_shade_km<3>(d, fc, B, launches);
-  else if (df <= 4) launch_shade_km<4>(d, fc, B, launches);
-  else if (df <= 8) launch_shade_km<8>(d, fc, B, launches);
+  // KM == df exactly up to 8 (the filter capacity is then a compile-time constant)
+  if (df == 1) launch_shade_km<1>(d, fc, B, launches);
+  else if (df == 2) launch_shade_km<2>(d, fc, B, launches);
+  else if (df == 3) launch_shade_km<3>(d, fc, B, launches);
+  else if (df == 4) launch_shade_km<4>(d, fc, B, launches);
+  else if (df == 5) launch_shade_km<5>(d, fc, B, launches);
+  else if (df == 6) launch_shade_km<6>(d, fc, B, launches);
+  else if (df == 7) launch_shade_km<7>(d, fc, B, launches);
+  else if (df == 8) launch_shade_km<8>(d, fc, B, launches);
   else if (df <= 16) launch_shade_km<16>(d, fc, B, launches);
   else if (df <= 32) launch_shade_km<32>(d, fc, B, launches);
   else throw Error(VEIL_ERR_INVALID_ARG, "depth_filter_size above 32 is not supported on the device path");
