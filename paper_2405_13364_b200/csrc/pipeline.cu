@@ -781,6 +781,7 @@ struct Tbr {  // one triangle's coverage of a 32x8 block-row (packing.hpp:108-14
   uint32_t meta;   // bits 0-3 block-column mask, bit 4 large
   uint32_t b[2];   // 8 row begins, one byte each
   uint32_t l[2];   // 8 row lasts, one byte each; empty row = (31, 0)
+  uint32_t slot;   // position in the bin's triangle list (k_shade staging)
 };
 
 __device__ __forceinline__ uint32_t byte_of(const uint32_t* w, int i) {
@@ -1036,7 +1037,7 @@ struct __align__(16) StagedTri {
   uint32_t pad[2];
 };
 static_assert(sizeof(StagedTri) == 208, "StagedTri layout");
-constexpr int kStageTris = 224;
+constexpr int kStageTris = 320;
 
 __device__ __forceinline__ void stage_triangle(const Buffers& B, uint32_t tri, StagedTri* dst) {
   const TriRec& t = B.tri[tri];
@@ -1469,8 +1470,8 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
   // compacted with warp ballots, so the FP64 row-span loop runs dense.
   const uint32_t nq = B.qcnt[bin], nt = B.tcnt[bin], o = B.off[bin];
   const uint32_t T = 2 * nq + nt;
-  uint32_t* cand = reinterpret_cast<uint32_t*>(V.keys);  // keys are free until phase B
-  const uint32_t cand_cap = 8u * cap_tb;
+  uint64_t* cand = V.keys;  // keys are free until phase B
+  const uint32_t cand_cap = 4u * cap_tb;
   for (uint32_t round = 0; round < T; round += cand_cap) {
     const uint32_t end = min(T, round + cand_cap);
     if (threadIdx.x == 0) st->ncand = 0;
@@ -1478,7 +1479,7 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
     for (uint32_t i0 = round; i0 < end; i0 += blockDim.x) {
       const uint32_t i = i0 + threadIdx.x;
       bool keep = false;
-      uint32_t code = 0;
+      uint64_t code = 0;
       if (i < end) {
         uint32_t ti, large;
         if (i < 2 * nq) {
@@ -1491,7 +1492,7 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
         const uint32_t yy = __ldg(&B.tri_y[ti]);
         const int y_lo = (int)(int16_t)(yy & 0xffffu), y_hi = (int)(int16_t)(yy >> 16);
         keep = max(y_lo, ry0) <= min(y_hi, ry1);
-        code = ti | (large << 31);
+        code = ((uint64_t)i << 32) | ti | (large << 31);
       }
       const unsigned m = __ballot_sync(0xffffffffu, keep);
       uint32_t wbase = 0;
@@ -1502,8 +1503,8 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
     __syncthreads();
     const uint32_t nc = st->ncand;
     for (uint32_t j = threadIdx.x; j < nc; j += blockDim.x) {
-      const uint32_t code = cand[j];
-      const uint32_t ti = code & 0x7fffffffu, large = code >> 31;
+      const uint64_t code = cand[j];
+      const uint32_t ti = (uint32_t)code & 0x7fffffffu, large = ((uint32_t)code) >> 31;
       const TriRec& t = B.tri[ti];
       const int yb = max(t.y_min, ry0), ye = min(t.y_max, ry1);
       uint32_t rb0 = 0x1f1f1f1fu, rb1 = 0x1f1f1f1fu, rl0 = 0u, rl1 = 0u, cols = 0;
@@ -1533,6 +1534,7 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
         rec.b[1] = rb1;
         rec.l[0] = rl0;
         rec.l[1] = rl1;
+        rec.slot = (uint32_t)(code >> 32);
         V.tbr[slot] = rec;
       }
     }
@@ -1689,7 +1691,7 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
           B.pool_tri[at] = tri;
           B.pool_mask[at] = hm[h];
           B.pool_pre[at] = frags[h] + incl - fr;
-          B.pool_slot[at] = (uint16_t)ref;
+          B.pool_slot[at] = (uint16_t)min(V.tbr[ref].slot, 65535u);
         }
         nthb[h] += __popc(m);
         frags[h] += __shfl_sync(0xffffffffu, incl, 31);
@@ -1844,9 +1846,12 @@ __global__ void __launch_bounds__(256, 2) k_shade(FrameConst fc, Buffers B) {
   __shared__ uint32_t item_s;
   if (B.ctr->error) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // modes 0/2: CTA items = (bin, block-row), warp w = half-block w of the row
+  __shared__ int hb_next;
+  // modes 0/2: CTA items = bins, warps pull the bin's 32 half-blocks;
   // mode 1: warp items from the queue mode 0 filled
-  const uint32_t nitems = kMode == 1 ? B.ctr->seg_count : (uint32_t)fc.nbins * 4u;
+  const uint32_t nitems = kMode == 1 ? B.ctr->seg_count : (uint32_t)fc.nbins;
+  uint32_t cta_bin = 0xffffffffu;
+  bool staged_ok = false;
   for (;;) {
     uint32_t item;
     if (kMode == 1) {
@@ -1856,27 +1861,50 @@ __global__ void __launch_bounds__(256, 2) k_shade(FrameConst fc, Buffers B) {
       if (item >= nitems) break;
       item = B.seg_queue[item];
     } else {
-      if (threadIdx.x == 0) item_s = atomicAdd(&B.ctr->shade_next[0], 1u);
-      __syncthreads();
-      item = item_s;
-      __syncthreads();
-      if (item >= nitems) break;
-      item = item * 8u + (uint32_t)warp;  // (bin * 32 + hb)
+      // next half-block of the CTA's bin, or the next bin
+      int hbi = 32;
+      if (cta_bin != 0xffffffffu) {
+        if (lane == 0) hbi = atomicAdd(&hb_next, 1);
+        hbi = __shfl_sync(0xffffffffu, hbi, 0);
+      }
+      if (hbi >= 32) {
+        __syncthreads();  // everyone is done with the staged bin
+        if (threadIdx.x == 0) {
+          item_s = atomicAdd(&B.ctr->shade_next[0], 1u);
+          hb_next = 0;
+        }
+        __syncthreads();
+        cta_bin = item_s;
+        if (cta_bin >= nitems) break;
+        const int bxi = (int)cta_bin % fc.bins_x, byi = (int)cta_bin / fc.bins_x;
+        const bool owned = fc.world <= 1 || ((bxi + 3 * byi) % fc.world) == fc.rank;
+        staged_ok = false;
+        if (kMode == 0 && owned && fc.decoded && B.cat[cta_bin] != 0) {
+          // stage the bin's triangles (bin-list expansion order) once
+          const uint32_t nq = B.qcnt[cta_bin], nt = B.tcnt[cta_bin], o = B.off[cta_bin];
+          const uint32_t T = 2 * nq + nt;
+          staged_ok = T <= (uint32_t)kStageTris;
+          if (staged_ok)
+            for (uint32_t j = threadIdx.x; j < T; j += blockDim.x) {
+              const uint32_t tri = j < 2 * nq ? B.items[o + (j >> 1)] * 2 + (j & 1) : B.items[o + nq + (j - 2 * nq)];
+              stage_triangle(B, tri, &row_tris[j]);
+            }
+        }
+        __syncthreads();
+        if (!owned) {
+          cta_bin = 0xffffffffu;
+          continue;
+        }
+        if (lane == 0) hbi = atomicAdd(&hb_next, 1);
+        hbi = __shfl_sync(0xffffffffu, hbi, 0);
+        if (hbi >= 32) continue;
+      }
+      item = cta_bin * 32u + (uint32_t)hbi;
     }
     const int bin = (int)(item >> 5), row = (int)((item >> 3) & 3u);
     const int bxi = bin % fc.bins_x, byi = bin / fc.bins_x;
-    if (!(fc.world <= 1 || ((bxi + 3 * byi) % fc.world) == fc.rank)) continue;
+    if (kMode == 1 && !(fc.world <= 1 || ((bxi + 3 * byi) % fc.world) == fc.rank)) continue;
     const int hb = (int)(item & 31u);  // reference half-block index in the bin
-    // mode 0: stage the bin-row's triangle records (one copy per row)
-    bool staged_ok = false;
-    if (kMode == 0 && fc.decoded && B.cat[bin] != 0) {
-      const uint2 rd = B.rowd[(size_t)bin * 4 + row];
-      staged_ok = rd.y <= (uint32_t)kStageTris;
-      if (staged_ok)
-        for (uint32_t j = threadIdx.x; j < rd.y; j += blockDim.x)
-          stage_triangle(B, B.rowtri[rd.x + j], &row_tris[j]);
-      __syncthreads();
-    }
     const int block = hb >> 1;
     const int hpx0 = bxi * kBin + (block & 3) * 8;
     const int hpy0 = byi * kBin + (block >> 2) * 8 + (hb & 1) * 4;
@@ -2347,7 +2375,7 @@ void launch_shade_mode(DeviceScene* d, const dev::FrameConst& fc, const dev::Buf
   }
   static int per_sm = -1;  // per instantiation (same on every B200)
   if (per_sm < 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_shade<KM, kMode>, 256, dyn);
-  const long long items = kMode == 1 ? ((long long)fc.nbins * 32 + 7) / 8 : (long long)fc.nbins * 4;
+  const long long items = kMode == 1 ? ((long long)fc.nbins * 32 + 7) / 8 : (long long)fc.nbins;
   const int grid = int(std::max<long long>(1, std::min<long long>((long long)std::max(1, per_sm) * d->sm_count,
                                                                    items)));
   dev::k_shade<KM, kMode><<<grid, 256, dyn, d->stream>>>(fc, B);
