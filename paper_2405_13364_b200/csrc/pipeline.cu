@@ -1371,7 +1371,10 @@ __device__ __forceinline__ void shade_waves(const FrameConst& fc, const Buffers&
       const uint32_t tri = tri_l[my_r];
       uint32_t qd;
       float4 col;
-      if (staged) {
+      if (fc.debug == 1) {
+        col = make_float4(0.01f, 0.01f, 0.01f, 0.01f);
+        qd = my_r;
+      } else if (staged) {
         col = shade_staged(fc, staged[slot_l[my_r]], px, py, &qd);
       } else if (fc.decoded) {
         col = shade_decoded_bf(fc, B, tri, px, py, &qd);
@@ -1383,7 +1386,11 @@ __device__ __forceinline__ void shade_waves(const FrameConst& fc, const Buffers&
       uint64_t pk;
       float4 pc;
       bool ooo;
-      if (f.push(fc.df, sample_key(fc, qd, tri), col, &pk, &pc, &ooo)) commit(o, pk, pc, ooo);
+      if (fc.debug == 2) {
+        commit(o, sample_key(fc, qd, tri), col, false);
+      } else if (f.push(fc.df, sample_key(fc, qd, tri), col, &pk, &pc, &ooo)) {
+        commit(o, pk, pc, ooo);
+      }
     }
   }
   while (f.n > 0) {
