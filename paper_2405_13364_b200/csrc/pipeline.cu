@@ -881,6 +881,85 @@ struct RegFilter {
   }
 };
 
+// Depth filter variant with the colours in shared memory: the registers hold
+// only (key << 4 | slot), sorted ascending (keys are unique, so the slot
+// bits never affect the order), and each slot's colour lives in this lane's
+// column of a per-warp [K][32] float4 array. Same emission semantics as
+// RegFilter (depth_filter.hpp:31-92); moves 2 registers per merge step
+// instead of 6.
+template <int K>
+struct SlotFilter {
+  uint64_t sk[K];
+  int n;
+  uint64_t max_key;
+  bool any;
+  float4* cols;  // this lane's slot 0; slot s at cols[s * 32]
+
+  __device__ __forceinline__ void reset(float4* lane_cols) {
+    n = 0;
+    max_key = 0;
+    any = false;
+    cols = lane_cols;
+  }
+  __device__ __forceinline__ void note(uint64_t pk, bool* ooo) {
+    *ooo = any && pk < max_key;
+    if (!any || pk > max_key) max_key = pk;
+    any = true;
+  }
+  __device__ __forceinline__ bool push(int, uint64_t k, float4 c, uint64_t* pk, float4* pc,
+                                       bool* ooo) {
+    if (n < K) {  // not full: store the colour in slot n, bubble the key in
+      cols[n * 32] = c;
+      uint64_t ck = (k << 4) | (uint64_t)n;
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        if (i < n) {
+          const uint64_t x = sk[i];
+          const bool sw = x > ck;
+          sk[i] = sw ? ck : x;
+          ck = sw ? x : ck;
+        } else if (i == n) {
+          sk[i] = ck;
+        }
+      }
+      ++n;
+      return false;
+    }
+    const uint64_t k0 = sk[0];
+    if (k < (k0 >> 4)) {  // the new sample is the minimum: it falls straight out
+      *pk = k;
+      *pc = c;
+      note(k, ooo);
+      return true;
+    }
+    const uint32_t s0 = (uint32_t)k0 & 15u;
+    *pk = k0 >> 4;
+    *pc = cols[s0 * 32];
+    cols[s0 * 32] = c;
+    note(*pk, ooo);
+    uint64_t ck = (k << 4) | s0;  // slots <- sorted(sk[1..K-1] + {new})
+#pragma unroll
+    for (int i = 0; i + 1 < K; ++i) {
+      const uint64_t x = sk[i + 1];
+      const bool lt = x < ck;
+      sk[i] = lt ? x : ck;
+      ck = lt ? ck : x;
+    }
+    sk[K - 1] = ck;
+    return true;
+  }
+  __device__ __forceinline__ void pop(uint64_t* pk, float4* pc, bool* ooo) {
+    const uint64_t k0 = sk[0];
+    *pk = k0 >> 4;
+    *pc = cols[((uint32_t)k0 & 15u) * 32];
+#pragma unroll
+    for (int i = 0; i + 1 < K; ++i)
+      if (i + 1 < n) sk[i] = sk[i + 1];
+    --n;
+    note(*pk, ooo);
+  }
+};
+
 __device__ __forceinline__ float4 blend(float4 acc, float4 s) {
   float t = __fsub_rn(1.0f, acc.w);
   return make_float4(__fadd_rn(acc.x, __fmul_rn(t, s.x)), __fadd_rn(acc.y, __fmul_rn(t, s.y)),
@@ -1348,15 +1427,14 @@ __device__ __forceinline__ void shade_walk(const FrameConst& fc, const Buffers& 
 // reference's per-pixel sequence (raster.cpp:232-267) while a warp step
 // shades up to 32 samples from several triangles (e.g. both triangles of a
 // quad, which are adjacent in the sort order and disjoint).
-template <int KM>
+template <int KM, typename Filter>
 __device__ __forceinline__ void shade_waves(const FrameConst& fc, const Buffers& B, int px0,
                                             int py0, const uint32_t* tri_l,
                                             const uint32_t* mask_l, const uint16_t* slot_l,
-                                            const StagedTri* staged, uint32_t n, PixelOut& o) {
+                                            const StagedTri* staged, uint32_t n, PixelOut& o,
+                                            Filter& f) {
   const int lane = threadIdx.x & 31;
   const int px = px0 + (lane & 7), py = py0 + (lane >> 3);
-  RegFilter<KM, (KM <= 8)> f;
-  f.reset();
   uint32_t r = 0;
   while (r < n) {
     uint32_t acc_mask = 0, my_r = 0xffffffffu;
@@ -1951,8 +2029,20 @@ __global__ void __launch_bounds__(256, 2) k_shade(FrameConst fc, Buffers B) {
       if (kMode == 2)
         shade_walk<KM, true>(fc, B, hpx0, hpy0, tri_l, mask_l, d.cnt, po, &enumerated);
       else if (kMode == 0)  // big THBs: wave walk
-        shade_waves<KM>(fc, B, hpx0, hpy0, tri_l, mask_l, slot_l, staged_ok ? row_tris : nullptr,
-                        d.cnt, po);
+      {
+        if constexpr (KM <= 8) {
+          SlotFilter<KM> f;
+          f.reset(reinterpret_cast<float4*>(shade_dyn + (size_t)kStageTris * sizeof(StagedTri)) +
+                  (size_t)warp * KM * 32 + lane);
+          shade_waves<KM>(fc, B, hpx0, hpy0, tri_l, mask_l, slot_l, staged_ok ? row_tris : nullptr,
+                          d.cnt, po, f);
+        } else {
+          RegFilter<KM> f;
+          f.reset();
+          shade_waves<KM>(fc, B, hpx0, hpy0, tri_l, mask_l, slot_l, staged_ok ? row_tris : nullptr,
+                          d.cnt, po, f);
+        }
+      }
       else if (d.frags)  // small THBs: dense segments + routing
         shade_segments<KM>(fc, B, hpx0, hpy0, tri_l, mask_l, pre_l, d.cnt, d.frags, route_s[warp], po);
     }
@@ -2372,7 +2462,9 @@ void launch_extract(DeviceScene* d, const dev::FrameConst& fc, const dev::Buffer
 template <int KM, int kMode>
 void launch_shade_mode(DeviceScene* d, const dev::FrameConst& fc, const dev::Buffers& B,
                        int* launches) {
-  const size_t dyn = kMode == 0 ? size_t(dev::kStageTris) * sizeof(dev::StagedTri) : 0;
+  const size_t dyn = kMode == 0 ? size_t(dev::kStageTris) * sizeof(dev::StagedTri) +
+                                       (KM <= 8 ? size_t(8) * KM * 32 * sizeof(float4) : 0)
+                                 : 0;
   static bool configured = false;  // per instantiation
   if (!configured && dyn) {
     ck(cudaFuncSetAttribute(dev::k_shade<KM, kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize,
