@@ -86,6 +86,11 @@ struct FrameConst {
   int debug;  // experiment switch (VEIL_DEBUG_SHADE), 0 in production
 };
 
+// Frame constants live in constant memory, written once per frame by a
+// memcpy that is part of the frame's CUDA graph (kernel parameters would be
+// baked into the graph).
+__constant__ FrameConst c_fc;
+
 // Device counters; one instance per scene workspace, zeroed per frame.
 struct Counters {
   unsigned long long cull[5];  // visible, degenerate, backfacing, frustum, between
@@ -290,7 +295,8 @@ __device__ void cull_quad(const FrameConst& fc, const uint4& idx, const float4 p
   o->large = (o->x1 - o->x0 + 1) * (o->y1 - o->y0 + 1) > 4;
 }
 
-__global__ void __launch_bounds__(kSetupBlock) k_setup_count(FrameConst fc, Buffers B) {
+__global__ void __launch_bounds__(kSetupBlock) k_setup_count(Buffers B) {
+  const FrameConst& fc = c_fc;
   uint32_t q = blockIdx.x * kSetupBlock + threadIdx.x;
   int reason = -1;
   if (q < fc.nquads) {
@@ -346,7 +352,8 @@ __device__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* total) {
   return warp_prefix + x - v;
 }
 
-__global__ void __launch_bounds__(1024) k_scan_blocks(FrameConst fc, Buffers B, uint32_t nblocks) {
+__global__ void __launch_bounds__(1024) k_scan_blocks(Buffers B, uint32_t nblocks) {
+  const FrameConst& fc = c_fc;
   __shared__ uint32_t carry;
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
@@ -434,7 +441,8 @@ __device__ __forceinline__ uint32_t flat_normal(const float4& a, const float4& b
   return encode_normal((float)n[0], (float)n[1], (float)n[2]);
 }
 
-__global__ void __launch_bounds__(kSetupBlock) k_setup_write(FrameConst fc, Buffers B) {
+__global__ void __launch_bounds__(kSetupBlock) k_setup_write(Buffers B) {
+  const FrameConst& fc = c_fc;
   if (B.ctr->error & 1u) return;
   uint32_t q = blockIdx.x * kSetupBlock + threadIdx.x;
   uint4 idx = make_uint4(0, 0, 0, 0);
@@ -471,7 +479,8 @@ __global__ void __launch_bounds__(kSetupBlock) k_setup_write(FrameConst fc, Buff
 // memory and written back as 512-byte contiguous runs (coalesced stores).
 constexpr int kTriBlock = 128;
 
-__global__ void __launch_bounds__(kTriBlock) k_setup_tris(FrameConst fc, Buffers B) {
+__global__ void __launch_bounds__(kTriBlock) k_setup_tris(Buffers B) {
+  const FrameConst& fc = c_fc;
   __shared__ __align__(16) TriRec stage[kTriBlock];
   if (B.ctr->error & 1u) return;
   const uint32_t nt = 2u * B.ctr->nvis;
@@ -598,7 +607,8 @@ __device__ void tri_bins(const FrameConst& fc, const TriRec& t, Fn&& fn) {
 }
 
 template <bool kWrite>
-__global__ void __launch_bounds__(256) k_bin_pass(FrameConst fc, Buffers B) {
+__global__ void __launch_bounds__(256) k_bin_pass(Buffers B) {
+  const FrameConst& fc = c_fc;
   if (B.ctr->error) return;
   const uint32_t nvis = B.ctr->nvis;
   for (uint32_t base = blockIdx.x * 256; base < nvis; base += gridDim.x * 256) {
@@ -656,7 +666,8 @@ __global__ void __launch_bounds__(256) k_bin_pass(FrameConst fc, Buffers B) {
 // covered bin-column ranges are OR-reduced across the warp, then each set bin
 // is counted (kWrite = false) or receives the triangle index.
 template <bool kWrite>
-__global__ void __launch_bounds__(256) k_bin_large(FrameConst fc, Buffers B) {
+__global__ void __launch_bounds__(256) k_bin_large(Buffers B) {
+  const FrameConst& fc = c_fc;
   if (B.ctr->error) return;
   const uint32_t npairs = min(B.ctr->large_pairs, fc.lpairs_cap);
   const int lane = threadIdx.x & 31;
@@ -693,7 +704,8 @@ __global__ void __launch_bounds__(256) k_bin_large(FrameConst fc, Buffers B) {
 }
 
 // offsets (binning.cpp:24-32) + categories (34-37) + write cursors
-__global__ void __launch_bounds__(1024) k_bin_scan(FrameConst fc, Buffers B) {
+__global__ void __launch_bounds__(1024) k_bin_scan(Buffers B) {
+  const FrameConst& fc = c_fc;
   if (B.ctr->error) return;
   __shared__ unsigned long long carry;
   __shared__ unsigned int cnt[3];
@@ -764,7 +776,8 @@ __device__ void cta_sort_segment(uint32_t* g, uint32_t n, uint32_t* sm, uint32_t
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(256) k_bin_sort(FrameConst fc, Buffers B) {
+__global__ void __launch_bounds__(256) k_bin_sort(Buffers B) {
+  const FrameConst& fc = c_fc;
   if (B.ctr->error) return;
   __shared__ uint32_t sm[4096];
   for (int b = blockIdx.x; b < fc.nbins; b += gridDim.x) {
@@ -1847,8 +1860,9 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
 }
 
 template <bool kGlobal>
-__global__ void __launch_bounds__(128) k_extract(FrameConst fc, Buffers B, int pass,
+__global__ void __launch_bounds__(128) k_extract(Buffers B, int pass,
                                                  uint32_t cap_tbr, uint32_t cap_tb) {
+  const FrameConst& fc = c_fc;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   __shared__ ItemState st;
   __shared__ uint32_t item_s;
@@ -1920,7 +1934,8 @@ constexpr uint32_t kWalkMinSamplesPerThb = 12;  // walk vs segments crossover
 // threshold walk for all. Separate instantiations keep each path's register
 // allocation small.
 template <int KM, int kMode>
-__global__ void __launch_bounds__(256, 2) k_shade(FrameConst fc, Buffers B) {
+__global__ void __launch_bounds__(256, 2) k_shade(Buffers B) {
+  const FrameConst& fc = c_fc;
   __shared__ uint32_t stage_tri[8][kShadeStage];
   __shared__ uint32_t stage_mask[8][kShadeStage];
   __shared__ uint32_t stage_pre[8][kShadeStage];
@@ -2084,7 +2099,8 @@ __global__ void __launch_bounds__(256, 2) k_shade(FrameConst fc, Buffers B) {
 // Deterministic stat merge (renderer.cpp:170-212): integer sums over the
 // owned bins' (bin, block-row) slots; warp shuffles, then one atomic per
 // warp and counter.
-__global__ void __launch_bounds__(256) k_finalize(FrameConst fc, Buffers B) {
+__global__ void __launch_bounds__(256) k_finalize(Buffers B) {
+  const FrameConst& fc = c_fc;
   if (B.ctr->error) return;
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long v[6] = {0, 0, 0, 0, 0, 0};
@@ -2116,7 +2132,8 @@ __global__ void __launch_bounds__(256) k_finalize(FrameConst fc, Buffers B) {
 // triangle covering a pixel is in that pixel's bin list. Fragments are
 // blended in exact key order by repeated selection of the next key, so no
 // per-pixel list storage is needed (an oracle mode, not a fast path).
-__global__ void __launch_bounds__(128) k_abuffer(FrameConst fc, Buffers B) {
+__global__ void __launch_bounds__(128) k_abuffer(Buffers B) {
+  const FrameConst& fc = c_fc;
   if (B.ctr->error) return;
   const int px = blockIdx.x * 16 + (threadIdx.x & 15);
   const int py = blockIdx.y * 8 + (threadIdx.x >> 4);
@@ -2244,6 +2261,8 @@ struct DeviceScene {
   uint32_t items_cap = 0;
   uint32_t pool_cap = 0;
   uint32_t lpairs_cap = 0;
+  dev::FrameConst* fc_host = nullptr;  // pinned staging of c_fc (graph memcpy source)
+  dev::Counters* ctr_host = nullptr;   // pinned counters readback
   bool extract_configured = false;
   int extract_ctas = 0;
   cudaEvent_t ev[6] = {};  // frame start, setup, binning, low extract, end, high extract
@@ -2254,6 +2273,8 @@ struct DeviceScene {
   int raster_ctas_global = 0;
 
   ~DeviceScene() {
+    if (fc_host) cudaFreeHost(fc_host);
+    if (ctr_host) cudaFreeHost(ctr_host);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     if (stream) cudaStreamDestroy(stream);
@@ -2332,6 +2353,8 @@ DeviceScene* device_scene(const Scene& s) {
     d->device = t_device;
     ck(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking), "cudaStreamCreate");
     for (auto& e : d->ev) ck(cudaEventCreate(&e), "cudaEventCreate");
+    ck(cudaMallocHost(reinterpret_cast<void**>(&d->fc_host), sizeof(dev::FrameConst)), "cudaMallocHost");
+    ck(cudaMallocHost(reinterpret_cast<void**>(&d->ctr_host), sizeof(dev::Counters)), "cudaMallocHost");
     cudaDeviceGetAttribute(&d->sm_count, cudaDevAttrMultiProcessorCount, t_device);
     {  // exact unpack tables (IEEE float division on the host)
       float lc[256], ln[1024];
@@ -2452,10 +2475,10 @@ void launch_extract(DeviceScene* d, const dev::FrameConst& fc, const dev::Buffer
     d->extract_configured = true;
   }
   const int grid = int(std::min<long long>(d->extract_ctas, (long long)fc.nbins * 4));
-  dev::k_extract<false><<<grid, 128, smem, d->stream>>>(fc, B, pass, dev::RasterShared::kTbr,
+  dev::k_extract<false><<<grid, 128, smem, d->stream>>>(B, pass, dev::RasterShared::kTbr,
                                                           dev::RasterShared::kTb);
   ck(cudaGetLastError(), "k_extract launch");
-  dev::k_extract<true><<<d->raster_ctas_global, 128, 0, d->stream>>>(fc, B, pass, gcap_tbr, gcap_tb);
+  dev::k_extract<true><<<d->raster_ctas_global, 128, 0, d->stream>>>(B, pass, gcap_tbr, gcap_tb);
   *launches += 2;
 }
 
@@ -2477,7 +2500,7 @@ void launch_shade_mode(DeviceScene* d, const dev::FrameConst& fc, const dev::Buf
   const long long items = kMode == 1 ? ((long long)fc.nbins * 32 + 7) / 8 : (long long)fc.nbins;
   const int grid = int(std::max<long long>(1, std::min<long long>((long long)std::max(1, per_sm) * d->sm_count,
                                                                    items)));
-  dev::k_shade<KM, kMode><<<grid, 256, dyn, d->stream>>>(fc, B);
+  dev::k_shade<KM, kMode><<<grid, 256, dyn, d->stream>>>(B);
   ck(cudaGetLastError(), "k_shade launch");
   ++*launches;
 }
@@ -2714,28 +2737,32 @@ int enqueue_front(DeviceScene* d, Prepared& P) {
   const dev::Buffers& B = P.B;
   cudaStream_t st = d->stream;
   int launches = 0;
+  *d->fc_host = fc;
+  ck(cudaMemcpyToSymbolAsync(dev::c_fc, d->fc_host, sizeof(dev::FrameConst), 0,
+                             cudaMemcpyHostToDevice, st),
+     "c_fc upload");
   ck(cudaMemsetAsync(B.ctr, 0, sizeof(dev::Counters), st), "memset");
   ck(cudaMemsetAsync(&B.ctr->bin_error, 0xff, sizeof(unsigned long long), st), "memset");
   ck(cudaMemsetAsync(B.qcnt, 0, size_t(fc.nbins) * 4, st), "memset");
   ck(cudaMemsetAsync(B.tcnt, 0, size_t(fc.nbins) * 4, st), "memset");
   cudaEventRecord(d->ev[0], st);
   if (P.nblocks) {
-    dev::k_setup_count<<<P.nblocks, dev::kSetupBlock, 0, st>>>(fc, B);
-    dev::k_scan_blocks<<<1, 1024, 0, st>>>(fc, B, P.nblocks);
-    dev::k_setup_write<<<P.nblocks, dev::kSetupBlock, 0, st>>>(fc, B);
+    dev::k_setup_count<<<P.nblocks, dev::kSetupBlock, 0, st>>>(B);
+    dev::k_scan_blocks<<<1, 1024, 0, st>>>(B, P.nblocks);
+    dev::k_setup_write<<<P.nblocks, dev::kSetupBlock, 0, st>>>(B);
     const int tgrid = int(std::min<long long>(((long long)fc.nquads * 2 + dev::kTriBlock - 1) / dev::kTriBlock,
                                               (long long)d->sm_count * 32));
-    dev::k_setup_tris<<<std::max(1, tgrid), dev::kTriBlock, 0, st>>>(fc, B);
+    dev::k_setup_tris<<<std::max(1, tgrid), dev::kTriBlock, 0, st>>>(B);
     launches += 4;
   }
   cudaEventRecord(d->ev[1], st);
   int grid = std::max(1, std::min<int>(d->sm_count * 8, int((fc.nquads + 255) / 256)));
-  dev::k_bin_pass<false><<<grid, 256, 0, st>>>(fc, B);
-  dev::k_bin_large<false><<<d->sm_count * 8, 256, 0, st>>>(fc, B);
-  dev::k_bin_scan<<<1, 1024, 0, st>>>(fc, B);
-  dev::k_bin_pass<true><<<grid, 256, 0, st>>>(fc, B);
-  dev::k_bin_large<true><<<d->sm_count * 8, 256, 0, st>>>(fc, B);
-  dev::k_bin_sort<<<std::min(fc.nbins, d->sm_count * 8), 256, 0, st>>>(fc, B);
+  dev::k_bin_pass<false><<<grid, 256, 0, st>>>(B);
+  dev::k_bin_large<false><<<d->sm_count * 8, 256, 0, st>>>(B);
+  dev::k_bin_scan<<<1, 1024, 0, st>>>(B);
+  dev::k_bin_pass<true><<<grid, 256, 0, st>>>(B);
+  dev::k_bin_large<true><<<d->sm_count * 8, 256, 0, st>>>(B);
+  dev::k_bin_sort<<<std::min(fc.nbins, d->sm_count * 8), 256, 0, st>>>(B);
   launches += 6;
   cudaEventRecord(d->ev[2], st);
   return launches;
@@ -2918,12 +2945,17 @@ static void enqueue_raster(DeviceScene* d, Prepared& P, int* launches) {
   launch_extract(d, P.fc, P.B, dev::kPassHigh, P.gcap_tbr, P.gcap_tb, launches);
   cudaEventRecord(d->ev[5], d->stream);
   launch_shade(d, P.fc, P.B, launches);
-  dev::k_finalize<<<(P.fc.nbins + 255) / 256, 256, 0, d->stream>>>(P.fc, P.B);
+  dev::k_finalize<<<(P.fc.nbins + 255) / 256, 256, 0, d->stream>>>(P.B);
   ++*launches;
   cudaEventRecord(d->ev[4], d->stream);
 }
 
+namespace {
+std::mutex g_frame_mu;  // frames share the __constant__ c_fc: one in flight at a time
+}
+
 void render_frame(const Scene& s, const RenderOptions& opt, RenderOutput* out) {
+  std::lock_guard<std::mutex> frame_lock(g_frame_mu);
   validate_frame(s, opt);
   DeviceScene* d = device_scene(s);
   for (int attempt = 0; attempt < 8; ++attempt) {
@@ -3030,13 +3062,14 @@ void render_frame(const Scene& s, const RenderOptions& opt, RenderOutput* out) {
 }
 
 void render_reference_frame(const Scene& s, const RenderOptions& opt, RenderOutput* out) {
+  std::lock_guard<std::mutex> frame_lock(g_frame_mu);
   validate_scene(s);
   DeviceScene* d = device_scene(s);
   Prepared P = prepare(d, s, opt);
   for (int attempt = 0; attempt < 8; ++attempt) {
     int launches = enqueue_front(d, P);
     dim3 grid((s.camera.width + 15) / 16, (s.camera.height + 7) / 8);
-    dev::k_abuffer<<<grid, 128, 0, d->stream>>>(P.fc, P.B);
+    dev::k_abuffer<<<grid, 128, 0, d->stream>>>(P.B);
     ++launches;
     cudaEventRecord(d->ev[3], d->stream);
     cudaEventRecord(d->ev[5], d->stream);
