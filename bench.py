@@ -113,6 +113,18 @@ def bytes_model(stats, width, height, a_q=32, a_v=8):
     return frame, raster, b_min
 
 
+def traffic_per_frame(workload):
+    """DRAM bytes (read + write) of the bin-rasterizer kernels for one frame,
+    from the committed ncu --set full capture (profiles/*_traffic.json,
+    written by tools/ncu_traffic.py); None when no capture exists."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(workload, {}).get("raster_dram_bytes")
+    except (OSError, ValueError):
+        return None
+
+
 # ------------------------------------------------------------------- clocks
 
 class ClockSampler:
@@ -356,7 +368,8 @@ def run_ours(args):
             pass
         b_frame, b_raster, b_min = bytes_model(info, W, H)
         peak, peak_kind = peaks()
-        raster_ms = statistics.median([float(s.low_raster_ms + s.hi_raster_ms) for s in stats])
+        raster_ms = statistics.median([float(s.low_raster_ms + s.hi_raster_ms + s.shade_ms)
+                                       for s in stats])
         achieved = b_raster / (raster_ms * 1e-3) / 1e9
         launches = sum(int(s.kernel_launches) for s in stats)
         if world > 1:
@@ -390,8 +403,9 @@ def run_ours(args):
                            l2="flushed between timed frames (256 MiB write, outside the events)"),
             "e2e": e2e,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
-                         "kernel": "k_raster (bin rasterizer, low+high passes)",
+                         "frac": achieved / peak, "traffic": traffic_per_frame(cfg["workload"]),
+                         "kernel": "bin rasterizer: k_extract (low+high) + k_shade + k_finalize",
+                         "kernel_ms": raster_ms,
                          "algorithmic_bytes_per_launch": b_raster,
                          "peak_source": peak_kind,
                          "frame_bytes": b_frame, "frame_bytes_min": b_min,
@@ -400,7 +414,8 @@ def run_ours(args):
             "clocks": clk,
             "gpu_launches": launches,
             "stages_ms": {"setup": float(s0.setup_ms), "binning": float(s0.binning_ms),
-                          "low_raster": float(s0.low_raster_ms), "hi_raster": float(s0.hi_raster_ms),
+                          "low_extract": float(s0.low_raster_ms), "hi_extract": float(s0.hi_raster_ms),
+                          "shade": float(s0.shade_ms),
                           "total": float(s0.total_ms)},
         }
     if world > 1:

@@ -2263,6 +2263,11 @@ struct DeviceScene {
   uint32_t lpairs_cap = 0;
   dev::FrameConst* fc_host = nullptr;  // pinned staging of c_fc (graph memcpy source)
   dev::Counters* ctr_host = nullptr;   // pinned counters readback
+  // Cached CUDA graph of one whole frame (c_fc upload .. counters readback),
+  // valid while the launch-shaping inputs in graph_key are unchanged.
+  cudaGraphExec_t graph_exec = nullptr;
+  std::vector<uint8_t> graph_key;
+  int graph_launches = 0;
   bool extract_configured = false;
   int extract_ctas = 0;
   cudaEvent_t ev[6] = {};  // frame start, setup, binning, low extract, end, high extract
@@ -2273,6 +2278,7 @@ struct DeviceScene {
   int raster_ctas_global = 0;
 
   ~DeviceScene() {
+    if (graph_exec) cudaGraphExecDestroy(graph_exec);
     if (fc_host) cudaFreeHost(fc_host);
     if (ctr_host) cudaFreeHost(ctr_host);
     for (auto& e : ev)
@@ -2731,6 +2737,18 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   return P;
 }
 
+// Stage events: inside a graph capture they must be external event-record
+// nodes (a plain record only expresses a dependency there).
+void record_event(cudaEvent_t e, cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  if (cs == cudaStreamCaptureStatusActive) {
+    cudaEventRecordWithFlags(e, st, cudaEventRecordExternal);
+  } else {
+    cudaEventRecord(e, st);
+  }
+}
+
 // Enqueues setup + binning; returns kernel launches.
 int enqueue_front(DeviceScene* d, Prepared& P) {
   const dev::FrameConst& fc = P.fc;
@@ -2745,7 +2763,7 @@ int enqueue_front(DeviceScene* d, Prepared& P) {
   ck(cudaMemsetAsync(&B.ctr->bin_error, 0xff, sizeof(unsigned long long), st), "memset");
   ck(cudaMemsetAsync(B.qcnt, 0, size_t(fc.nbins) * 4, st), "memset");
   ck(cudaMemsetAsync(B.tcnt, 0, size_t(fc.nbins) * 4, st), "memset");
-  cudaEventRecord(d->ev[0], st);
+  record_event(d->ev[0], st);
   if (P.nblocks) {
     dev::k_setup_count<<<P.nblocks, dev::kSetupBlock, 0, st>>>(B);
     dev::k_scan_blocks<<<1, 1024, 0, st>>>(B, P.nblocks);
@@ -2755,7 +2773,7 @@ int enqueue_front(DeviceScene* d, Prepared& P) {
     dev::k_setup_tris<<<std::max(1, tgrid), dev::kTriBlock, 0, st>>>(B);
     launches += 4;
   }
-  cudaEventRecord(d->ev[1], st);
+  record_event(d->ev[1], st);
   int grid = std::max(1, std::min<int>(d->sm_count * 8, int((fc.nquads + 255) / 256)));
   dev::k_bin_pass<false><<<grid, 256, 0, st>>>(B);
   dev::k_bin_large<false><<<d->sm_count * 8, 256, 0, st>>>(B);
@@ -2764,7 +2782,7 @@ int enqueue_front(DeviceScene* d, Prepared& P) {
   dev::k_bin_large<true><<<d->sm_count * 8, 256, 0, st>>>(B);
   dev::k_bin_sort<<<std::min(fc.nbins, d->sm_count * 8), 256, 0, st>>>(B);
   launches += 6;
-  cudaEventRecord(d->ev[2], st);
+  record_event(d->ev[2], st);
   return launches;
 }
 
@@ -2826,7 +2844,12 @@ void check_frame_errors(const dev::Counters& c, const dev::FrameConst& fc) {
 }
 
 void validate_frame(const Scene& s, const RenderOptions& opt) {
-  validate_scene(s);
+  if (s.validated_version != s.geometry_version) {  // index checks once per geometry version
+    validate_scene(s);
+    s.validated_version = s.geometry_version;
+  } else {
+    validate_camera(s.camera, s.extended);
+  }
   for (const veil_material& m : s.materials)
     if (m.texture >= 0)
       throw Error(VEIL_ERR_INVALID_ARG,
@@ -2941,13 +2964,13 @@ void collect_dumps(DeviceScene* d, Prepared& P, const dev::Counters& c, RenderOu
 
 static void enqueue_raster(DeviceScene* d, Prepared& P, int* launches) {
   launch_extract(d, P.fc, P.B, dev::kPassLow, P.gcap_tbr, P.gcap_tb, launches);
-  cudaEventRecord(d->ev[3], d->stream);
+  record_event(d->ev[3], d->stream);
   launch_extract(d, P.fc, P.B, dev::kPassHigh, P.gcap_tbr, P.gcap_tb, launches);
-  cudaEventRecord(d->ev[5], d->stream);
+  record_event(d->ev[5], d->stream);
   launch_shade(d, P.fc, P.B, launches);
   dev::k_finalize<<<(P.fc.nbins + 255) / 256, 256, 0, d->stream>>>(P.B);
   ++*launches;
-  cudaEventRecord(d->ev[4], d->stream);
+  record_event(d->ev[4], d->stream);
 }
 
 namespace {
@@ -2958,13 +2981,67 @@ void render_frame(const Scene& s, const RenderOptions& opt, RenderOutput* out) {
   std::lock_guard<std::mutex> frame_lock(g_frame_mu);
   validate_frame(s, opt);
   DeviceScene* d = device_scene(s);
+  static const bool graphs_enabled = [] {
+    const char* e = std::getenv("VEIL_NO_GRAPH");
+    return !(e && *e && *e != '0');
+  }();
   for (int attempt = 0; attempt < 8; ++attempt) {
     Prepared P = prepare(d, s, opt);
-    int launches = enqueue_front(d, P);
-    enqueue_raster(d, P, &launches);
-    dev::Counters c;
-    ck(cudaMemcpyAsync(&c, P.B.ctr, sizeof c, cudaMemcpyDeviceToHost, d->stream), "counters");
+    int launches = 0;
+    if (graphs_enabled && !opt.dump) {
+      // One graph launch per frame. Everything a launch configuration or a
+      // kernel pointer depends on is in the key; per-frame values (camera,
+      // colours) reach the kernels through the c_fc memcpy node, which reads
+      // the pinned staging copy when the graph executes.
+      std::vector<uint8_t> key(sizeof(dev::Buffers) + sizeof(dev::FrameConst) + 12);
+      dev::FrameConst kf = P.fc;
+      std::memset(kf.m, 0, sizeof kf.m);
+      std::memset(kf.eye, 0, sizeof kf.eye);
+      std::memset(kf.fwd, 0, sizeof kf.fwd);
+      std::memset(kf.light, 0, sizeof kf.light);
+      std::memset(kf.bg, 0, sizeof kf.bg);
+      kf.ambient = 0;
+      std::memcpy(key.data(), &P.B, sizeof(dev::Buffers));
+      std::memcpy(key.data() + sizeof(dev::Buffers), &kf, sizeof kf);
+      uint32_t extra[3] = {P.nblocks, P.gcap_tbr, P.gcap_tb};
+      std::memcpy(key.data() + sizeof(dev::Buffers) + sizeof kf, extra, sizeof extra);
+      if (!d->graph_exec || key != d->graph_key) {
+        if (d->graph_exec) {
+          cudaGraphExecDestroy(d->graph_exec);
+          d->graph_exec = nullptr;
+        }
+        cudaGraph_t g = nullptr;
+        ck(cudaStreamBeginCapture(d->stream, cudaStreamCaptureModeRelaxed), "graph capture");
+        int n = 0;
+        try {
+          n = enqueue_front(d, P);
+          enqueue_raster(d, P, &n);
+          ck(cudaMemcpyAsync(d->ctr_host, P.B.ctr, sizeof(dev::Counters), cudaMemcpyDeviceToHost,
+                             d->stream),
+             "counters");
+        } catch (...) {
+          if (cudaStreamEndCapture(d->stream, &g) == cudaSuccess && g) cudaGraphDestroy(g);
+          throw;
+        }
+        ck(cudaStreamEndCapture(d->stream, &g), "graph capture");
+        cudaError_t ie = cudaGraphInstantiate(&d->graph_exec, g, 0);
+        cudaGraphDestroy(g);
+        ck(ie, "cudaGraphInstantiate");
+        d->graph_key = std::move(key);
+        d->graph_launches = n;
+      }
+      *d->fc_host = P.fc;
+      ck(cudaGraphLaunch(d->graph_exec, d->stream), "cudaGraphLaunch");
+      launches = d->graph_launches;
+    } else {
+      launches = enqueue_front(d, P);
+      enqueue_raster(d, P, &launches);
+      ck(cudaMemcpyAsync(d->ctr_host, P.B.ctr, sizeof(dev::Counters), cudaMemcpyDeviceToHost,
+                         d->stream),
+         "counters");
+    }
     ck(cudaStreamSynchronize(d->stream), "frame");
+    const dev::Counters c = *d->ctr_host;
     if (c.error & 2u) {  // bin item capacity: grow and re-run (first frames only)
       d->items_cap = uint32_t(std::min<unsigned long long>(c.pairs + c.pairs / 4 + 1024, 0xffffffffull));
       continue;
@@ -3071,9 +3148,9 @@ void render_reference_frame(const Scene& s, const RenderOptions& opt, RenderOutp
     dim3 grid((s.camera.width + 15) / 16, (s.camera.height + 7) / 8);
     dev::k_abuffer<<<grid, 128, 0, d->stream>>>(P.B);
     ++launches;
-    cudaEventRecord(d->ev[3], d->stream);
-    cudaEventRecord(d->ev[5], d->stream);
-    cudaEventRecord(d->ev[4], d->stream);
+    record_event(d->ev[3], d->stream);
+    record_event(d->ev[5], d->stream);
+    record_event(d->ev[4], d->stream);
     dev::Counters c;
     ck(cudaMemcpyAsync(&c, P.B.ctr, sizeof c, cudaMemcpyDeviceToHost, d->stream), "counters");
     ck(cudaStreamSynchronize(d->stream), "frame");

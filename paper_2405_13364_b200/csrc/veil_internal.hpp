@@ -62,6 +62,7 @@ struct Scene {
   Camera camera;
   bool extended = false;
   uint64_t geometry_version = 1;  // bumped on every geometry/material change
+  mutable uint64_t validated_version = 0;  // geometry_version last checked by validate_scene
 
   Scene();
   ~Scene();
