@@ -40,11 +40,18 @@ struct __align__(16) TriRec {
 };
 static_assert(sizeof(TriRec) == 128, "TriRec must be one cache line");
 
+// llround for 0 <= v < 2^31: truncate, then round half away from zero on
+// the exact fractional part (v - trunc(v) is representable).
+__device__ __forceinline__ uint32_t round_half_away_pos(double v) {
+  const uint32_t t = __double2uint_rz(v);
+  return t + (__dsub_rn(v, (double)t) >= 0.5 ? 1u : 0u);
+}
+
 // quantize_depth, packing.hpp:190-195
 __device__ __forceinline__ uint32_t quantize_depth(double d) {
   if (!(d > 0.0)) return 0u;
   if (d >= 1.0) return 4194303u;
-  return (uint32_t)llround(__dmul_rn(d, 4194303.0));
+  return round_half_away_pos(__dmul_rn(d, 4194303.0));
 }
 
 // quantize_channel, raster.hpp:86-90

@@ -979,10 +979,8 @@ __device__ __forceinline__ float4 blend(float4 acc, float4 s) {
                      __fadd_rn(acc.z, __fmul_rn(t, s.z)), __fadd_rn(acc.w, __fmul_rn(t, s.w)));
 }
 
-// normalize + Lambert + premultiply (shade_sample, shading.cpp:123-139) with
-// texture factor 1; mat = (base rgb, opacity).
-__device__ __forceinline__ float4 light_and_premultiply(const FrameConst& fc, float n[3],
-                                                        float4 color, float4 mat) {
+// normalize + Lambert (shade_sample, shading.cpp:123-136): the light factor.
+__device__ __forceinline__ float light_factor(const FrameConst& fc, float n[3]) {
   // normalize (float), math.hpp:80-85
   float len2 = __fadd_rn(__fadd_rn(__fmul_rn(n[0], n[0]), __fmul_rn(n[1], n[1])), __fmul_rn(n[2], n[2]));
   if (len2 <= 0.0f) {
@@ -996,12 +994,23 @@ __device__ __forceinline__ float4 light_and_premultiply(const FrameConst& fc, fl
   float d = __fadd_rn(__fadd_rn(__fmul_rn(n[0], fc.light[0]), __fmul_rn(n[1], fc.light[1])),
                       __fmul_rn(n[2], fc.light[2]));
   float lam = smaxf(0.0f, -d);
-  float light = sminf(1.0f, __fadd_rn(fc.ambient, lam));
+  return sminf(1.0f, __fadd_rn(fc.ambient, lam));
+}
+
+// base * colour * texture(1) * light, premultiplied (shading.cpp:137-139);
+// mat = (base rgb, opacity).
+__device__ __forceinline__ float4 premultiply(float4 color, float4 mat, float light) {
   float r = __fmul_rn(__fmul_rn(__fmul_rn(mat.x, color.x), 1.0f), light);
   float g = __fmul_rn(__fmul_rn(__fmul_rn(mat.y, color.y), 1.0f), light);
   float b = __fmul_rn(__fmul_rn(__fmul_rn(mat.z, color.z), 1.0f), light);
   float a = __fmul_rn(__fmul_rn(mat.w, color.w), 1.0f);
   return make_float4(__fmul_rn(r, a), __fmul_rn(g, a), __fmul_rn(b, a), a);
+}
+
+__device__ __forceinline__ float4 light_and_premultiply(const FrameConst& fc, float n[3],
+                                                        float4 color, float4 mat) {
+  const float light = light_factor(fc, n);
+  return premultiply(color, mat, light);
 }
 
 // make_sample_context (shading.cpp:24-77) + shade_sample (123-139), no
@@ -1118,7 +1127,11 @@ __device__ __forceinline__ float4 shade_decoded_bf(const FrameConst& fc, const B
 
 // A bin-row's triangle, staged in shared memory by k_shade: edge and depth
 // planes plus the decoded shading record (one copy per bin-row instead of
-// one L1/L2 load per sample).
+// one L1/L2 load per sample). Per-triangle constants are folded at staging:
+// without vertex normals the light factor is constant over the triangle
+// (flag 4, in `light`), and with neither vertex colours nor normals so is the
+// whole premultiplied colour (flag 8, in c[0]). Same float operations in the
+// same order, so bit-identical to shading every sample in full.
 struct __align__(16) StagedTri {
   double e[9];
   double dz[3];
@@ -1126,12 +1139,14 @@ struct __align__(16) StagedTri {
   float4 mat;
   float n[9];
   uint32_t flags;
-  uint32_t pad[2];
+  float light;
+  uint32_t pad;
 };
 static_assert(sizeof(StagedTri) == 208, "StagedTri layout");
 constexpr int kStageTris = 320;
 
-__device__ __forceinline__ void stage_triangle(const Buffers& B, uint32_t tri, StagedTri* dst) {
+__device__ __forceinline__ void stage_triangle(const FrameConst& fc, const Buffers& B, uint32_t tri,
+                                               StagedTri* dst) {
   const TriRec& t = B.tri[tri];
   const ShadeRec& sr = B.shade[tri];
   const double2* e2 = reinterpret_cast<const double2*>(&t.e[0]);
@@ -1145,10 +1160,11 @@ __device__ __forceinline__ void stage_triangle(const Buffers& B, uint32_t tri, S
   dst->dz[0] = t.dz.a;
   dst->dz[1] = t.dz.b;
   dst->dz[2] = t.dz.c;
+  const float4 mat = sr.mat;
   dst->c[0] = sr.c[0];
   dst->c[1] = sr.c[1];
   dst->c[2] = sr.c[2];
-  dst->mat = sr.mat;
+  dst->mat = mat;
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     const float4 nn = sr.n[k];
@@ -1156,7 +1172,19 @@ __device__ __forceinline__ void stage_triangle(const Buffers& B, uint32_t tri, S
     dst->n[3 * k + 1] = nn.y;
     dst->n[3 * k + 2] = nn.z;
   }
-  dst->flags = sr.flags;
+  uint32_t fl = sr.flags;
+  if (!(fl & 2u)) {
+    const float4 n0 = sr.n[0];
+    float n[3] = {n0.x, n0.y, n0.z};
+    const float light = light_factor(fc, n);
+    dst->light = light;
+    fl |= 4u;
+    if (!(fl & 1u)) {
+      dst->c[0] = premultiply(make_float4(1.0f, 1.0f, 1.0f, 1.0f), mat, light);
+      fl |= 8u;
+    }
+  }
+  dst->flags = fl;
 }
 
 // shade_decoded_bf on a staged triangle (bit-identical).
@@ -1165,26 +1193,33 @@ __device__ __forceinline__ float4 shade_staged(const FrameConst& fc, const Stage
   const double x = (double)px + 0.5, y = (double)py + 0.5;
   const Fn3 f0 = {T.e[0], T.e[1], T.e[2]}, f1 = {T.e[3], T.e[4], T.e[5]}, f2 = {T.e[6], T.e[7], T.e[8]};
   const Fn3 fz = {T.dz[0], T.dz[1], T.dz[2]};
+  *qd = quantize_depth(eval(fz, x, y));
+  const uint32_t fl = T.flags;
+  if (fl & 8u) return T.c[0];  // constant colour (barycentrics unused)
   const double e0 = eval(f0, x, y), e1 = eval(f1, x, y), e2 = eval(f2, x, y);
   const double sum = __dadd_rn(__dadd_rn(e0, e1), e2);
   const double inv = __ddiv_rn(1.0, sum);
   const float b0 = (float)__dmul_rn(e0, inv), b1 = (float)__dmul_rn(e1, inv),
               b2 = (float)__dmul_rn(e2, inv);
-  *qd = quantize_depth(eval(fz, x, y));
-  const uint32_t fl = T.flags;
-  const float4 c0 = T.c[0], c1 = T.c[1], c2 = T.c[2];
-  const bool hc = fl & 1u, hn = fl & 2u;
-  float4 color;
-  color.x = hc ? __fadd_rn(__fadd_rn(__fmul_rn(c0.x, b0), __fmul_rn(c1.x, b1)), __fmul_rn(c2.x, b2)) : 1.0f;
-  color.y = hc ? __fadd_rn(__fadd_rn(__fmul_rn(c0.y, b0), __fmul_rn(c1.y, b1)), __fmul_rn(c2.y, b2)) : 1.0f;
-  color.z = hc ? __fadd_rn(__fadd_rn(__fmul_rn(c0.z, b0), __fmul_rn(c1.z, b1)), __fmul_rn(c2.z, b2)) : 1.0f;
-  color.w = hc ? __fadd_rn(__fadd_rn(__fmul_rn(c0.w, b0), __fmul_rn(c1.w, b1)), __fmul_rn(c2.w, b2)) : 1.0f;
-  float n[3];
+  float4 color = make_float4(1.0f, 1.0f, 1.0f, 1.0f);
+  if (fl & 1u) {
+    const float4 c0 = T.c[0], c1 = T.c[1], c2 = T.c[2];
+    color.x = __fadd_rn(__fadd_rn(__fmul_rn(c0.x, b0), __fmul_rn(c1.x, b1)), __fmul_rn(c2.x, b2));
+    color.y = __fadd_rn(__fadd_rn(__fmul_rn(c0.y, b0), __fmul_rn(c1.y, b1)), __fmul_rn(c2.y, b2));
+    color.z = __fadd_rn(__fadd_rn(__fmul_rn(c0.z, b0), __fmul_rn(c1.z, b1)), __fmul_rn(c2.z, b2));
+    color.w = __fadd_rn(__fadd_rn(__fmul_rn(c0.w, b0), __fmul_rn(c1.w, b1)), __fmul_rn(c2.w, b2));
+  }
+  float light;
+  if (fl & 4u) {
+    light = T.light;
+  } else {
+    float n[3];
 #pragma unroll
-  for (int k = 0; k < 3; ++k)
-    n[k] = hn ? __fadd_rn(__fadd_rn(__fmul_rn(T.n[k], b0), __fmul_rn(T.n[3 + k], b1)), __fmul_rn(T.n[6 + k], b2))
-              : T.n[k];
-  return light_and_premultiply(fc, n, color, T.mat);
+    for (int k = 0; k < 3; ++k)
+      n[k] = __fadd_rn(__fadd_rn(__fmul_rn(T.n[k], b0), __fmul_rn(T.n[3 + k], b1)), __fmul_rn(T.n[6 + k], b2));
+    light = light_factor(fc, n);
+  }
+  return premultiply(color, T.mat, light);
 }
 
 __device__ __forceinline__ uint64_t sample_key(const FrameConst& fc, uint32_t qd, uint32_t tri) {
@@ -1987,7 +2022,7 @@ __global__ void __launch_bounds__(256, 2) k_shade(Buffers B) {
           if (staged_ok)
             for (uint32_t j = threadIdx.x; j < T; j += blockDim.x) {
               const uint32_t tri = j < 2 * nq ? B.items[o + (j >> 1)] * 2 + (j & 1) : B.items[o + nq + (j - 2 * nq)];
-              stage_triangle(B, tri, &row_tris[j]);
+              stage_triangle(fc, B, tri, &row_tris[j]);
             }
         }
         __syncthreads();
