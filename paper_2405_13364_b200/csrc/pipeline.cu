@@ -84,6 +84,7 @@ struct FrameConst {
   uint32_t pool_cap;
   uint32_t lpairs_cap;
   int debug;  // experiment switch (VEIL_DEBUG_SHADE), 0 in production
+  int sort_bins;  // host-side: canonical bin-list order (k_bin_sort) this frame
 };
 
 // Frame constants live in constant memory, written once per frame by a
@@ -2653,6 +2654,12 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   fc.world = opt.world_size;
   fc.dump = opt.dump ? 1 : 0;
   if (const char* dbg = std::getenv("VEIL_DEBUG_SHADE")) fc.debug = std::atoi(dbg);
+  // Only the parity dumps need each bin's list in the reference's canonical
+  // order: the rasterizer orders tri-blocks by (depth, large, triangle) keys
+  // and counts limits, so it is independent of the order of a bin's items.
+  // VEIL_BIN_SORT=0/1 forces the choice (tests check dumps of unsorted lists).
+  fc.sort_bins = opt.dump ? 1 : 0;
+  if (const char* bs = std::getenv("VEIL_BIN_SORT")) fc.sort_bins = std::atoi(bs) ? 1 : 0;
 
   const uint32_t Q = d->nquads;
   const size_t nb = size_t(fc.nbins);
@@ -2815,8 +2822,11 @@ int enqueue_front(DeviceScene* d, Prepared& P) {
   dev::k_bin_scan<<<1, 1024, 0, st>>>(B);
   dev::k_bin_pass<true><<<grid, 256, 0, st>>>(B);
   dev::k_bin_large<true><<<d->sm_count * 8, 256, 0, st>>>(B);
-  dev::k_bin_sort<<<std::min(fc.nbins, d->sm_count * 8), 256, 0, st>>>(B);
-  launches += 6;
+  launches += 5;
+  if (fc.sort_bins) {
+    dev::k_bin_sort<<<std::min(fc.nbins, d->sm_count * 8), 256, 0, st>>>(B);
+    ++launches;
+  }
   record_event(d->ev[2], st);
   return launches;
 }

@@ -261,3 +261,23 @@ def test_graph_replay_across_cameras_and_params():
         exp = bindings.oracle_render(arr.with_camera(m, eye), p, names=["image", "mask"])
         assert np.array_equal(r.pixels().reshape(-1), exp["image"].reshape(-1)), (f, df, flags)
         assert np.array_equal(r.invalid_mask().reshape(-1), exp["mask"].reshape(-1)), (f, df, flags)
+
+
+@pytest.mark.parametrize("kind,size", [("random_soup", (160, 128)), ("dense_bin", (256, 256))])
+def test_rasterizer_independent_of_bin_item_order(kind, size, monkeypatch):
+    """Frames skip the canonical per-bin sort (only dumps need it): with the
+    lists left in atomic-scatter order every THB list, per-pixel blend-order
+    hash, image byte and counter must still equal the restatement, and each
+    bin must hold the same items."""
+    arr = veil.Scene.synthetic(kind, 5, *size).arrays()
+    p = default_params()
+    expect = bindings.oracle_render(arr, p)
+    monkeypatch.setenv("VEIL_BIN_SORT", "0")
+    got = gpu_dump(arr, p)
+    names = [n for n in PARITY_ARRAYS if n != "bin_items"]
+    bad = compare(got, expect, names)
+    assert not bad, bad
+    offs, qc, tc = expect["bin_offsets"], expect["bin_quad_counts"], expect["bin_tri_counts"]
+    for b in range(len(offs)):
+        o, n = int(offs[b]), int(qc[b]) + int(tc[b])
+        assert np.array_equal(np.sort(got["bin_items"][o:o + n]), np.sort(expect["bin_items"][o:o + n])), b
