@@ -156,6 +156,7 @@ struct Buffers {
   uint8_t* cat;
   uint8_t* prop;
   uint32_t* items;
+  uint8_t* item_rows;  // per item: block-rows (of its bin) each triangle's y range meets
   // raster
   unsigned long long* slots;  // per (bin, row): samples, frags, thb, segments, invalid
   uint32_t* spill[2];
@@ -607,6 +608,20 @@ __device__ void tri_bins(const FrameConst& fc, const TriRec& t, Fn&& fn) {
   }
 }
 
+// Which of a bin's four 8-row block-rows a triangle's pixel-row range meets
+// (the candidate test of k_extract's phase A, precomputed at binning so the
+// extraction scans a 1-byte mask per item instead of gathering tri_y).
+__device__ __forceinline__ uint32_t block_rows_mask(uint32_t yy, int by, int height) {
+  const int y_lo = (int)(int16_t)(yy & 0xffffu), y_hi = (int)(int16_t)(yy >> 16);
+  uint32_t m = 0;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int ry0 = by * kBin + r * 8, ry1 = min(ry0 + 7, height - 1);
+    if (max(y_lo, ry0) <= min(y_hi, ry1)) m |= 1u << r;
+  }
+  return m;
+}
+
 template <bool kWrite>
 __global__ void __launch_bounds__(256) k_bin_pass(Buffers B) {
   const FrameConst& fc = c_fc;
@@ -653,7 +668,12 @@ __global__ void __launch_bounds__(256) k_bin_pass(Buffers B) {
         if (kWrite) {
           uint32_t slot = 0;
           warp_agg_add(B.qcur, bin, act, &slot);
-          if (act && slot < fc.items_cap) B.items[slot] = q;
+          if (act && slot < fc.items_cap) {
+            B.items[slot] = q;
+            const uint2 ty = *reinterpret_cast<const uint2*>(&B.tri_y[2 * q]);
+            B.item_rows[slot] = (uint8_t)(block_rows_mask(ty.x, (int)by, fc.height) |
+                                          (block_rows_mask(ty.y, (int)by, fc.height) << 4));
+          }
         } else {
           warp_agg_add(B.qcnt, bin, act, nullptr);
         }
@@ -695,7 +715,10 @@ __global__ void __launch_bounds__(256) k_bin_large(Buffers B) {
         const int bin = R * fc.bins_x + wd * 32 + lane;
         if (kWrite) {
           const uint32_t slot = atomicAdd(&B.tcur[bin], 1u);
-          if (slot < fc.items_cap) B.items[slot] = ti;
+          if (slot < fc.items_cap) {
+            B.items[slot] = ti;
+            B.item_rows[slot] = (uint8_t)block_rows_mask(B.tri_y[ti], R, fc.height);
+          }
         } else {
           atomicAdd(&B.tcnt[bin], 1u);
         }
@@ -785,6 +808,16 @@ __global__ void __launch_bounds__(256) k_bin_sort(Buffers B) {
     uint32_t qc = B.qcnt[b], tc = B.tcnt[b], o = B.off[b];
     cta_sort_segment(B.items + o, qc, sm, 4096);
     cta_sort_segment(B.items + o + qc, tc, sm, 4096);
+    __syncthreads();
+    const int by = b / fc.bins_x;  // the row masks follow their items
+    for (uint32_t i = threadIdx.x; i < qc + tc; i += blockDim.x) {
+      const uint32_t it = B.items[o + i];
+      B.item_rows[o + i] =
+          i < qc ? (uint8_t)(block_rows_mask(B.tri_y[2 * it], by, fc.height) |
+                             (block_rows_mask(B.tri_y[2 * it + 1], by, fc.height) << 4))
+                 : (uint8_t)block_rows_mask(B.tri_y[it], by, fc.height);
+    }
+    __syncthreads();
   }
 }
 
@@ -1615,18 +1648,15 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
       bool keep = false;
       uint64_t code = 0;
       if (i < end) {
-        uint32_t ti, large;
-        if (i < 2 * nq) {
-          ti = B.items[o + (i >> 1)] * 2 + (i & 1);
-          large = 0;
-        } else {
-          ti = B.items[o + nq + (i - 2 * nq)];
-          large = 1;
+        const uint32_t large = i < 2 * nq ? 0u : 1u;
+        const uint32_t at = large ? o + nq + (i - 2 * nq) : o + (i >> 1);
+        const uint32_t rows = (uint32_t)B.item_rows[at] >> (large ? 0 : 4 * (i & 1));
+        keep = (rows >> row) & 1u;
+        if (keep) {
+          const uint32_t it = B.items[at];
+          const uint32_t ti = large ? it : it * 2 + (i & 1);
+          code = ((uint64_t)i << 32) | ti | (large << 31);
         }
-        const uint32_t yy = __ldg(&B.tri_y[ti]);
-        const int y_lo = (int)(int16_t)(yy & 0xffffu), y_hi = (int)(int16_t)(yy >> 16);
-        keep = max(y_lo, ry0) <= min(y_hi, ry1);
-        code = ((uint64_t)i << 32) | ti | (large << 31);
       }
       const unsigned m = __ballot_sync(0xffffffffu, keep);
       uint32_t wbase = 0;
@@ -2291,7 +2321,7 @@ struct DeviceScene {
   DevBuf pos, vcol, vnrm, quads, qmat, mats;
   DevBuf block_cnt, block_off, vq_src, vq_box, vq_flags, vq_mat, vq_col, vq_nrm, tri, tri_meta, shade,
       tri_y;
-  DevBuf qcnt, tcnt, off, qcur, tcur, cat, prop, items, slots, spill0, spill1, scratch, fb, mask,
+  DevBuf qcnt, tcnt, off, qcur, tcur, cat, prop, items, item_rows, slots, spill0, spill1, scratch, fb, mask,
       hash, emit, ctr, tile_ids, hbd, pool_tri, pool_mask, pool_pre, seg_queue, pool_slot, rowd,
       rowtri, lpairs;
   uint32_t items_cap = 0;
@@ -2692,6 +2722,7 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   d->spill1.ensure(nb * 4 * 4);
   if (d->items_cap == 0) d->items_cap = std::max<uint32_t>(1u << 20, Q * 6u);
   d->items.ensure(size_t(d->items_cap) * 4);
+  d->item_rows.ensure(size_t(d->items_cap));
   fc.items_cap = d->items_cap;
   const size_t npx = size_t(cam.width) * cam.height;
   d->fb.ensure(npx * 4);
@@ -2757,6 +2788,7 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   B.cat = d->cat.as<uint8_t>();
   B.prop = d->prop.as<uint8_t>();
   B.items = d->items.as<uint32_t>();
+  B.item_rows = d->item_rows.as<uint8_t>();
   B.slots = d->slots.as<unsigned long long>();
   B.spill[0] = d->spill0.as<uint32_t>();
   B.spill[1] = d->spill1.as<uint32_t>();
