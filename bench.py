@@ -47,6 +47,13 @@ def parse():
                     help="bound on the CPU-baseline sample (rank 0, N=1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo gathers tiles through host memory (orchestration tests)")
+    ap.add_argument("--single-device", action="store_true",
+                    help="every rank on cuda:0 (orchestration tests with --dist-backend gloo; "
+                         "ranks never wait on each other inside kernels)")
+    ap.add_argument("--check-frame", action="store_true",
+                    help="rank 0 compares the gathered frame with an unsharded render")
     return ap.parse_args()
 
 
@@ -232,9 +239,16 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.single_device:
+        local = 0
+    gloo = args.dist_backend == "gloo"
+    cdev = "cpu" if gloo else "cuda"  # where collective tensors live
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if gloo:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     torch.cuda.set_device(local)
     veil.set_device(local)
 
@@ -249,7 +263,8 @@ def run_ours(args):
     counts = [veil.shard_tile_count(bx, by, r, world) for r in range(world)]
     max_tiles = max(counts)
     tiles = torch.empty(max_tiles * 5120, dtype=torch.uint8, device="cuda")
-    gathered = [torch.empty_like(tiles) for _ in range(world)] if (world > 1 and rank == 0) else None
+    gathered = ([torch.empty_like(tiles, device=cdev) for _ in range(world)]
+                if (world > 1 and rank == 0) else None)
 
     def frame(i, timed_events=None):
         if camera_fn:
@@ -261,13 +276,16 @@ def run_ours(args):
         if world > 1:
             veil.pack_tiles_device(scene, rank, world, tiles.data_ptr(), tiles.numel())
             with torch.cuda.stream(stream):
+                mine = tiles.cpu() if gloo else tiles
                 if rank == 0:
-                    dist.gather(tiles, gathered, dst=0)
+                    dist.gather(mine, gathered, dst=0)
                     for r in range(1, world):
-                        veil.unpack_tiles_device(scene, r, world, gathered[r].data_ptr(),
-                                                 gathered[r].numel())
+                        g = gathered[r].to("cuda", non_blocking=False) if gloo else gathered[r]
+                        veil.unpack_tiles_device(scene, r, world, g.data_ptr(), g.numel())
+                        if gloo:
+                            stream.synchronize()  # g is freed on return
                 else:
-                    dist.gather(tiles, None, dst=0)
+                    dist.gather(mine, None, dst=0)
         if timed_events:
             timed_events[1].record(stream)
         return st
@@ -292,9 +310,9 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     ms = [a.elapsed_time(b) for a, b in evs]
-    ms_sum = torch.tensor([sum(ms)], dtype=torch.float64, device="cuda")
+    ms_sum = torch.tensor([sum(ms)], dtype=torch.float64, device=cdev)
     frag_local = torch.tensor([sum(int(s.fragments) for s in stats)], dtype=torch.float64,
-                              device="cuda")
+                              device=cdev)
     if world > 1:
         dist.all_reduce(ms_sum, op=dist.ReduceOp.MAX)
         dist.all_reduce(frag_local, op=dist.ReduceOp.SUM)
@@ -333,13 +351,14 @@ def run_ours(args):
                 dist.barrier()
                 t0 = time.perf_counter()
                 frame(i)
-                if rank == 0:  # D2H of the assembled framebuffer + mask
+                if rank == 0:  # D2H of the assembled framebuffer + mask (renderer's stream)
                     rgba, msk = scene.device_framebuffer()
-                    host[: W * H * 4].copy_(device_bytes(rgba, W * H * 4))
-                    host[W * H * 4:].copy_(device_bytes(msk, W * H))
+                    with torch.cuda.stream(stream):
+                        host[: W * H * 4].copy_(device_bytes(rgba, W * H * 4))
+                        host[W * H * 4:].copy_(device_bytes(msk, W * H))
                 torch.cuda.synchronize()
                 dt = torch.tensor([(time.perf_counter() - t0) * 1e3], dtype=torch.float64,
-                                  device="cuda")
+                                  device=cdev)
                 dist.all_reduce(dt, op=dist.ReduceOp.MAX)
                 e2e_ms.append(float(dt.item()))
             e2e_ms = statistics.median(e2e_ms)
@@ -347,6 +366,26 @@ def run_ours(args):
                    "ms_per_step": e2e_ms, "h2d_bytes_per_step": 128 + 64,
                    "d2h_bytes_per_step": W * H * 5,
                    "path": "sharded device frame + NCCL tile gather + rank-0 readback"}
+
+    frame_check = None
+    if args.check_frame:  # gathered frame vs an unsharded render of the same camera
+        k = args.warmup + args.steps
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        frame(k)
+        torch.cuda.synchronize()
+        if rank == 0:
+            rgba, msk = scene.device_framebuffer()
+            with torch.cuda.stream(stream):
+                got = torch.cat([device_bytes(rgba, W * H * 4), device_bytes(msk, W * H)]).cpu()
+            full = veil.render(scene, params)
+            ref = np.concatenate([full.pixels().reshape(-1), full.invalid_mask().reshape(-1)])
+            diff = int((got.numpy() != ref).sum())
+            frame_check = {"identical": diff == 0, "differing_bytes": diff, "camera_index": k,
+                           "backend": args.dist_backend}
+        if world > 1:
+            dist.barrier()
 
     s0 = stats[-1]
     info = {
@@ -412,6 +451,7 @@ def run_ours(args):
                          "frame_frac": b_frame / (ms_per_frame * 1e-3) / 1e9 / peak},
             "cpu_baseline": cpu,
             "clocks": clk,
+            **({"frame_check": frame_check} if frame_check else {}),
             "gpu_launches": launches,
             "stages_ms": {"setup": float(s0.setup_ms), "binning": float(s0.binning_ms),
                           "low_extract": float(s0.low_raster_ms), "hi_extract": float(s0.hi_raster_ms),

@@ -138,6 +138,7 @@ struct Buffers {
   uint32_t* block_cnt;
   uint32_t* block_off;
   uint32_t* vq_src;
+  uint4* vq_idx;  // the visible quad's vertex indices (k_setup_tris gathers without vq_src -> quads)
   uint2* vq_box;  // (x0 | x1 << 16, y0 | y1 << 16)
   uint32_t* vq_flags;  // bit0 large, 1 colors, 2 normals, 3 uvs, 4-5 cull flags
   uint32_t* vq_mat;
@@ -464,6 +465,7 @@ __global__ void __launch_bounds__(kSetupBlock) k_setup_write(Buffers B) {
   MatDev md = B.mats[mat];
   bool has_c = md.flags & 1u, has_n = md.flags & 2u;
   B.vq_src[slot] = q;
+  B.vq_idx[slot] = idx;
   B.vq_box[slot] = make_uint2((uint32_t)o.x0 | ((uint32_t)o.x1 << 16),
                               (uint32_t)o.y0 | ((uint32_t)o.y1 << 16));
   B.vq_flags[slot] = (o.large ? 1u : 0u) | (has_c ? 2u : 0u) | (has_n ? 4u : 0u) | (o.flags << 4);
@@ -500,10 +502,9 @@ __global__ void __launch_bounds__(kTriBlock) k_setup_tris(Buffers B) {
       slot = ti >> 1;
       t = ti & 1u;
       vf = B.vq_flags[slot];
+      const uint4 idx = B.vq_idx[slot];
+      mat = B.vq_mat[slot];
       if (!((vf >> 4) & (1u << t))) {  // not individually culled
-        const uint32_t q = B.vq_src[slot];
-        mat = B.vq_mat[slot];
-        const uint4 idx = B.quads[q];
         const uint32_t i1 = t == 0 ? idx.y : idx.z, i2 = t == 0 ? idx.z : idx.w;
         const float4 p0 = __ldg(&B.pos[idx.x]), p1 = __ldg(&B.pos[i1]), p2 = __ldg(&B.pos[i2]);
         double c0[4], c1[4], c2[4];
@@ -2319,7 +2320,7 @@ struct DeviceScene {
   uint64_t uploaded_version = 0;
   uint32_t nverts = 0, nquads = 0;
   DevBuf pos, vcol, vnrm, quads, qmat, mats;
-  DevBuf block_cnt, block_off, vq_src, vq_box, vq_flags, vq_mat, vq_col, vq_nrm, tri, tri_meta, shade,
+  DevBuf block_cnt, block_off, vq_src, vq_idx, vq_box, vq_flags, vq_mat, vq_col, vq_nrm, tri, tri_meta, shade,
       tri_y;
   DevBuf qcnt, tcnt, off, qcur, tcur, cat, prop, items, item_rows, slots, spill0, spill1, scratch, fb, mask,
       hash, emit, ctr, tile_ids, hbd, pool_tri, pool_mask, pool_pre, seg_queue, pool_slot, rowd,
@@ -2697,6 +2698,7 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   d->block_cnt.ensure(std::max<size_t>(1, P.nblocks) * 4);
   d->block_off.ensure(std::max<size_t>(1, P.nblocks) * 4);
   d->vq_src.ensure(size_t(Q) * 4);
+  d->vq_idx.ensure(size_t(Q) * 16);
   d->vq_box.ensure(size_t(Q) * 8);
   d->vq_flags.ensure(size_t(Q) * 4);
   d->vq_mat.ensure(size_t(Q) * 4);
@@ -2771,6 +2773,7 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   B.block_cnt = d->block_cnt.as<uint32_t>();
   B.block_off = d->block_off.as<uint32_t>();
   B.vq_src = d->vq_src.as<uint32_t>();
+  B.vq_idx = d->vq_idx.as<uint4>();
   B.vq_box = d->vq_box.as<uint2>();
   B.vq_flags = d->vq_flags.as<uint32_t>();
   B.vq_mat = d->vq_mat.as<uint32_t>();
