@@ -1267,6 +1267,7 @@ struct RasterView {
   Tbr* tbr;
   uint64_t* keys;  // [4][cap_tb]
   uint16_t* refs;  // [4][cap_tb]
+  uint32_t* rows;  // phase A: [4 warps][32 candidates][b0 b1 l0 l1] (aliases refs in SMEM)
 };
 
 struct RasterShared {
@@ -1275,11 +1276,12 @@ struct RasterShared {
   static constexpr int kTbr = 1024, kTb = 256;
   Tbr tbr[kTbr];
   uint64_t keys[4 * kTb];
-  uint16_t refs[4 * kTb];
+  __align__(16) uint16_t refs[4 * kTb];
 };
+static_assert(sizeof(uint16_t) * 4 * RasterShared::kTb >= 4 * 32 * 16, "phase-A row scratch");
 
 __host__ __device__ inline size_t global_scratch_bytes(uint32_t cap_tbr, uint32_t cap_tb) {
-  return (size_t)cap_tbr * sizeof(Tbr) + (size_t)4 * cap_tb * (8 + 2) + 64;
+  return (size_t)cap_tbr * sizeof(Tbr) + (size_t)4 * cap_tb * (8 + 2) + 64 + 2048 + 16;
 }
 
 struct ItemState {
@@ -1667,40 +1669,110 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
     }
     __syncthreads();
     const uint32_t nc = st->ncand;
-    for (uint32_t j = threadIdx.x; j < nc; j += blockDim.x) {
-      const uint64_t code = cand[j];
-      const uint32_t ti = (uint32_t)code & 0x7fffffffu, large = ((uint32_t)code) >> 31;
-      const TriRec& t = B.tri[ti];
-      const int yb = max(t.y_min, ry0), ye = min(t.y_max, ry1);
-      uint32_t rb0 = 0x1f1f1f1fu, rb1 = 0x1f1f1f1fu, rl0 = 0u, rl1 = 0u, cols = 0;
-      for (int py = yb; py <= ye; ++py) {
-        int b, l;
-        if (!row_span(t, py, px0, px_last, &b, &l)) continue;
-        const int ly = py - ry0;
-        const uint32_t bb = (uint32_t)(b - px0), ll = (uint32_t)(l - px0);
-        const int sh8 = (ly & 3) * 8;
-        const uint32_t keepm = ~(0xffu << sh8);
-        if (ly < 4) {
-          rb0 = (rb0 & keepm) | (bb << sh8);
-          rl0 = (rl0 & keepm) | (ll << sh8);
-        } else {
-          rb1 = (rb1 & keepm) | (bb << sh8);
-          rl1 = (rl1 & keepm) | (ll << sh8);
-        }
-        cols |= ((2u << (ll >> 3)) - 1u) & ~((1u << (bb >> 3)) - 1u);
+    // Row spans, load-balanced per warp: a warp takes 32 candidates, scans
+    // their row counts and spreads the (candidate, row) pairs over its lanes,
+    // so tall and short triangles keep all lanes busy; each candidate's lane
+    // then assembles its tri-block-row from the per-row bytes.
+    uint32_t* rs = V.rows + (size_t)warp * 128u;  // [candidate][b0 b1 l0 l1]
+    for (uint32_t g = (uint32_t)warp * 32u; g < nc; g += (blockDim.x >> 5) * 32u) {
+      const uint32_t j = g + lane;
+      uint32_t ti = 0, large = 0, nrows = 0;
+      int yb = 0;
+      uint64_t code = 0;
+      if (j < nc) {
+        code = cand[j];
+        ti = (uint32_t)code & 0x7fffffffu;
+        large = ((uint32_t)code) >> 31;
+        const TriRec& t = B.tri[ti];
+        yb = max(t.y_min, ry0);
+        const int ye = min(t.y_max, ry1);
+        nrows = ye >= yb ? (uint32_t)(ye - yb + 1) : 0u;
       }
-      if (!cols) continue;
-      const int slot = atomicAdd(&st->ntbr, 1);
-      if ((uint32_t)slot < cap_tbr) {
-        Tbr rec;
-        rec.tri = ti;
-        rec.meta = cols | (large << 4);
-        rec.b[0] = rb0;
-        rec.b[1] = rb1;
-        rec.l[0] = rl0;
-        rec.l[1] = rl1;
-        rec.slot = (uint32_t)(code >> 32);
-        V.tbr[slot] = rec;
+      const uint32_t total = __reduce_add_sync(0xffffffffu, nrows);
+      const uint32_t ngroup = min(32u, nc - g);
+      uint32_t rb0 = 0x1f1f1f1fu, rb1 = 0x1f1f1f1fu, rl0 = 0u, rl1 = 0u, cols = 0;
+      if (total < 3u * ngroup) {
+        // short triangles (tiny-quad meshes): each lane walks its own rows
+        if (nrows) {
+          const TriRec& t = B.tri[ti];
+          for (uint32_t k = 0; k < nrows; ++k) {
+            const int py = yb + (int)k;
+            int b, l;
+            if (!row_span(t, py, px0, px_last, &b, &l)) continue;
+            const int ly = py - ry0;
+            const int sh8 = (ly & 3) * 8;
+            const uint32_t keepm = ~(0xffu << sh8);
+            const uint32_t bb = (uint32_t)(b - px0), ll = (uint32_t)(l - px0);
+            if (ly < 4) {
+              rb0 = (rb0 & keepm) | (bb << sh8);
+              rl0 = (rl0 & keepm) | (ll << sh8);
+            } else {
+              rb1 = (rb1 & keepm) | (bb << sh8);
+              rl1 = (rl1 & keepm) | (ll << sh8);
+            }
+            cols |= ((2u << (ll >> 3)) - 1u) & ~((1u << (bb >> 3)) - 1u);
+          }
+        }
+      } else {
+        // tall triangles: spread the (candidate, row) pairs over the lanes
+        reinterpret_cast<uint4*>(rs)[lane] = make_uint4(0x1f1f1f1fu, 0x1f1f1f1fu, 0u, 0u);
+        uint32_t incl = nrows;
+#pragma unroll
+        for (int sft = 1; sft < 32; sft <<= 1) {
+          const uint32_t v = __shfl_up_sync(0xffffffffu, incl, sft);
+          if (lane >= sft) incl += v;
+        }
+        const uint32_t excl = incl - nrows;
+        __syncwarp();
+        for (uint32_t p0 = 0; p0 < total; p0 += 32) {
+          const uint32_t p = p0 + lane;
+          uint32_t c = 0;  // largest c with excl[c] <= p (shuffle binary search)
+#pragma unroll
+          for (uint32_t sft = 16; sft > 0; sft >>= 1) {
+            const uint32_t e = __shfl_sync(0xffffffffu, excl, c + sft);
+            if (e <= p) c += sft;
+          }
+          const uint32_t ec = __shfl_sync(0xffffffffu, excl, c);
+          const uint32_t tc = __shfl_sync(0xffffffffu, ti, c);
+          const int yc = __shfl_sync(0xffffffffu, yb, c);
+          if (p < total) {
+            const int py = yc + (int)(p - ec);
+            int b, l;
+            if (row_span(B.tri[tc], py, px0, px_last, &b, &l)) {
+              const int ly = py - ry0;
+              reinterpret_cast<uint8_t*>(rs + c * 4)[ly] = (uint8_t)(b - px0);
+              reinterpret_cast<uint8_t*>(rs + c * 4 + 2)[ly] = (uint8_t)(l - px0);
+            }
+          }
+        }
+        __syncwarp();
+        const uint4 rr = reinterpret_cast<const uint4*>(rs)[lane];
+        rb0 = rr.x, rb1 = rr.y, rl0 = rr.z, rl1 = rr.w;
+        __syncwarp();
+        if (nrows) {
+#pragma unroll
+          for (int y = 0; y < 8; ++y) {
+            const uint32_t bb = ((y < 4 ? rb0 : rb1) >> ((y & 3) * 8)) & 0xffu;
+            const uint32_t ll = ((y < 4 ? rl0 : rl1) >> ((y & 3) * 8)) & 0xffu;
+            if (bb <= ll) cols |= ((2u << (ll >> 3)) - 1u) & ~((1u << (bb >> 3)) - 1u);
+          }
+        }
+      }
+      if (nrows) {
+        if (cols) {
+          const int slot = atomicAdd(&st->ntbr, 1);
+          if ((uint32_t)slot < cap_tbr) {
+            Tbr rec;
+            rec.tri = ti;
+            rec.meta = cols | (large << 4);
+            rec.b[0] = rb0;
+            rec.b[1] = rb1;
+            rec.l[0] = rl0;
+            rec.l[1] = rl1;
+            rec.slot = (uint32_t)(code >> 32);
+            V.tbr[slot] = rec;
+          }
+        }
       }
     }
     __syncthreads();
@@ -1943,11 +2015,14 @@ __global__ void __launch_bounds__(128) k_extract(Buffers B, int pass,
     V.keys = reinterpret_cast<uint64_t*>(g);
     g += (size_t)4 * cap_tb * 8;
     V.refs = reinterpret_cast<uint16_t*>(g);
+    g += (size_t)4 * cap_tb * 2;
+    V.rows = reinterpret_cast<uint32_t*>(((uintptr_t)g + 15) & ~(uintptr_t)15);
   } else {
     RasterShared* sh = reinterpret_cast<RasterShared*>(smem_raw);
     V.tbr = sh->tbr;
     V.keys = sh->keys;
     V.refs = sh->refs;
+    V.rows = reinterpret_cast<uint32_t*>(sh->refs);  // refs are unused until phase B
   }
   const uint32_t nitems = kGlobal ? B.ctr->spill_count[pass] : (uint32_t)fc.nbins * 4u;
   unsigned int* counter = &B.ctr->work_next[pass * 2 + (kGlobal ? 1 : 0)];

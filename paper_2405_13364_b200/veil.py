@@ -24,7 +24,8 @@ from .abi import (
 )
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libveil.so")
+# VEIL_LIB selects another build of the library (A/B timing of kernel variants)
+LIB_PATH = os.environ.get("VEIL_LIB") or os.path.join(HERE, "libveil.so")
 
 STATUS_NAMES = {0: "VEIL_OK", 1: "VEIL_ERR_IO", 2: "VEIL_ERR_PARSE", 3: "VEIL_ERR_INVALID_ARG",
                 4: "VEIL_ERR_CAPACITY", 5: "VEIL_ERR_INTERNAL"}
