@@ -31,13 +31,16 @@ Scene::~Scene() {
 
 double Scene::degenerate_quad_percent() const {
   if (quads.empty()) return 0.0;
+  if (degenerate_version == geometry_version) return degenerate_cache;  // per-frame report
   size_t n = 0;
   for (const veil_quad& q : quads) {
     bool t0 = q.v[0] == q.v[1] || q.v[1] == q.v[2] || q.v[0] == q.v[2];
     bool t1 = q.v[0] == q.v[2] || q.v[2] == q.v[3] || q.v[0] == q.v[3];
     if (t0 || t1) ++n;
   }
-  return 100.0 * double(n) / double(quads.size());
+  degenerate_cache = 100.0 * double(n) / double(quads.size());
+  degenerate_version = geometry_version;
+  return degenerate_cache;
 }
 
 void validate_camera(const Camera& c, bool extended) {

@@ -63,6 +63,8 @@ struct Scene {
   bool extended = false;
   uint64_t geometry_version = 1;  // bumped on every geometry/material change
   mutable uint64_t validated_version = 0;  // geometry_version last checked by validate_scene
+  mutable uint64_t degenerate_version = 0;  // geometry_version of degenerate_cache
+  mutable double degenerate_cache = 0.0;
 
   Scene();
   ~Scene();
