@@ -483,7 +483,7 @@ __global__ void __launch_bounds__(kSetupBlock) k_setup_write(Buffers B) {
 // memory and written back as 512-byte contiguous runs (coalesced stores).
 constexpr int kTriBlock = 128;
 
-__global__ void __launch_bounds__(kTriBlock) k_setup_tris(Buffers B) {
+__global__ void __launch_bounds__(kTriBlock, 6) k_setup_tris(Buffers B) {
   const FrameConst& fc = c_fc;
   __shared__ __align__(16) TriRec stage[kTriBlock];
   if (B.ctr->error & 1u) return;
