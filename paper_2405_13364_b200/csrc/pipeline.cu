@@ -2076,7 +2076,7 @@ constexpr uint32_t kWalkMinSamplesPerThb = 12;  // walk vs segments crossover
 // threshold walk for all. Separate instantiations keep each path's register
 // allocation small.
 template <int KM, int kMode>
-__global__ void __launch_bounds__(256, 2) k_shade(Buffers B) {
+__global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
   const FrameConst& fc = c_fc;
   __shared__ uint32_t stage_tri[8][kShadeStage];
   __shared__ uint32_t stage_mask[8][kShadeStage];
