@@ -85,6 +85,8 @@ struct FrameConst {
   uint32_t lpairs_cap;
   int debug;  // experiment switch (VEIL_DEBUG_SHADE), 0 in production
   int sort_bins;  // host-side: canonical bin-list order (k_bin_sort) this frame
+  int walk_min;   // experiment override of kWalkMinSamplesPerThb (VEIL_WALK_MIN), 0 = default
+  int walk_min_u; // the same for bins whose triangles are not staged (VEIL_WALK_MIN_U)
 };
 
 // Frame constants live in constant memory, written once per frame by a
@@ -2069,7 +2071,11 @@ __global__ void __launch_bounds__(128) k_extract(Buffers B, int pass,
 // mapping's dependent lookups on-chip. Empty bins and half-blocks without
 // samples composite the background.
 constexpr int kShadeStage = 256;  // THB entries staged per warp; longer lists stream
-constexpr uint32_t kWalkMinSamplesPerThb = 12;  // walk vs segments crossover
+// Wave walk (mode 0) vs dense segments (mode 1) crossover, in samples per
+// THB: lower when the bin's triangles are staged in shared memory (waves read
+// them there), higher when each lane gathers its triangle from global memory.
+constexpr uint32_t kWalkMinSamplesPerThbStaged = 6;
+constexpr uint32_t kWalkMinSamplesPerThb = 12;
 
 // kMode: 0 = broadcast walk for half-blocks with big THBs (also writes every
 // half-block without samples), 1 = segment routing for the rest, 2 = alpha
@@ -2159,7 +2165,9 @@ __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
     bool live = B.cat[bin] != 0;
     HbDesc d = {0, 0, 0, 0};
     if (live) d = B.hbd[(size_t)bin * 32 + hb];
-    const bool walk = !live || d.frags >= kWalkMinSamplesPerThb * d.cnt;
+    const uint32_t wmin = staged_ok ? (fc.walk_min ? (uint32_t)fc.walk_min : kWalkMinSamplesPerThbStaged)
+                                    : (fc.walk_min_u ? (uint32_t)fc.walk_min_u : kWalkMinSamplesPerThb);
+    const bool walk = !live || d.frags >= wmin * d.cnt;
     if (kMode == 0 && !walk) {  // small THBs: hand over to the routing kernel
       if (lane == 0) B.seg_queue[atomicAdd(&B.ctr->seg_count, 1u)] = item;
       continue;
@@ -2766,6 +2774,8 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   // VEIL_BIN_SORT=0/1 forces the choice (tests check dumps of unsorted lists).
   fc.sort_bins = opt.dump ? 1 : 0;
   if (const char* bs = std::getenv("VEIL_BIN_SORT")) fc.sort_bins = std::atoi(bs) ? 1 : 0;
+  if (const char* wm = std::getenv("VEIL_WALK_MIN")) fc.walk_min = std::atoi(wm);
+  if (const char* wm = std::getenv("VEIL_WALK_MIN_U")) fc.walk_min_u = std::atoi(wm);
 
   const uint32_t Q = d->nquads;
   const size_t nb = size_t(fc.nbins);

@@ -8,7 +8,8 @@ import os, sys, statistics, json
 sys.path.insert(0, os.environ["ROOT"])
 from paper_2405_13364_b200 import veil
 out = {}
-for name, seed in [("stack64k", 2), ("tiny4m", 4)]:
+for name in os.environ.get("AB_WORKLOADS", "stack64k,tiny4m").split(","):
+    seed = {"stack64k": 2, "tiny4m": 4, "mixed16m": 5}[name]
     sc = veil.Scene.workload(name, seed)
     for i in range(5): veil.render_device(sc)
     st = [veil.render_device(sc) for i in range(20)]
@@ -28,7 +29,7 @@ for rnd in range(2):
             print(l, "FAILED", p.stderr[-500:]); continue
         res[l].append(json.loads(p.stdout.strip().splitlines()[-1]))
 for l in libs:
-    for w in ("stack64k", "tiny4m"):
+    for w in os.environ.get("AB_WORKLOADS", "stack64k,tiny4m").split(","):
         rows = [r[w] for r in res[l]]
         if not rows: continue
         keys = rows[0].keys()
