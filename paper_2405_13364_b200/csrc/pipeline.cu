@@ -110,6 +110,7 @@ struct Counters {
   unsigned int shade_next[2];
   unsigned int seg_count;  // half-blocks queued for the segment-routing kernel
   unsigned int large_pairs;  // (large triangle, bin row) work pairs
+  unsigned int setup_ticket;  // k_setup: block order for the decoupled look-back
 };
 
 // Decoded per-triangle shading inputs (unpack_color / decode_normal of the
@@ -137,8 +138,7 @@ struct Buffers {
   const uint32_t* qmat;
   const MatDev* mats;
   // setup
-  uint32_t* block_cnt;
-  uint32_t* block_off;
+  unsigned long long* block_state;  // k_setup look-back: status << 32 | count
   uint32_t* vq_src;
   uint4* vq_idx;  // the visible quad's vertex indices (k_setup_tris gathers without vq_src -> quads)
   uint2* vq_box;  // (x0 | x1 << 16, y0 | y1 << 16)
@@ -300,34 +300,6 @@ __device__ void cull_quad(const FrameConst& fc, const uint4& idx, const float4 p
   o->large = (o->x1 - o->x0 + 1) * (o->y1 - o->y0 + 1) > 4;
 }
 
-__global__ void __launch_bounds__(kSetupBlock) k_setup_count(Buffers B) {
-  const FrameConst& fc = c_fc;
-  uint32_t q = blockIdx.x * kSetupBlock + threadIdx.x;
-  int reason = -1;
-  if (q < fc.nquads) {
-    uint4 idx;
-    float4 p[4];
-    load_quad(B, q, &idx, p);
-    double clip[4][4];
-    CullOut o;
-    cull_quad(fc, idx, p, clip, &o);
-    reason = o.reason;
-  }
-  int vis = __syncthreads_count(reason == 0);
-  int deg = __syncthreads_count(reason == 1);
-  int back = __syncthreads_count(reason == 2);
-  int fru = __syncthreads_count(reason == 3);
-  int bet = __syncthreads_count(reason == 4);
-  if (threadIdx.x == 0) {
-    B.block_cnt[blockIdx.x] = (uint32_t)vis;
-    if (vis) atomicAdd(&B.ctr->cull[0], (unsigned long long)vis);
-    if (deg) atomicAdd(&B.ctr->cull[1], (unsigned long long)deg);
-    if (back) atomicAdd(&B.ctr->cull[2], (unsigned long long)back);
-    if (fru) atomicAdd(&B.ctr->cull[3], (unsigned long long)fru);
-    if (bet) atomicAdd(&B.ctr->cull[4], (unsigned long long)bet);
-  }
-}
-
 // Exclusive scan of up to 1024*kPer values with one CTA.
 template <int kThreads>
 __device__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* total) {
@@ -357,27 +329,6 @@ __device__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* total) {
   return warp_prefix + x - v;
 }
 
-__global__ void __launch_bounds__(1024) k_scan_blocks(Buffers B, uint32_t nblocks) {
-  const FrameConst& fc = c_fc;
-  __shared__ uint32_t carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  for (uint32_t base = 0; base < nblocks; base += 1024) {
-    uint32_t i = base + threadIdx.x;
-    uint32_t v = i < nblocks ? B.block_cnt[i] : 0;
-    uint32_t total;
-    uint32_t ex = block_exclusive_scan<1024>(v, &total);
-    if (i < nblocks) B.block_off[i] = carry + ex;
-    __syncthreads();
-    if (threadIdx.x == 0) carry += total;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    B.ctr->nvis = carry;
-    // setup.cpp:298-299: 2 * visible > 2^24 is a capacity error
-    if ((unsigned long long)carry * 2ull > (unsigned long long)fc.tri_cap) atomicOr(&B.ctr->error, 1u);
-  }
-}
 
 // triangle setup, setup.cpp:209-239 (+ flat normal, setup.cpp:342-343)
 __device__ void triangle_setup(const FrameConst& fc, const double c0[4], const double c1[4],
@@ -446,10 +397,22 @@ __device__ __forceinline__ uint32_t flat_normal(const float4& a, const float4& b
   return encode_normal((float)n[0], (float)n[1], (float)n[2]);
 }
 
-__global__ void __launch_bounds__(kSetupBlock) k_setup_write(Buffers B) {
+// Phase 1 of setup in one pass (setup.cpp:252-302): cull every quad, then
+// compact the visible ones in ascending input order. Blocks take tickets in
+// launch order and chain their visible counts with a decoupled look-back
+// (status word per block: 1 = own count, 2 = inclusive prefix), so the
+// compaction needs no second cull pass and no separate scan kernel.
+__device__ __forceinline__ unsigned long long ld_state(const unsigned long long* p) {
+  return *reinterpret_cast<const volatile unsigned long long*>(p);
+}
+
+__global__ void __launch_bounds__(kSetupBlock) k_setup(Buffers B, uint32_t nblocks) {
   const FrameConst& fc = c_fc;
-  if (B.ctr->error & 1u) return;
-  uint32_t q = blockIdx.x * kSetupBlock + threadIdx.x;
+  __shared__ uint32_t s_bid, s_excl;
+  if (threadIdx.x == 0) s_bid = atomicAdd(&B.ctr->setup_ticket, 1u);
+  __syncthreads();
+  const uint32_t bid = s_bid;
+  const uint32_t q = bid * kSetupBlock + threadIdx.x;
   uint4 idx = make_uint4(0, 0, 0, 0);
   float4 p[4];
   double clip[4][4];
@@ -460,9 +423,54 @@ __global__ void __launch_bounds__(kSetupBlock) k_setup_write(Buffers B) {
     cull_quad(fc, idx, p, clip, &o);
   }
   uint32_t total;
-  uint32_t rank = block_exclusive_scan<kSetupBlock>(o.reason == 0 ? 1u : 0u, &total);
+  const uint32_t rank = block_exclusive_scan<kSetupBlock>(o.reason == 0 ? 1u : 0u, &total);
+  const int deg = __syncthreads_count(o.reason == 1);
+  const int back = __syncthreads_count(o.reason == 2);
+  const int fru = __syncthreads_count(o.reason == 3);
+  const int bet = __syncthreads_count(o.reason == 4);
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    unsigned long long* state = B.block_state;
+    if (lane == 0)
+      atomicExch(&state[bid], ((bid == 0 ? 2ull : 1ull) << 32) | (unsigned long long)total);
+    uint32_t excl = 0;
+    if (bid > 0) {
+      long long top = (long long)bid - 1;
+      for (;;) {
+        const long long j = top - lane;
+        unsigned long long w = j >= 0 ? ld_state(&state[j]) : (2ull << 32);
+        while (__any_sync(0xffffffffu, (w >> 32) == 0ull))
+          if ((w >> 32) == 0ull) w = ld_state(&state[j]);
+        const uint32_t v = (uint32_t)w;
+        const unsigned inc = __ballot_sync(0xffffffffu, (w >> 32) == 2ull);
+        if (inc) {  // nearest inclusive prefix: add it and the counts after it
+          const int k = __ffs(inc) - 1;
+          excl += __reduce_add_sync(0xffffffffu, lane <= k ? v : 0u);
+          break;
+        }
+        excl += __reduce_add_sync(0xffffffffu, v);
+        top -= 32;
+      }
+      if (lane == 0) atomicExch(&state[bid], (2ull << 32) | (unsigned long long)(excl + total));
+    }
+    if (lane == 0) {
+      s_excl = excl;
+      if (total) atomicAdd(&B.ctr->cull[0], (unsigned long long)total);
+      if (deg) atomicAdd(&B.ctr->cull[1], (unsigned long long)deg);
+      if (back) atomicAdd(&B.ctr->cull[2], (unsigned long long)back);
+      if (fru) atomicAdd(&B.ctr->cull[3], (unsigned long long)fru);
+      if (bet) atomicAdd(&B.ctr->cull[4], (unsigned long long)bet);
+      if (bid == nblocks - 1) {
+        const uint32_t nvis = excl + total;
+        B.ctr->nvis = nvis;
+        // setup.cpp:298-299: 2 * visible > 2^24 is a capacity error
+        if ((unsigned long long)nvis * 2ull > (unsigned long long)fc.tri_cap) atomicOr(&B.ctr->error, 1u);
+      }
+    }
+  }
+  __syncthreads();
   if (o.reason != 0) return;
-  uint32_t slot = B.block_off[blockIdx.x] + rank;
+  const uint32_t slot = s_excl + rank;
   uint32_t mat = B.qmat[q];
   MatDev md = B.mats[mat];
   bool has_c = md.flags & 1u, has_n = md.flags & 2u;
@@ -2403,7 +2411,7 @@ struct DeviceScene {
   uint64_t uploaded_version = 0;
   uint32_t nverts = 0, nquads = 0;
   DevBuf pos, vcol, vnrm, quads, qmat, mats;
-  DevBuf block_cnt, block_off, vq_src, vq_idx, vq_box, vq_flags, vq_mat, vq_col, vq_nrm, tri, tri_meta, shade,
+  DevBuf block_state, vq_src, vq_idx, vq_box, vq_flags, vq_mat, vq_col, vq_nrm, tri, tri_meta, shade,
       tri_y;
   DevBuf qcnt, tcnt, off, qcur, tcur, cat, prop, items, item_rows, slots, spill0, spill1, scratch, fb, mask,
       hash, emit, ctr, tile_ids, hbd, pool_tri, pool_mask, pool_pre, seg_queue, pool_slot, rowd,
@@ -2780,8 +2788,7 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   const uint32_t Q = d->nquads;
   const size_t nb = size_t(fc.nbins);
   P.nblocks = (Q + dev::kSetupBlock - 1) / dev::kSetupBlock;
-  d->block_cnt.ensure(std::max<size_t>(1, P.nblocks) * 4);
-  d->block_off.ensure(std::max<size_t>(1, P.nblocks) * 4);
+  d->block_state.ensure(std::max<size_t>(1, P.nblocks) * 8);
   d->vq_src.ensure(size_t(Q) * 4);
   d->vq_idx.ensure(size_t(Q) * 16);
   d->vq_box.ensure(size_t(Q) * 8);
@@ -2855,8 +2862,7 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   B.quads = d->quads.as<uint4>();
   B.qmat = d->qmat.as<uint32_t>();
   B.mats = d->mats.as<dev::MatDev>();
-  B.block_cnt = d->block_cnt.as<uint32_t>();
-  B.block_off = d->block_off.as<uint32_t>();
+  B.block_state = d->block_state.as<unsigned long long>();
   B.vq_src = d->vq_src.as<uint32_t>();
   B.vq_idx = d->vq_idx.as<uint4>();
   B.vq_box = d->vq_box.as<uint2>();
@@ -2927,13 +2933,12 @@ int enqueue_front(DeviceScene* d, Prepared& P) {
   ck(cudaMemsetAsync(B.tcnt, 0, size_t(fc.nbins) * 4, st), "memset");
   record_event(d->ev[0], st);
   if (P.nblocks) {
-    dev::k_setup_count<<<P.nblocks, dev::kSetupBlock, 0, st>>>(B);
-    dev::k_scan_blocks<<<1, 1024, 0, st>>>(B, P.nblocks);
-    dev::k_setup_write<<<P.nblocks, dev::kSetupBlock, 0, st>>>(B);
+    ck(cudaMemsetAsync(B.block_state, 0, size_t(P.nblocks) * 8, st), "memset");
+    dev::k_setup<<<P.nblocks, dev::kSetupBlock, 0, st>>>(B, P.nblocks);
     const int tgrid = int(std::min<long long>(((long long)fc.nquads * 2 + dev::kTriBlock - 1) / dev::kTriBlock,
                                               (long long)d->sm_count * 32));
     dev::k_setup_tris<<<std::max(1, tgrid), dev::kTriBlock, 0, st>>>(B);
-    launches += 4;
+    launches += 2;
   }
   record_event(d->ev[1], st);
   int grid = std::max(1, std::min<int>(d->sm_count * 8, int((fc.nquads + 255) / 256)));
