@@ -1804,6 +1804,8 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
   uint64_t* keys = V.keys + (size_t)warp * cap_tb;
   uint16_t* refs = V.refs + (size_t)warp * cap_tb;
   const bool packable = cap_tbr <= 16384u;  // TBR index fits the key's low 14 bits
+  // select the tri-block-rows touching this block's columns (selection
+  // order = TBR order; compacted first so the centroid pass runs dense)
   uint32_t n = 0;
   for (uint32_t base = 0; base < ntbr; base += 32) {
     const uint32_t i = base + lane;
@@ -1811,37 +1813,40 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
     const unsigned m = __ballot_sync(0xffffffffu, sel);
     if (sel) {
       const uint32_t pos = n + __popc(m & ((1u << lane) - 1u));
-      if (pos < cap_tb) {
-        const Tbr& rw = V.tbr[i];
-        uint32_t count = 0, sx = 0, sy = 0;
-#pragma unroll
-        for (int y = 0; y < 8; ++y) {
-          uint32_t b = byte_of(rw.b, y), l = byte_of(rw.l, y);
-          if (b > l) continue;
-          b = max(b, c0);
-          l = min(l, c1);
-          if (b > l) continue;
-          const uint32_t k = l - b + 1;
-          count += k;
-          sx += (b + l) * k / 2 - c0 * k;
-          sy += (uint32_t)y * k;
-        }
-        uint32_t qd = 0x3fffffu;
-        if (count) {
-          const double cx = __dadd_rn(__dadd_rn(bpx0, __ddiv_rn((double)sx, (double)count)), 0.5);
-          const double cy = __dadd_rn(__dadd_rn(bpy0, __ddiv_rn((double)sy, (double)count)), 0.5);
-          qd = quantize_depth(eval(B.tri[rw.tri].dz, cx, cy));
-        }
-        // (depth, is_large, triangle) orders exactly like the reference's
-        // (depth, selection index): selection order is bin-list order. The
-        // packed form carries the TBR reference in the low 14 bits.
-        const uint64_t large = (rw.meta >> 4) & 1u;
-        keys[pos] = packable ? (((uint64_t)qd << 42) | (large << 41) | ((uint64_t)rw.tri << 14) | i)
-                             : (((uint64_t)qd << 33) | (large << 32) | rw.tri);
-        refs[pos] = (uint16_t)i;
-      }
+      if (pos < cap_tb) refs[pos] = (uint16_t)i;
     }
     n += __popc(m);
+  }
+  __syncwarp();
+  const uint32_t nsel = min(n, cap_tb);
+  for (uint32_t pos = lane; pos < nsel; pos += 32) {
+    const uint32_t i = refs[pos];
+    const Tbr& rw = V.tbr[i];
+    uint32_t count = 0, sx = 0, sy = 0;
+#pragma unroll
+    for (int y = 0; y < 8; ++y) {
+      uint32_t b = byte_of(rw.b, y), l = byte_of(rw.l, y);
+      if (b > l) continue;
+      b = max(b, c0);
+      l = min(l, c1);
+      if (b > l) continue;
+      const uint32_t k = l - b + 1;
+      count += k;
+      sx += (b + l) * k / 2 - c0 * k;
+      sy += (uint32_t)y * k;
+    }
+    uint32_t qd = 0x3fffffu;
+    if (count) {
+      const double cx = __dadd_rn(__dadd_rn(bpx0, __ddiv_rn((double)sx, (double)count)), 0.5);
+      const double cy = __dadd_rn(__dadd_rn(bpy0, __ddiv_rn((double)sy, (double)count)), 0.5);
+      qd = quantize_depth(eval(B.tri[rw.tri].dz, cx, cy));
+    }
+    // (depth, is_large, triangle) orders exactly like the reference's
+    // (depth, selection index): selection order is bin-list order. The
+    // packed form carries the TBR reference in the low 14 bits.
+    const uint64_t large = (rw.meta >> 4) & 1u;
+    keys[pos] = packable ? (((uint64_t)qd << 42) | (large << 41) | ((uint64_t)rw.tri << 14) | i)
+                         : (((uint64_t)qd << 33) | (large << 32) | rw.tri);
   }
   if (n > lim.tb) {
     if (lane == 0) set_status(st, pass == kPassLow ? 1 : 3, 1 + 3 * block);
