@@ -1358,8 +1358,8 @@ __device__ __forceinline__ uint32_t find_thb(const uint32_t* pre_l, uint32_t lo,
   return lo;
 }
 
-template <int KM>
-__device__ __forceinline__ void blend_routed(const FrameConst& fc, RegFilter<KM, (KM <= 8)>& f, PixelOut& o,
+template <typename Filter>
+__device__ __forceinline__ void blend_routed(const FrameConst& fc, Filter& f, PixelOut& o,
                                              uint32_t mine, uint64_t key, float4 col) {
   while (__any_sync(0xffffffffu, mine != 0u)) {
     const int src = mine ? __ffs(mine) - 1 : (threadIdx.x & 31);
@@ -1391,15 +1391,13 @@ __device__ __forceinline__ uint32_t route_mask(uint32_t* route, uint32_t pix, bo
   return mine;
 }
 
-template <int KM>
+template <int KM, typename Filter>
 __device__ __forceinline__ void shade_segments(const FrameConst& fc, const Buffers& B, int px0,
                                                int py0, const uint32_t* tri_l,
                                                const uint32_t* mask_l, const uint32_t* pre_l,
                                                uint32_t n, uint32_t total, uint32_t* route,
-                                               PixelOut& o) {
+                                               PixelOut& o, Filter& f) {
   const int lane = threadIdx.x & 31;
-  RegFilter<KM, (KM <= 8)> f;
-  f.reset();
   uint32_t r_lo = 0;
   for (uint32_t base = 0; base < total; base += 32) {
     // THB r_lo holds a sample < base and every THB holds >= 1 sample, so
@@ -1422,7 +1420,7 @@ __device__ __forceinline__ void shade_segments(const FrameConst& fc, const Buffe
     const uint64_t key0 = sample_key(fc, q0, t0);
     r_lo = __shfl_sync(0xffffffffu, r0, 31);
     const uint32_t m0 = route_mask(route, v0 ? p0 : 32u + lane, v0);
-    blend_routed<KM>(fc, f, o, m0, key0, col0);
+    blend_routed(fc, f, o, m0, key0, col0);
   }
   while (f.n > 0) {
     uint64_t pk;
@@ -2221,8 +2219,17 @@ __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
                           d.cnt, po, f);
         }
       }
-      else if (d.frags)  // small THBs: dense segments + routing
-        shade_segments<KM>(fc, B, hpx0, hpy0, tri_l, mask_l, pre_l, d.cnt, d.frags, route_s[warp], po);
+      else if (d.frags) {  // small THBs: dense segments + routing
+        if constexpr (KM <= 8) {
+          SlotFilter<KM> f;
+          f.reset(reinterpret_cast<float4*>(shade_dyn) + (size_t)warp * KM * 32 + lane);
+          shade_segments<KM>(fc, B, hpx0, hpy0, tri_l, mask_l, pre_l, d.cnt, d.frags, route_s[warp], po, f);
+        } else {
+          RegFilter<KM> f;
+          f.reset();
+          shade_segments<KM>(fc, B, hpx0, hpy0, tri_l, mask_l, pre_l, d.cnt, d.frags, route_s[warp], po, f);
+        }
+      }
     }
     const int px = hpx0 + (lane & 7), py = hpy0 + (lane >> 3);
     unsigned invalid_px = 0;
@@ -2654,9 +2661,8 @@ void launch_extract(DeviceScene* d, const dev::FrameConst& fc, const dev::Buffer
 template <int KM, int kMode>
 void launch_shade_mode(DeviceScene* d, const dev::FrameConst& fc, const dev::Buffers& B,
                        int* launches) {
-  const size_t dyn = kMode == 0 ? size_t(dev::kStageTris) * sizeof(dev::StagedTri) +
-                                       (KM <= 8 ? size_t(8) * KM * 32 * sizeof(float4) : 0)
-                                 : 0;
+  const size_t dyn = (kMode == 0 ? size_t(dev::kStageTris) * sizeof(dev::StagedTri) : 0) +
+                     (kMode != 2 && KM <= 8 ? size_t(8) * KM * 32 * sizeof(float4) : 0);
   static bool configured = false;  // per instantiation
   if (!configured && dyn) {
     ck(cudaFuncSetAttribute(dev::k_shade<KM, kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize,
