@@ -83,7 +83,6 @@ struct FrameConst {
   int decoded;  // setup writes per-triangle decoded shading records
   uint32_t pool_cap;
   uint32_t lpairs_cap;
-  int debug;  // experiment switch (VEIL_DEBUG_SHADE), 0 in production
   int sort_bins;  // host-side: canonical bin-list order (k_bin_sort) this frame
   int walk_min;   // experiment override of kWalkMinSamplesPerThb (VEIL_WALK_MIN), 0 = default
   int walk_min_u; // the same for bins whose triangles are not staged (VEIL_WALK_MIN_U)
@@ -1324,7 +1323,7 @@ struct PixelOut {
 // raster.cpp:248-255).
 __device__ __forceinline__ void commit(PixelOut& o, uint64_t pk, float4 pc, bool ooo) {
   o.acc = blend(o.acc, pc);
-  o.hash = (o.hash ^ pk) * kHashPrime;
+  if (c_fc.dump) o.hash = (o.hash ^ pk) * kHashPrime;  // blend-order evidence (parity dumps)
   ++o.emitted;
   if (ooo) o.invalid = true;
 }
@@ -1455,10 +1454,7 @@ __device__ __forceinline__ void shade_walk(const FrameConst& fc, const Buffers& 
     const bool covered = (m >> lane) & 1u;
     float4 col = make_float4(0.f, 0.f, 0.f, 0.f);
     uint64_t key = 0;
-    if (covered && fc.debug == 1) {
-      col = make_float4(0.01f, 0.01f, 0.01f, 0.01f);
-      key = ((uint64_t)r << 24) | tri;
-    } else if (covered) {
+    if (covered) {
       uint32_t qd;
       if (fc.decoded) {
         col = shade_decoded_bf(fc, B, tri, px, py, &qd);
@@ -1483,9 +1479,7 @@ __device__ __forceinline__ void shade_walk(const FrameConst& fc, const Buffers& 
       }
       enumerated += __popc(m & (commit_until == 32 ? 0xffffffffu : ((1u << commit_until) - 1u)));
     }
-    if (covered && fc.debug == 2) {
-      commit(o, key, col, false);
-    } else if (covered && lane < commit_until) {
+    if (covered && lane < commit_until) {
       uint64_t pk;
       float4 pc;
       bool ooo;
@@ -1542,10 +1536,7 @@ __device__ __forceinline__ void shade_waves(const FrameConst& fc, const Buffers&
       const uint32_t tri = tri_l[my_r];
       uint32_t qd;
       float4 col;
-      if (fc.debug == 1) {
-        col = make_float4(0.01f, 0.01f, 0.01f, 0.01f);
-        qd = my_r;
-      } else if (staged) {
+      if (staged) {
         col = shade_staged(fc, staged[slot_l[my_r]], px, py, &qd);
       } else if (fc.decoded) {
         col = shade_decoded_bf(fc, B, tri, px, py, &qd);
@@ -1557,11 +1548,7 @@ __device__ __forceinline__ void shade_waves(const FrameConst& fc, const Buffers&
       uint64_t pk;
       float4 pc;
       bool ooo;
-      if (fc.debug == 2) {
-        commit(o, sample_key(fc, qd, tri), col, false);
-      } else if (f.push(fc.df, sample_key(fc, qd, tri), col, &pk, &pc, &ooo)) {
-        commit(o, pk, pc, ooo);
-      }
+      if (f.push(fc.df, sample_key(fc, qd, tri), col, &pk, &pc, &ooo)) commit(o, pk, pc, ooo);
     }
   }
   while (f.n > 0) {
@@ -2210,8 +2197,12 @@ __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
           SlotFilter<KM> f;
           f.reset(reinterpret_cast<float4*>(shade_dyn + (size_t)kStageTris * sizeof(StagedTri)) +
                   (size_t)warp * KM * 32 + lane);
-          shade_waves<KM>(fc, B, hpx0, hpy0, tri_l, mask_l, slot_l, staged_ok ? row_tris : nullptr,
-                          d.cnt, po, f);
+          if (staged_ok && d.cnt <= (uint32_t)kShadeStage)  // all operands in shared memory
+            shade_waves<KM>(fc, B, hpx0, hpy0, stage_tri[warp], stage_mask[warp], stage_slot[warp],
+                            row_tris, d.cnt, po, f);
+          else
+            shade_waves<KM>(fc, B, hpx0, hpy0, tri_l, mask_l, slot_l, staged_ok ? row_tris : nullptr,
+                            d.cnt, po, f);
         } else {
           RegFilter<KM> f;
           f.reset();
@@ -2786,7 +2777,6 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   fc.rank = opt.rank;
   fc.world = opt.world_size;
   fc.dump = opt.dump ? 1 : 0;
-  if (const char* dbg = std::getenv("VEIL_DEBUG_SHADE")) fc.debug = std::atoi(dbg);
   // Only the parity dumps need each bin's list in the reference's canonical
   // order: the rasterizer orders tri-blocks by (depth, large, triangle) keys
   // and counts limits, so it is independent of the order of a bin's items.
