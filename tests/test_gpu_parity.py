@@ -281,3 +281,39 @@ def test_rasterizer_independent_of_bin_item_order(kind, size, monkeypatch):
     for b in range(len(offs)):
         o, n = int(offs[b]), int(qc[b]) + int(tc[b])
         assert np.array_equal(np.sort(got["bin_items"][o:o + n]), np.sort(expect["bin_items"][o:o + n])), b
+
+
+@pytest.mark.parametrize("df", [2, 5, 16, 32])
+@pytest.mark.parametrize("flags", [0, RENDER_ALPHA_THRESHOLD])
+def test_depth_filter_capacities_vs_restatement(df, flags):
+    """Depth-filter sizes beyond the default: exact-capacity register/slot
+    filters (2, 5), the runtime-capacity ones (16, 32), with and without the
+    alpha threshold, on a high-disorder scene."""
+    arr = veil.Scene.synthetic("dense_bin", 4, 192, 160).arrays()
+    p = default_params(flags=flags, depth_filter_size=df)
+    bad = compare(gpu_dump(arr, p), bindings.oracle_render(arr, p), PARITY_ARRAYS)
+    assert not bad, bad
+
+
+def test_mixed_workload_window_vs_restatement():
+    """The C5 generator (jittered grid + stacked translucent quads, extended
+    limits) through a camera window of 512x480 grid cells at the original
+    pixel density (960x540): the segment-routing shade path runs next to the
+    wave walk in the same bins."""
+    arr = veil.Scene.workload("mixed16m", 5, 7680, 4320).arrays()
+    pos = arr.vertices["position"]
+    q = arr.quads["v"].astype(np.int64)
+    qx, qy = pos[q, 0], pos[q, 1]
+    lo, hi = -1.0, -1.0 + 2.0 * 512 / 4096  # x window; y uses 480 of 3840 rows (same 1/8)
+    keep = (qx.max(1) >= lo) & (qx.min(1) <= hi) & (qy.max(1) >= lo) & (qy.min(1) <= hi)
+    arr.quads = arr.quads[keep].copy()
+    assert 200_000 < len(arr.quads) < 400_000
+    m = np.array([8, 0, 0, 7, 0, 8, 0, 7, 0, 0, 1, 0, 0, 0, 0, 1], dtype=np.float64)
+    arr = arr.with_camera(m, None, 960, 540)
+    p = default_params()
+    exp = bindings.oracle_render(arr, p, extended=True)
+    sc = veil.Scene.from_arrays(arr)
+    sc.set_extended_limits(True)  # the C5 encodings (32-bit triangle keys, 16-bit bin boxes)
+    got = veil.render_dump(sc, p)
+    bad = compare(got, exp, PARITY_ARRAYS)
+    assert not bad, bad
