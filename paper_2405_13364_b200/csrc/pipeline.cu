@@ -105,7 +105,7 @@ struct Counters {
   unsigned int spill_count[2];
   unsigned long long samples, fragments, thb, segments, invalid;
   unsigned long long bins_empty, bins_low, bins_high, bins_propagated;
-  unsigned long long pool_pair;  // low 32: THB pool entries, high 32: row-list entries
+  unsigned long long pool_pair;  // THB pool entries allocated
   unsigned int shade_next[2];
   unsigned int seg_count;  // half-blocks queued for the segment-routing kernel
   unsigned int large_pairs;  // (large triangle, bin row) work pairs
@@ -172,10 +172,8 @@ struct Buffers {
   uint32_t* pool_tri;
   uint32_t* pool_mask;  // coverage, bit = ly * 8 + lx
   uint32_t* pool_pre;   // exclusive fragment prefix
-  uint32_t* seg_queue;  // (bin * 32 + hb) of half-blocks for k_shade<.., 1>
+  uint32_t* seg_queue;  // half-blocks for the segment kernel: bin * 32 + hb, bit 31 = high pass
   uint16_t* pool_slot;  // per THB: row-local triangle slot (index into the row list)
-  uint2* rowd;          // per (bin, block-row): row triangle list (offset, count)
-  uint32_t* rowtri;     // row triangle lists (visible triangle indices)
   uint2* lpairs;        // (large triangle, bin row) pairs for k_bin_large
   Counters* ctr;
 };
@@ -1189,6 +1187,12 @@ struct __align__(16) StagedTri {
 static_assert(sizeof(StagedTri) == 208, "StagedTri layout");
 constexpr int kStageTris = 320;
 
+// Wave walk (mode 0) vs dense segments (mode 1) crossover, in samples per
+// THB: lower when the bin's triangles are staged in shared memory (waves read
+// them there), higher when each lane gathers its triangle from global memory.
+constexpr uint32_t kWalkMinSamplesPerThbStaged = 6;
+constexpr uint32_t kWalkMinSamplesPerThb = 12;
+
 __device__ __forceinline__ void stage_triangle(const FrameConst& fc, const Buffers& B, uint32_t tri,
                                                StagedTri* dst) {
   const TriRec& t = B.tri[tri];
@@ -1298,7 +1302,7 @@ struct ItemState {
   int status;  // 0 ok, 1 overflow (soft), 2 spill, 3 hard error
   int err_code;
   uint32_t warp_n[4];
-  uint32_t pool_base, row_base;
+  uint32_t pool_base;
   int alloc_ok;
   uint32_t ncand;
   uint32_t hb_cnt[8];
@@ -1873,23 +1877,19 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
         __syncwarp();
       }
   }
-  // one pool allocation per item: the row's triangle list and 2n THB slots
-  // per warp (each tri-block yields <= 1 THB per half), a single 64-bit
-  // atomic for both regions
+  // one pool allocation per item: 2n THB slots per warp (each tri-block
+  // yields <= 1 THB per half)
   if (lane == 0) st->warp_n[warp] = ok ? n : 0u;
   __syncthreads();
   if (threadIdx.x == 0) {
     st->alloc_ok = 0;
     if (!st->status) {
       const uint32_t tot = 2u * (st->warp_n[0] + st->warp_n[1] + st->warp_n[2] + st->warp_n[3]);
-      const unsigned long long old =
-          atomicAdd(&B.ctr->pool_pair, ((unsigned long long)ntbr << 32) | tot);
-      const uint32_t pb = (uint32_t)old, rb = (uint32_t)(old >> 32);
-      if ((unsigned long long)pb + tot > fc.pool_cap || (unsigned long long)rb + ntbr > fc.pool_cap) {
+      const unsigned long long pb = atomicAdd(&B.ctr->pool_pair, (unsigned long long)tot);
+      if (pb + tot > fc.pool_cap) {
         atomicOr(&B.ctr->error, 8u);  // pool capacity: grow and re-run
       } else {
-        st->pool_base = pb;
-        st->row_base = rb;
+        st->pool_base = (uint32_t)pb;
         st->alloc_ok = 1;
       }
     }
@@ -1961,26 +1961,28 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
   __syncthreads();
   if (st->status || !st->alloc_ok) return;
   // the block-row's triangle list (TBR order): k_shade stages these records
-  if (threadIdx.x == 0) B.rowd[(size_t)bin * 4 + row] = make_uint2(st->row_base, ntbr);
-  for (uint32_t i = threadIdx.x; i < ntbr; i += blockDim.x) B.rowtri[st->row_base + i] = V.tbr[i].tri;
   if (lane < 2) {
+    // Small THBs (few samples each) are shaded by k_shade_seg's dense
+    // segments, the rest by k_shade's wave walk; the choice is made here so
+    // the segment queue is complete when shading starts. The crossover is
+    // lower when k_shade stages the bin's triangles in shared memory.
     HbDesc d;
     d.off = pbase + (uint32_t)lane * n;
     d.cnt = nthb[lane];
     d.frags = frags[lane];
-    d.pad = 0;
-    B.hbd[(size_t)bin * 32 + row * 8 + warp * 2 + lane] = d;
+    const bool staged = fc.decoded && T <= (uint32_t)kStageTris;
+    const uint32_t wmin = staged ? (fc.walk_min ? (uint32_t)fc.walk_min : kWalkMinSamplesPerThbStaged)
+                                 : (fc.walk_min_u ? (uint32_t)fc.walk_min_u : kWalkMinSamplesPerThb);
+    const bool seg = !fc.threshold && d.frags < wmin * d.cnt;
+    d.pad = seg ? 1u : 0u;
+    const uint32_t hbi = (uint32_t)bin * 32u + (uint32_t)(row * 8 + warp * 2 + lane);
+    B.hbd[hbi] = d;
+    // low-pass entries of a bin that later propagates are stale (k_shade_seg skips them)
+    if (seg) B.seg_queue[atomicAdd(&B.ctr->seg_count, 1u)] = hbi | (pass == kPassLow ? 0u : 0x80000000u);
   }
   if (threadIdx.x == 0) {
     unsigned long long* slot = B.slots + ((size_t)bin * 4 + row) * 5;
     slot[0] = slot[3] = slot[4] = 0;
-    uint64_t fr = 0, th = 0;
-    for (int h = 0; h < 8; ++h) {
-      fr += st->hb_frags[h];
-      th += st->hb_cnt[h];
-    }
-    (void)fr;
-    (void)th;
   }
   if (lane == 0) {
     st->hb_frags[warp * 2] = frags[0];
@@ -2069,11 +2071,6 @@ __global__ void __launch_bounds__(128) k_extract(Buffers B, int pass,
 // mapping's dependent lookups on-chip. Empty bins and half-blocks without
 // samples composite the background.
 constexpr int kShadeStage = 256;  // THB entries staged per warp; longer lists stream
-// Wave walk (mode 0) vs dense segments (mode 1) crossover, in samples per
-// THB: lower when the bin's triangles are staged in shared memory (waves read
-// them there), higher when each lane gathers its triangle from global memory.
-constexpr uint32_t kWalkMinSamplesPerThbStaged = 6;
-constexpr uint32_t kWalkMinSamplesPerThb = 12;
 
 // kMode: 0 = broadcast walk for half-blocks with big THBs (also writes every
 // half-block without samples), 1 = segment routing for the rest, 2 = alpha
@@ -2106,6 +2103,8 @@ __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
       item = __shfl_sync(0xffffffffu, item, 0);
       if (item >= nitems) break;
       item = B.seg_queue[item];
+      if (!(item & 0x80000000u) && B.prop[item >> 5]) continue;  // stale low-pass entry
+      item &= 0x7fffffffu;
     } else {
       // next half-block of the CTA's bin, or the next bin
       int hbi = 32;
@@ -2163,13 +2162,7 @@ __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
     bool live = B.cat[bin] != 0;
     HbDesc d = {0, 0, 0, 0};
     if (live) d = B.hbd[(size_t)bin * 32 + hb];
-    const uint32_t wmin = staged_ok ? (fc.walk_min ? (uint32_t)fc.walk_min : kWalkMinSamplesPerThbStaged)
-                                    : (fc.walk_min_u ? (uint32_t)fc.walk_min_u : kWalkMinSamplesPerThb);
-    const bool walk = !live || d.frags >= wmin * d.cnt;
-    if (kMode == 0 && !walk) {  // small THBs: hand over to the routing kernel
-      if (lane == 0) B.seg_queue[atomicAdd(&B.ctr->seg_count, 1u)] = item;
-      continue;
-    }
+    if (kMode == 0 && live && d.pad) continue;  // queued for the segment kernel by k_extract
     if (live) {
       enumerated = d.frags;
       const uint32_t* tri_l = B.pool_tri + d.off;
@@ -2417,8 +2410,7 @@ struct DeviceScene {
   DevBuf block_state, vq_src, vq_idx, vq_box, vq_flags, vq_mat, vq_col, vq_nrm, tri, tri_meta, shade,
       tri_y;
   DevBuf qcnt, tcnt, off, qcur, tcur, cat, prop, items, item_rows, slots, spill0, spill1, scratch, fb, mask,
-      hash, emit, ctr, tile_ids, hbd, pool_tri, pool_mask, pool_pre, seg_queue, pool_slot, rowd,
-      rowtri, lpairs;
+      hash, emit, ctr, tile_ids, hbd, pool_tri, pool_mask, pool_pre, seg_queue, pool_slot, lpairs;
   uint32_t items_cap = 0;
   uint32_t pool_cap = 0;
   uint32_t lpairs_cap = 0;
@@ -2829,7 +2821,6 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   d->ctr.ensure(sizeof(dev::Counters));
   d->hbd.ensure(nb * 32 * sizeof(dev::HbDesc));
   d->seg_queue.ensure(nb * 32 * 4);
-  d->rowd.ensure(nb * 4 * sizeof(uint2));
   if (d->lpairs_cap == 0) d->lpairs_cap = std::max<uint32_t>(1u << 16, std::min<uint32_t>(Q * 2u, 1u << 26));
   d->lpairs.ensure(size_t(d->lpairs_cap) * sizeof(uint2));
   fc.lpairs_cap = d->lpairs_cap;
@@ -2838,7 +2829,6 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   d->pool_mask.ensure(size_t(d->pool_cap) * 4);
   d->pool_pre.ensure(size_t(d->pool_cap) * 4);
   d->pool_slot.ensure(size_t(d->pool_cap) * 2);
-  d->rowtri.ensure(size_t(d->pool_cap) * 4);
   fc.pool_cap = d->pool_cap;
   // global scratch for spilled items: capacities follow the active limits
   P.gcap_tbr = std::min<uint32_t>(std::max(fc.low.tbr, fc.high.tbr), 1u << 16);
@@ -2899,8 +2889,6 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   B.pool_pre = d->pool_pre.as<uint32_t>();
   B.seg_queue = d->seg_queue.as<uint32_t>();
   B.pool_slot = d->pool_slot.as<uint16_t>();
-  B.rowd = d->rowd.as<uint2>();
-  B.rowtri = d->rowtri.as<uint32_t>();
   B.lpairs = d->lpairs.as<uint2>();
   B.ctr = d->ctr.as<dev::Counters>();
   return P;
