@@ -1641,30 +1641,37 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
   const uint32_t T = 2 * nq + nt;
   uint64_t* cand = V.keys;  // keys are free until phase B
   const uint32_t cand_cap = 4u * cap_tb;
-  for (uint32_t round = 0; round < T; round += cand_cap) {
-    const uint32_t end = min(T, round + cand_cap);
+  // rounds over bin items (a small quad's item holds its 2 triangles), sized
+  // so that a round's candidates fit the candidate buffer
+  const uint32_t nitem = nq + nt, round_items = cand_cap / 2u;
+  for (uint32_t round = 0; round < nitem; round += round_items) {
+    const uint32_t end = min(nitem, round + round_items);
     if (threadIdx.x == 0) st->ncand = 0;
     __syncthreads();
-    for (uint32_t i0 = round; i0 < end; i0 += blockDim.x) {
-      const uint32_t i = i0 + threadIdx.x;
-      bool keep = false;
-      uint64_t code = 0;
-      if (i < end) {
-        const uint32_t large = i < 2 * nq ? 0u : 1u;
-        const uint32_t at = large ? o + nq + (i - 2 * nq) : o + (i >> 1);
-        const uint32_t rows = (uint32_t)B.item_rows[at] >> (large ? 0 : 4 * (i & 1));
-        keep = (rows >> row) & 1u;
-        if (keep) {
-          const uint32_t it = B.items[at];
-          const uint32_t ti = large ? it : it * 2 + (i & 1);
-          code = ((uint64_t)i << 32) | ti | (large << 31);
-        }
+    for (uint32_t j0 = round; j0 < end; j0 += blockDim.x) {
+      const uint32_t j = j0 + threadIdx.x;
+      uint32_t rows = 0, it = 0;
+      if (j < end) {
+        rows = (uint32_t)B.item_rows[o + j];
+        rows = j < nq ? ((rows >> row) & 1u) | (((rows >> (4 + row)) & 1u) << 1) : ((rows >> row) & 1u);
+        if (rows) it = B.items[o + j];
       }
-      const unsigned m = __ballot_sync(0xffffffffu, keep);
+      // candidate triangles in bin-list expansion order: 2j, 2j+1 (small
+      // quads) or 2nq + (j - nq) (large triangles)
+      const unsigned m0 = __ballot_sync(0xffffffffu, rows & 1u);
+      const unsigned m1 = __ballot_sync(0xffffffffu, (rows >> 1) & 1u);
       uint32_t wbase = 0;
-      if (lane == 0 && m) wbase = atomicAdd(&st->ncand, (uint32_t)__popc(m));
+      if (lane == 0 && (m0 | m1)) wbase = atomicAdd(&st->ncand, (uint32_t)(__popc(m0) + __popc(m1)));
       wbase = __shfl_sync(0xffffffffu, wbase, 0);
-      if (keep) cand[wbase + __popc(m & ((1u << lane) - 1u))] = code;
+      const unsigned below = (1u << lane) - 1u;
+      if (rows & 1u) {
+        const bool large = j >= nq;
+        const uint32_t i = large ? 2 * nq + (j - nq) : 2 * j;
+        const uint32_t ti = large ? it : it * 2;
+        cand[wbase + __popc(m0 & below)] = ((uint64_t)i << 32) | ti | ((large ? 1u : 0u) << 31);
+      }
+      if (rows & 2u)
+        cand[wbase + __popc(m0) + __popc(m1 & below)] = ((uint64_t)(2 * j + 1) << 32) | (it * 2 + 1);
     }
     __syncthreads();
     const uint32_t nc = st->ncand;
