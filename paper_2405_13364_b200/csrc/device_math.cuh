@@ -177,23 +177,33 @@ __device__ __forceinline__ bool covers(const TriRec& t, int px, int py) {
 }
 
 // scanline_row_interval, scanline.hpp:47-86 (caller checks valid / y range).
-// Returns false when the row is empty within [x_first, x_last].
+// Returns false when the row is empty within [x_first, x_last]. The four
+// functions' b*y products are formed once per row and reused by every
+// covers_pixel test of the refinement, which evaluates ((a*x + b*y) + c) with
+// the same roundings as eval().
 __device__ __forceinline__ bool row_span(const TriRec& t, int py, int x_first, int x_last,
                                          int* b_out, int* l_out) {
-  double y = (double)py + 0.5;
+  const double y = (double)py + 0.5;
   double lo = (double)x_first + 0.5;
   double hi = (double)x_last + 0.5;
+  double fa[4], fby[4], fc[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const Fn3& f = i < 3 ? t.e[i] : t.iw;
-    double k = __dadd_rn(__dmul_rn(f.b, y), f.c);
-    if (f.a == 0.0) {
-      bool ok = i == 3 ? k > 0.0 : k >= 0.0;
+    fa[i] = f.a;
+    fby[i] = __dmul_rn(f.b, y);
+    fc[i] = f.c;
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const double k = __dadd_rn(fby[i], fc[i]);
+    if (fa[i] == 0.0) {
+      const bool ok = i == 3 ? k > 0.0 : k >= 0.0;
       if (!ok) return false;
       continue;
     }
-    double root = __ddiv_rn(-k, f.a);
-    if (f.a > 0.0)
+    const double root = __ddiv_rn(-k, fa[i]);
+    if (fa[i] > 0.0)
       lo = smax(lo, root);
     else
       hi = smin(hi, root);
@@ -203,10 +213,21 @@ __device__ __forceinline__ bool row_span(const TriRec& t, int py, int x_first, i
   int last = (int)floor(__dsub_rn(hi, 0.5));
   if (begin < x_first) begin = x_first;
   if (last > x_last) last = x_last;
-  while (begin <= last && !covers(t, begin, py)) ++begin;
-  while (begin > x_first && covers(t, begin - 1, py)) --begin;
-  while (last >= begin && !covers(t, last, py)) --last;
-  while (last < x_last && last >= begin && covers(t, last + 1, py)) ++last;
+  // covers_pixel (scanline.hpp:38-42) at (px + 0.5, y)
+  auto cov = [&](int px) {
+    const double x = (double)px + 0.5;
+    bool in = true;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const double v = __dadd_rn(__dadd_rn(__dmul_rn(fa[i], x), fby[i]), fc[i]);
+      in = in && (i == 3 ? v > 0.0 : v >= 0.0);
+    }
+    return in;
+  };
+  while (begin <= last && !cov(begin)) ++begin;
+  while (begin > x_first && cov(begin - 1)) --begin;
+  while (last >= begin && !cov(last)) --last;
+  while (last < x_last && last >= begin && cov(last + 1)) ++last;
   if (begin > last) return false;
   *b_out = begin;
   *l_out = last;
