@@ -1286,7 +1286,7 @@ struct RasterView {
 struct RasterShared {
   // Shared-memory capacities; larger items (within the active limits) run
   // again with global scratch.
-  static constexpr int kTbr = 1024, kTb = 256;
+  static constexpr int kTbr = 512, kTb = 256;
   Tbr tbr[kTbr];
   uint64_t keys[4 * kTb];
   __align__(16) uint16_t refs[4 * kTb];
