@@ -2008,7 +2008,7 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
 }
 
 template <bool kGlobal>
-__global__ void __launch_bounds__(128) k_extract(Buffers B, int pass,
+__global__ void __launch_bounds__(128, 7) k_extract(Buffers B, int pass,
                                                  uint32_t cap_tbr, uint32_t cap_tb) {
   const FrameConst& fc = c_fc;
   extern __shared__ __align__(16) uint8_t smem_raw[];
