@@ -120,16 +120,17 @@ def bytes_model(stats, width, height, a_q=32, a_v=8):
     return frame, raster, b_min
 
 
-def traffic_per_frame(workload):
-    """DRAM bytes (read + write) of the bin-rasterizer kernels for one frame,
-    from the committed ncu --set full capture (profiles/*_traffic.json,
-    written by tools/ncu_traffic.py); None when no capture exists."""
+def ncu_summary(workload):
+    """The committed ncu --set full capture of one frame's bin-rasterizer
+    kernels (profiles/traffic.json, written by tools/ncu_traffic.py): DRAM
+    bytes (read + write) per frame and the dominant kernel's issue-slot
+    utilisation; empty when no capture exists."""
     path = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(path) as f:
-            return json.load(f).get(workload, {}).get("raster_dram_bytes")
+            return json.load(f).get(workload, {})
     except (OSError, ValueError):
-        return None
+        return {}
 
 
 # ------------------------------------------------------------------- clocks
@@ -407,6 +408,7 @@ def run_ours(args):
             pass
         b_frame, b_raster, b_min = bytes_model(info, W, H)
         peak, peak_kind = peaks()
+        ncu = ncu_summary(cfg["workload"])
         raster_ms = statistics.median([float(s.low_raster_ms + s.hi_raster_ms + s.shade_ms)
                                        for s in stats])
         achieved = b_raster / (raster_ms * 1e-3) / 1e9
@@ -442,13 +444,16 @@ def run_ours(args):
                            l2="flushed between timed frames (256 MiB write, outside the events)"),
             "e2e": e2e,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic_per_frame(cfg["workload"]),
+                         "frac": achieved / peak, "traffic": ncu.get("raster_dram_bytes"),
                          "kernel": "bin rasterizer: k_extract (low+high) + k_shade + k_finalize",
                          "kernel_ms": raster_ms,
                          "algorithmic_bytes_per_launch": b_raster,
                          "peak_source": peak_kind,
                          "frame_bytes": b_frame, "frame_bytes_min": b_min,
-                         "frame_frac": b_frame / (ms_per_frame * 1e-3) / 1e9 / peak},
+                         "frame_frac": b_frame / (ms_per_frame * 1e-3) / 1e9 / peak,
+                         # the dominant kernel is issue-bound, not HBM-bound (ncu capture)
+                         "issue_slots_busy": (ncu.get("top_issue_active_pct", 0) / 100.0) or None,
+                         "issue_source": ncu.get("source")},
             "cpu_baseline": cpu,
             "clocks": clk,
             **({"frame_check": frame_check} if frame_check else {}),

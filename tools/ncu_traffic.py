@@ -15,7 +15,8 @@ import sys
 
 rep, workload = sys.argv[1], sys.argv[2]
 out_path = sys.argv[3] if len(sys.argv) > 3 else "profiles/traffic.json"
-metrics = "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum"
+metrics = ("dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,"
+           "smsp__issue_active.avg.pct_of_peak_sustained_active,smsp__inst_executed.sum")
 txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics", metrics],
                      capture_output=True, text=True, check=True).stdout
 rows = list(csv.reader(io.StringIO(txt)))
@@ -37,14 +38,18 @@ for r in data:
     kernels.append({"kernel": name.split("(")[0],
                     "dram_read_bytes": val(r, "dram__bytes_read.sum"),
                     "dram_write_bytes": val(r, "dram__bytes_write.sum"),
-                    "ncu_ms": val(r, "gpu__time_duration.sum")})
+                    "ncu_ms": val(r, "gpu__time_duration.sum"),
+                    "issue_active_pct": val(r, "smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                    "warp_instructions": val(r, "smsp__inst_executed.sum")})
 total = sum(k["dram_read_bytes"] + k["dram_write_bytes"] for k in kernels)
 try:
     with open(out_path) as f:
         doc = json.load(f)
 except (OSError, ValueError):
     doc = {}
-doc[workload] = {"raster_dram_bytes": total, "kernels": kernels, "source": rep.split("/")[-1]}
+top = max(kernels, key=lambda k: k["ncu_ms"])
+doc[workload] = {"raster_dram_bytes": total, "kernels": kernels, "source": rep.split("/")[-1],
+                 "top_kernel": top["kernel"], "top_issue_active_pct": top["issue_active_pct"]}
 with open(out_path, "w") as f:
     json.dump(doc, f, indent=1)
 print(json.dumps(doc[workload], indent=1))
