@@ -110,6 +110,7 @@ struct Counters {
   unsigned int seg_count;  // half-blocks queued for the segment-routing kernel
   unsigned int large_pairs;  // (large triangle, bin row) work pairs
   unsigned int setup_ticket;  // k_setup: block order for the decoupled look-back
+  unsigned int list_count[2];  // owned bins to extract in the low / high pass
 };
 
 // Decoded per-triangle shading inputs (unpack_color / decode_normal of the
@@ -158,7 +159,9 @@ struct Buffers {
   uint8_t* cat;
   uint8_t* prop;
   uint32_t* items;
-  uint8_t* item_rows;  // per item: block-rows (of its bin) each triangle's y range meets
+  uint8_t* item_rows;
+  uint32_t* bin_list[2];  // owned bins per extraction pass (high: + propagated ones)
+  uint32_t* prop_q;       // per bin: already appended to the high-pass list  // per item: block-rows (of its bin) each triangle's y range meets
   // raster
   unsigned long long* slots;  // per (bin, row): samples, frags, thb, segments, invalid
   uint32_t* spill[2];
@@ -757,7 +760,24 @@ __global__ void __launch_bounds__(1024) k_bin_scan(Buffers B) {
       uint8_t c = eq == 0 ? 0 : (eq < 1024u ? 1 : 2);
       B.cat[b] = c;
       B.prop[b] = 0;
+      B.prop_q[b] = 0;
       atomicAdd(&cnt[c], 1u);
+    }
+    {  // extraction work lists (renderer.cpp:150-190: low bins, then high bins)
+      const int bxi = b % fc.bins_x, byi = b / fc.bins_x;
+      const bool owned = b < fc.nbins && (fc.world <= 1 || ((bxi + 3 * byi) % fc.world) == fc.rank);
+      const uint8_t c = owned ? B.cat[b] : 0;
+      const bool lo = c == 1 && !fc.force_high, hi = c == 2 || (c == 1 && fc.force_high);
+      const int lane = threadIdx.x & 31;
+#pragma unroll
+      for (int ps = 0; ps < 2; ++ps) {
+        const bool in = ps == 0 ? lo : hi;
+        const unsigned m = __ballot_sync(0xffffffffu, in);
+        uint32_t at = 0;
+        if (lane == 0 && m) at = atomicAdd(&B.ctr->list_count[ps], (unsigned)__popc(m));
+        at = __shfl_sync(0xffffffffu, at, 0);
+        if (in) B.bin_list[ps][at + __popc(m & ((1u << lane) - 1u))] = (uint32_t)b;
+      }
     }
     __syncthreads();
     if (threadIdx.x == 0) carry += total;
@@ -2033,7 +2053,7 @@ __global__ void __launch_bounds__(128, 7) k_extract(Buffers B, int pass,
     V.refs = sh->refs;
     V.rows = reinterpret_cast<uint32_t*>(sh->refs);  // refs are unused until phase B
   }
-  const uint32_t nitems = kGlobal ? B.ctr->spill_count[pass] : (uint32_t)fc.nbins * 4u;
+  const uint32_t nitems = kGlobal ? B.ctr->spill_count[pass] : B.ctr->list_count[pass] * 4u;
   unsigned int* counter = &B.ctr->work_next[pass * 2 + (kGlobal ? 1 : 0)];
   for (;;) {
     if (threadIdx.x == 0) item_s = atomicAdd(counter, 1u);
@@ -2041,7 +2061,7 @@ __global__ void __launch_bounds__(128, 7) k_extract(Buffers B, int pass,
     const uint32_t item = item_s;
     __syncthreads();
     if (item >= nitems) break;
-    const uint32_t code = kGlobal ? B.spill[pass][item] : item;
+    const uint32_t code = kGlobal ? B.spill[pass][item] : (B.bin_list[pass][item >> 2] << 2) | (item & 3u);
     const int bin = (int)(code >> 2), row = (int)(code & 3u);
     const int bxi = bin % fc.bins_x, byi = bin / fc.bins_x;
     const uint8_t cat = B.cat[bin];
@@ -2057,8 +2077,10 @@ __global__ void __launch_bounds__(128, 7) k_extract(Buffers B, int pass,
     extract_item<kGlobal>(fc, B, pass, bin, row, V, &st, cap_tbr, cap_tb);
     __syncthreads();
     if (threadIdx.x == 0 && st.status) {
-      if (st.status == 1) {
+      if (st.status == 1) {  // soft overflow: the whole bin goes to the high pass
         B.prop[bin] = 1;
+        if (atomicAdd(&B.prop_q[bin], 1u) == 0u)
+          B.bin_list[1][atomicAdd(&B.ctr->list_count[1], 1u)] = (uint32_t)bin;
       } else if (st.status == 2) {
         const uint32_t s = atomicAdd(&B.ctr->spill_count[pass], 1u);
         B.spill[pass][s] = code;
@@ -2416,7 +2438,7 @@ struct DeviceScene {
   DevBuf pos, vcol, vnrm, quads, qmat, mats;
   DevBuf block_state, vq_src, vq_idx, vq_box, vq_flags, vq_mat, vq_col, vq_nrm, tri, tri_meta, shade,
       tri_y;
-  DevBuf qcnt, tcnt, off, qcur, tcur, cat, prop, items, item_rows, slots, spill0, spill1, scratch, fb, mask,
+  DevBuf qcnt, tcnt, off, qcur, tcur, cat, bin_list0, bin_list1, prop_q, prop, items, item_rows, slots, spill0, spill1, scratch, fb, mask,
       hash, emit, ctr, tile_ids, hbd, pool_tri, pool_mask, pool_pre, seg_queue, pool_slot, lpairs;
   uint32_t items_cap = 0;
   uint32_t pool_cap = 0;
@@ -2810,6 +2832,9 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   d->qcur.ensure(nb * 4);
   d->tcur.ensure(nb * 4);
   d->cat.ensure(nb);
+  d->bin_list0.ensure(nb * 4);
+  d->bin_list1.ensure(nb * 4);
+  d->prop_q.ensure(nb * 4);
   d->prop.ensure(nb);
   d->slots.ensure(nb * 4 * 5 * 8);
   d->spill0.ensure(nb * 4 * 4);
@@ -2878,6 +2903,9 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   B.qcur = d->qcur.as<uint32_t>();
   B.tcur = d->tcur.as<uint32_t>();
   B.cat = d->cat.as<uint8_t>();
+  B.bin_list[0] = d->bin_list0.as<uint32_t>();
+  B.bin_list[1] = d->bin_list1.as<uint32_t>();
+  B.prop_q = d->prop_q.as<uint32_t>();
   B.prop = d->prop.as<uint8_t>();
   B.items = d->items.as<uint32_t>();
   B.item_rows = d->item_rows.as<uint8_t>();
