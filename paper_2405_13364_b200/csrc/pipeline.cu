@@ -2839,7 +2839,11 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   d->slots.ensure(nb * 4 * 5 * 8);
   d->spill0.ensure(nb * 4 * 4);
   d->spill1.ensure(nb * 4 * 4);
-  if (d->items_cap == 0) d->items_cap = std::max<uint32_t>(1u << 20, Q * 6u);
+  // VEIL_INITIAL_CAPACITY (tests): start every grow-on-demand buffer at this
+  // many entries so the capacity-retry paths run on small scenes
+  uint32_t init_cap = 0;
+  if (const char* ic = std::getenv("VEIL_INITIAL_CAPACITY")) init_cap = uint32_t(std::strtoul(ic, nullptr, 10));
+  if (d->items_cap == 0) d->items_cap = init_cap ? init_cap : std::max<uint32_t>(1u << 20, Q * 6u);
   d->items.ensure(size_t(d->items_cap) * 4);
   d->item_rows.ensure(size_t(d->items_cap));
   fc.items_cap = d->items_cap;
@@ -2853,10 +2857,12 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   d->ctr.ensure(sizeof(dev::Counters));
   d->hbd.ensure(nb * 32 * sizeof(dev::HbDesc));
   d->seg_queue.ensure(nb * 32 * 4);
-  if (d->lpairs_cap == 0) d->lpairs_cap = std::max<uint32_t>(1u << 16, std::min<uint32_t>(Q * 2u, 1u << 26));
+  if (d->lpairs_cap == 0)
+    d->lpairs_cap = init_cap ? init_cap : std::max<uint32_t>(1u << 16, std::min<uint32_t>(Q * 2u, 1u << 26));
   d->lpairs.ensure(size_t(d->lpairs_cap) * sizeof(uint2));
   fc.lpairs_cap = d->lpairs_cap;
-  if (d->pool_cap == 0) d->pool_cap = std::max<uint32_t>(1u << 22, uint32_t(std::min<size_t>(nb * 2048, 1u << 26)));
+  if (d->pool_cap == 0)
+    d->pool_cap = init_cap ? init_cap : std::max<uint32_t>(1u << 22, uint32_t(std::min<size_t>(nb * 2048, 1u << 26)));
   d->pool_tri.ensure(size_t(d->pool_cap) * 4);
   d->pool_mask.ensure(size_t(d->pool_cap) * 4);
   d->pool_pre.ensure(size_t(d->pool_cap) * 4);
@@ -3236,18 +3242,28 @@ void render_frame(const Scene& s, const RenderOptions& opt, RenderOutput* out) {
     }
     ck(cudaStreamSynchronize(d->stream), "frame");
     const dev::Counters c = *d->ctr_host;
-    if (c.error & 2u) {  // bin item capacity: grow and re-run (first frames only)
-      d->items_cap = uint32_t(std::min<unsigned long long>(c.pairs + c.pairs / 4 + 1024, 0xffffffffull));
-      continue;
+    // Grow-on-demand buffers (first frames of a scene only): the device
+    // counters keep counting past a capacity, so each overflowed buffer is
+    // grown to the demand seen (+25%) and the frame re-runs. A stage that
+    // could not run because an earlier one overflowed shows its demand on
+    // the next attempt.
+    bool grow = false;
+    auto grown = [](unsigned long long need) {
+      return uint32_t(std::min<unsigned long long>(need + need / 4 + 1024, 0xffffffffull));
+    };
+    if (c.error & 2u) {  // bin items
+      d->items_cap = std::max(d->items_cap, grown(c.pairs));
+      grow = true;
     }
-    if (c.error & 8u) {  // THB pool capacity: grow and re-run
-      d->pool_cap = uint32_t(std::min<unsigned long long>(2ull * d->pool_cap, 0xffffffffull));
-      continue;
+    if (c.error & 8u) {  // THB pool
+      d->pool_cap = std::max(grown(c.pool_pair), uint32_t(std::min<unsigned long long>(2ull * d->pool_cap, 0xffffffffull)));
+      grow = true;
     }
-    if (c.error & 16u) {  // large-triangle pair list: grow and re-run
-      d->lpairs_cap = uint32_t(std::min<unsigned long long>(c.large_pairs + c.large_pairs / 4 + 1024, 0xffffffffull));
-      continue;
+    if (c.error & 16u) {  // large-triangle (triangle, bin row) pairs
+      d->lpairs_cap = std::max(d->lpairs_cap, grown(c.large_pairs));
+      grow = true;
     }
+    if (grow) continue;
     check_frame_errors(c, P.fc);
     out->width = s.camera.width;
     out->height = s.camera.height;
@@ -3329,7 +3345,7 @@ void render_frame(const Scene& s, const RenderOptions& opt, RenderOutput* out) {
     }
     return;
   }
-  throw Error(VEIL_ERR_INTERNAL, "bin item buffer could not be sized");
+  throw Error(VEIL_ERR_INTERNAL, "frame buffers could not be sized after 8 attempts");
 }
 
 void render_reference_frame(const Scene& s, const RenderOptions& opt, RenderOutput* out) {
@@ -3380,7 +3396,7 @@ void render_reference_frame(const Scene& s, const RenderOptions& opt, RenderOutp
     }
     return;
   }
-  throw Error(VEIL_ERR_INTERNAL, "bin item buffer could not be sized");
+  throw Error(VEIL_ERR_INTERNAL, "frame buffers could not be sized after 8 attempts");
 }
 
 void shard_tiles_device(const Scene& s, int rank, int world, void* tiles, uint64_t bytes,

@@ -317,3 +317,20 @@ def test_mixed_workload_window_vs_restatement():
     got = veil.render_dump(sc, p)
     bad = compare(got, exp, PARITY_ARRAYS)
     assert not bad, bad
+
+
+@pytest.mark.parametrize("kind,size", [("dense_bin", (256, 256)), ("intersecting_shells", (200, 150))])
+def test_capacity_growth_retry(kind, size, monkeypatch):
+    """Every grow-on-demand buffer (bin items, large-triangle pairs, THB pool)
+    starts tiny, so the first frames overflow and re-run with grown
+    capacities (also through the cached frame graph); dumps and plain frames
+    must still equal the restatement."""
+    monkeypatch.setenv("VEIL_INITIAL_CAPACITY", "64")
+    arr = veil.Scene.synthetic(kind, 9, *size).arrays()
+    p = default_params()
+    exp = bindings.oracle_render(arr, p)
+    sc = veil.Scene.from_arrays(arr)
+    r = veil.render(sc, p)  # graph path first: grows inside render_frame's retry loop
+    assert np.array_equal(r.pixels().reshape(-1), exp["image"].reshape(-1))
+    bad = compare(veil.render_dump(veil.Scene.from_arrays(arr), p), exp, PARITY_ARRAYS)
+    assert not bad, bad
