@@ -161,6 +161,8 @@ struct Buffers {
   uint32_t* items;
   uint8_t* item_rows;
   uint32_t* bin_list[2];  // owned bins per extraction pass (high: + propagated ones)
+  uint32_t* lpair_cols;   // per large pair: covered bin-column words from the count pass
+  uint32_t lpair_cols_cap;  // words
   uint32_t* prop_q;       // per bin: already appended to the high-pass list  // per item: block-rows (of its bin) each triangle's y range meets
   // raster
   unsigned long long* slots;  // per (bin, row): samples, frags, thb, segments, invalid
@@ -710,18 +712,28 @@ __global__ void __launch_bounds__(256) k_bin_large(Buffers B) {
     const uint2 pr = B.lpairs[w];
     const uint32_t ti = pr.x;
     const int R = (int)pr.y;
-    const TriRec& tr = B.tri[ti];
-    const int y = R * kBin + lane;
+    // the count pass stores the pair's column words; the write pass reuses
+    // them instead of repeating the row spans (when they fit the cache)
+    const bool cached = (unsigned long long)(w + 1) * (unsigned long long)nwords <= B.lpair_cols_cap;
     int b0 = 1, b1 = 0;
-    if (y >= tr.y_min && y <= tr.y_max) {
-      int b, l;
-      if (row_span(tr, y, 0, fc.width - 1, &b, &l)) b0 = b / kBin, b1 = l / kBin;
+    if (!(kWrite && cached)) {
+      const TriRec& tr = B.tri[ti];
+      const int y = R * kBin + lane;
+      if (y >= tr.y_min && y <= tr.y_max) {
+        int b, l;
+        if (row_span(tr, y, 0, fc.width - 1, &b, &l)) b0 = b / kBin, b1 = l / kBin;
+      }
     }
     for (int wd = 0; wd < nwords; ++wd) {
-      const int lo = max(b0, wd * 32), hi = min(b1, wd * 32 + 31);
       uint32_t word = 0;
-      if (lo <= hi) word = (hi - lo == 31 ? 0xffffffffu : ((2u << (hi - lo)) - 1u)) << (lo - wd * 32);
-      word = __reduce_or_sync(0xffffffffu, word);
+      if (kWrite && cached) {
+        word = B.lpair_cols[(size_t)w * nwords + wd];
+      } else {
+        const int lo = max(b0, wd * 32), hi = min(b1, wd * 32 + 31);
+        if (lo <= hi) word = (hi - lo == 31 ? 0xffffffffu : ((2u << (hi - lo)) - 1u)) << (lo - wd * 32);
+        word = __reduce_or_sync(0xffffffffu, word);
+        if (!kWrite && cached && lane == 0) B.lpair_cols[(size_t)w * nwords + wd] = word;
+      }
       if ((word >> lane) & 1u) {
         const int bin = R * fc.bins_x + wd * 32 + lane;
         if (kWrite) {
@@ -2439,7 +2451,7 @@ struct DeviceScene {
   DevBuf block_state, vq_src, vq_idx, vq_box, vq_flags, vq_mat, vq_col, vq_nrm, tri, tri_meta, shade,
       tri_y;
   DevBuf qcnt, tcnt, off, qcur, tcur, cat, bin_list0, bin_list1, prop_q, prop, items, item_rows, slots, spill0, spill1, scratch, fb, mask,
-      hash, emit, ctr, tile_ids, hbd, pool_tri, pool_mask, pool_pre, seg_queue, pool_slot, lpairs;
+      hash, emit, ctr, tile_ids, hbd, pool_tri, pool_mask, pool_pre, seg_queue, pool_slot, lpairs, lpair_cols;
   uint32_t items_cap = 0;
   uint32_t pool_cap = 0;
   uint32_t lpairs_cap = 0;
@@ -2744,6 +2756,7 @@ struct Prepared {
   dev::FrameConst fc;
   dev::Buffers B;
   uint32_t nblocks;
+  uint32_t lpair_cols_cap;
   uint32_t gcap_tbr, gcap_tb;
 };
 
@@ -2860,6 +2873,11 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   if (d->lpairs_cap == 0)
     d->lpairs_cap = init_cap ? init_cap : std::max<uint32_t>(1u << 16, std::min<uint32_t>(Q * 2u, 1u << 26));
   d->lpairs.ensure(size_t(d->lpairs_cap) * sizeof(uint2));
+  {  // column-word cache of the large pairs: sized to the pair capacity, at most 64 MB
+    const size_t words = std::min<size_t>(size_t(d->lpairs_cap) * size_t((fc.bins_x + 31) / 32), size_t(16) << 20);
+    d->lpair_cols.ensure(words * 4);
+    P.lpair_cols_cap = uint32_t(words);
+  }
   fc.lpairs_cap = d->lpairs_cap;
   if (d->pool_cap == 0)
     d->pool_cap = init_cap ? init_cap : std::max<uint32_t>(1u << 22, uint32_t(std::min<size_t>(nb * 2048, 1u << 26)));
@@ -2931,6 +2949,8 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   B.seg_queue = d->seg_queue.as<uint32_t>();
   B.pool_slot = d->pool_slot.as<uint16_t>();
   B.lpairs = d->lpairs.as<uint2>();
+  B.lpair_cols = d->lpair_cols.as<uint32_t>();
+  B.lpair_cols_cap = P.lpair_cols_cap;
   B.ctr = d->ctr.as<dev::Counters>();
   return P;
 }
