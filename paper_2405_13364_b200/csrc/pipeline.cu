@@ -2131,6 +2131,7 @@ __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
   if (B.ctr->error) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __shared__ int hb_next;
+  __shared__ uint8_t hb_order[32];  // the bin's half-blocks, most samples first
   // modes 0/2: CTA items = bins, warps pull the bin's 32 half-blocks;
   // mode 1: warp items from the queue mode 0 filled
   const uint32_t nitems = kMode == 1 ? B.ctr->seg_count : (uint32_t)fc.nbins;
@@ -2176,6 +2177,26 @@ __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
               stage_triangle(fc, B, tri, &row_tris[j]);
             }
         }
+        if (warp == 0) {
+          // longest-first order of the bin's half-blocks (their sample counts
+          // are known), so the warps' last pulls are short ones
+          uint32_t cost = 0;
+          if (owned && B.cat[cta_bin] != 0) {
+            const HbDesc hd = B.hbd[(size_t)cta_bin * 32 + lane];
+            cost = (kMode == 0 && hd.pad) ? 0u : min(hd.frags + 4u * hd.cnt, 0x7ffffffu);
+          }
+          uint32_t key = (cost << 5) | (31u - (uint32_t)lane);  // descending, ties by index
+#pragma unroll
+          for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+            for (int j = k >> 1; j > 0; j >>= 1) {
+              const uint32_t other = __shfl_xor_sync(0xffffffffu, key, j);
+              const bool desc = (lane & k) == 0, lower = (lane & j) == 0;
+              const uint32_t hi = max(key, other), lo = min(key, other);
+              key = (desc == lower) ? hi : lo;
+            }
+          hb_order[lane] = (uint8_t)(31u - (key & 31u));
+        }
         __syncthreads();
         if (!owned) {
           cta_bin = 0xffffffffu;
@@ -2185,7 +2206,7 @@ __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
         hbi = __shfl_sync(0xffffffffu, hbi, 0);
         if (hbi >= 32) continue;
       }
-      item = cta_bin * 32u + (uint32_t)hbi;
+      item = cta_bin * 32u + (uint32_t)hb_order[hbi];
     }
     const int bin = (int)(item >> 5), row = (int)((item >> 3) & 3u);
     const int bxi = bin % fc.bins_x, byi = bin / fc.bins_x;
