@@ -163,7 +163,9 @@ struct Buffers {
   uint32_t* bin_list[2];  // owned bins per extraction pass (high: + propagated ones)
   uint32_t* lpair_cols;   // per large pair: covered bin-column words from the count pass
   uint32_t lpair_cols_cap;  // words
-  uint32_t* prop_q;       // per bin: already appended to the high-pass list  // per item: block-rows (of its bin) each triangle's y range meets
+  uint32_t* prop_q;       // per bin: already appended to the high-pass list
+  uint32_t* bin_cost;     // per bin: wave-walk shading cost (samples + 4 per THB)
+  uint32_t* bin_order;    // bins in descending cost, k_shade's bin order  // per item: block-rows (of its bin) each triangle's y range meets
   // raster
   unsigned long long* slots;  // per (bin, row): samples, frags, thb, segments, invalid
   uint32_t* spill[2];
@@ -773,6 +775,7 @@ __global__ void __launch_bounds__(1024) k_bin_scan(Buffers B) {
       B.cat[b] = c;
       B.prop[b] = 0;
       B.prop_q[b] = 0;
+      B.bin_cost[b] = 0;
       atomicAdd(&cnt[c], 1u);
     }
     {  // extraction work lists (renderer.cpp:150-190: low bins, then high bins)
@@ -2016,6 +2019,9 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
     d.pad = seg ? 1u : 0u;
     const uint32_t hbi = (uint32_t)bin * 32u + (uint32_t)(row * 8 + warp * 2 + lane);
     B.hbd[hbi] = d;
+    const uint32_t cost = seg ? 0u : min(d.frags + 4u * d.cnt, 0x00ffffffu);
+    const uint32_t both = cost + __shfl_down_sync(0x3u, cost, 1);  // the block's two halves
+    if (lane == 0 && both) atomicAdd(&B.bin_cost[bin], both);
     // low-pass entries of a bin that later propagates are stale (k_shade_seg skips them)
     if (seg) B.seg_queue[atomicAdd(&B.ctr->seg_count, 1u)] = hbi | (pass == kPassLow ? 0u : 0x80000000u);
   }
@@ -2161,8 +2167,8 @@ __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
           hb_next = 0;
         }
         __syncthreads();
-        cta_bin = item_s;
-        if (cta_bin >= nitems) break;
+        cta_bin = item_s < nitems ? B.bin_order[item_s] : 0xffffffffu;
+        if (cta_bin == 0xffffffffu) break;
         const int bxi = (int)cta_bin % fc.bins_x, byi = (int)cta_bin / fc.bins_x;
         const bool owned = fc.world <= 1 || ((bxi + 3 * byi) % fc.world) == fc.rank;
         staged_ok = false;
@@ -2315,6 +2321,43 @@ __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
 // Deterministic stat merge (renderer.cpp:170-212): integer sums over the
 // owned bins' (bin, block-row) slots; warp shuffles, then one atomic per
 // warp and counter.
+// Longest-first bin order for k_shade (bins with the most wave-walk work
+// first, so the kernel's tail is made of short bins): a 256-bucket
+// log-scale counting sort of the per-bin costs k_extract accumulated.
+__global__ void __launch_bounds__(1024) k_order_bins(Buffers B) {
+  const FrameConst& fc = c_fc;
+  __shared__ uint32_t hist[256];
+  __shared__ uint32_t base[256];
+  if (B.ctr->error) return;
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  auto bucket = [](uint32_t c) -> uint32_t {  // 8 sub-buckets per octave, descending
+    if (c == 0) return 255u;
+    const uint32_t e = 31u - (uint32_t)__clz(c);
+    const uint32_t m = e >= 3 ? (c >> (e - 3)) & 7u : (c << (3 - e)) & 7u;
+    return 255u - min(254u, e * 8u + m);
+  };
+  for (int b = threadIdx.x; b < fc.nbins; b += blockDim.x) atomicAdd(&hist[bucket(B.bin_cost[b])], 1u);
+  __syncthreads();
+  if (threadIdx.x < 32) {  // exclusive scan of 256 buckets by one warp
+    uint32_t run = 0;
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t v = hist[k * 32 + threadIdx.x];
+      uint32_t x = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if ((int)threadIdx.x >= o) x += y;
+      }
+      base[k * 32 + threadIdx.x] = run + x - v;
+      run += __shfl_sync(0xffffffffu, x, 31);
+    }
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < fc.nbins; b += blockDim.x)
+    B.bin_order[atomicAdd(&base[bucket(B.bin_cost[b])], 1u)] = (uint32_t)b;
+}
+
 __global__ void __launch_bounds__(256) k_finalize(Buffers B) {
   const FrameConst& fc = c_fc;
   if (B.ctr->error) return;
@@ -2471,7 +2514,7 @@ struct DeviceScene {
   DevBuf pos, vcol, vnrm, quads, qmat, mats;
   DevBuf block_state, vq_src, vq_idx, vq_box, vq_flags, vq_mat, vq_col, vq_nrm, tri, tri_meta, shade,
       tri_y;
-  DevBuf qcnt, tcnt, off, qcur, tcur, cat, bin_list0, bin_list1, prop_q, prop, items, item_rows, slots, spill0, spill1, scratch, fb, mask,
+  DevBuf qcnt, tcnt, off, qcur, tcur, cat, bin_list0, bin_list1, prop_q, bin_cost, bin_order, prop, items, item_rows, slots, spill0, spill1, scratch, fb, mask,
       hash, emit, ctr, tile_ids, hbd, pool_tri, pool_mask, pool_pre, seg_queue, pool_slot, lpairs, lpair_cols;
   uint32_t items_cap = 0;
   uint32_t pool_cap = 0;
@@ -2869,6 +2912,8 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   d->bin_list0.ensure(nb * 4);
   d->bin_list1.ensure(nb * 4);
   d->prop_q.ensure(nb * 4);
+  d->bin_cost.ensure(nb * 4);
+  d->bin_order.ensure(nb * 4);
   d->prop.ensure(nb);
   d->slots.ensure(nb * 4 * 5 * 8);
   d->spill0.ensure(nb * 4 * 4);
@@ -2951,6 +2996,8 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   B.bin_list[0] = d->bin_list0.as<uint32_t>();
   B.bin_list[1] = d->bin_list1.as<uint32_t>();
   B.prop_q = d->prop_q.as<uint32_t>();
+  B.bin_cost = d->bin_cost.as<uint32_t>();
+  B.bin_order = d->bin_order.as<uint32_t>();
   B.prop = d->prop.as<uint8_t>();
   B.items = d->items.as<uint32_t>();
   B.item_rows = d->item_rows.as<uint8_t>();
@@ -3208,6 +3255,8 @@ static void enqueue_raster(DeviceScene* d, Prepared& P, int* launches) {
   record_event(d->ev[3], d->stream);
   launch_extract(d, P.fc, P.B, dev::kPassHigh, P.gcap_tbr, P.gcap_tb, launches);
   record_event(d->ev[5], d->stream);
+  dev::k_order_bins<<<1, 1024, 0, d->stream>>>(P.B);
+  ++*launches;
   launch_shade(d, P.fc, P.B, launches);
   dev::k_finalize<<<(P.fc.nbins + 255) / 256, 256, 0, d->stream>>>(P.B);
   ++*launches;
