@@ -87,6 +87,14 @@ def main():
     s = RefScene.synthetic("layered_quads", 2, 96, 80)
     save("layered_s2_threshold", s, default_params(flags=RENDER_ALPHA_THRESHOLD, depth_filter_size=2),
          "alpha threshold with ragged viewport 96x80")
+    # textured materials (map_Kd, mip-mapped, repeat wrap, perspective UV
+    # gradients): the scene is the OBJ/MTL/PNG set in tests/golden/textured
+    tex = os.path.join(OUT, "textured")
+    s = RefScene.load(os.path.join(tex, "scene.obj"), None, os.path.join(tex, "camera.cfg"))
+    save("textured_scene", s, default_params(), "tests/golden/textured: 3 materials, 2 mip-mapped textures")
+    save("textured_scene_df1_backface", s,
+         default_params(depth_filter_size=1, flags=RENDER_BACKFACE_CULLING | RENDER_VISUALIZE_ERRORS),
+         "textured scene with DF=1, backface culling, error overlay")
 
 
 if __name__ == "__main__":

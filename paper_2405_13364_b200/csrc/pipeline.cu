@@ -58,8 +58,9 @@ struct Limits {
 struct MatDev {
   float base[4];
   float opacity;
-  uint32_t flags;  // bit0 colors, bit1 normals (already AND-ed with scene flags)
-  uint32_t pad[2];
+  uint32_t flags;  // bit0 colors, bit1 normals, bit2 uvs (AND-ed with the scene flags)
+  int32_t texture;  // -1: none
+  uint32_t pad;
 };
 
 struct FrameConst {
@@ -137,6 +138,10 @@ struct Buffers {
   const uint4* quads;
   const uint32_t* qmat;
   const MatDev* mats;
+  const float2* vuv;     // per vertex, when the scene has UVs
+  const float4* texels;  // every texture's mip levels, straight RGBA
+  const uint4* texlev;   // per level: texel offset, width, height
+  const uint2* texdesc;  // per texture: first level, level count
   // setup
   unsigned long long* block_state;  // k_setup look-back: status << 32 | count
   uint32_t* vq_src;
@@ -146,6 +151,7 @@ struct Buffers {
   uint32_t* vq_mat;
   uint4* vq_col;
   uint4* vq_nrm;
+  float4* vq_uv;  // per visible quad with UVs: (uv0, uv1), (uv2, uv3)
   TriRec* tri;
   uint4* tri_meta;  // flat normal, material, quad index, tri | valid << 8
   uint32_t* tri_y;  // int16 y_min | int16 y_max << 16 (empty range when invalid)
@@ -482,8 +488,15 @@ __global__ void __launch_bounds__(kSetupBlock) k_setup(Buffers B, uint32_t nbloc
   B.vq_idx[slot] = idx;
   B.vq_box[slot] = make_uint2((uint32_t)o.x0 | ((uint32_t)o.x1 << 16),
                               (uint32_t)o.y0 | ((uint32_t)o.y1 << 16));
-  B.vq_flags[slot] = (o.large ? 1u : 0u) | (has_c ? 2u : 0u) | (has_n ? 4u : 0u) | (o.flags << 4);
+  const bool has_uv = md.flags & 4u;
+  B.vq_flags[slot] = (o.large ? 1u : 0u) | (has_c ? 2u : 0u) | (has_n ? 4u : 0u) | (has_uv ? 8u : 0u) |
+                     (o.flags << 4);
   B.vq_mat[slot] = mat;
+  if (has_uv) {  // setup.cpp:326-328
+    const float2 u0 = B.vuv[idx.x], u1 = B.vuv[idx.y], u2 = B.vuv[idx.z], u3 = B.vuv[idx.w];
+    B.vq_uv[2 * (size_t)slot] = make_float4(u0.x, u0.y, u1.x, u1.y);
+    B.vq_uv[2 * (size_t)slot + 1] = make_float4(u2.x, u2.y, u3.x, u3.y);
+  }
   uint4 col = make_uint4(0, 0, 0, 0), nrm = make_uint4(0, 0, 0, 0);
   if (has_c) col = make_uint4(B.vcol[idx.x], B.vcol[idx.y], B.vcol[idx.z], B.vcol[idx.w]);
   if (has_n) nrm = make_uint4(B.vnrm[idx.x], B.vnrm[idx.y], B.vnrm[idx.z], B.vnrm[idx.w]);
@@ -1090,6 +1103,73 @@ __device__ __forceinline__ float4 light_and_premultiply(const FrameConst& fc, fl
   return premultiply(color, mat, light);
 }
 
+// bilinear (shading.cpp:81-101): repeat wrapping, texel centres at +0.5,
+// float arithmetic in the reference's order.
+__device__ __forceinline__ float4 tex_bilinear(const Buffers& B, uint4 lev, float u, float v) {
+  const int w = (int)lev.y, h = (int)lev.z;
+  const float x = __fsub_rn(__fmul_rn(u, (float)w), 0.5f);
+  const float y = __fsub_rn(__fmul_rn(v, (float)h), 0.5f);
+  const float fx = floorf(x), fy = floorf(y);
+  const float wx = __fsub_rn(x, fx), wy = __fsub_rn(y, fy);
+  auto wrap = [](int i, int n) {
+    const int m = i % n;
+    return m < 0 ? m + n : m;
+  };
+  const int x0 = wrap((int)fx, w), x1 = wrap((int)fx + 1, w);
+  const int y0 = wrap((int)fy, h), y1 = wrap((int)fy + 1, h);
+  const float4* t = B.texels + lev.x;
+  const float4 t00 = __ldg(&t[(size_t)y0 * w + x0]), t10 = __ldg(&t[(size_t)y0 * w + x1]);
+  const float4 t01 = __ldg(&t[(size_t)y1 * w + x0]), t11 = __ldg(&t[(size_t)y1 * w + x1]);
+  const float ax = __fsub_rn(1.0f, wx), ay = __fsub_rn(1.0f, wy);
+  auto lerp4 = [](float4 a, float4 b, float ka, float kb) {
+    return make_float4(__fadd_rn(__fmul_rn(a.x, ka), __fmul_rn(b.x, kb)),
+                       __fadd_rn(__fmul_rn(a.y, ka), __fmul_rn(b.y, kb)),
+                       __fadd_rn(__fmul_rn(a.z, ka), __fmul_rn(b.z, kb)),
+                       __fadd_rn(__fmul_rn(a.w, ka), __fmul_rn(b.w, kb)));
+  };
+  const float4 top = lerp4(t00, t10, ax, wx), bot = lerp4(t01, t11, ax, wx);
+  return lerp4(top, bot, ay, wy);
+}
+
+// sample_texture (shading.cpp:105-121): mip level log2(rho) of the UV
+// footprint, trilinear between levels. The level uses CUDA's log2f (1 ulp)
+// where the reference calls the C library's log2f, so a frac one ulp apart
+// can move a blended texel by one unit in the last place; everything else is
+// the reference's float arithmetic.
+__device__ __forceinline__ float4 sample_texture(const Buffers& B, int texi, float2 uv, float2 dx,
+                                                 float2 dy) {
+  const uint2 td = __ldg(&B.texdesc[texi]);
+  const uint4 base = __ldg(&B.texlev[td.x]);
+  const float bw = (float)base.y, bh = (float)base.z;
+  const float gx0 = __fmul_rn(dx.x, bw), gx1 = __fmul_rn(dx.y, bh);
+  const float gy0 = __fmul_rn(dy.x, bw), gy1 = __fmul_rn(dy.y, bh);
+  const float gx = __fsqrt_rn(__fadd_rn(__fmul_rn(gx0, gx0), __fmul_rn(gx1, gx1)));
+  const float gy = __fsqrt_rn(__fadd_rn(__fmul_rn(gy0, gy0), __fmul_rn(gy1, gy1)));
+  const float rho = smaxf(gx, gy);
+  const float level = rho > 0.0f ? log2f(rho) : 0.0f;
+  if (!(level > 0.0f)) return tex_bilinear(B, base, uv.x, uv.y);
+  const float max_level = (float)(td.y - 1u);
+  if (level >= max_level) return tex_bilinear(B, __ldg(&B.texlev[td.x + td.y - 1u]), uv.x, uv.y);
+  const int l0 = (int)level;
+  const float frac = __fsub_rn(level, (float)l0);
+  const float4 a = tex_bilinear(B, __ldg(&B.texlev[td.x + l0]), uv.x, uv.y);
+  const float4 b = tex_bilinear(B, __ldg(&B.texlev[td.x + l0 + 1]), uv.x, uv.y);
+  const float ka = __fsub_rn(1.0f, frac);
+  return make_float4(__fadd_rn(__fmul_rn(a.x, ka), __fmul_rn(b.x, frac)),
+                     __fadd_rn(__fmul_rn(a.y, ka), __fmul_rn(b.y, frac)),
+                     __fadd_rn(__fmul_rn(a.z, ka), __fmul_rn(b.z, frac)),
+                     __fadd_rn(__fmul_rn(a.w, ka), __fmul_rn(b.w, frac)));
+}
+
+// shade_sample's products with a texture factor (shading.cpp:134-138).
+__device__ __forceinline__ float4 premultiply_tex(float4 color, float4 mat, float4 tex, float light) {
+  float r = __fmul_rn(__fmul_rn(__fmul_rn(mat.x, color.x), tex.x), light);
+  float g = __fmul_rn(__fmul_rn(__fmul_rn(mat.y, color.y), tex.y), light);
+  float b = __fmul_rn(__fmul_rn(__fmul_rn(mat.z, color.z), tex.z), light);
+  float a = __fmul_rn(__fmul_rn(mat.w, color.w), tex.w);
+  return make_float4(__fmul_rn(r, a), __fmul_rn(g, a), __fmul_rn(b, a), a);
+}
+
 // make_sample_context (shading.cpp:24-77) + shade_sample (123-139), no
 // textures. Returns the premultiplied colour and the sample depth.
 __device__ __forceinline__ float4 shade_sample(const FrameConst& fc, const Buffers& B,
@@ -1153,8 +1233,36 @@ __device__ __forceinline__ float4 shade_sample(const FrameConst& fc, const Buffe
     for (int k = 0; k < 3; ++k) n[k] = lut_n(meta.x, 10 * k);
   }
   const MatDev& m = B.mats[meta.y];
-  return light_and_premultiply(
-      fc, n, color, make_float4(__ldg(&m.base[0]), __ldg(&m.base[1]), __ldg(&m.base[2]), __ldg(&m.opacity)));
+  const float4 mat = make_float4(__ldg(&m.base[0]), __ldg(&m.base[1]), __ldg(&m.base[2]), __ldg(&m.opacity));
+  const int texi = __ldg(&m.texture);
+  if (texi < 0) return light_and_premultiply(fc, n, color, mat);
+  // UVs by the quotient rule with analytic gradients (shading.cpp:55-74),
+  // in double; zero when the quad carries no UVs (SampleContext defaults)
+  float2 uv = make_float2(0.f, 0.f), duv_dx = uv, duv_dy = uv;
+  if (qf & 8u) {
+    const float4 ua = __ldg(&B.vq_uv[2 * (size_t)q]), ub = __ldg(&B.vq_uv[2 * (size_t)q + 1]);
+    const float2 c0 = make_float2(ua.x, ua.y);
+    const float2 c1 = ltri == 0 ? make_float2(ua.z, ua.w) : make_float2(ub.x, ub.y);
+    const float2 c2 = ltri == 0 ? make_float2(ub.x, ub.y) : make_float2(ub.z, ub.w);
+    auto dot3d = [](double a0, double a1, double a2, double b0, double b1, double b2) {
+      return __dadd_rn(__dadd_rn(__dmul_rn(a0, b0), __dmul_rn(a1, b1)), __dmul_rn(a2, b2));
+    };
+    const double nu = dot3d(c0.x, c1.x, c2.x, e0, e1, e2), nv = dot3d(c0.y, c1.y, c2.y, e0, e1, e2);
+    const double nu_dx = dot3d(c0.x, c1.x, c2.x, t.e[0].a, t.e[1].a, t.e[2].a);
+    const double nv_dx = dot3d(c0.y, c1.y, c2.y, t.e[0].a, t.e[1].a, t.e[2].a);
+    const double nu_dy = dot3d(c0.x, c1.x, c2.x, t.e[0].b, t.e[1].b, t.e[2].b);
+    const double nv_dy = dot3d(c0.y, c1.y, c2.y, t.e[0].b, t.e[1].b, t.e[2].b);
+    const double d_dx = __dadd_rn(__dadd_rn(t.e[0].a, t.e[1].a), t.e[2].a);
+    const double d_dy = __dadd_rn(__dadd_rn(t.e[0].b, t.e[1].b), t.e[2].b);
+    const double inv2 = __dmul_rn(inv, inv);
+    uv = make_float2((float)__dmul_rn(nu, inv), (float)__dmul_rn(nv, inv));
+    duv_dx = make_float2((float)__dmul_rn(__dsub_rn(__dmul_rn(nu_dx, sum), __dmul_rn(nu, d_dx)), inv2),
+                         (float)__dmul_rn(__dsub_rn(__dmul_rn(nv_dx, sum), __dmul_rn(nv, d_dx)), inv2));
+    duv_dy = make_float2((float)__dmul_rn(__dsub_rn(__dmul_rn(nu_dy, sum), __dmul_rn(nu, d_dy)), inv2),
+                         (float)__dmul_rn(__dsub_rn(__dmul_rn(nv_dy, sum), __dmul_rn(nv, d_dy)), inv2));
+  }
+  const float4 tex = sample_texture(B, texi, uv, duv_dx, duv_dy);
+  return premultiply_tex(color, mat, tex, light_factor(fc, n));
 }
 
 // Branch-free variant of shade_sample for the decoded-record path (selects
@@ -2511,8 +2619,9 @@ struct DeviceScene {
   cudaStream_t stream = nullptr;
   uint64_t uploaded_version = 0;
   uint32_t nverts = 0, nquads = 0;
-  DevBuf pos, vcol, vnrm, quads, qmat, mats;
-  DevBuf block_state, vq_src, vq_idx, vq_box, vq_flags, vq_mat, vq_col, vq_nrm, tri, tri_meta, shade,
+  DevBuf pos, vcol, vnrm, quads, qmat, mats, vuv, texels, texlev, texdesc;
+  bool textured = false;  // some material samples a texture (generic shading path)
+  DevBuf block_state, vq_uv, vq_src, vq_idx, vq_box, vq_flags, vq_mat, vq_col, vq_nrm, tri, tri_meta, shade,
       tri_y;
   DevBuf qcnt, tcnt, off, qcur, tcur, cat, bin_list0, bin_list1, prop_q, bin_cost, bin_order, prop, items, item_rows, slots, spill0, spill1, scratch, fb, mask,
       hash, emit, ctr, tile_ids, hbd, pool_tri, pool_mask, pool_pre, seg_queue, pool_slot, lpairs, lpair_cols;
@@ -2665,8 +2774,41 @@ DeviceScene* device_scene(const Scene& s) {
       md.opacity = m.opacity;
       bool hc = (m.flags & VEIL_MATERIAL_VERTEX_COLORS) && (s.flags & VEIL_SCENE_HAS_COLORS);
       bool hn = (m.flags & VEIL_MATERIAL_VERTEX_NORMALS) && (s.flags & VEIL_SCENE_HAS_NORMALS);
-      md.flags = (hc ? 1u : 0u) | (hn ? 2u : 0u);
+      // record.has_uvs (setup.cpp:326-328): the material samples a texture
+      // with UVs and the scene has them
+      bool hu = (m.flags & VEIL_MATERIAL_UVS) && (s.flags & VEIL_SCENE_HAS_UVS) && m.texture >= 0;
+      md.flags = (hc ? 1u : 0u) | (hn ? 2u : 0u) | (hu ? 4u : 0u);
+      md.texture = m.texture;
       mats[i] = md;
+    }
+    d->textured = false;
+    for (const veil_material& m : s.materials) d->textured |= m.texture >= 0;
+    {  // vertex UVs and textures (mip levels as float4 texels)
+      std::vector<float2> vuv((s.flags & VEIL_SCENE_HAS_UVS) ? V : 0);
+      for (size_t i = 0; i < vuv.size(); ++i) vuv[i] = make_float2(s.vertices[i].uv[0], s.vertices[i].uv[1]);
+      std::vector<float4> texels;
+      std::vector<uint4> levels;
+      std::vector<uint2> descs;
+      for (const Texture& t : s.textures) {
+        descs.push_back(make_uint2(uint32_t(levels.size()), uint32_t(t.levels.size())));
+        for (const TextureLevel& l : t.levels) {
+          levels.push_back(make_uint4(uint32_t(texels.size()), uint32_t(l.width), uint32_t(l.height), 0));
+          for (size_t k = 0; k + 3 < l.texels.size(); k += 4)
+            texels.push_back(make_float4(l.texels[k], l.texels[k + 1], l.texels[k + 2], l.texels[k + 3]));
+        }
+      }
+      d->vuv.ensure(std::max<size_t>(1, vuv.size()) * sizeof(float2));
+      d->texels.ensure(std::max<size_t>(1, texels.size()) * sizeof(float4));
+      d->texlev.ensure(std::max<size_t>(1, levels.size()) * sizeof(uint4));
+      d->texdesc.ensure(std::max<size_t>(1, descs.size()) * sizeof(uint2));
+      if (!vuv.empty())
+        ck(cudaMemcpy(d->vuv.p, vuv.data(), vuv.size() * sizeof(float2), cudaMemcpyHostToDevice), "upload");
+      if (!texels.empty())
+        ck(cudaMemcpy(d->texels.p, texels.data(), texels.size() * sizeof(float4), cudaMemcpyHostToDevice), "upload");
+      if (!levels.empty())
+        ck(cudaMemcpy(d->texlev.p, levels.data(), levels.size() * sizeof(uint4), cudaMemcpyHostToDevice), "upload");
+      if (!descs.empty())
+        ck(cudaMemcpy(d->texdesc.p, descs.data(), descs.size() * sizeof(uint2), cudaMemcpyHostToDevice), "upload");
     }
     d->pos.ensure(V * sizeof(float4));
     d->vcol.ensure(V * 4);
@@ -2895,13 +3037,16 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   d->vq_mat.ensure(size_t(Q) * 4);
   d->vq_col.ensure(size_t(Q) * 16);
   d->vq_nrm.ensure(size_t(Q) * 16);
+  d->vq_uv.ensure(d->textured ? size_t(Q) * 32 : 32);
   d->tri.ensure(size_t(Q) * 2 * sizeof(dev::TriRec));
   d->tri_meta.ensure(size_t(Q) * 2 * 16);
   d->tri_y.ensure(size_t(Q) * 2 * 4);
   // Decoded shading records pay off when triangles cover many pixels (each
   // record is read by every sample of its triangle): >= 8 px per quad at
   // depth complexity 1.
-  fc.decoded = (double)cam.width * cam.height >= 8.0 * std::max<double>(1.0, Q) ? 1 : 0;
+  // Decoded shading records (and the shared-memory staging built on them)
+  // carry no UVs: scenes with textured materials shade on the generic path.
+  fc.decoded = !d->textured && (double)cam.width * cam.height >= 8.0 * std::max<double>(1.0, Q) ? 1 : 0;
   if (fc.decoded) d->shade.ensure(size_t(Q) * 2 * sizeof(dev::ShadeRec));
   d->qcnt.ensure(nb * 4);
   d->tcnt.ensure(nb * 4);
@@ -2975,6 +3120,11 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   B.quads = d->quads.as<uint4>();
   B.qmat = d->qmat.as<uint32_t>();
   B.mats = d->mats.as<dev::MatDev>();
+  B.vuv = d->vuv.as<float2>();
+  B.texels = d->texels.as<float4>();
+  B.texlev = d->texlev.as<uint4>();
+  B.texdesc = d->texdesc.as<uint2>();
+  B.vq_uv = d->vq_uv.as<float4>();
   B.block_state = d->block_state.as<unsigned long long>();
   B.vq_src = d->vq_src.as<uint32_t>();
   B.vq_idx = d->vq_idx.as<uint4>();
@@ -3138,10 +3288,6 @@ void validate_frame(const Scene& s, const RenderOptions& opt) {
   } else {
     validate_camera(s.camera, s.extended);
   }
-  for (const veil_material& m : s.materials)
-    if (m.texture >= 0)
-      throw Error(VEIL_ERR_INVALID_ARG,
-                  "textured materials are not supported by the device shading path");
   const veil_render_params& p = opt.params;
   bool reference = p.flags & VEIL_RENDER_REFERENCE;
   if (!reference && p.depth_filter_size < 1)
@@ -3191,7 +3337,7 @@ void collect_dumps(DeviceScene* d, Prepared& P, const dev::Counters& c, RenderOu
     uint32_t cf = (flags[i] >> 4) & 3u;
     aabb[i] = fc.extended ? (uint64_t(x0) | (uint64_t(y0) << 16) | (uint64_t(x1) << 32) | (uint64_t(y1) << 48))
                           : uint64_t(x0 | (y0 << 7) | (x1 << 14) | (y1 << 21) | (cf << 28));
-    cls[i] = uint8_t((flags[i] & 1u) | (flags[i] & 2u) | (flags[i] & 4u) | (cf << 4));
+    cls[i] = uint8_t((flags[i] & 15u) | (cf << 4));  // large, colours, normals, uvs, cull bits
     const uint32_t cc[4] = {col[i].x, col[i].y, col[i].z, col[i].w};
     const uint32_t nn[4] = {nrm[i].x, nrm[i].y, nrm[i].z, nrm[i].w};
     for (int k = 0; k < 4; ++k) attr[i * 9 + k] = cc[k], attr[i * 9 + 4 + k] = nn[k];

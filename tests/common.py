@@ -31,7 +31,13 @@ PARITY_ARRAYS = [
 
 
 def golden_names():
-    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz")))
+    """Array-scene fixtures (the textured OBJ fixtures load their scene from
+    tests/golden/textured and have their own tests)."""
+    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz"))
+                  if not os.path.basename(p).startswith("textured"))
+
+
+TEXTURED = os.path.join(GOLDEN, "textured")
 
 
 def load_golden(name):

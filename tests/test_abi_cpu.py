@@ -231,3 +231,13 @@ def test_render_without_gpu_fails_loudly():
     with pytest.raises(veil.VeilError) as e:
         veil.render(veil.Scene.synthetic("layered_quads", 1, 32, 32))
     assert "no CUDA device" in e.value.message
+
+
+@needs_ref
+def test_textured_obj_ingest_matches_reference():
+    from common import TEXTURED
+    mine = veil.Scene.load(f"{TEXTURED}/scene.obj", None, f"{TEXTURED}/camera.cfg").arrays()
+    ref = bindings.RefScene.load(f"{TEXTURED}/scene.obj", None, f"{TEXTURED}/camera.cfg").arrays()
+    assert np.array_equal(mine.vertices, ref.vertices) and np.array_equal(mine.quads, ref.quads)
+    assert np.array_equal(mine.materials, ref.materials) and mine.flags == ref.flags
+    assert np.array_equal(mine.matrix, ref.matrix)
