@@ -1170,8 +1170,42 @@ __device__ __forceinline__ float4 premultiply_tex(float4 color, float4 mat, floa
   return make_float4(__fmul_rn(r, a), __fmul_rn(g, a), __fmul_rn(b, a), a);
 }
 
+// The texture factor of one sample (compiled only into the textured
+// instantiations of the shading kernels). UVs by
+// the quotient rule with analytic gradients (shading.cpp:55-74), in double;
+// zero when the quad carries no UVs (SampleContext defaults).
+__device__ __forceinline__ float4 texture_factor(const Buffers& B, const TriRec& t, uint32_t q, int ltri,
+                                              bool has_uv, int texi, double e0, double e1, double e2,
+                                              double sum, double inv) {
+  float2 uv = make_float2(0.f, 0.f), duv_dx = uv, duv_dy = uv;
+  if (has_uv) {
+    const float4 ua = __ldg(&B.vq_uv[2 * (size_t)q]), ub = __ldg(&B.vq_uv[2 * (size_t)q + 1]);
+    const float2 c0 = make_float2(ua.x, ua.y);
+    const float2 c1 = ltri == 0 ? make_float2(ua.z, ua.w) : make_float2(ub.x, ub.y);
+    const float2 c2 = ltri == 0 ? make_float2(ub.x, ub.y) : make_float2(ub.z, ub.w);
+    auto dot3d = [](double a0, double a1, double a2, double b0, double b1, double b2) {
+      return __dadd_rn(__dadd_rn(__dmul_rn(a0, b0), __dmul_rn(a1, b1)), __dmul_rn(a2, b2));
+    };
+    const double nu = dot3d(c0.x, c1.x, c2.x, e0, e1, e2), nv = dot3d(c0.y, c1.y, c2.y, e0, e1, e2);
+    const double nu_dx = dot3d(c0.x, c1.x, c2.x, t.e[0].a, t.e[1].a, t.e[2].a);
+    const double nv_dx = dot3d(c0.y, c1.y, c2.y, t.e[0].a, t.e[1].a, t.e[2].a);
+    const double nu_dy = dot3d(c0.x, c1.x, c2.x, t.e[0].b, t.e[1].b, t.e[2].b);
+    const double nv_dy = dot3d(c0.y, c1.y, c2.y, t.e[0].b, t.e[1].b, t.e[2].b);
+    const double d_dx = __dadd_rn(__dadd_rn(t.e[0].a, t.e[1].a), t.e[2].a);
+    const double d_dy = __dadd_rn(__dadd_rn(t.e[0].b, t.e[1].b), t.e[2].b);
+    const double inv2 = __dmul_rn(inv, inv);
+    uv = make_float2((float)__dmul_rn(nu, inv), (float)__dmul_rn(nv, inv));
+    duv_dx = make_float2((float)__dmul_rn(__dsub_rn(__dmul_rn(nu_dx, sum), __dmul_rn(nu, d_dx)), inv2),
+                         (float)__dmul_rn(__dsub_rn(__dmul_rn(nv_dx, sum), __dmul_rn(nv, d_dx)), inv2));
+    duv_dy = make_float2((float)__dmul_rn(__dsub_rn(__dmul_rn(nu_dy, sum), __dmul_rn(nu, d_dy)), inv2),
+                         (float)__dmul_rn(__dsub_rn(__dmul_rn(nv_dy, sum), __dmul_rn(nv, d_dy)), inv2));
+  }
+  return sample_texture(B, texi, uv, duv_dx, duv_dy);
+}
+
 // make_sample_context (shading.cpp:24-77) + shade_sample (123-139), no
 // textures. Returns the premultiplied colour and the sample depth.
+template <bool kTex>
 __device__ __forceinline__ float4 shade_sample(const FrameConst& fc, const Buffers& B,
                                                uint32_t tri, int px, int py, double* depth) {
   const TriRec& t = B.tri[tri];
@@ -1234,35 +1268,14 @@ __device__ __forceinline__ float4 shade_sample(const FrameConst& fc, const Buffe
   }
   const MatDev& m = B.mats[meta.y];
   const float4 mat = make_float4(__ldg(&m.base[0]), __ldg(&m.base[1]), __ldg(&m.base[2]), __ldg(&m.opacity));
-  const int texi = __ldg(&m.texture);
-  if (texi < 0) return light_and_premultiply(fc, n, color, mat);
-  // UVs by the quotient rule with analytic gradients (shading.cpp:55-74),
-  // in double; zero when the quad carries no UVs (SampleContext defaults)
-  float2 uv = make_float2(0.f, 0.f), duv_dx = uv, duv_dy = uv;
-  if (qf & 8u) {
-    const float4 ua = __ldg(&B.vq_uv[2 * (size_t)q]), ub = __ldg(&B.vq_uv[2 * (size_t)q + 1]);
-    const float2 c0 = make_float2(ua.x, ua.y);
-    const float2 c1 = ltri == 0 ? make_float2(ua.z, ua.w) : make_float2(ub.x, ub.y);
-    const float2 c2 = ltri == 0 ? make_float2(ub.x, ub.y) : make_float2(ub.z, ub.w);
-    auto dot3d = [](double a0, double a1, double a2, double b0, double b1, double b2) {
-      return __dadd_rn(__dadd_rn(__dmul_rn(a0, b0), __dmul_rn(a1, b1)), __dmul_rn(a2, b2));
-    };
-    const double nu = dot3d(c0.x, c1.x, c2.x, e0, e1, e2), nv = dot3d(c0.y, c1.y, c2.y, e0, e1, e2);
-    const double nu_dx = dot3d(c0.x, c1.x, c2.x, t.e[0].a, t.e[1].a, t.e[2].a);
-    const double nv_dx = dot3d(c0.y, c1.y, c2.y, t.e[0].a, t.e[1].a, t.e[2].a);
-    const double nu_dy = dot3d(c0.x, c1.x, c2.x, t.e[0].b, t.e[1].b, t.e[2].b);
-    const double nv_dy = dot3d(c0.y, c1.y, c2.y, t.e[0].b, t.e[1].b, t.e[2].b);
-    const double d_dx = __dadd_rn(__dadd_rn(t.e[0].a, t.e[1].a), t.e[2].a);
-    const double d_dy = __dadd_rn(__dadd_rn(t.e[0].b, t.e[1].b), t.e[2].b);
-    const double inv2 = __dmul_rn(inv, inv);
-    uv = make_float2((float)__dmul_rn(nu, inv), (float)__dmul_rn(nv, inv));
-    duv_dx = make_float2((float)__dmul_rn(__dsub_rn(__dmul_rn(nu_dx, sum), __dmul_rn(nu, d_dx)), inv2),
-                         (float)__dmul_rn(__dsub_rn(__dmul_rn(nv_dx, sum), __dmul_rn(nv, d_dx)), inv2));
-    duv_dy = make_float2((float)__dmul_rn(__dsub_rn(__dmul_rn(nu_dy, sum), __dmul_rn(nu, d_dy)), inv2),
-                         (float)__dmul_rn(__dsub_rn(__dmul_rn(nv_dy, sum), __dmul_rn(nv, d_dy)), inv2));
+  if constexpr (kTex) {  // scenes with textured materials (see launch_shade)
+    const int texi = __ldg(&m.texture);
+    if (texi >= 0) {
+      const float4 tex = texture_factor(B, t, q, ltri, (qf & 8u) != 0u, texi, e0, e1, e2, sum, inv);
+      return premultiply_tex(color, mat, tex, light_factor(fc, n));
+    }
   }
-  const float4 tex = sample_texture(B, texi, uv, duv_dx, duv_dy);
-  return premultiply_tex(color, mat, tex, light_factor(fc, n));
+  return light_and_premultiply(fc, n, color, mat);
 }
 
 // Branch-free variant of shade_sample for the decoded-record path (selects
@@ -1537,7 +1550,7 @@ __device__ __forceinline__ uint32_t route_mask(uint32_t* route, uint32_t pix, bo
   return mine;
 }
 
-template <int KM, typename Filter>
+template <int KM, bool kTex, typename Filter>
 __device__ __forceinline__ void shade_segments(const FrameConst& fc, const Buffers& B, int px0,
                                                int py0, const uint32_t* tri_l,
                                                const uint32_t* mask_l, const uint32_t* pre_l,
@@ -1560,7 +1573,7 @@ __device__ __forceinline__ void shade_segments(const FrameConst& fc, const Buffe
       col0 = shade_decoded_bf(fc, B, t0, px0 + (int)(p0 & 7u), py0 + (int)(p0 >> 3), &q0);
     } else {
       double d0;
-      col0 = shade_sample(fc, B, t0, px0 + (int)(p0 & 7u), py0 + (int)(p0 >> 3), &d0);
+      col0 = shade_sample<kTex>(fc, B, t0, px0 + (int)(p0 & 7u), py0 + (int)(p0 >> 3), &d0);
       q0 = quantize_depth(d0);
     }
     const uint64_t key0 = sample_key(fc, q0, t0);
@@ -1583,7 +1596,7 @@ __device__ __forceinline__ void shade_segments(const FrameConst& fc, const Buffe
 // many pixels (samples/THB high) and, with kThreshold, for the alpha
 // threshold, where the 32nd saturation must be located at its exact stream
 // position.
-template <int KM, bool kThreshold>
+template <int KM, bool kThreshold, bool kTex>
 __device__ __forceinline__ void shade_walk(const FrameConst& fc, const Buffers& B, int px0,
                                            int py0, const uint32_t* tri_l, const uint32_t* mask_l,
                                            uint32_t n, PixelOut& o,
@@ -1607,7 +1620,7 @@ __device__ __forceinline__ void shade_walk(const FrameConst& fc, const Buffers& 
         col = shade_decoded_bf(fc, B, tri, px, py, &qd);
       } else {
         double depth;
-        col = shade_sample(fc, B, tri, px, py, &depth);
+        col = shade_sample<kTex>(fc, B, tri, px, py, &depth);
         qd = quantize_depth(depth);
       }
       key = sample_key(fc, qd, tri);
@@ -1661,7 +1674,7 @@ __device__ __forceinline__ void shade_walk(const FrameConst& fc, const Buffers& 
 // reference's per-pixel sequence (raster.cpp:232-267) while a warp step
 // shades up to 32 samples from several triangles (e.g. both triangles of a
 // quad, which are adjacent in the sort order and disjoint).
-template <int KM, typename Filter>
+template <int KM, bool kTex, typename Filter>
 __device__ __forceinline__ void shade_waves(const FrameConst& fc, const Buffers& B, int px0,
                                             int py0, const uint32_t* tri_l,
                                             const uint32_t* mask_l, const uint16_t* slot_l,
@@ -1689,7 +1702,7 @@ __device__ __forceinline__ void shade_waves(const FrameConst& fc, const Buffers&
         col = shade_decoded_bf(fc, B, tri, px, py, &qd);
       } else {
         double depth;
-        col = shade_sample(fc, B, tri, px, py, &depth);
+        col = shade_sample<kTex>(fc, B, tri, px, py, &depth);
         qd = quantize_depth(depth);
       }
       uint64_t pk;
@@ -2231,7 +2244,7 @@ constexpr int kShadeStage = 256;  // THB entries staged per warp; longer lists s
 // half-block without samples), 1 = segment routing for the rest, 2 = alpha
 // threshold walk for all. Separate instantiations keep each path's register
 // allocation small.
-template <int KM, int kMode>
+template <int KM, int kMode, bool kTex>
 __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
   const FrameConst& fc = c_fc;
   __shared__ uint32_t stage_tri[8][kShadeStage];
@@ -2359,7 +2372,7 @@ __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
         slot_l = stage_slot[warp];
       }
       if (kMode == 2)
-        shade_walk<KM, true>(fc, B, hpx0, hpy0, tri_l, mask_l, d.cnt, po, &enumerated);
+        shade_walk<KM, true, kTex>(fc, B, hpx0, hpy0, tri_l, mask_l, d.cnt, po, &enumerated);
       else if (kMode == 0)  // big THBs: wave walk
       {
         if constexpr (KM <= 8) {
@@ -2367,15 +2380,15 @@ __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
           f.reset(reinterpret_cast<float4*>(shade_dyn + (size_t)kStageTris * sizeof(StagedTri)) +
                   (size_t)warp * KM * 32 + lane);
           if (staged_ok && d.cnt <= (uint32_t)kShadeStage)  // all operands in shared memory
-            shade_waves<KM>(fc, B, hpx0, hpy0, stage_tri[warp], stage_mask[warp], stage_slot[warp],
+            shade_waves<KM, kTex>(fc, B, hpx0, hpy0, stage_tri[warp], stage_mask[warp], stage_slot[warp],
                             row_tris, d.cnt, po, f);
           else
-            shade_waves<KM>(fc, B, hpx0, hpy0, tri_l, mask_l, slot_l, staged_ok ? row_tris : nullptr,
+            shade_waves<KM, kTex>(fc, B, hpx0, hpy0, tri_l, mask_l, slot_l, staged_ok ? row_tris : nullptr,
                             d.cnt, po, f);
         } else {
           RegFilter<KM> f;
           f.reset();
-          shade_waves<KM>(fc, B, hpx0, hpy0, tri_l, mask_l, slot_l, staged_ok ? row_tris : nullptr,
+          shade_waves<KM, kTex>(fc, B, hpx0, hpy0, tri_l, mask_l, slot_l, staged_ok ? row_tris : nullptr,
                           d.cnt, po, f);
         }
       }
@@ -2383,11 +2396,11 @@ __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
         if constexpr (KM <= 8) {
           SlotFilter<KM> f;
           f.reset(reinterpret_cast<float4*>(shade_dyn) + (size_t)warp * KM * 32 + lane);
-          shade_segments<KM>(fc, B, hpx0, hpy0, tri_l, mask_l, pre_l, d.cnt, d.frags, route_s[warp], po, f);
+          shade_segments<KM, kTex>(fc, B, hpx0, hpy0, tri_l, mask_l, pre_l, d.cnt, d.frags, route_s[warp], po, f);
         } else {
           RegFilter<KM> f;
           f.reset();
-          shade_segments<KM>(fc, B, hpx0, hpy0, tri_l, mask_l, pre_l, d.cnt, d.frags, route_s[warp], po, f);
+          shade_segments<KM, kTex>(fc, B, hpx0, hpy0, tri_l, mask_l, pre_l, d.cnt, d.frags, route_s[warp], po, f);
         }
       }
     }
@@ -2533,7 +2546,7 @@ __global__ void __launch_bounds__(128) k_abuffer(Buffers B) {
     }
     if (!found) break;
     double depth;
-    float4 c = shade_sample(fc, B, best_t, px, py, &depth);
+    float4 c = shade_sample<true>(fc, B, best_t, px, py, &depth);
     acc = blend(acc, c);
     hash = (hash ^ best) * kHashPrime;
     ++n;
@@ -2888,53 +2901,63 @@ void launch_extract(DeviceScene* d, const dev::FrameConst& fc, const dev::Buffer
   *launches += 2;
 }
 
-template <int KM, int kMode>
+template <int KM, int kMode, bool kTex>
 void launch_shade_mode(DeviceScene* d, const dev::FrameConst& fc, const dev::Buffers& B,
                        int* launches) {
   const size_t dyn = (kMode == 0 ? size_t(dev::kStageTris) * sizeof(dev::StagedTri) : 0) +
                      (kMode != 2 && KM <= 8 ? size_t(8) * KM * 32 * sizeof(float4) : 0);
   static bool configured = false;  // per instantiation
   if (!configured && dyn) {
-    ck(cudaFuncSetAttribute(dev::k_shade<KM, kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    ck(cudaFuncSetAttribute(dev::k_shade<KM, kMode, kTex>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             int(dyn)),
        "cudaFuncSetAttribute");
     configured = true;
   }
   static int per_sm = -1;  // per instantiation (same on every B200)
-  if (per_sm < 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_shade<KM, kMode>, 256, dyn);
+  if (per_sm < 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_shade<KM, kMode, kTex>, 256, dyn);
   const long long items = kMode == 1 ? ((long long)fc.nbins * 32 + 7) / 8 : (long long)fc.nbins;
   const int grid = int(std::max<long long>(1, std::min<long long>((long long)std::max(1, per_sm) * d->sm_count,
                                                                    items)));
-  dev::k_shade<KM, kMode><<<grid, 256, dyn, d->stream>>>(B);
+  dev::k_shade<KM, kMode, kTex><<<grid, 256, dyn, d->stream>>>(B);
   ck(cudaGetLastError(), "k_shade launch");
   ++*launches;
 }
 
-template <int KM>
+template <int KM, bool kTex>
 void launch_shade_km(DeviceScene* d, const dev::FrameConst& fc, const dev::Buffers& B,
                      int* launches) {
   if (fc.threshold) {
-    launch_shade_mode<KM, 2>(d, fc, B, launches);
+    launch_shade_mode<KM, 2, kTex>(d, fc, B, launches);
   } else {
-    launch_shade_mode<KM, 0>(d, fc, B, launches);
-    launch_shade_mode<KM, 1>(d, fc, B, launches);
+    launch_shade_mode<KM, 0, kTex>(d, fc, B, launches);
+    launch_shade_mode<KM, 1, kTex>(d, fc, B, launches);
   }
 }
 
-void launch_shade(DeviceScene* d, const dev::FrameConst& fc, const dev::Buffers& B, int* launches) {
+template <bool kTex>
+void launch_shade_tex(DeviceScene* d, const dev::FrameConst& fc, const dev::Buffers& B, int* launches) {
   const int df = fc.df;
   // KM == df exactly up to 8 (the filter capacity is then a compile-time constant)
-  if (df == 1) launch_shade_km<1>(d, fc, B, launches);
-  else if (df == 2) launch_shade_km<2>(d, fc, B, launches);
-  else if (df == 3) launch_shade_km<3>(d, fc, B, launches);
-  else if (df == 4) launch_shade_km<4>(d, fc, B, launches);
-  else if (df == 5) launch_shade_km<5>(d, fc, B, launches);
-  else if (df == 6) launch_shade_km<6>(d, fc, B, launches);
-  else if (df == 7) launch_shade_km<7>(d, fc, B, launches);
-  else if (df == 8) launch_shade_km<8>(d, fc, B, launches);
-  else if (df <= 16) launch_shade_km<16>(d, fc, B, launches);
-  else if (df <= 32) launch_shade_km<32>(d, fc, B, launches);
+  if (df == 1) launch_shade_km<1, kTex>(d, fc, B, launches);
+  else if (df == 2) launch_shade_km<2, kTex>(d, fc, B, launches);
+  else if (df == 3) launch_shade_km<3, kTex>(d, fc, B, launches);
+  else if (df == 4) launch_shade_km<4, kTex>(d, fc, B, launches);
+  else if (df == 5) launch_shade_km<5, kTex>(d, fc, B, launches);
+  else if (df == 6) launch_shade_km<6, kTex>(d, fc, B, launches);
+  else if (df == 7) launch_shade_km<7, kTex>(d, fc, B, launches);
+  else if (df == 8) launch_shade_km<8, kTex>(d, fc, B, launches);
+  else if (df <= 16) launch_shade_km<16, kTex>(d, fc, B, launches);
+  else if (df <= 32) launch_shade_km<32, kTex>(d, fc, B, launches);
   else throw Error(VEIL_ERR_INVALID_ARG, "depth_filter_size above 32 is not supported on the device path");
+}
+
+// Scenes with textured materials get the shading kernels compiled with the
+// texture path; the others keep it out of their register allocation.
+void launch_shade(DeviceScene* d, const dev::FrameConst& fc, const dev::Buffers& B, int* launches) {
+  if (d->textured)
+    launch_shade_tex<true>(d, fc, B, launches);
+  else
+    launch_shade_tex<false>(d, fc, B, launches);
 }
 
 template <typename T>
