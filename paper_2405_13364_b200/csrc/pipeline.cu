@@ -87,6 +87,11 @@ struct FrameConst {
   int sort_bins;  // host-side: canonical bin-list order (k_bin_sort) this frame
   int walk_min;   // experiment override of kWalkMinSamplesPerThb (VEIL_WALK_MIN), 0 = default
   int walk_min_u; // the same for bins whose triangles are not staged (VEIL_WALK_MIN_U)
+  // zero-copy readback: the frame's pinned host RGBA8 / mask (device-mapped),
+  // written by the shading kernels next to the device framebuffer; null when
+  // the caller does not want host pixels
+  uint32_t* host_fb;
+  uint8_t* host_mask;
 };
 
 // Frame constants live in constant memory, written once per frame by a
@@ -2418,6 +2423,10 @@ __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
       }
       B.fb[pix] = word;
       B.mask[pix] = po.invalid ? 1 : 0;
+      if (fc.host_fb) {  // over the host link, overlapped with the rest of the frame
+        fc.host_fb[pix] = word;
+        fc.host_mask[pix] = po.invalid ? 1 : 0;
+      }
       if (fc.dump) {
         B.hash[pix] = po.hash;
         B.emit[pix] = po.emitted;
@@ -3444,8 +3453,32 @@ void render_frame(const Scene& s, const RenderOptions& opt, RenderOutput* out) {
     const char* e = std::getenv("VEIL_NO_GRAPH");
     return !(e && *e && *e != '0');
   }();
+  static const bool zero_copy_enabled = [] {
+    const char* e = std::getenv("VEIL_NO_ZEROCOPY");
+    return !(e && *e && *e != '0');
+  }();
+  // Zero-copy readback: the shading kernels write the final pixels straight
+  // into the render's pinned host frame (device-mapped), so the transfer
+  // overlaps the frame instead of following it.
+  const size_t npx_frame = size_t(s.camera.width) * s.camera.height;
+  std::shared_ptr<uint8_t> zc;
+  uint8_t* zc_dev = nullptr;
+  if (zero_copy_enabled && opt.host_readback && !opt.dump && opt.world_size <= 1) {
+    zc = acquire_host_frame(npx_frame * 5);
+    void* dp = nullptr;
+    if (cudaHostGetDevicePointer(&dp, zc.get(), 0) == cudaSuccess) {
+      zc_dev = static_cast<uint8_t*>(dp);
+    } else {
+      cudaGetLastError();
+      zc.reset();
+    }
+  }
   for (int attempt = 0; attempt < 8; ++attempt) {
     Prepared P = prepare(d, s, opt);
+    if (zc_dev) {
+      P.fc.host_fb = reinterpret_cast<uint32_t*>(zc_dev);
+      P.fc.host_mask = zc_dev + npx_frame * 4;
+    }
     int launches = 0;
     if (graphs_enabled && !opt.dump) {
       // One graph launch per frame. Everything a launch configuration or a
@@ -3460,6 +3493,8 @@ void render_frame(const Scene& s, const RenderOptions& opt, RenderOutput* out) {
       std::memset(kf.light, 0, sizeof kf.light);
       std::memset(kf.bg, 0, sizeof kf.bg);
       kf.ambient = 0;
+      kf.host_fb = nullptr;  // per-frame host frame: in c_fc, not the graph
+      kf.host_mask = nullptr;
       std::memcpy(key.data(), &P.B, sizeof(dev::Buffers));
       std::memcpy(key.data() + sizeof(dev::Buffers), &kf, sizeof kf);
       uint32_t extra[3] = {P.nblocks, P.gcap_tbr, P.gcap_tb};
@@ -3580,7 +3615,9 @@ void render_frame(const Scene& s, const RenderOptions& opt, RenderOutput* out) {
       dump_put(out, "emit_count", P.B.emit, npx, d->stream);
       ck(cudaStreamSynchronize(d->stream), "dump");
     }
-    if (opt.host_readback || opt.dump) {
+    if (zc) {
+      out->host = zc;  // already written by the kernels
+    } else if (opt.host_readback || opt.dump) {
       const size_t npx = size_t(s.camera.width) * s.camera.height;
       out->host = acquire_host_frame(npx * 5);
       ck(cudaMemcpyAsync(out->rgba(), P.B.fb, npx * 4, cudaMemcpyDeviceToHost, d->stream), "readback");
