@@ -425,6 +425,11 @@ def run_ours(args):
                        "sample": f"{ref['frames']} full frame(s) of {cfg['workload']} via the "
                                  f"reference's veil_render_scene (oracle/_ref), "
                                  f"{ref['ms_per_frame']:.1f} ms/frame"}
+                # the reference is also timed with one worker thread
+                one = cpu_reference_run(arrays, 3, min(6.0, args.cpu_seconds), 1, camera_fn)
+                if one:
+                    cpu["single_thread"] = {"value": one["gfrag_s"], "ms_per_frame": one["ms_per_frame"],
+                                            "frames": one["frames"]}
         clk = clocks.summary()
         result = {
             "metric": METRIC,
