@@ -210,6 +210,20 @@ __device__ __forceinline__ float lut_n(uint32_t w, int shift) {
   return __ldg(&g_lut_n[q + 512]);
 }
 
+// Shared-memory copies of the tables for the shading kernels (per-sample
+// unpacking on the generic path); filled by load_shared_luts at kernel start.
+__shared__ float s_lut_c[256];
+__shared__ float s_lut_n[1024];
+__device__ __forceinline__ void load_shared_luts() {
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) s_lut_c[i] = g_lut_c[i];
+  for (int i = threadIdx.x; i < 1024; i += blockDim.x) s_lut_n[i] = g_lut_n[i];
+}
+__device__ __forceinline__ float slut_c(uint32_t w, int shift) { return s_lut_c[(w >> shift) & 0xffu]; }
+__device__ __forceinline__ float slut_n(uint32_t w, int shift) {
+  const int32_t q = (int32_t)(((w >> shift) & 0x3ffu) << 22) >> 22;
+  return s_lut_n[q + 512];
+}
+
 // ------------------------------------------------------------ setup
 
 __device__ __forceinline__ void load_quad(const Buffers& B, uint32_t q, uint4* idx,
@@ -1255,8 +1269,8 @@ __device__ __forceinline__ float4 shade_sample(const FrameConst& fc, const Buffe
     float r[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k)
-      r[k] = __fadd_rn(__fadd_rn(__fmul_rn(lut_c(w0, 8 * k), b0), __fmul_rn(lut_c(w1, 8 * k), b1)),
-                       __fmul_rn(lut_c(w2, 8 * k), b2));
+      r[k] = __fadd_rn(__fadd_rn(__fmul_rn(slut_c(w0, 8 * k), b0), __fmul_rn(slut_c(w1, 8 * k), b1)),
+                       __fmul_rn(slut_c(w2, 8 * k), b2));
     color = make_float4(r[0], r[1], r[2], r[3]);
   }
   float n[3];
@@ -1265,11 +1279,11 @@ __device__ __forceinline__ float4 shade_sample(const FrameConst& fc, const Buffe
     const uint32_t w0 = c.x, w1 = ltri == 0 ? c.y : c.z, w2 = ltri == 0 ? c.z : c.w;
 #pragma unroll
     for (int k = 0; k < 3; ++k)
-      n[k] = __fadd_rn(__fadd_rn(__fmul_rn(lut_n(w0, 10 * k), b0), __fmul_rn(lut_n(w1, 10 * k), b1)),
-                       __fmul_rn(lut_n(w2, 10 * k), b2));
+      n[k] = __fadd_rn(__fadd_rn(__fmul_rn(slut_n(w0, 10 * k), b0), __fmul_rn(slut_n(w1, 10 * k), b1)),
+                       __fmul_rn(slut_n(w2, 10 * k), b2));
   } else {
 #pragma unroll
-    for (int k = 0; k < 3; ++k) n[k] = lut_n(meta.x, 10 * k);
+    for (int k = 0; k < 3; ++k) n[k] = slut_n(meta.x, 10 * k);
   }
   const MatDev& m = B.mats[meta.y];
   const float4 mat = make_float4(__ldg(&m.base[0]), __ldg(&m.base[1]), __ldg(&m.base[2]), __ldg(&m.opacity));
@@ -2252,6 +2266,8 @@ constexpr int kShadeStage = 256;  // THB entries staged per warp; longer lists s
 template <int KM, int kMode, bool kTex>
 __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
   const FrameConst& fc = c_fc;
+  load_shared_luts();
+  __syncthreads();
   __shared__ uint32_t stage_tri[8][kShadeStage];
   __shared__ uint32_t stage_mask[8][kShadeStage];
   __shared__ uint32_t stage_pre[8][kShadeStage];
@@ -2523,6 +2539,8 @@ __global__ void __launch_bounds__(256) k_finalize(Buffers B) {
 // per-pixel list storage is needed (an oracle mode, not a fast path).
 __global__ void __launch_bounds__(128) k_abuffer(Buffers B) {
   const FrameConst& fc = c_fc;
+  load_shared_luts();
+  __syncthreads();
   if (B.ctr->error) return;
   const int px = blockIdx.x * 16 + (threadIdx.x & 15);
   const int py = blockIdx.y * 8 + (threadIdx.x >> 4);
