@@ -1,31 +1,30 @@
 // libveil device pipeline: sort-middle exact-OIT frame render on sm_100a.
 //
 // Stage map (reference -> kernel):
-//   setup phase 1 + compaction   setup.cpp:255-302   k_setup_count, k_scan_blocks
-//   setup phase 2 (records)      setup.cpp:305-349   k_setup_write
-//   binning count / offsets      binning.cpp:124-145 k_bin_count, k_bin_scan
-//   binning write                binning.cpp:147-186 k_bin_scatter, k_bin_sort
-//   bin rasterization low/high   raster.cpp:41-335,  k_raster<kGlobal>
-//                                renderer.cpp:117-165
+//   setup phase 1 + compaction   setup.cpp:255-302    k_setup (single pass, decoupled look-back)
+//   setup phase 2 (records)      setup.cpp:305-349    k_setup_tris
+//   binning count / offsets      binning.cpp:124-145  k_bin_pass<false>, k_bin_large<false>, k_bin_scan
+//   binning write                binning.cpp:147-186  k_bin_pass<true>, k_bin_large<true>
+//                                                     (+ k_bin_sort for parity dumps)
+//   tri-block rows / THB lists   raster.cpp:41-199    k_extract<kGlobal> (low pass, high pass)
+//   shading, filter, blend       raster.cpp:201-321   k_order_bins, k_shade<KM, mode, kTex>
 //   stats merge                  renderer.cpp:170-212 k_finalize
 //
 // Design notes (DESIGN.md has the full version):
-//  * Setup is two passes over the quad stream (count, then recompute+write)
-//    with a block-offset scan in between, so visible quads land in ascending
-//    input order without a per-quad intermediate array.
-//  * Per-bin lists are filled with warp-aggregated atomics and then sorted
-//    per bin, giving the reference's order (small quads ascending, then large
-//    triangles ascending, binning.cpp:147-166).
-//  * The rasterizer is a persistent kernel over (bin, block-row) work items.
-//    A CTA of 4 warps builds the block-row's tri-block-rows in shared
-//    memory; warp w then owns block w of the row: it sorts the block's
-//    tri-blocks by (quantized centroid depth, is_large, triangle) -- the
-//    same order as the reference's (depth, selection index) key because
-//    selection index is monotone in (is_large, triangle) -- splits them into
-//    tri-half-blocks and shades both half-blocks with lane == pixel, keeping
-//    the depth filter in registers.
-//  * Items that do not fit the shared-memory capacities but are within the
-//    rasterizer limits are re-run by the same kernel with global scratch.
+//  * One frame is one CUDA graph replay; frame constants live in __constant__
+//    memory written by the graph's first node from pinned staging.
+//  * Per-bin lists are filled with warp-aggregated atomics in any order: the
+//    extraction orders tri-blocks by (quantized centroid depth, is_large,
+//    triangle), the same order as the reference's (depth, selection index)
+//    because the selection index is monotone in (is_large, triangle).
+//  * k_extract is a persistent kernel over (bin, block-row) items: a CTA of 4
+//    warps builds the block-row's tri-block-rows in shared memory, then warp
+//    w sorts block w's tri-blocks and splits them into tri-half-blocks (THB
+//    pool). It also decides, per half-block, wave walk (k_shade mode 0:
+//    lane = pixel, disjoint consecutive THBs per step) or dense segments
+//    (mode 1: lane = sample, warp routing) and queues the latter.
+//  * Items over the shared-memory capacities but within the rasterizer
+//    limits are re-run by the same kernel with global scratch.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -191,7 +190,7 @@ struct Buffers {
   uint32_t* pool_mask;  // coverage, bit = ly * 8 + lx
   uint32_t* pool_pre;   // exclusive fragment prefix
   uint32_t* seg_queue;  // half-blocks for the segment kernel: bin * 32 + hb, bit 31 = high pass
-  uint16_t* pool_slot;  // per THB: row-local triangle slot (index into the row list)
+  uint16_t* pool_slot;  // per THB: the triangle's position in the bin list (k_shade staging slot)
   uint2* lpairs;        // (large triangle, bin row) pairs for k_bin_large
   Counters* ctr;
 };
@@ -2272,7 +2271,7 @@ __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
   __shared__ uint32_t stage_mask[8][kShadeStage];
   __shared__ uint32_t stage_pre[8][kShadeStage];
   __shared__ uint16_t stage_slot[8][kShadeStage];
-  extern __shared__ __align__(16) uint8_t shade_dyn[];  // mode 0: staged row triangles
+  extern __shared__ __align__(16) uint8_t shade_dyn[];  // staged bin triangles, filter slots
   StagedTri* row_tris = reinterpret_cast<StagedTri*>(shade_dyn);
   __shared__ uint32_t route_s[8][32];
   __shared__ uint32_t item_s;
