@@ -116,6 +116,7 @@ struct Counters {
   unsigned int large_pairs;  // (large triangle, bin row) work pairs
   unsigned int setup_ticket;  // k_setup: block order for the decoupled look-back
   unsigned int list_count[2];  // owned bins to extract in the low / high pass
+  unsigned int order_count;    // bins in k_shade's (mode 0/2) order list
 };
 
 // Decoded per-triangle shading inputs (unpack_color / decode_normal of the
@@ -2160,7 +2161,10 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
     B.hbd[hbi] = d;
     const uint32_t cost = seg ? 0u : min(d.frags + 4u * d.cnt, 0x00ffffffu);
     const uint32_t both = cost + __shfl_down_sync(0x3u, cost, 1);  // the block's two halves
-    if (lane == 0 && both) atomicAdd(&B.bin_cost[bin], both);
+    const unsigned walks = __ballot_sync(0x3u, !seg);
+    // bit 31: the bin has half-blocks for k_shade's wave walk (or background)
+    if (lane == 0 && (both || walks)) atomicAdd(&B.bin_cost[bin], both);
+    if (lane == 0 && walks) atomicOr(&B.bin_cost[bin], 0x80000000u);
     // low-pass entries of a bin that later propagates are stale (k_shade_seg skips them)
     if (seg) B.seg_queue[atomicAdd(&B.ctr->seg_count, 1u)] = hbi | (pass == kPassLow ? 0u : 0x80000000u);
   }
@@ -2281,7 +2285,7 @@ __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
   __shared__ uint8_t hb_order[32];  // the bin's half-blocks, most samples first
   // modes 0/2: CTA items = bins, warps pull the bin's 32 half-blocks;
   // mode 1: warp items from the queue mode 0 filled
-  const uint32_t nitems = kMode == 1 ? B.ctr->seg_count : (uint32_t)fc.nbins;
+  const uint32_t nitems = kMode == 1 ? B.ctr->seg_count : B.ctr->order_count;
   uint32_t cta_bin = 0xffffffffu;
   bool staged_ok = false;
   for (;;) {
@@ -2482,7 +2486,16 @@ __global__ void __launch_bounds__(1024) k_order_bins(Buffers B) {
     const uint32_t m = e >= 3 ? (c >> (e - 3)) & 7u : (c << (3 - e)) & 7u;
     return 255u - min(254u, e * 8u + m);
   };
-  for (int b = threadIdx.x; b < fc.nbins; b += blockDim.x) atomicAdd(&hist[bucket(B.bin_cost[b])], 1u);
+  // bins with no wave-walk work (every half-block queued for the segment
+  // kernel) and bins another rank owns are left out; empty bins stay (their
+  // half-blocks get the background)
+  auto wanted = [&](int b) {
+    const int bxi = b % fc.bins_x, byi = b / fc.bins_x;
+    if (fc.world > 1 && ((bxi + 3 * byi) % fc.world) != fc.rank) return false;
+    return B.cat[b] == 0 || (B.bin_cost[b] & 0x80000000u) != 0u;
+  };
+  for (int b = threadIdx.x; b < fc.nbins; b += blockDim.x)
+    if (wanted(b)) atomicAdd(&hist[bucket(B.bin_cost[b] & 0x7fffffffu)], 1u);
   __syncthreads();
   if (threadIdx.x < 32) {  // exclusive scan of 256 buckets by one warp
     uint32_t run = 0;
@@ -2497,10 +2510,11 @@ __global__ void __launch_bounds__(1024) k_order_bins(Buffers B) {
       base[k * 32 + threadIdx.x] = run + x - v;
       run += __shfl_sync(0xffffffffu, x, 31);
     }
+    if (threadIdx.x == 0) B.ctr->order_count = run;
   }
   __syncthreads();
   for (int b = threadIdx.x; b < fc.nbins; b += blockDim.x)
-    B.bin_order[atomicAdd(&base[bucket(B.bin_cost[b])], 1u)] = (uint32_t)b;
+    if (wanted(b)) B.bin_order[atomicAdd(&base[bucket(B.bin_cost[b] & 0x7fffffffu)], 1u)] = (uint32_t)b;
 }
 
 __global__ void __launch_bounds__(256) k_finalize(Buffers B) {
