@@ -190,7 +190,7 @@ struct Buffers {
   uint32_t* pool_tri;
   uint32_t* pool_mask;  // coverage, bit = ly * 8 + lx
   uint32_t* pool_pre;   // exclusive fragment prefix
-  uint32_t* seg_queue;  // half-blocks for the segment kernel: bin * 32 + hb, bit 31 = high pass
+  uint4* seg_queue;  // half-blocks for the segment kernel: (bin * 32 + hb | high pass << 31, off, cnt, frags)
   uint16_t* pool_slot;  // per THB: the triangle's position in the bin list (k_shade staging slot)
   uint2* lpairs;        // (large triangle, bin row) pairs for k_bin_large
   Counters* ctr;
@@ -2166,7 +2166,9 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
     if (lane == 0 && (both || walks)) atomicAdd(&B.bin_cost[bin], both);
     if (lane == 0 && walks) atomicOr(&B.bin_cost[bin], 0x80000000u);
     // low-pass entries of a bin that later propagates are stale (k_shade_seg skips them)
-    if (seg) B.seg_queue[atomicAdd(&B.ctr->seg_count, 1u)] = hbi | (pass == kPassLow ? 0u : 0x80000000u);
+    if (seg)
+      B.seg_queue[atomicAdd(&B.ctr->seg_count, 1u)] =
+          make_uint4(hbi | (pass == kPassLow ? 0u : 0x80000000u), d.off, d.cnt, d.frags);
   }
   if (threadIdx.x == 0) {
     unsigned long long* slot = B.slots + ((size_t)bin * 4 + row) * 5;
@@ -2288,16 +2290,21 @@ __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
   const uint32_t nitems = kMode == 1 ? B.ctr->seg_count : B.ctr->order_count;
   uint32_t cta_bin = 0xffffffffu;
   bool staged_ok = false;
+  uint32_t seg_ticket = 0;
+  HbDesc seg_desc = {0, 0, 0, 0};
+  if (kMode == 1 && lane == 0) seg_ticket = atomicAdd(&B.ctr->shade_next[1], 1u);
   for (;;) {
     uint32_t item;
     if (kMode == 1) {
-      item = 0;
-      if (lane == 0) item = atomicAdd(&B.ctr->shade_next[1], 1u);
-      item = __shfl_sync(0xffffffffu, item, 0);
-      if (item >= nitems) break;
-      item = B.seg_queue[item];
-      if (!(item & 0x80000000u) && B.prop[item >> 5]) continue;  // stale low-pass entry
+      // the ticket for the next entry is taken one iteration ahead (lane 0)
+      const uint32_t t = __shfl_sync(0xffffffffu, seg_ticket, 0);
+      if (t >= nitems) break;
+      if (lane == 0) seg_ticket = atomicAdd(&B.ctr->shade_next[1], 1u);
+      const uint4 e = B.seg_queue[t];
+      item = e.x;
+      if (!(item & 0x80000000u) && B.prop[(item & 0x7fffffffu) >> 5]) continue;  // stale low-pass entry
       item &= 0x7fffffffu;
+      seg_desc = HbDesc{e.y, e.z, e.w, 1u};
     } else {
       // next half-block of the CTA's bin, or the next bin
       int hbi = 32;
@@ -2372,9 +2379,15 @@ __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
     po.hash = kHashSeed;
     po.emitted = 0;
     unsigned long long enumerated = 0;
-    bool live = B.cat[bin] != 0;
+    bool live;
     HbDesc d = {0, 0, 0, 0};
-    if (live) d = B.hbd[(size_t)bin * 32 + hb];
+    if (kMode == 1) {  // queued entries carry their descriptor
+      live = true;
+      d = seg_desc;
+    } else {
+      live = B.cat[bin] != 0;
+      if (live) d = B.hbd[(size_t)bin * 32 + hb];
+    }
     if (kMode == 0 && live && d.pad) continue;  // queued for the segment kernel by k_extract
     if (live) {
       enumerated = d.frags;
@@ -3143,7 +3156,7 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   }
   d->ctr.ensure(sizeof(dev::Counters));
   d->hbd.ensure(nb * 32 * sizeof(dev::HbDesc));
-  d->seg_queue.ensure(nb * 32 * 4);
+  d->seg_queue.ensure(nb * 32 * 16);
   if (d->lpairs_cap == 0)
     d->lpairs_cap = init_cap ? init_cap : std::max<uint32_t>(1u << 16, std::min<uint32_t>(Q * 2u, 1u << 26));
   d->lpairs.ensure(size_t(d->lpairs_cap) * sizeof(uint2));
@@ -3227,7 +3240,7 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   B.pool_tri = d->pool_tri.as<uint32_t>();
   B.pool_mask = d->pool_mask.as<uint32_t>();
   B.pool_pre = d->pool_pre.as<uint32_t>();
-  B.seg_queue = d->seg_queue.as<uint32_t>();
+  B.seg_queue = d->seg_queue.as<uint4>();
   B.pool_slot = d->pool_slot.as<uint16_t>();
   B.lpairs = d->lpairs.as<uint2>();
   B.lpair_cols = d->lpair_cols.as<uint32_t>();
