@@ -1262,9 +1262,12 @@ __device__ __forceinline__ float4 shade_sample(const FrameConst& fc, const Buffe
   const uint32_t q = tri >> 1;
   const uint32_t qf = __ldg(&B.vq_flags[q]);
   const int ltri = (int)(meta.w & 0xffu);
+  // corner attributes loaded with the flags (one round trip; unused when the
+  // quad has none)
+  const uint4 qcol = __ldg(&B.vq_col[q]), qnrm = __ldg(&B.vq_nrm[q]);
   float4 color = make_float4(1.0f, 1.0f, 1.0f, 1.0f);
   if (qf & 2u) {
-    const uint4 c = __ldg(&B.vq_col[q]);
+    const uint4 c = qcol;
     const uint32_t w0 = c.x, w1 = ltri == 0 ? c.y : c.z, w2 = ltri == 0 ? c.z : c.w;
     float r[4];
 #pragma unroll
@@ -1275,7 +1278,7 @@ __device__ __forceinline__ float4 shade_sample(const FrameConst& fc, const Buffe
   }
   float n[3];
   if (qf & 4u) {
-    const uint4 c = __ldg(&B.vq_nrm[q]);
+    const uint4 c = qnrm;
     const uint32_t w0 = c.x, w1 = ltri == 0 ? c.y : c.z, w2 = ltri == 0 ? c.z : c.w;
 #pragma unroll
     for (int k = 0; k < 3; ++k)
