@@ -672,7 +672,10 @@ __device__ __forceinline__ uint32_t block_rows_mask(uint32_t yy, int by, int hei
 template <bool kWrite>
 __global__ void __launch_bounds__(256) k_bin_pass(Buffers B) {
   const FrameConst& fc = c_fc;
+  __shared__ unsigned int n_small, n_large;  // per-block counts, one global atomic each
   if (B.ctr->error) return;
+  if (threadIdx.x == 0) n_small = n_large = 0;
+  __syncthreads();
   const uint32_t nvis = B.ctr->nvis;
   for (uint32_t base = blockIdx.x * 256; base < nvis; base += gridDim.x * 256) {
     uint32_t q = base + threadIdx.x;
@@ -685,7 +688,7 @@ __global__ void __launch_bounds__(256) k_bin_pass(Buffers B) {
     uint32_t nb = small ? (x1 - x0 + 1) * (y1 - y0 + 1) : 0u;
     if (!kWrite) {
       unsigned sm = __ballot_sync(0xffffffffu, small);
-      if ((threadIdx.x & 31) == 0 && sm) atomicAdd(&B.ctr->small_quads, (unsigned long long)__popc(sm));
+      if ((threadIdx.x & 31) == 0 && sm) atomicAdd(&n_small, (unsigned)__popc(sm));
     }
     if (!kWrite && in && (flags & 1u)) {
       // large quad: one (triangle, bin row) pair per bin row of each valid
@@ -695,7 +698,7 @@ __global__ void __launch_bounds__(256) k_bin_pass(Buffers B) {
         if (!(B.tri_meta[ti].w & 0x100u)) continue;
         const uint32_t yy = B.tri_y[ti];
         const int y_lo = (int)(int16_t)(yy & 0xffffu), y_hi = (int)(int16_t)(yy >> 16);
-        atomicAdd(&B.ctr->large_tris, 1ull);
+        atomicAdd(&n_large, 1u);
         if (y_lo > y_hi) continue;
         const uint32_t r0 = (uint32_t)y_lo / kBin, nr = (uint32_t)y_hi / kBin - r0 + 1u;
         const uint32_t at = atomicAdd(&B.ctr->large_pairs, nr);
@@ -725,6 +728,13 @@ __global__ void __launch_bounds__(256) k_bin_pass(Buffers B) {
           warp_agg_add(B.qcnt, bin, act, nullptr);
         }
       }
+    }
+  }
+  if (!kWrite) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (n_small) atomicAdd(&B.ctr->small_quads, (unsigned long long)n_small);
+      if (n_large) atomicAdd(&B.ctr->large_tris, (unsigned long long)n_large);
     }
   }
 }
