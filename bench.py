@@ -52,6 +52,9 @@ def parse():
     ap.add_argument("--single-device", action="store_true",
                     help="every rank on cuda:0 (orchestration tests with --dist-backend gloo; "
                          "ranks never wait on each other inside kernels)")
+    ap.add_argument("--gather", default="peer", choices=["peer", "nccl"],
+                    help="N>1: sharded ranks write into rank 0's framebuffer over NVLink (CUDA IPC, "
+                         "'peer') or pack tiles for an NCCL gather ('nccl')")
     ap.add_argument("--check-frame", action="store_true",
                     help="rank 0 compares the gathered frame with an unsharded render")
     return ap.parse_args()
@@ -267,6 +270,24 @@ def run_ours(args):
     gathered = ([torch.empty_like(tiles, device=cdev) for _ in range(world)]
                 if (world > 1 and rank == 0) else None)
 
+    peer = False
+    if world > 1 and args.gather == "peer":
+        # rank 0's framebuffer as CUDA IPC handles; the other ranks' shading
+        # kernels then write their finished pixels straight into it
+        blob = [veil.export_framebuffer(scene) if rank == 0 else None]
+        dist.broadcast_object_list(blob, src=0)
+        try:
+            if rank != 0:
+                veil.import_peer_framebuffer(scene, blob[0])
+            ok = 1
+        except veil.VeilError:
+            ok = 0
+        okt = torch.tensor([ok], dtype=torch.int32, device=cdev)
+        dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+        peer = bool(okt.item())
+        if not peer and rank != 0:
+            veil.import_peer_framebuffer(scene, None)
+
     def frame(i, timed_events=None):
         if camera_fn:
             m, eye = camera_fn(i)
@@ -274,6 +295,13 @@ def run_ours(args):
         if timed_events:
             timed_events[0].record(stream)
         st = veil.render_device(scene, params, shard)
+        if peer:
+            # every rank's pixels are in rank 0's framebuffer once all ranks'
+            # frames completed (render_device synchronises its stream)
+            if timed_events:
+                timed_events[1].record(stream)
+            dist.barrier()
+            return st
         if world > 1:
             veil.pack_tiles_device(scene, rank, world, tiles.data_ptr(), tiles.numel())
             with torch.cuda.stream(stream):
@@ -444,7 +472,9 @@ def run_ours(args):
             "vs_baseline": None,
             "dtype": "f64+f32",
             "data": "synthetic",
-            "config": dict(cfg, parallelism=f"bins interleaved over {world} GPU(s), setup replicated",
+            "config": dict(cfg, parallelism=f"bins interleaved over {world} GPU(s), setup replicated"
+                                              + (", peer-memory framebuffer gather" if peer else
+                                                 (", NCCL tile gather" if world > 1 else "")),
                            fragments_per_frame=int(fragments_per_frame),
                            l2="flushed between timed frames (256 MiB write, outside the events)"),
             "e2e": e2e,

@@ -129,6 +129,22 @@ veil_status veil_shard_pack_tiles_device(const veil_scene* scene, const veil_sha
 veil_status veil_shard_unpack_tiles_device(const veil_scene* scene, const veil_shard* shard,
                                            const void* dev_tiles, uint64_t bytes);
 
+/* Peer framebuffer gather (one process per GPU on one node): the root rank
+ * (shard rank 0) exports its device framebuffer as CUDA IPC handles; every
+ * other rank imports them, after which its sharded frames also write their
+ * finished pixels straight into the root's framebuffer over NVLink during
+ * shading -- no pack, collective or unpack. The caller orders frames with a
+ * host barrier after each rank's frame. Import NULL to detach. */
+typedef struct veil_ipc_framebuffer {
+  uint8_t rgba[64];
+  uint8_t mask[64];
+  int32_t width;
+  int32_t height;
+} veil_ipc_framebuffer;
+
+veil_status veil_export_framebuffer(const veil_scene* scene, veil_ipc_framebuffer* out);
+veil_status veil_import_peer_framebuffer(const veil_scene* scene, const veil_ipc_framebuffer* fb);
+
 /* ---- device-resident frame loop ------------------------------------------- */
 
 /* Renders into device memory only (no host copies); for benchmarks that time

@@ -96,6 +96,14 @@ class ImageDiff(C.Structure):
     ]
 
 
+class IpcFramebuffer(C.Structure):
+    """veil_ipc_framebuffer (include/veil_cuda.h): CUDA IPC handles of a
+    device framebuffer (RGBA8 and invalid mask) plus its size."""
+
+    _fields_ = [("rgba", C.c_uint8 * 64), ("mask", C.c_uint8 * 64),
+                ("width", C.c_int32), ("height", C.c_int32)]
+
+
 class Shard(C.Structure):
     _fields_ = [("rank", C.c_int32), ("world_size", C.c_int32)]
 

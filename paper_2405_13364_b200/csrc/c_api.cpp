@@ -391,6 +391,16 @@ veil_status veil_shard_unpack_tiles_device(const veil_scene* scene, const veil_s
   });
 }
 
+veil_status veil_export_framebuffer(const veil_scene* scene, veil_ipc_framebuffer* out) {
+  if (!scene || !out) return bad_arg("scene and out are required");
+  return guard([&] { veil::export_framebuffer(scene->s, out); });
+}
+
+veil_status veil_import_peer_framebuffer(const veil_scene* scene, const veil_ipc_framebuffer* fb) {
+  if (!scene) return bad_arg("scene is required");
+  return guard([&] { veil::import_peer_framebuffer(scene->s, fb); });
+}
+
 veil_status veil_device_framebuffer(const veil_scene* scene, void** rgba, void** mask) {
   if (!scene) return bad_arg("scene is required");
   return guard([&] { veil::device_framebuffer(scene->s, rgba, mask); });

@@ -91,6 +91,10 @@ struct FrameConst {
   // the caller does not want host pixels
   uint32_t* host_fb;
   uint8_t* host_mask;
+  // peer gather: the root rank's framebuffer (CUDA IPC, over NVLink); a
+  // sharded rank writes its finished pixels there as well
+  uint32_t* peer_fb;
+  uint8_t* peer_mask;
 };
 
 // Frame constants live in constant memory, written once per frame by a
@@ -2472,6 +2476,10 @@ __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
         fc.host_fb[pix] = word;
         fc.host_mask[pix] = po.invalid ? 1 : 0;
       }
+      if (fc.peer_fb) {  // into the root rank's framebuffer (peer memory)
+        fc.peer_fb[pix] = word;
+        fc.peer_mask[pix] = po.invalid ? 1 : 0;
+      }
       if (fc.dump) {
         B.hash[pix] = po.hash;
         B.emit[pix] = po.emitted;
@@ -2708,6 +2716,8 @@ struct DeviceScene {
   uint32_t pool_cap = 0;
   uint32_t lpairs_cap = 0;
   dev::FrameConst* fc_host = nullptr;  // pinned staging of c_fc (graph memcpy source)
+  void* peer_fb = nullptr;    // imported root framebuffer (cudaIpcOpenMemHandle)
+  void* peer_mask = nullptr;
   dev::Counters* ctr_host = nullptr;   // pinned counters readback
   // Cached CUDA graph of one whole frame (c_fc upload .. counters readback),
   // valid while the launch-shaping inputs in graph_key are unchanged.
@@ -2724,6 +2734,8 @@ struct DeviceScene {
   int raster_ctas_global = 0;
 
   ~DeviceScene() {
+    if (peer_fb) cudaIpcCloseMemHandle(peer_fb);
+    if (peer_mask) cudaIpcCloseMemHandle(peer_mask);
     if (graph_exec) cudaGraphExecDestroy(graph_exec);
     if (fc_host) cudaFreeHost(fc_host);
     if (ctr_host) cudaFreeHost(ctr_host);
@@ -3105,6 +3117,10 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   fc.tri_cap = s.extended ? (1u << 27) : (1u << 24);
   fc.rank = opt.rank;
   fc.world = opt.world_size;
+  if (opt.world_size > 1 && opt.rank != 0 && d->peer_fb) {
+    fc.peer_fb = static_cast<uint32_t*>(d->peer_fb);
+    fc.peer_mask = static_cast<uint8_t*>(d->peer_mask);
+  }
   fc.dump = opt.dump ? 1 : 0;
   // Only the parity dumps need each bin's list in the reference's canonical
   // order: the rasterizer orders tri-blocks by (depth, large, triangle) keys
@@ -3557,6 +3573,8 @@ void render_frame(const Scene& s, const RenderOptions& opt, RenderOutput* out) {
       kf.ambient = 0;
       kf.host_fb = nullptr;  // per-frame host frame: in c_fc, not the graph
       kf.host_mask = nullptr;
+      kf.peer_fb = nullptr;
+      kf.peer_mask = nullptr;
       std::memcpy(key.data(), &P.B, sizeof(dev::Buffers));
       std::memcpy(key.data() + sizeof(dev::Buffers), &kf, sizeof kf);
       uint32_t extra[3] = {P.nblocks, P.gcap_tbr, P.gcap_tb};
@@ -3785,6 +3803,36 @@ void shard_tiles_device(const Scene& s, int rank, int world, void* tiles, uint64
                                                  uint32_t(bins.size()), unpack ? 1 : 0);
   ck(cudaGetLastError(), "k_tile_copy");
   ck(cudaStreamSynchronize(d->stream), "tiles");
+}
+
+void export_framebuffer(const Scene& s, veil_ipc_framebuffer* out) {
+  DeviceScene* d = device_scene(s);
+  const size_t npx = size_t(s.camera.width) * s.camera.height;
+  d->fb.ensure(npx * 4);
+  d->mask.ensure(npx);
+  cudaIpcMemHandle_t h;
+  ck(cudaIpcGetMemHandle(&h, d->fb.p), "cudaIpcGetMemHandle");
+  std::memcpy(out->rgba, &h, sizeof h);
+  ck(cudaIpcGetMemHandle(&h, d->mask.p), "cudaIpcGetMemHandle");
+  std::memcpy(out->mask, &h, sizeof h);
+  out->width = s.camera.width;
+  out->height = s.camera.height;
+}
+
+void import_peer_framebuffer(const Scene& s, const veil_ipc_framebuffer* fb) {
+  DeviceScene* d = device_scene(s);
+  if (d->peer_fb) cudaIpcCloseMemHandle(d->peer_fb);
+  if (d->peer_mask) cudaIpcCloseMemHandle(d->peer_mask);
+  d->peer_fb = d->peer_mask = nullptr;
+  d->graph_key.clear();  // re-capture with the new constants layout
+  if (!fb) return;
+  if (fb->width != s.camera.width || fb->height != s.camera.height)
+    throw Error(VEIL_ERR_INVALID_ARG, "peer framebuffer has another viewport");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, fb->rgba, sizeof h);
+  ck(cudaIpcOpenMemHandle(&d->peer_fb, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+  std::memcpy(&h, fb->mask, sizeof h);
+  ck(cudaIpcOpenMemHandle(&d->peer_mask, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
 }
 
 void device_framebuffer(const Scene& s, void** rgba, void** mask) {

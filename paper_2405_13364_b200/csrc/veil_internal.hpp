@@ -128,6 +128,8 @@ void render_frame(const Scene& scene, const RenderOptions& opt, RenderOutput* ou
 void render_reference_frame(const Scene& scene, const RenderOptions& opt, RenderOutput* out);
 void release_device_scene(DeviceScene* d);
 void device_framebuffer(const Scene& scene, void** rgba, void** mask);
+void export_framebuffer(const Scene& scene, veil_ipc_framebuffer* out);
+void import_peer_framebuffer(const Scene& scene, const veil_ipc_framebuffer* fb);
 void shard_tiles_device(const Scene& scene, int rank, int world, void* tiles, uint64_t bytes,
                         bool unpack);
 void* device_stream(const Scene& scene);

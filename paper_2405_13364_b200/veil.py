@@ -16,6 +16,7 @@ from .abi import (
     DUMP_DTYPES,
     FrameStats,
     ImageDiff,
+    IpcFramebuffer,
     RenderParams,
     SceneArrays,
     SceneDesc,
@@ -90,6 +91,8 @@ def lib():
         "veil_shard_unpack_tiles_device": ([_P, C.POINTER(Shard), _P, C.c_uint64], C.c_int),
         "veil_render_device": ([_P, C.POINTER(RenderParams), C.POINTER(Shard)], C.c_int),
         "veil_device_framebuffer": ([_P, _PP, _PP], C.c_int),
+        "veil_export_framebuffer": ([_P, C.POINTER(IpcFramebuffer)], C.c_int),
+        "veil_import_peer_framebuffer": ([_P, C.POINTER(IpcFramebuffer)], C.c_int),
         "veil_scene_stream": ([_P], C.c_void_p),
         "veil_render_stats": ([_P, C.POINTER(FrameStats)], C.c_int),
         "veil_scene_last_stats": ([_P, C.POINTER(FrameStats)], C.c_int),
@@ -294,6 +297,23 @@ def render_device(scene: Scene, params=None, shard=None):
     sh = None if shard is None else C.byref(Shard(*shard))
     _check(lib().veil_render_device(scene.h, C.byref(params), sh))
     return scene.last_stats()
+
+
+def export_framebuffer(scene: Scene) -> bytes:
+    """The scene's device framebuffer as CUDA IPC handles (root rank)."""
+    fb = IpcFramebuffer()
+    _check(lib().veil_export_framebuffer(scene.h, C.byref(fb)))
+    return bytes(fb)
+
+
+def import_peer_framebuffer(scene: Scene, blob):
+    """Write this rank's sharded frames into the root's framebuffer too
+    (blob from export_framebuffer on the root; None detaches)."""
+    if blob is None:
+        _check(lib().veil_import_peer_framebuffer(scene.h, None))
+        return
+    fb = IpcFramebuffer.from_buffer_copy(blob)
+    _check(lib().veil_import_peer_framebuffer(scene.h, C.byref(fb)))
 
 
 def pack_tiles_device(scene: Scene, rank, world, dev_ptr, nbytes):

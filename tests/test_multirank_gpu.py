@@ -1,7 +1,10 @@
-"""bench.py's multi-rank path on one GPU: two torchrun ranks (gloo through
-host memory, both on cuda:0 -- their kernels never wait on each other) render
-their interleaved bins, pack tiles on the device, gather to rank 0 and unpack;
-rank 0's frame must equal the unsharded render byte for byte."""
+"""bench.py's multi-rank path on one GPU: torchrun ranks (gloo for the host
+collectives, all on cuda:0 -- their kernels never wait on each other) render
+their interleaved bins and either pack tiles for a gather to rank 0 ('nccl'
+path, through host memory under gloo) or write their pixels straight into
+rank 0's framebuffer through CUDA IPC ('peer' path, NVLink peer memory on a
+multi-GPU node); rank 0's frame must equal the unsharded render byte for
+byte."""
 import json
 import os
 import socket
@@ -20,17 +23,21 @@ def _free_port():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world,workload", [(2, "boxes1080"), (3, "stack64k")])
-def test_bench_multirank_frame_identical(world, workload):
+@pytest.mark.parametrize("world,workload,gather", [(2, "boxes1080", "nccl"), (3, "stack64k", "nccl"),
+                                                   (2, "boxes1080", "peer"), (3, "stack64k", "peer")])
+def test_bench_multirank_frame_identical(world, workload, gather):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={world}", "--master-addr", "127.0.0.1",
            "--master-port", str(_free_port()), os.path.join(ROOT, "bench.py"),
            "--gpus", str(world), "--steps", "3", "--warmup", "3", "--workload", workload,
-           "--dist-backend", "gloo", "--single-device", "--check-frame", "--no-cpu-baseline"]
+           "--dist-backend", "gloo", "--single-device", "--check-frame", "--no-cpu-baseline",
+           "--gather", gather]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-3000:]
     line = [l for l in out.stdout.splitlines() if l.startswith("{")][-1]
     res = json.loads(line)
     assert res["n_gpus"] == world
     assert res["frame_check"]["identical"], res["frame_check"]
+    if gather == "peer":  # CUDA IPC between processes on one device works as across NVLink
+        assert "peer-memory" in res["config"]["parallelism"], res["config"]["parallelism"]
     assert res["value"] > 0 and res["e2e"]["value"] > 0
