@@ -1889,7 +1889,10 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
       const uint32_t total = __reduce_add_sync(0xffffffffu, nrows);
       const uint32_t ngroup = min(32u, nc - g);
       uint32_t rb0 = 0x1f1f1f1fu, rb1 = 0x1f1f1f1fu, rl0 = 0u, rl1 = 0u, cols = 0;
-      if (total < 3u * ngroup) {
+      // per-lane walk for groups of short triangles, unless a few tall ones
+      // would leave most lanes idle (mixed scenes)
+      const uint32_t max_rows = __reduce_max_sync(0xffffffffu, nrows);
+      if (total < 3u * ngroup && max_rows <= (total + 31u) / 32u + 2u) {
         // short triangles (tiny-quad meshes): each lane walks its own rows
         if (nrows) {
           const TriRec& t = B.tri[ti];
