@@ -548,7 +548,23 @@ __global__ void __launch_bounds__(kTriBlock, 6) k_setup_tris(Buffers B) {
     uint4 meta = make_uint4(0, 0, 0, 0);
     bool valid = false;
     uint32_t slot = 0, t = 0, vf = 0, mat = 0;
-    if (ti < nt) {
+    bool needed = ti < nt;
+    if (needed && fc.world > 1) {
+      // a sharded rank sets up only the triangles its bins can use: every
+      // large quad's (its bin coverage comes from the triangles) and the
+      // small quads whose bin box meets an owned bin
+      const uint32_t f = B.vq_flags[ti >> 1];
+      if (!(f & 1u)) {
+        const uint2 box = B.vq_box[ti >> 1];
+        const int x0 = (int)(box.x & 0xffffu), x1 = (int)(box.x >> 16), y0 = (int)(box.y & 0xffffu),
+                  y1 = (int)(box.y >> 16);
+        bool any = false;
+        for (int by = y0; by <= y1; ++by)
+          for (int bx = x0; bx <= x1; ++bx) any |= ((bx + 3 * by) % fc.world) == fc.rank;
+        needed = any;
+      }
+    }
+    if (needed) {
       slot = ti >> 1;
       t = ti & 1u;
       vf = B.vq_flags[slot];
@@ -569,6 +585,7 @@ __global__ void __launch_bounds__(kTriBlock, 6) k_setup_tris(Buffers B) {
       }
     }
     stage[threadIdx.x] = rec;
+    const unsigned needm = __ballot_sync(0xffffffffu, needed);
     __syncwarp();
     {  // coalesced copy-out of this warp's 32 records (4 KB)
       const uint32_t wbase = base + (uint32_t)warp * 32u;
@@ -578,11 +595,11 @@ __global__ void __launch_bounds__(kTriBlock, 6) k_setup_tris(Buffers B) {
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const uint32_t e = (uint32_t)k * 32u + lane;  // 16-byte chunk index within the warp
-        if (e < nrec * 8u) dst[e] = src[e];
+        if (e < nrec * 8u && ((needm >> (e >> 3)) & 1u)) dst[e] = src[e];
       }
     }
     __syncwarp();
-    if (ti < nt) {
+    if (needed) {
       B.tri_meta[ti] = meta;
       B.tri_y[ti] = valid ? ((uint32_t)(uint16_t)(int16_t)rec.y_min |
                              ((uint32_t)(uint16_t)(int16_t)rec.y_max << 16))

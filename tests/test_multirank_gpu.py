@@ -24,7 +24,8 @@ def _free_port():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("world,workload,gather", [(2, "boxes1080", "nccl"), (3, "stack64k", "nccl"),
-                                                   (2, "boxes1080", "peer"), (3, "stack64k", "peer")])
+                                                   (2, "boxes1080", "peer"), (3, "stack64k", "peer"),
+                                                   (2, "tiny4m", "peer")])
 def test_bench_multirank_frame_identical(world, workload, gather):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={world}", "--master-addr", "127.0.0.1",
