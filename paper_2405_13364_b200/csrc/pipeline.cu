@@ -734,6 +734,8 @@ __global__ void __launch_bounds__(256) k_bin_pass(Buffers B) {
       bool act = k < nb;
       uint32_t bx = x0 + (k % (x1 - x0 + 1 > 0 ? x1 - x0 + 1 : 1));
       uint32_t by = y0 + (k / (x1 - x0 + 1 > 0 ? x1 - x0 + 1 : 1));
+      // a sharded rank fills only its own bins' lists
+      if (fc.world > 1 && ((bx + 3u * by) % (uint32_t)fc.world) != (uint32_t)fc.rank) act = false;
       uint32_t bin = act ? by * (uint32_t)fc.bins_x + bx : 0u;
       if (__any_sync(0xffffffffu, act)) {
         if (kWrite) {
@@ -799,7 +801,8 @@ __global__ void __launch_bounds__(256) k_bin_large(Buffers B) {
         word = __reduce_or_sync(0xffffffffu, word);
         if (!kWrite && cached && lane == 0) B.lpair_cols[(size_t)w * nwords + wd] = word;
       }
-      if ((word >> lane) & 1u) {
+      const bool mine = fc.world <= 1 || ((wd * 32 + lane + 3 * R) % fc.world) == fc.rank;
+      if (((word >> lane) & 1u) && mine) {
         const int bin = R * fc.bins_x + wd * 32 + lane;
         if (kWrite) {
           const uint32_t slot = atomicAdd(&B.tcur[bin], 1u);
