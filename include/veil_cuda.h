@@ -134,7 +134,9 @@ veil_status veil_shard_unpack_tiles_device(const veil_scene* scene, const veil_s
  * other rank imports them, after which its sharded frames also write their
  * finished pixels straight into the root's framebuffer over NVLink during
  * shading -- no pack, collective or unpack. The caller orders frames with a
- * host barrier after each rank's frame. Import NULL to detach. */
+ * host barrier after each rank's frame. The handles stay valid while the
+ * root keeps its viewport (a larger viewport reallocates the framebuffer:
+ * export and import again). Import NULL to detach. */
 typedef struct veil_ipc_framebuffer {
   uint8_t rgba[64];
   uint8_t mask[64];
