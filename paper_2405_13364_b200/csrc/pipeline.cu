@@ -533,6 +533,7 @@ __global__ void __launch_bounds__(kSetupBlock) k_setup(Buffers B, uint32_t nbloc
 // memory and written back as 512-byte contiguous runs (coalesced stores).
 constexpr int kTriBlock = 128;
 
+template <bool kShard>
 __global__ void __launch_bounds__(kTriBlock, 6) k_setup_tris(Buffers B) {
   const FrameConst& fc = c_fc;
   __shared__ __align__(16) TriRec stage[kTriBlock];
@@ -549,7 +550,7 @@ __global__ void __launch_bounds__(kTriBlock, 6) k_setup_tris(Buffers B) {
     bool valid = false;
     uint32_t slot = 0, t = 0, vf = 0, mat = 0;
     bool needed = ti < nt;
-    if (needed && fc.world > 1) {
+    if (kShard && needed) {
       // a sharded rank sets up only the triangles its bins can use: every
       // large quad's (its bin coverage comes from the triangles) and the
       // small quads whose bin box meets an owned bin
@@ -585,7 +586,7 @@ __global__ void __launch_bounds__(kTriBlock, 6) k_setup_tris(Buffers B) {
       }
     }
     stage[threadIdx.x] = rec;
-    const unsigned needm = __ballot_sync(0xffffffffu, needed);
+    const unsigned needm = kShard ? __ballot_sync(0xffffffffu, needed) : 0xffffffffu;
     __syncwarp();
     {  // coalesced copy-out of this warp's 32 records (4 KB)
       const uint32_t wbase = base + (uint32_t)warp * 32u;
@@ -595,7 +596,7 @@ __global__ void __launch_bounds__(kTriBlock, 6) k_setup_tris(Buffers B) {
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const uint32_t e = (uint32_t)k * 32u + lane;  // 16-byte chunk index within the warp
-        if (e < nrec * 8u && ((needm >> (e >> 3)) & 1u)) dst[e] = src[e];
+        if (e < nrec * 8u && (!kShard || ((needm >> (e >> 3)) & 1u))) dst[e] = src[e];
       }
     }
     __syncwarp();
@@ -3333,7 +3334,10 @@ int enqueue_front(DeviceScene* d, Prepared& P) {
     dev::k_setup<<<P.nblocks, dev::kSetupBlock, 0, st>>>(B, P.nblocks);
     const int tgrid = int(std::min<long long>(((long long)fc.nquads * 2 + dev::kTriBlock - 1) / dev::kTriBlock,
                                               (long long)d->sm_count * 32));
-    dev::k_setup_tris<<<std::max(1, tgrid), dev::kTriBlock, 0, st>>>(B);
+    if (fc.world > 1)
+      dev::k_setup_tris<true><<<std::max(1, tgrid), dev::kTriBlock, 0, st>>>(B);
+    else
+      dev::k_setup_tris<false><<<std::max(1, tgrid), dev::kTriBlock, 0, st>>>(B);
     launches += 2;
   }
   record_event(d->ev[1], st);
