@@ -352,3 +352,48 @@ def test_textured_scene_vs_reference_fixture(name):
     diff = np.abs(got["image"].astype(int) - expect["image"].astype(int))
     assert diff.max() <= 1, diff.max()
     assert (diff > 0).mean() < 1e-3
+
+
+def _edge_case(b, params=None, extended=False):
+    arr = b.build()
+    p = params or default_params()
+    exp = bindings.oracle_render(arr, p, extended=extended)
+    sc = veil.Scene.from_arrays(arr)
+    if extended:
+        sc.set_extended_limits(True)
+    got = veil.render_dump(sc, p)
+    bad = compare(got, exp, PARITY_ARRAYS)
+    assert not bad, bad
+    r = veil.render(sc, p)  # the graph / zero-copy path as well
+    assert np.array_equal(r.pixels().reshape(-1), exp["image"].reshape(-1))
+    return got
+
+
+def test_edge_all_culled():
+    """Every quad culled (behind the camera, degenerate, outside, between samples)."""
+    b = clip_scene(96, 64)
+    b.pixel_rect(10, 10, 40, 40, -0.5)          # z < 0: outside the clip volume
+    b.pixel_rect(200, 10, 240, 40, 0.5)         # right of the viewport
+    b.pixel_rect(10.2, 10.2, 10.4, 10.4, 0.5)   # covers no pixel centre
+    v = b.vertex(0.1, 0.1, 0.5)
+    b.quad_ids([v, v, v, v])                    # degenerate
+    got = _edge_case(b)
+    assert int(got["counters"][1]) == 0
+
+
+@pytest.mark.parametrize("w,h", [(1, 1), (33, 1), (1, 65), (31, 33)])
+def test_edge_tiny_and_ragged_viewports(w, h):
+    b = clip_scene(w, h)
+    b.pixel_rect(-2, -2, w + 2, h + 2, 0.4, (0.9, 0.2, 0.1, 0.5))
+    b.pixel_rect(0, 0, max(1, w // 2), max(1, h // 2), 0.3, (0.1, 0.8, 0.2, 0.7))
+    _edge_case(b)
+
+
+def test_edge_wide_extended_viewport():
+    """A 16384-pixel-wide viewport (extended limits): 512 bin columns, the
+    128-bit column masks of large-triangle binning widened."""
+    b = clip_scene(16384, 48)
+    b.pixel_rect(100, 4, 16300, 40, 0.5, (0.4, 0.4, 0.9, 0.6))
+    b.pixel_rect(8000, 0, 8100, 48, 0.4, (0.9, 0.4, 0.1, 0.8))
+    b.pixel_triangle((30, 2), (16000, 20), (40, 46), 0.45, (0.2, 0.9, 0.5, 0.5))
+    _edge_case(b, extended=True)
