@@ -209,3 +209,17 @@ def test_prefix_sum_offsets():
     assert o["bin_quad_counts"].tolist() == [3, 0, 5]
     assert o["bin_offsets"].tolist() == [0, 3, 3]
     assert o["bin_items"].tolist() == [0, 1, 2, 3, 4, 5, 6, 7]
+
+
+@needs_ref
+@pytest.mark.parametrize("name", ["textured_scene", "textured_scene_df1_backface"])
+def test_textured_fixture_is_the_reference(name):
+    """The textured fixtures (checked against libveil on the GPU) are the
+    reference's own output for tests/golden/textured: regenerate and compare."""
+    from common import TEXTURED
+    _, params, expect = load_golden(name)
+    rs = bindings.RefScene.load(f"{TEXTURED}/scene.obj", None, f"{TEXTURED}/camera.cfg")
+    got = rs.dump(params)
+    assert np.array_equal(got["reenum_image"], got["image"])
+    bad = compare(got, expect)
+    assert not bad, bad
