@@ -294,14 +294,14 @@ def run_ours(args):
             scene.set_camera(m, eye)
         if timed_events:
             timed_events[0].record(stream)
-        st = veil.render_device(scene, params, shard)
+        veil.render_device(scene, params, shard, stats=False)
         if peer:
             # every rank's pixels are in rank 0's framebuffer once all ranks'
             # frames completed (render_device synchronises its stream)
             if timed_events:
                 timed_events[1].record(stream)
             dist.barrier()
-            return st
+            return scene.last_stats()
         if world > 1:
             veil.pack_tiles_device(scene, rank, world, tiles.data_ptr(), tiles.numel())
             with torch.cuda.stream(stream):
@@ -317,7 +317,7 @@ def run_ours(args):
                     dist.gather(mine, None, dst=0)
         if timed_events:
             timed_events[1].record(stream)
-        return st
+        return scene.last_stats()
 
     for i in range(args.warmup):
         frame(i)

@@ -107,7 +107,7 @@ struct Counters {
   unsigned long long cull[5];  // visible, degenerate, backfacing, frustum, between
   unsigned long long pairs;
   unsigned long long small_quads, large_tris;
-  unsigned long long bin_error;  // min(bin * 64 + code)
+  unsigned long long bin_error;  // ~min(bin * 64 + code), 0 = none (zeroed with the counters)
   unsigned int nvis;
   unsigned int error;  // bit0 visible capacity, bit1 item capacity
   unsigned int work_next[4];
@@ -2289,8 +2289,8 @@ __global__ void __launch_bounds__(128, 7) k_extract(Buffers B, int pass,
         const uint32_t s = atomicAdd(&B.ctr->spill_count[pass], 1u);
         B.spill[pass][s] = code;
       } else {
-        atomicMin(&B.ctr->bin_error, (unsigned long long)bin * 64ull +
-                                         (unsigned long long)min(st.err_code, 63));
+        atomicMax(&B.ctr->bin_error, ~((unsigned long long)bin * 64ull +
+                                         (unsigned long long)min(st.err_code, 63)));
       }
     }
     __syncthreads();
@@ -2732,10 +2732,10 @@ struct DeviceScene {
   uint32_t nverts = 0, nquads = 0;
   DevBuf pos, vcol, vnrm, quads, qmat, mats, vuv, texels, texlev, texdesc;
   bool textured = false;  // some material samples a texture (generic shading path)
-  DevBuf block_state, vq_uv, vq_src, vq_idx, vq_box, vq_flags, vq_mat, vq_col, vq_nrm, tri, tri_meta, shade,
+  DevBuf zero, vq_uv, vq_src, vq_idx, vq_box, vq_flags, vq_mat, vq_col, vq_nrm, tri, tri_meta, shade,
       tri_y;
-  DevBuf qcnt, tcnt, off, qcur, tcur, cat, bin_list0, bin_list1, prop_q, bin_cost, bin_order, prop, items, item_rows, slots, spill0, spill1, scratch, fb, mask,
-      hash, emit, ctr, tile_ids, hbd, pool_tri, pool_mask, pool_pre, seg_queue, pool_slot, lpairs, lpair_cols;
+  DevBuf off, qcur, tcur, cat, bin_list0, bin_list1, prop_q, bin_cost, bin_order, prop, items, item_rows, slots, spill0, spill1, scratch, fb, mask,
+      hash, emit, tile_ids, hbd, pool_tri, pool_mask, pool_pre, seg_queue, pool_slot, lpairs, lpair_cols;
   uint32_t items_cap = 0;
   uint32_t pool_cap = 0;
   uint32_t lpairs_cap = 0;
@@ -3086,6 +3086,7 @@ void dump_put_host(RenderOutput* out, const char* name, const std::vector<T>& v)
 struct Prepared {
   dev::FrameConst fc;
   dev::Buffers B;
+  size_t zero_bytes;
   uint32_t nblocks;
   uint32_t lpair_cols_cap;
   uint32_t gcap_tbr, gcap_tb;
@@ -3158,7 +3159,12 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   const uint32_t Q = d->nquads;
   const size_t nb = size_t(fc.nbins);
   P.nblocks = (Q + dev::kSetupBlock - 1) / dev::kSetupBlock;
-  d->block_state.ensure(std::max<size_t>(1, P.nblocks) * 8);
+  // counters, per-bin counts and the setup look-back states share one
+  // region, zeroed by a single memset per frame
+  const size_t zero_ctr = (sizeof(dev::Counters) + 255) & ~size_t(255);
+  const size_t zero_cnt = ((size_t(fc.nbins) * 8 + 255) & ~size_t(255));
+  P.zero_bytes = zero_ctr + zero_cnt + std::max<size_t>(1, P.nblocks) * 8;
+  d->zero.ensure(P.zero_bytes);
   d->vq_src.ensure(size_t(Q) * 4);
   d->vq_idx.ensure(size_t(Q) * 16);
   d->vq_box.ensure(size_t(Q) * 8);
@@ -3177,8 +3183,6 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   // carry no UVs: scenes with textured materials shade on the generic path.
   fc.decoded = !d->textured && (double)cam.width * cam.height >= 8.0 * std::max<double>(1.0, Q) ? 1 : 0;
   if (fc.decoded) d->shade.ensure(size_t(Q) * 2 * sizeof(dev::ShadeRec));
-  d->qcnt.ensure(nb * 4);
-  d->tcnt.ensure(nb * 4);
   d->off.ensure(nb * 4);
   d->qcur.ensure(nb * 4);
   d->tcur.ensure(nb * 4);
@@ -3207,7 +3211,6 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
     d->hash.ensure(npx * 8);
     d->emit.ensure(npx * 4);
   }
-  d->ctr.ensure(sizeof(dev::Counters));
   d->hbd.ensure(nb * 32 * sizeof(dev::HbDesc));
   d->seg_queue.ensure(nb * 32 * 16);
   if (d->lpairs_cap == 0)
@@ -3254,7 +3257,10 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   B.texlev = d->texlev.as<uint4>();
   B.texdesc = d->texdesc.as<uint2>();
   B.vq_uv = d->vq_uv.as<float4>();
-  B.block_state = d->block_state.as<unsigned long long>();
+  B.ctr = d->zero.as<dev::Counters>();
+  B.qcnt = reinterpret_cast<uint32_t*>(d->zero.as<uint8_t>() + zero_ctr);
+  B.tcnt = B.qcnt + fc.nbins;
+  B.block_state = reinterpret_cast<unsigned long long*>(d->zero.as<uint8_t>() + zero_ctr + zero_cnt);
   B.vq_src = d->vq_src.as<uint32_t>();
   B.vq_idx = d->vq_idx.as<uint4>();
   B.vq_box = d->vq_box.as<uint2>();
@@ -3266,8 +3272,6 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   B.tri_meta = d->tri_meta.as<uint4>();
   B.tri_y = d->tri_y.as<uint32_t>();
   B.shade = fc.decoded ? d->shade.as<dev::ShadeRec>() : nullptr;
-  B.qcnt = d->qcnt.as<uint32_t>();
-  B.tcnt = d->tcnt.as<uint32_t>();
   B.off = d->off.as<uint32_t>();
   B.qcur = d->qcur.as<uint32_t>();
   B.tcur = d->tcur.as<uint32_t>();
@@ -3298,7 +3302,6 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   B.lpairs = d->lpairs.as<uint2>();
   B.lpair_cols = d->lpair_cols.as<uint32_t>();
   B.lpair_cols_cap = P.lpair_cols_cap;
-  B.ctr = d->ctr.as<dev::Counters>();
   return P;
 }
 
@@ -3324,13 +3327,9 @@ int enqueue_front(DeviceScene* d, Prepared& P) {
   ck(cudaMemcpyToSymbolAsync(dev::c_fc, d->fc_host, sizeof(dev::FrameConst), 0,
                              cudaMemcpyHostToDevice, st),
      "c_fc upload");
-  ck(cudaMemsetAsync(B.ctr, 0, sizeof(dev::Counters), st), "memset");
-  ck(cudaMemsetAsync(&B.ctr->bin_error, 0xff, sizeof(unsigned long long), st), "memset");
-  ck(cudaMemsetAsync(B.qcnt, 0, size_t(fc.nbins) * 4, st), "memset");
-  ck(cudaMemsetAsync(B.tcnt, 0, size_t(fc.nbins) * 4, st), "memset");
+  ck(cudaMemsetAsync(B.ctr, 0, P.zero_bytes, st), "memset");  // counters, bin counts, look-back
   record_event(d->ev[0], st);
   if (P.nblocks) {
-    ck(cudaMemsetAsync(B.block_state, 0, size_t(P.nblocks) * 8, st), "memset");
     dev::k_setup<<<P.nblocks, dev::kSetupBlock, 0, st>>>(B, P.nblocks);
     const int tgrid = int(std::min<long long>(((long long)fc.nquads * 2 + dev::kTriBlock - 1) / dev::kTriBlock,
                                               (long long)d->sm_count * 32));
@@ -3405,8 +3404,9 @@ void check_frame_errors(const dev::Counters& c, const dev::FrameConst& fc) {
   if (c.error & 1u)
     throw Error(VEIL_ERR_CAPACITY, "visible primitive count exceeds 24-bit index space");
   if (c.error & 4u) throw Error(VEIL_ERR_CAPACITY, "a-buffer fragment list capacity exceeded");
-  if (c.bin_error != ~0ull) {
-    int bin = int(c.bin_error / 64), code = int(c.bin_error % 64);
+  if (c.bin_error != 0ull) {
+    const unsigned long long be = ~c.bin_error;
+    int bin = int(be / 64), code = int(be % 64);
     throw Error(VEIL_ERR_CAPACITY, "bin (" + std::to_string(bin % fc.bins_x) + "," +
                                        std::to_string(bin / fc.bins_x) +
                                        ") exceeds high-rasterizer limit: " + limit_name(code));

@@ -291,12 +291,14 @@ def render_dump(scene: Scene, params=None, names=None):
     return Render(r.value).dumps(names)
 
 
-def render_device(scene: Scene, params=None, shard=None):
-    """One frame into device memory only (bench path); returns FrameStats."""
+def render_device(scene: Scene, params=None, shard=None, stats=True):
+    """One frame into device memory only (bench path); returns FrameStats
+    (or None with stats=False, so a caller can close its timed region first
+    and read scene.last_stats() afterwards)."""
     params = params or default_params()
     sh = None if shard is None else C.byref(Shard(*shard))
     _check(lib().veil_render_device(scene.h, C.byref(params), sh))
-    return scene.last_stats()
+    return scene.last_stats() if stats else None
 
 
 def export_framebuffer(scene: Scene) -> bytes:
