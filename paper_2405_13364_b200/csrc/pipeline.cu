@@ -1828,6 +1828,33 @@ __device__ __forceinline__ void warp_bitonic(uint64_t (&v)[4], int lane) {
 // THB pool (L2-resident) with one descriptor per half-block; shading runs
 // in k_shade. kGlobal selects global-memory scratch for items that exceed
 // the shared-memory capacities (but not the active limits).
+// Bitonic sort of a block's (key, ref) pairs in scratch memory, for blocks
+// with more tri-blocks than the register sort holds (out of line: rare).
+__device__ __noinline__ void sort_keys_scratch(uint64_t* keys, uint16_t* refs, uint32_t n, int lane) {
+  uint32_t N = 1;
+  while (N < n) N <<= 1;
+  for (uint32_t i = n + lane; i < N; i += 32) keys[i] = ~0ull, refs[i] = 0;
+  __syncwarp();
+  for (uint32_t k = 2; k <= N; k <<= 1)
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = lane; i < N; i += 32) {
+        const uint32_t ixj = i ^ j;
+        if (ixj > i) {
+          const uint64_t x = keys[i], y = keys[ixj];
+          const bool up = (i & k) == 0;
+          if ((x > y) == up) {
+            keys[i] = y;
+            keys[ixj] = x;
+            const uint16_t t = refs[i];
+            refs[i] = refs[ixj];
+            refs[ixj] = t;
+          }
+        }
+      }
+      __syncwarp();
+    }
+}
+
 template <bool kGlobal>
 __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers& B, int pass,
                                              int bin, int row, const RasterView& V,
@@ -2077,28 +2104,7 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
     else if (n <= 64) warp_bitonic<2>(v, lane);
     else warp_bitonic<4>(v, lane);
   } else if (ok && n > 1) {
-    uint32_t N = 1;
-    while (N < n) N <<= 1;
-    for (uint32_t i = n + lane; i < N; i += 32) keys[i] = ~0ull, refs[i] = 0;
-    __syncwarp();
-    for (uint32_t k = 2; k <= N; k <<= 1)
-      for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-        for (uint32_t i = lane; i < N; i += 32) {
-          const uint32_t ixj = i ^ j;
-          if (ixj > i) {
-            const uint64_t x = keys[i], y = keys[ixj];
-            const bool up = (i & k) == 0;
-            if ((x > y) == up) {
-              keys[i] = y;
-              keys[ixj] = x;
-              const uint16_t t = refs[i];
-              refs[i] = refs[ixj];
-              refs[ixj] = t;
-            }
-          }
-        }
-        __syncwarp();
-      }
+    sort_keys_scratch(keys, refs, n, lane);
   }
   // one pool allocation per item: 2n THB slots per warp (each tri-block
   // yields <= 1 THB per half)
@@ -2157,18 +2163,21 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
         frags[h] += __shfl_sync(0xffffffffu, incl, 31);
       }
     };
-    if (in_regs) {
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if ((uint32_t)(j * 32) < n) {
-          const uint32_t k = j * 32 + lane;
-          chunk(k, k < n ? (uint32_t)(v[j] & 0x3fffu) : 0u);
+    // one call site for the THB split (keeps the kernel's code compact)
+#pragma unroll 1
+    for (uint32_t base = 0; base < n; base += 32) {
+      const uint32_t k = base + lane;
+      uint32_t ref = 0;
+      if (k < n) {
+        if (in_regs) {
+          const uint32_t j = base >> 5;
+          const uint64_t vj = j == 0 ? v[0] : (j == 1 ? v[1] : (j == 2 ? v[2] : v[3]));
+          ref = (uint32_t)(vj & 0x3fffu);
+        } else {
+          ref = refs[k];
         }
-    } else {
-      for (uint32_t base = 0; base < n; base += 32) {
-        const uint32_t k = base + lane;
-        chunk(k, k < n ? (uint32_t)refs[k] : 0u);
       }
+      chunk(k, ref);
     }
     {
 #pragma unroll
