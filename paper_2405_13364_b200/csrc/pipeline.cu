@@ -1936,22 +1936,55 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
       }
       const uint32_t total = __reduce_add_sync(0xffffffffu, nrows);
       const uint32_t ngroup = min(32u, nc - g);
-      uint32_t rb0 = 0x1f1f1f1fu, rb1 = 0x1f1f1f1fu, rl0 = 0u, rl1 = 0u, cols = 0;
       // per-lane walk for groups of short triangles, unless a few tall ones
       // would leave most lanes idle (mixed scenes)
       const uint32_t max_rows = __reduce_max_sync(0xffffffffu, nrows);
-      if (total < 3u * ngroup && max_rows <= (total + 31u) / 32u + 2u) {
-        // short triangles (tiny-quad meshes): each lane walks its own rows
-        if (nrows) {
-          const TriRec& t = B.tri[ti];
-          for (uint32_t k = 0; k < nrows; ++k) {
-            const int py = yb + (int)k;
-            int b, l;
-            if (!row_span(t, py, px0, px_last, &b, &l)) continue;
-            const int ly = py - ry0;
+      // Row spans with one call site: per lane for groups of short
+      // triangles, (candidate, row) pairs spread over the lanes otherwise;
+      // each row's (begin, last) bytes land in the candidate's scratch slot.
+      const bool pairs = !(total < 3u * ngroup && max_rows <= (total + 31u) / 32u + 2u);
+      uint32_t rb0 = 0x1f1f1f1fu, rb1 = 0x1f1f1f1fu, rl0 = 0u, rl1 = 0u, cols = 0;
+      uint32_t excl = 0;
+      if (pairs) {
+        reinterpret_cast<uint4*>(rs)[lane] = make_uint4(0x1f1f1f1fu, 0x1f1f1f1fu, 0u, 0u);
+        uint32_t incl = nrows;
+#pragma unroll
+        for (int sft = 1; sft < 32; sft <<= 1) {
+          const uint32_t v = __shfl_up_sync(0xffffffffu, incl, sft);
+          if (lane >= sft) incl += v;
+        }
+        excl = incl - nrows;
+      }
+      __syncwarp();
+      const uint32_t iters = pairs ? (total + 31u) / 32u : max_rows;
+#pragma unroll 1
+      for (uint32_t it = 0; it < iters; ++it) {
+        uint32_t c = (uint32_t)lane, tcur = ti;
+        int py = yb + (int)it;
+        bool act = it < nrows;
+        if (pairs) {
+          const uint32_t p = it * 32u + lane;
+          c = 0;  // largest c with excl[c] <= p (shuffle binary search)
+#pragma unroll
+          for (uint32_t sft = 16; sft > 0; sft >>= 1) {
+            const uint32_t e = __shfl_sync(0xffffffffu, excl, c + sft);
+            if (e <= p) c += sft;
+          }
+          const uint32_t ec = __shfl_sync(0xffffffffu, excl, c);
+          tcur = __shfl_sync(0xffffffffu, ti, c);
+          py = __shfl_sync(0xffffffffu, yb, c) + (int)(p - ec);
+          act = p < total;
+        }
+        int b, l;
+        if (act && row_span(B.tri[tcur], py, px0, px_last, &b, &l)) {
+          const int ly = py - ry0;
+          const uint32_t bb = (uint32_t)(b - px0), ll = (uint32_t)(l - px0);
+          if (pairs) {
+            reinterpret_cast<uint8_t*>(rs + c * 4)[ly] = (uint8_t)bb;
+            reinterpret_cast<uint8_t*>(rs + c * 4 + 2)[ly] = (uint8_t)ll;
+          } else {  // the lane's own candidate: keep its row bytes in registers
             const int sh8 = (ly & 3) * 8;
             const uint32_t keepm = ~(0xffu << sh8);
-            const uint32_t bb = (uint32_t)(b - px0), ll = (uint32_t)(l - px0);
             if (ly < 4) {
               rb0 = (rb0 & keepm) | (bb << sh8);
               rl0 = (rl0 & keepm) | (ll << sh8);
@@ -1962,38 +1995,8 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
             cols |= ((2u << (ll >> 3)) - 1u) & ~((1u << (bb >> 3)) - 1u);
           }
         }
-      } else {
-        // tall triangles: spread the (candidate, row) pairs over the lanes
-        reinterpret_cast<uint4*>(rs)[lane] = make_uint4(0x1f1f1f1fu, 0x1f1f1f1fu, 0u, 0u);
-        uint32_t incl = nrows;
-#pragma unroll
-        for (int sft = 1; sft < 32; sft <<= 1) {
-          const uint32_t v = __shfl_up_sync(0xffffffffu, incl, sft);
-          if (lane >= sft) incl += v;
-        }
-        const uint32_t excl = incl - nrows;
-        __syncwarp();
-        for (uint32_t p0 = 0; p0 < total; p0 += 32) {
-          const uint32_t p = p0 + lane;
-          uint32_t c = 0;  // largest c with excl[c] <= p (shuffle binary search)
-#pragma unroll
-          for (uint32_t sft = 16; sft > 0; sft >>= 1) {
-            const uint32_t e = __shfl_sync(0xffffffffu, excl, c + sft);
-            if (e <= p) c += sft;
-          }
-          const uint32_t ec = __shfl_sync(0xffffffffu, excl, c);
-          const uint32_t tc = __shfl_sync(0xffffffffu, ti, c);
-          const int yc = __shfl_sync(0xffffffffu, yb, c);
-          if (p < total) {
-            const int py = yc + (int)(p - ec);
-            int b, l;
-            if (row_span(B.tri[tc], py, px0, px_last, &b, &l)) {
-              const int ly = py - ry0;
-              reinterpret_cast<uint8_t*>(rs + c * 4)[ly] = (uint8_t)(b - px0);
-              reinterpret_cast<uint8_t*>(rs + c * 4 + 2)[ly] = (uint8_t)(l - px0);
-            }
-          }
-        }
+      }
+      if (pairs) {
         __syncwarp();
         const uint4 rr = reinterpret_cast<const uint4*>(rs)[lane];
         rb0 = rr.x, rb1 = rr.y, rl0 = rr.z, rl1 = rr.w;
