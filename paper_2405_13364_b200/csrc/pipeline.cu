@@ -2103,8 +2103,9 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
 #pragma unroll
     for (int j = 0; j < 4; ++j)
       if ((uint32_t)(j * 32 + lane) < n) v[j] = keys[j * 32 + lane];
-    if (n <= 32) warp_bitonic<1>(v, lane);
-    else if (n <= 64) warp_bitonic<2>(v, lane);
+    // two register sorts only: a third (32-key) variant costs more in
+    // instruction-cache misses than it saves in compare-exchanges
+    if (n <= 64) warp_bitonic<2>(v, lane);
     else warp_bitonic<4>(v, lane);
   } else if (ok && n > 1) {
     sort_keys_scratch(keys, refs, n, lane);
