@@ -1518,8 +1518,6 @@ struct ItemState {
   uint32_t pool_base;
   int alloc_ok;
   uint32_t ncand;
-  uint32_t hb_cnt[8];
-  uint32_t hb_frags[8];
 };
 
 enum { kPassLow = 0, kPassHigh = 1 };
@@ -2029,15 +2027,12 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
     }
     __syncthreads();
   }
-  __syncthreads();
+  // (the rounds loop ends with a barrier; with no items ntbr is still 0)
   const uint32_t ntbr = (uint32_t)st->ntbr;
-  if (ntbr > lim.tbr) {
-    if (threadIdx.x == 0) set_status(st, pass == kPassLow ? 1 : 3, 0);
-  } else if (ntbr > cap_tbr) {
-    if (threadIdx.x == 0) set_status(st, 2, 0);
+  if (ntbr > lim.tbr || ntbr > cap_tbr) {  // uniform: every thread leaves
+    if (threadIdx.x == 0) set_status(st, ntbr > lim.tbr ? (pass == kPassLow ? 1 : 3) : 2, 0);
+    return;
   }
-  __syncthreads();
-  if (st->status) return;
 
   // ---- phase B: warp w extracts block (row, w) (raster.cpp:100-199)
   const int block = row * 4 + warp;
@@ -2116,6 +2111,8 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
   __syncthreads();
   if (threadIdx.x == 0) {
     st->alloc_ok = 0;
+    unsigned long long* slot = B.slots + ((size_t)bin * 4 + row) * 5;
+    slot[1] = slot[2] = 0;  // fragment / THB sums, added per warp below
     if (!st->status) {
       const uint32_t tot = 2u * (st->warp_n[0] + st->warp_n[1] + st->warp_n[2] + st->warp_n[3]);
       const unsigned long long pb = atomicAdd(&B.ctr->pool_pair, (unsigned long long)tot);
@@ -2229,18 +2226,9 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
     slot[0] = slot[3] = slot[4] = 0;
   }
   if (lane == 0) {
-    st->hb_frags[warp * 2] = frags[0];
-    st->hb_frags[warp * 2 + 1] = frags[1];
-    st->hb_cnt[warp * 2] = nthb[0];
-    st->hb_cnt[warp * 2 + 1] = nthb[1];
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
     unsigned long long* slot = B.slots + ((size_t)bin * 4 + row) * 5;
-    unsigned long long fr = 0, th = 0;
-    for (int h = 0; h < 8; ++h) fr += st->hb_frags[h], th += st->hb_cnt[h];
-    slot[1] = fr;
-    slot[2] = th;
+    atomicAdd(&slot[1], (unsigned long long)(frags[0] + frags[1]));
+    atomicAdd(&slot[2], (unsigned long long)(nthb[0] + nthb[1]));
   }
 }
 
@@ -2306,7 +2294,6 @@ __global__ void __launch_bounds__(128, 7) k_extract(Buffers B, int pass,
                                          (unsigned long long)min(st.err_code, 63)));
       }
     }
-    __syncthreads();
   }
 }
 
