@@ -120,3 +120,57 @@ def boxes_arrays(width=256, height=256):
     scene, _, _ = load_golden("c1_boxes_256")
     scene.width, scene.height = width, height
     return scene
+
+
+def fuzz_scene(seed):
+    """Seeded random scene + render parameters for the fuzz parity tests:
+    random quads and triangles (some degenerate, some reaching behind the
+    eye), random per-vertex colours/normals (zero normals included), several
+    materials with mixed flags, a random perspective camera (sometimes inside
+    the geometry) and viewport, random render flags and depth-filter size."""
+    from paper_2405_13364_b200 import veil
+    from paper_2405_13364_b200.abi import (
+        RENDER_ALPHA_THRESHOLD, RENDER_BACKFACE_CULLING, RENDER_FORCE_HIGH_PATH,
+        RENDER_VISUALIZE_ERRORS)
+    rng = np.random.default_rng(1000 + seed)
+    w, h = int(rng.integers(8, 300)), int(rng.integers(8, 200))
+    nq = int(rng.integers(1, 600))
+    spread = float(rng.choice([0.5, 2.0, 6.0]))
+    centres = rng.uniform(-2, 2, (nq, 3))
+    size = rng.choice([0.02, 0.2, 1.0, 3.0], nq)[:, None, None]
+    v = np.zeros(4 * nq, dtype=VERTEX_DTYPE)
+    pos = centres[:, None, :] + size * rng.normal(0, 1, (nq, 4, 3)) * spread / 2
+    v["position"] = pos.reshape(-1, 3)
+    nrm = rng.normal(0, 1, (4 * nq, 3))
+    nrm[rng.random(4 * nq) < 0.05] = 0.0
+    v["normal"] = nrm
+    col = rng.uniform(0, 1, (4 * nq, 4))
+    col[:, 3] = rng.choice([0.05, 0.3, 0.6, 0.95, 1.0], 4 * nq)
+    v["color"] = col
+    q = np.zeros(nq, dtype=QUAD_DTYPE)
+    ids = np.arange(4 * nq, dtype=np.uint32).reshape(nq, 4)
+    tri = rng.random(nq) < 0.3
+    ids[tri, 3] = ids[tri, 2]  # triangles
+    dup = rng.random(nq) < 0.05
+    ids[dup, 1] = ids[dup, 0]  # degenerate
+    q["v"] = ids
+    nm = int(rng.integers(1, 4))
+    q["material"] = rng.integers(0, nm, nq)
+    m = np.zeros(nm, dtype=MATERIAL_DTYPE)
+    for i in range(nm):
+        m[i] = (tuple(rng.uniform(0.2, 1, 4)), float(rng.choice([0.1, 0.5, 1.0])), -1,
+                int(rng.integers(0, 4)))
+    eye = rng.uniform(-1, 1, 3) * (1.0 if rng.random() < 0.25 else 8.0)
+    at = rng.uniform(-1, 1, 3)
+    fov = float(rng.choice([30.0, 60.0, 100.0]))
+    near = float(rng.choice([0.01, 0.1, 1.0]))
+    mat = veil.look_at(list(eye), list(at), [0, 1, 0], fov, near, 50.0, w, h)
+    arr = SceneArrays(v, q, m, SCENE_HAS_COLORS | SCENE_HAS_NORMALS, mat, w, h,
+                      list(eye) if rng.random() < 0.5 else None)
+    flags = 0
+    for f in (RENDER_ALPHA_THRESHOLD, RENDER_FORCE_HIGH_PATH, RENDER_BACKFACE_CULLING,
+              RENDER_VISUALIZE_ERRORS):
+        if rng.random() < 0.3:
+            flags |= f
+    params = default_params(flags=flags, depth_filter_size=int(rng.choice([1, 2, 3, 5, 8, 16])))
+    return arr, params

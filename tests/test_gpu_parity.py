@@ -397,3 +397,21 @@ def test_edge_wide_extended_viewport():
     b.pixel_rect(8000, 0, 8100, 48, 0.4, (0.9, 0.4, 0.1, 0.8))
     b.pixel_triangle((30, 2), (16000, 20), (40, 46), 0.45, (0.2, 0.9, 0.5, 0.5))
     _edge_case(b, extended=True)
+
+
+@pytest.mark.parametrize("seed", range(48))
+def test_fuzz_vs_restatement(seed):
+    """Seeded random scenes, cameras, flags and depth-filter sizes (the same
+    generator the restatement is checked with against the live reference in
+    test_oracle.py); errors must match too."""
+    from common import fuzz_scene
+    arr, p = fuzz_scene(seed)
+    try:
+        expect = bindings.oracle_render(arr, p)
+    except bindings.CheckerError as e:
+        with pytest.raises(veil.VeilError) as g:
+            gpu_dump(arr, p)
+        assert (g.value.status, g.value.message) == (e.status, e.message)
+        return
+    bad = compare(gpu_dump(arr, p), expect, PARITY_ARRAYS)
+    assert not bad, bad

@@ -223,3 +223,11 @@ def test_textured_fixture_is_the_reference(name):
     assert np.array_equal(got["reenum_image"], got["image"])
     bad = compare(got, expect)
     assert not bad, bad
+
+
+@needs_ref
+@pytest.mark.parametrize("seed", range(48))
+def test_restatement_vs_reference_fuzz(seed):
+    """Seeded random scenes, cameras, flags and depth-filter sizes."""
+    from common import fuzz_scene
+    _vs_ref(*fuzz_scene(seed))
