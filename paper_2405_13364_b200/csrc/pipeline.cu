@@ -1563,15 +1563,6 @@ __device__ __forceinline__ uint32_t kth_pixel(uint32_t m, uint32_t k) {
 // the segment in stream order through per-warp routing masks and pushes them
 // into its register depth filter. Every pixel therefore sees exactly the
 // reference's per-pixel sequence.
-__device__ __forceinline__ uint32_t find_thb(const uint32_t* pre_l, uint32_t lo, uint32_t hi,
-                                             uint32_t s) {
-  while (lo < hi) {  // largest r in [lo, hi] with pre[r] <= s
-    const uint32_t mid = (lo + hi + 1) >> 1;
-    if (pre_l[mid] <= s) lo = mid; else hi = mid - 1;
-  }
-  return lo;
-}
-
 template <typename Filter>
 __device__ __forceinline__ void blend_routed(const FrameConst& fc, Filter& f, PixelOut& o,
                                              uint32_t mine, uint64_t key, float4 col) {
@@ -1619,7 +1610,17 @@ __device__ __forceinline__ void shade_segments(const FrameConst& fc, const Buffe
     const uint32_t s0 = base + lane;
     const bool v0 = s0 < total;
     const uint32_t c0 = v0 ? s0 : total - 1;
-    const uint32_t r0 = find_thb(pre_l, r_lo, min(n - 1, r_lo + (uint32_t)lane + 1u), c0);
+    // THBs r_lo+1 .. r_lo+32 start inside [base, base+32) or later (THB r_lo
+    // holds sample base-1, or base = 0 and r_lo = 0): one bit per start, and
+    // sample base+lane lies in THB r_lo + (starts at or before it)
+    const uint32_t rj = r_lo + 1u + (uint32_t)lane;
+    uint32_t start_bit = 0u;
+    if (rj < n) {
+      const uint32_t st = pre_l[rj] - base;
+      if (st < 32u) start_bit = 1u << st;
+    }
+    const uint32_t starts = __reduce_or_sync(0xffffffffu, start_bit);
+    const uint32_t r0 = r_lo + (uint32_t)__popc(starts & (0xffffffffu >> (31 - lane)));
     const uint32_t p0 = kth_pixel(mask_l[r0], c0 - pre_l[r0]);
     const uint32_t t0 = tri_l[r0];
     float4 col0;
