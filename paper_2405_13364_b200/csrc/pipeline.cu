@@ -1518,6 +1518,7 @@ struct ItemState {
   uint32_t pool_base;
   int alloc_ok;
   uint32_t ncand;
+  uint32_t gnext;  // next candidate group of the row-span pass
 };
 
 enum { kPassLow = 0, kPassHigh = 1 };
@@ -1885,7 +1886,7 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
   const uint32_t nitem = nq + nt, round_items = cand_cap / 2u;
   for (uint32_t round = 0; round < nitem; round += round_items) {
     const uint32_t end = min(nitem, round + round_items);
-    if (threadIdx.x == 0) st->ncand = 0;
+    if (threadIdx.x == 0) st->ncand = 0, st->gnext = 0;
     __syncthreads();
     for (uint32_t j0 = round; j0 < end; j0 += blockDim.x) {
       const uint32_t j = j0 + threadIdx.x;
@@ -1918,13 +1919,22 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
     // their row counts and spreads the (candidate, row) pairs over its lanes,
     // so tall and short triangles keep all lanes busy; each candidate's lane
     // then assembles its tri-block-row from the per-row bytes.
+    // Groups of G candidates are taken dynamically; with fewer than 32
+    // candidates G shrinks (down to 8) so that all four warps share the row
+    // spans (smaller groups for larger items cost short triangles more than
+    // they gain for tall ones, measured).
     uint32_t* rs = V.rows + (size_t)warp * 128u;  // [candidate][b0 b1 l0 l1]
-    for (uint32_t g = (uint32_t)warp * 32u; g < nc; g += (blockDim.x >> 5) * 32u) {
+    const uint32_t G = nc < 32u ? max(8u, ((nc + 3u) / 4u + 7u) & ~7u) : 32u;
+    for (;;) {
+      uint32_t g = 0;
+      if (lane == 0) g = atomicAdd(&st->gnext, G);
+      g = __shfl_sync(0xffffffffu, g, 0);
+      if (g >= nc) break;
       const uint32_t j = g + lane;
       uint32_t ti = 0, large = 0, nrows = 0;
       int yb = 0;
       uint64_t code = 0;
-      if (j < nc) {
+      if ((uint32_t)lane < G && j < nc) {
         code = cand[j];
         ti = (uint32_t)code & 0x7fffffffu;
         large = ((uint32_t)code) >> 31;
@@ -1934,7 +1944,7 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
         nrows = ye >= yb ? (uint32_t)(ye - yb + 1) : 0u;
       }
       const uint32_t total = __reduce_add_sync(0xffffffffu, nrows);
-      const uint32_t ngroup = min(32u, nc - g);
+      const uint32_t ngroup = min(G, nc - g);
       // per-lane walk for groups of short triangles, unless a few tall ones
       // would leave most lanes idle (mixed scenes)
       const uint32_t max_rows = __reduce_max_sync(0xffffffffu, nrows);
