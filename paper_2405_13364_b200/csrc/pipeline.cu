@@ -439,7 +439,9 @@ __device__ __forceinline__ unsigned long long ld_state(const unsigned long long*
   return *reinterpret_cast<const volatile unsigned long long*>(p);
 }
 
-__global__ void __launch_bounds__(kSetupBlock) k_setup(Buffers B, uint32_t nblocks) {
+// 4 CTAs/SM (64 registers, small spill) beats 3 at 80 registers: the cull is
+// gather- and FP64-latency bound (C4 setup -6%, measured; 5 or 6 spill more)
+__global__ void __launch_bounds__(kSetupBlock, 4) k_setup(Buffers B, uint32_t nblocks) {
   const FrameConst& fc = c_fc;
   __shared__ uint32_t s_bid, s_excl;
   if (threadIdx.x == 0) s_bid = atomicAdd(&B.ctr->setup_ticket, 1u);
@@ -534,7 +536,7 @@ __global__ void __launch_bounds__(kSetupBlock) k_setup(Buffers B, uint32_t nbloc
 constexpr int kTriBlock = 128;
 
 template <bool kShard>
-__global__ void __launch_bounds__(kTriBlock, 6) k_setup_tris(Buffers B) {
+__global__ void __launch_bounds__(kTriBlock, 7) k_setup_tris(Buffers B) {
   const FrameConst& fc = c_fc;
   __shared__ __align__(16) TriRec stage[kTriBlock];
   if (B.ctr->error & 1u) return;
