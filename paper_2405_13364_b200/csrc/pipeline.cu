@@ -1788,38 +1788,44 @@ __device__ __forceinline__ uint32_t span_mask(uint32_t b, uint32_t l, uint32_t c
   return ((2u << (l - b)) - 1u) << (b - c0);
 }
 
+// Compare-exchange of registers j and j ^ (M / 32) (stages with distance >= 32).
+template <int J, int M>
+__device__ __forceinline__ void bitonic_cross(uint64_t (&v)[4], int k, int lane) {
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    const int jp = j ^ (M >> 5);
+    if (jp > j) {
+      const int i = j * 32 + lane;
+      const bool up = (i & k) == 0;
+      const uint64_t x = v[j], y = v[jp];
+      const bool sw = (x > y) == up;
+      v[j] = sw ? y : x;
+      v[jp] = sw ? x : y;
+    }
+  }
+}
+
 // Warp bitonic sort of N = 32*J 64-bit keys held in registers, strided
-// layout (element i = j*32 + lane in v[j]); ascending.
+// layout (element i = j*32 + lane in v[j]); ascending. The stage loops run
+// at run time (only the register index is unrolled) to keep the kernel's
+// code small: the fully unrolled network cost instruction-cache stalls.
 template <int J>
 __device__ __forceinline__ void warp_bitonic(uint64_t (&v)[4], int lane) {
   constexpr int N = 32 * J;
-#pragma unroll
+#pragma unroll 1
   for (int k = 2; k <= N; k <<= 1) {
+    if (J == 4 && k >= 128) bitonic_cross<J, 64>(v, k, lane);
+    if (J >= 2 && k >= 64) bitonic_cross<J, 32>(v, k, lane);
+#pragma unroll 1
+    for (int m = min(k >> 1, 16); m > 0; m >>= 1) {
 #pragma unroll
-    for (int m = k >> 1; m > 0; m >>= 1) {
-      if (m >= 32) {
-#pragma unroll
-        for (int j = 0; j < J; ++j) {
-          const int jp = j ^ (m >> 5);
-          if (jp > j) {
-            const int i = j * 32 + lane;
-            const bool up = (i & k) == 0;
-            const uint64_t x = v[j], y = v[jp];
-            const bool sw = (x > y) == up;
-            v[j] = sw ? y : x;
-            v[jp] = sw ? x : y;
-          }
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < J; ++j) {
-          const int i = j * 32 + lane;
-          const uint64_t x = v[j];
-          const uint64_t y = __shfl_xor_sync(0xffffffffu, x, m);
-          const bool up = (i & k) == 0, lower = (lane & m) == 0;
-          const uint64_t lo = x < y ? x : y, hi = x < y ? y : x;
-          v[j] = (lower == up) ? lo : hi;
-        }
+      for (int j = 0; j < J; ++j) {
+        const int i = j * 32 + lane;
+        const uint64_t x = v[j];
+        const uint64_t y = __shfl_xor_sync(0xffffffffu, x, m);
+        const bool up = (i & k) == 0, lower = (lane & m) == 0;
+        const uint64_t lo = x < y ? x : y, hi = x < y ? y : x;
+        v[j] = (lower == up) ? lo : hi;
       }
     }
   }
