@@ -1812,11 +1812,12 @@ __device__ __forceinline__ void bitonic_cross(uint64_t (&v)[4], int k, int lane)
 template <int J>
 __device__ __forceinline__ void warp_bitonic(uint64_t (&v)[4], int lane) {
   constexpr int N = 32 * J;
+  constexpr int kMU = 2;  // measured: 1 and 5 are slower
 #pragma unroll 1
   for (int k = 2; k <= N; k <<= 1) {
     if (J == 4 && k >= 128) bitonic_cross<J, 64>(v, k, lane);
     if (J >= 2 && k >= 64) bitonic_cross<J, 32>(v, k, lane);
-#pragma unroll 1
+#pragma unroll kMU
     for (int m = min(k >> 1, 16); m > 0; m >>= 1) {
 #pragma unroll
       for (int j = 0; j < J; ++j) {
