@@ -1846,18 +1846,18 @@ __device__ __noinline__ void sort_keys_scratch(uint64_t* keys, uint16_t* refs, u
   __syncwarp();
   for (uint32_t k = 2; k <= N; k <<= 1)
     for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-      for (uint32_t i = lane; i < N; i += 32) {
-        const uint32_t ixj = i ^ j;
-        if (ixj > i) {
-          const uint64_t x = keys[i], y = keys[ixj];
-          const bool up = (i & k) == 0;
-          if ((x > y) == up) {
-            keys[i] = y;
-            keys[ixj] = x;
-            const uint16_t t = refs[i];
-            refs[i] = refs[ixj];
-            refs[ixj] = t;
-          }
+      // one compare-exchange pair per lane step: pair p -> (i, i + j), i
+      // with bit log2(j) clear
+      for (uint32_t p = lane; p < N / 2; p += 32) {
+        const uint32_t i = ((p & ~(j - 1u)) << 1) | (p & (j - 1u)), ixj = i | j;
+        const uint64_t x = keys[i], y = keys[ixj];
+        const bool up = (i & k) == 0;
+        if ((x > y) == up) {
+          keys[i] = y;
+          keys[ixj] = x;
+          const uint16_t t = refs[i];
+          refs[i] = refs[ixj];
+          refs[ixj] = t;
         }
       }
       __syncwarp();
