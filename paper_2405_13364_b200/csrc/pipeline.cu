@@ -457,12 +457,44 @@ __global__ void __launch_bounds__(kSetupBlock, 4) k_setup(Buffers B, uint32_t nb
     load_quad(B, q, &idx, p);
     cull_quad(fc, idx, p, clip, &o);
   }
-  uint32_t total;
-  const uint32_t rank = block_exclusive_scan<kSetupBlock>(o.reason == 0 ? 1u : 0u, &total);
-  const int deg = __syncthreads_count(o.reason == 1);
-  const int back = __syncthreads_count(o.reason == 2);
-  const int fru = __syncthreads_count(o.reason == 3);
-  const int bet = __syncthreads_count(o.reason == 4);
+  // visible-rank scan and the four cull-reason counts in two barriers: each
+  // warp posts its visible count and reason ballots, warp 0 scans and sums
+  constexpr int kWarps = kSetupBlock / 32;
+  __shared__ uint32_t s_wvis[kWarps], s_wreason[4][kWarps];
+  uint32_t rank, total;
+  {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned vis = __ballot_sync(0xffffffffu, o.reason == 0);
+    if (lane == 0) s_wvis[warp] = __popc(vis);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const unsigned m = __ballot_sync(0xffffffffu, o.reason == k + 1);
+      if (lane == 0) s_wreason[k][warp] = __popc(m);
+    }
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t x = lane < kWarps ? s_wvis[lane] : 0u;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+        if (lane >= d) x += y;
+      }
+      if (lane < kWarps) s_wvis[lane] = x;  // inclusive per-warp prefix
+    }
+    __syncthreads();
+    total = s_wvis[kWarps - 1];
+    rank = (warp ? s_wvis[warp - 1] : 0u) + __popc(vis & ((1u << lane) - 1u));
+  }
+  int deg = 0, back = 0, fru = 0, bet = 0;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      deg += (int)s_wreason[0][w];
+      back += (int)s_wreason[1][w];
+      fru += (int)s_wreason[2][w];
+      bet += (int)s_wreason[3][w];
+    }
+  }
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
     unsigned long long* state = B.block_state;
