@@ -1427,9 +1427,9 @@ struct __align__(16) StagedTri {
   float4 c[3];
   float4 mat;
   float n[9];
-  uint32_t flags;
+  uint32_t flags;  // 1 colours, 2 normals, 4 constant light, 8 constant colour, 16 flat depth
   float light;
-  uint32_t pad;
+  uint32_t pad;  // quantized depth when flag 16
 };
 static_assert(sizeof(StagedTri) == 208, "StagedTri layout");
 constexpr int kStageTris = 320;
@@ -1468,6 +1468,14 @@ __device__ __forceinline__ void stage_triangle(const FrameConst& fc, const Buffe
     dst->n[3 * k + 2] = nn.z;
   }
   uint32_t fl = sr.flags;
+  dst->pad = 0;
+  if (t.dz.a == 0.0 && t.dz.b == 0.0) {
+    // flat depth plane: (0*x + 0*y) + c is c (or a zero, which quantizes
+    // like c) for every finite pixel centre, so the quantized depth is the
+    // triangle's (bit-identical to evaluating it per sample)
+    dst->pad = quantize_depth(t.dz.c);
+    fl |= 16u;
+  }
   if (!(fl & 2u)) {
     const float4 n0 = sr.n[0];
     float n[3] = {n0.x, n0.y, n0.z};
@@ -1487,9 +1495,13 @@ __device__ __forceinline__ float4 shade_staged(const FrameConst& fc, const Stage
                                                int py, uint32_t* qd) {
   const double x = (double)px + 0.5, y = (double)py + 0.5;
   const Fn3 f0 = {T.e[0], T.e[1], T.e[2]}, f1 = {T.e[3], T.e[4], T.e[5]}, f2 = {T.e[6], T.e[7], T.e[8]};
-  const Fn3 fz = {T.dz[0], T.dz[1], T.dz[2]};
-  *qd = quantize_depth(eval(fz, x, y));
   const uint32_t fl = T.flags;
+  if (fl & 16u) {
+    *qd = T.pad;  // flat depth plane (stage_triangle)
+  } else {
+    const Fn3 fz = {T.dz[0], T.dz[1], T.dz[2]};
+    *qd = quantize_depth(eval(fz, x, y));
+  }
   if (fl & 8u) return T.c[0];  // constant colour (barycentrics unused)
   const double e0 = eval(f0, x, y), e1 = eval(f1, x, y), e2 = eval(f2, x, y);
   const double sum = __dadd_rn(__dadd_rn(e0, e1), e2);
