@@ -2138,9 +2138,14 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
     }
     uint32_t qd = 0x3fffffu;
     if (count) {
-      const double cx = __dadd_rn(__dadd_rn(bpx0, __ddiv_rn((double)sx, (double)count)), 0.5);
-      const double cy = __dadd_rn(__dadd_rn(bpy0, __ddiv_rn((double)sy, (double)count)), 0.5);
-      qd = quantize_depth(eval(B.tri[rw.tri].dz, cx, cy));
+      const Fn3 dz = B.tri[rw.tri].dz;
+      if (dz.a == 0.0 && dz.b == 0.0) {
+        qd = quantize_depth(dz.c);  // flat plane: (±0 + ±0) + c quantizes like c at any centroid
+      } else {
+        const double cx = __dadd_rn(__dadd_rn(bpx0, __ddiv_rn((double)sx, (double)count)), 0.5);
+        const double cy = __dadd_rn(__dadd_rn(bpy0, __ddiv_rn((double)sy, (double)count)), 0.5);
+        qd = quantize_depth(eval(dz, cx, cy));
+      }
     }
     // (depth, is_large, triangle) orders exactly like the reference's
     // (depth, selection index): selection order is bin-list order. The
