@@ -381,6 +381,25 @@ def test_edge_all_culled():
     assert int(got["counters"][1]) == 0
 
 
+@pytest.mark.parametrize("df", [1, 3, 8])
+def test_edge_flat_depth_planes(df):
+    """Screen-parallel quads (depth plane a = b = 0, the plane every C2 quad
+    has) at the clip-volume depth bounds and in between, over and under a
+    sloped quad: libveil's flat-plane shortcuts (quantized depth staged per
+    triangle for shading, no centroid divisions for the extraction keys)
+    must give the same keys, order and image as per-sample evaluation."""
+    b = clip_scene(96, 64)
+    b.pixel_rect(-4, -4, 100, 70, 0.0, (0.9, 0.1, 0.1, 0.4))    # z = 0: quantizes to 0
+    b.pixel_rect(8, 4, 90, 60, 1.0, (0.1, 0.9, 0.1, 0.4))       # z = w: quantizes to the max
+    b.pixel_rect(20, 10, 70, 50, 1e-30, (0.1, 0.1, 0.9, 0.5))   # below one depth quantum
+    b.pixel_rect(30, 0, 64, 64, 0.5, (0.7, 0.7, 0.2, 0.6))
+    b.pixel_rect(33, 3, 61, 61, 0.5, (0.2, 0.7, 0.7, 0.6))      # same depth: tie-break by triangle
+    ids = [b.vertex(-0.8, -0.8, 0.2, (1, 0.5, 0.2, 0.5)), b.vertex(0.8, -0.8, 0.6, (0.2, 1, 0.5, 0.5)),
+           b.vertex(0.8, 0.8, 0.9, (0.5, 0.2, 1, 0.5)), b.vertex(-0.8, 0.8, 0.4, (1, 1, 1, 0.5))]
+    b.quad_ids(ids)                                             # sloped depth plane
+    _edge_case(b, default_params(depth_filter_size=df))
+
+
 @pytest.mark.parametrize("w,h", [(1, 1), (33, 1), (1, 65), (31, 33)])
 def test_edge_tiny_and_ragged_viewports(w, h):
     b = clip_scene(w, h)
