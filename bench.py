@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="stack64k",
                     choices=["stack64k", "boxes1080", "tiny4m", "mixed16m"])
+    ap.add_argument("--df", type=int, default=3,
+                    help="depth_filter_size (reference default 3; >8 runs the heap filter)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="bound on the CPU-baseline sample (rank 0, N=1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -71,41 +73,89 @@ def peaks():
 
 # ----------------------------------------------------------------- workloads
 
-def boxes_orbit_camera(frame, w, h):
+def orbit_eye(frame):
+    """SURVEY.md 8(d) C3 camera path: 64 frames around the boxes."""
     import numpy as np
-    from paper_2405_13364_b200 import veil
 
     R = float(np.hypot(5.5, 9.0))
-    th = float(np.arctan2(5.5, 9.0)) + 2.0 * np.pi * frame / 64.0
-    eye = [R * np.sin(th), 4.5, R * np.cos(th)]
-    return veil.look_at(eye, [0, 0, 0], [0, 1, 0], 55.0, 0.5, 40.0, w, h), eye
+    th = float(np.arctan2(5.5, 9.0)) + 2.0 * np.pi * (frame % 64) / 64.0
+    return [R * np.sin(th), 4.5, R * np.cos(th)]
 
 
-def make_scene(workload):
-    """Returns (veil.Scene, description dict, camera_fn or None)."""
+# Every workload's description; identical in both arms' `config`.
+L2_NOTE = ("GPU arm: L2 flushed between timed frames (256 MiB write, outside the events); "
+           "CPU reference arm: not applicable")
+WORKLOADS = {
+    "stack64k": {"workload": "stack64k", "quads": 65536, "width": 1920, "height": 1080, "seed": 2,
+                 "depth_complexity": "~32", "baseline_config": 1},
+    "boxes1080": {"workload": "boxes1080", "quads": 54, "width": 1920, "height": 1080,
+                  "camera_path": "64-frame orbit", "baseline_config": 2},
+    "tiny4m": {"workload": "tiny4m", "quads": 4194304, "width": 3840, "height": 2160, "seed": 4,
+               "baseline_config": 3},
+    "mixed16m": {"workload": "mixed16m", "quads": 16777216, "width": 7680, "height": 4320, "seed": 5,
+                 "baseline_config": 4},
+}
+
+
+def workload_config(workload, df=3):
+    return dict(WORKLOADS[workload], depth_filter_size=df, l2=L2_NOTE)
+
+
+def workload_arrays(workload):
+    """The workload's host arrays WITHOUT libveil (numpy restatement of the
+    generators, oracle/workloads.py, checked equal to libveil's in
+    tests/test_workloads_cpu.py; the boxes scene from its golden fixture)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    if workload == "boxes1080":
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        from common import boxes_arrays
+
+        return boxes_arrays(1920, 1080)
+    import workloads
+
+    return workloads.workload(workload, WORKLOADS[workload]["seed"])
+
+
+def make_scene(workload, df=3):
+    """Our arm: (veil.Scene, config, camera_fn or None); camera_fn(i) ->
+    (matrix, eye) through libveil's look_at."""
     from paper_2405_13364_b200 import veil
 
-    if workload == "stack64k":
-        s = veil.Scene.workload("stack64k", 2)
-        return s, {"workload": "stack64k", "quads": 65536, "width": 1920, "height": 1080,
-                   "seed": 2, "depth_complexity": "~32"}, None
-    if workload == "tiny4m":
-        s = veil.Scene.workload("tiny4m", 4)
-        return s, {"workload": "tiny4m", "quads": 4194304, "width": 3840, "height": 2160,
-                   "seed": 4}, None
-    if workload == "mixed16m":
-        s = veil.Scene.workload("mixed16m", 5)
-        return s, {"workload": "mixed16m", "quads": 16777216, "width": 7680, "height": 4320,
-                   "seed": 5}, None
-    # boxes1080: the bundled boxes scene (captured from the reference loader
-    # into tests/golden/c1_boxes_256.npz) on the 64-frame orbit at 1080p
-    sys.path.insert(0, os.path.join(ROOT, "tests"))
-    from common import boxes_arrays
+    cfg = workload_config(workload, df)
+    if workload == "boxes1080":
+        s = veil.Scene.from_arrays(workload_arrays(workload))
 
-    arr = boxes_arrays(1920, 1080)
-    s = veil.Scene.from_arrays(arr)
-    return s, {"workload": "boxes1080", "quads": len(arr.quads), "width": 1920, "height": 1080,
-               "camera_path": "64-frame orbit"}, (lambda i: boxes_orbit_camera(i % 64, 1920, 1080))
+        def cam(i):
+            eye = orbit_eye(i)
+            return veil.look_at(eye, [0, 0, 0], [0, 1, 0], 55.0, 0.5, 40.0, 1920, 1080), eye
+
+        return s, cfg, cam
+    return veil.Scene.workload(workload, cfg["seed"]), cfg, None
+
+
+def reference_camera_fn(workload, lifted=False):
+    """The same orbit through the reference's own make_look_at_camera
+    (ref_shim vref_look_at; equal to libveil's, tests/test_workloads_cpu.py)."""
+    if workload != "boxes1080":
+        return None
+    import bindings
+
+    def cam(i):
+        eye = orbit_eye(i)
+        return bindings.ref_look_at(eye, [0, 0, 0], [0, 1, 0], 55.0, 0.5, 40.0, 1920, 1080, lifted), eye
+
+    return cam
+
+
+def reference_variant(arrays):
+    """Which reference build can render this viewport: the unmodified one
+    (<= 2560x2048), the limits-lifted one (<= 4096x4096, oracle/Makefile
+    ref-lifted), or none."""
+    if arrays.width <= 2560 and arrays.height <= 2048:
+        return False
+    if arrays.width <= 4096 and arrays.height <= 4096:
+        return True
+    return None
 
 
 def bytes_model(stats, width, height, a_q=32, a_v=8):
@@ -190,20 +240,21 @@ class ClockSampler:
 
 # ------------------------------------------------------------- CPU baseline
 
-def cpu_reference_run(arrays, frames_max, seconds, threads, camera_fn=None):
-    """The unmodified reference (oracle/_ref) through its own C API."""
+def cpu_reference_run(arrays, frames_max, seconds, threads, camera_fn=None, lifted=False,
+                      keep_first=False, depth_filter=3):
+    """The unmodified reference (oracle/_ref; the limits-lifted build for
+    viewports over 2560x2048) through its own C API, veil_render_scene.
+    keep_first: also return the first frame's image and mask (camera 0)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import bindings  # test/baseline infrastructure only
     from paper_2405_13364_b200.abi import default_params
 
-    if not bindings.ref_available():
+    if lifted is None or not bindings.ref_available(lifted):
         return None
-    fits = arrays.width <= 2560 and arrays.height <= 2048
-    if not fits:
-        return None
-    rs = bindings.RefScene.from_arrays(arrays)
-    p = default_params(thread_count=threads)
+    rs = bindings.RefScene.from_arrays(arrays, lifted)
+    p = default_params(thread_count=threads, depth_filter_size=depth_filter)
     times, frags = [], []
+    first = None
     t_end = time.perf_counter() + seconds
     i = 0
     while i < frames_max and (i == 0 or time.perf_counter() < t_end):
@@ -211,12 +262,35 @@ def cpu_reference_run(arrays, frames_max, seconds, threads, camera_fn=None):
             m, eye = camera_fn(i)
             rs.set_camera(m, eye)
         t0 = time.perf_counter()
-        _, _, rep = rs.render(p)
+        img, mask, rep = rs.render(p)
         times.append(time.perf_counter() - t0)
         frags.append(rep["fragments"])
+        if keep_first and first is None:
+            first = (img, mask, rep)
         i += 1
-    return {"frames": len(times), "seconds": sum(times), "fragments": sum(frags),
-            "gfrag_s": sum(frags) / sum(times) / 1e9, "ms_per_frame": 1e3 * sum(times) / len(times)}
+    out = {"frames": len(times), "seconds": sum(times), "fragments": sum(frags),
+           "gfrag_s": sum(frags) / sum(times) / 1e9, "ms_per_frame": 1e3 * sum(times) / len(times),
+           "build": "lifted" if lifted else "unmodified"}
+    if keep_first:
+        out["first"] = first
+    return out
+
+
+def image_parity(got_img, got_mask, ref_img, ref_mask, against):
+    """RGBA8 / invalid-mask comparison of one frame (north_star: <= 1/255 per
+    channel, max-abs and PSNR stated)."""
+    import numpy as np
+
+    a = np.asarray(got_img, dtype=np.int16).reshape(-1, 4)
+    b = np.asarray(ref_img, dtype=np.int16).reshape(-1, 4)
+    d = np.abs(a - b)
+    mse = float((d.astype(np.float64) ** 2).mean())
+    return {"identical": bool(np.array_equal(a, b) and np.array_equal(got_mask, ref_mask)),
+            "max_abs": int(d.max()) if d.size else 0,
+            "psnr": None if mse == 0 else 10.0 * float(np.log10(255.0 ** 2 / mse)),
+            "differing_px": int((d.max(axis=1) > 0).sum()),
+            "mask_differing_px": int((np.asarray(got_mask).reshape(-1) != np.asarray(ref_mask).reshape(-1)).sum()),
+            "against": against}
 
 
 # ------------------------------------------------------------------ our arm
@@ -256,10 +330,10 @@ def run_ours(args):
     torch.cuda.set_device(local)
     veil.set_device(local)
 
-    scene, cfg, camera_fn = make_scene(args.workload)
+    scene, cfg, camera_fn = make_scene(args.workload, args.df)
     arrays = scene.arrays() if rank == 0 else None
     W, H = cfg["width"], cfg["height"]
-    params = default_params()
+    params = default_params(depth_filter_size=args.df)
     shard = (rank, world)
     stream = torch.cuda.ExternalStream(scene.stream())
     flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device="cuda")
@@ -368,10 +442,11 @@ def run_ours(args):
                 del r
             e2e_ms = statistics.median(e2e_ms)
             e2e = {"value": fragments_per_frame / (e2e_ms * 1e-3) / 1e9, "unit": "Gfragments/s",
-                   "ms_per_step": e2e_ms, "h2d_bytes_per_step": 128 + 64,
+                   "ms_per_step": e2e_ms, "h2d_bytes_per_step": (128 + 64) if camera_fn else 64,
                    "d2h_bytes_per_step": int(px.nbytes + mk.nbytes),
-                   "path": "veil_scene_set_camera + veil_render_scene + veil_render_pixels/"
-                           "veil_render_invalid_mask (host RGBA8 + mask)"}
+                   "path": ("veil_scene_set_camera + " if camera_fn else "")
+                           + "veil_render_scene + veil_render_pixels/veil_render_invalid_mask "
+                             "(host RGBA8 + mask)"}
         else:
             host = torch.empty(W * H * 5, dtype=torch.uint8, pin_memory=True) if rank == 0 else None
             e2e_ms = []
@@ -394,7 +469,10 @@ def run_ours(args):
             e2e = {"value": fragments_per_frame / (e2e_ms * 1e-3) / 1e9, "unit": "Gfragments/s",
                    "ms_per_step": e2e_ms, "h2d_bytes_per_step": 128 + 64,
                    "d2h_bytes_per_step": W * H * 5,
-                   "path": "sharded device frame + NCCL tile gather + rank-0 readback"}
+                   "path": "sharded device frame + "
+                           + ("peer-memory framebuffer writes (CUDA IPC)" if peer
+                              else f"{args.dist_backend} tile gather")
+                           + " + rank-0 readback"}
 
     frame_check = None
     if args.check_frame:  # gathered frame vs an unsharded render of the same camera
@@ -444,20 +522,42 @@ def run_ours(args):
         if world > 1:
             launches += 2 * args.steps
         cpu = None
+        parity = None
         if world == 1 and not args.no_cpu_baseline:
             cores = os.cpu_count() or 1
-            ref = cpu_reference_run(arrays, 1000, args.cpu_seconds, cores, camera_fn)
+            lifted = reference_variant(arrays)
+            ref = cpu_reference_run(arrays, 1000, args.cpu_seconds, cores, camera_fn, lifted,
+                                    keep_first=True, depth_filter=args.df)
             if ref:
+                so = "oracle/_ref/libveilref_lifted.so" if lifted else "oracle/_ref/libveilref.so"
                 cpu = {"value": ref["gfrag_s"], "unit": "Gfragments/s", "cores": cores,
                        "kind": "reference",
                        "sample": f"{ref['frames']} full frame(s) of {cfg['workload']} via the "
-                                 f"reference's veil_render_scene (oracle/_ref), "
-                                 f"{ref['ms_per_frame']:.1f} ms/frame"}
+                                 f"reference's veil_render_scene ({so}"
+                                 + (", viewport/bin limits lifted" if lifted else "")
+                                 + f"), {ref['ms_per_frame']:.1f} ms/frame"}
                 # the reference is also timed with one worker thread
-                one = cpu_reference_run(arrays, 3, min(6.0, args.cpu_seconds), 1, camera_fn)
+                one = cpu_reference_run(arrays, 2, min(6.0, args.cpu_seconds), 1, camera_fn, lifted,
+                                        depth_filter=args.df)
                 if one:
                     cpu["single_thread"] = {"value": one["gfrag_s"], "ms_per_frame": one["ms_per_frame"],
                                             "frames": one["frames"]}
+                # parity of the timed frame: the reference's first frame (camera 0)
+                # against ours through the C ABI, same camera
+                if camera_fn:
+                    m, eye = camera_fn(0)
+                    scene.set_camera(m, eye)
+                r0 = veil.render(scene, params)
+                img, mask, rep = ref["first"]
+                parity = image_parity(r0.pixels(), r0.invalid_mask(), img, mask,
+                                      f"reference veil_render_scene ({so}), camera 0")
+                st0 = r0.stats()
+                parity["counters_equal"] = (
+                    [int(st0.samples), int(st0.fragments), int(st0.tri_half_blocks), int(st0.segments),
+                     int(st0.invalid_pixels)]
+                    == [int(rep["samples"]), int(rep["fragments"]), int(rep["tri_half_blocks"]),
+                        int(rep["segments"]), int(rep["invalid_pixels"]["count"])])
+                del r0
         clk = clocks.summary()
         result = {
             "metric": METRIC,
@@ -472,11 +572,12 @@ def run_ours(args):
             "vs_baseline": None,
             "dtype": "f64+f32",
             "data": "synthetic",
-            "config": dict(cfg, parallelism=f"bins interleaved over {world} GPU(s), setup replicated"
-                                              + (", peer-memory framebuffer gather" if peer else
-                                                 (", NCCL tile gather" if world > 1 else "")),
-                           fragments_per_frame=int(fragments_per_frame),
-                           l2="flushed between timed frames (256 MiB write, outside the events)"),
+            "config": cfg,
+            "parallelism": f"bins interleaved over {world} GPU(s), setup replicated"
+                           + (", peer-memory framebuffer gather" if peer else
+                              (f", {args.dist_backend} tile gather" if world > 1 else "")),
+            "fragments_per_frame": int(fragments_per_frame),
+            "parity": parity,
             "e2e": e2e,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu.get("raster_dram_bytes"),
@@ -504,28 +605,49 @@ def run_ours(args):
     return result
 
 
+def loaded_native_libs():
+    """Shared objects from this repo mapped into the process (/proc/self/maps)."""
+    libs = set()
+    try:
+        with open("/proc/self/maps") as f:
+            for line in f:
+                p = line.split()[-1] if line.split() else ""
+                if p.startswith(ROOT) and p.endswith(".so"):
+                    libs.add(os.path.relpath(p, ROOT))
+    except OSError:
+        pass
+    return sorted(libs)
+
+
 def run_reference(args):
+    """The reference arm: the unmodified reference's own CPU implementation
+    (oracle/_ref, built from /root/reference by oracle/Makefile; the
+    limits-lifted build for 3840x2160) through its own C API, on all host
+    cores, on our arm's workload/config. The input arrays come from the numpy
+    generators, so libveil.so is never mapped into this process."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return None
-    from paper_2405_13364_b200 import veil
-
-    scene, cfg, camera_fn = make_scene(args.workload)
-    arrays = scene.arrays()
+    cfg = workload_config(args.workload, args.df)
+    arrays = workload_arrays(args.workload)
     cores = os.cpu_count() or 1
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import bindings
 
-    fits = arrays.width <= 2560 and arrays.height <= 2048
-    if not bindings.ref_available() or not fits:
-        why = ("oracle/_ref missing" if not bindings.ref_available()
-               else "viewport exceeds the reference's 2560x2048 limit")
-        return {"impl": "reference", "unavailable": why, "metric": METRIC}
+    lifted = reference_variant(arrays)
+    if lifted is None or not bindings.ref_available(lifted):
+        why = ("viewport exceeds the reference's limits (2560x2048; 4096x4096 lifted)" if lifted is None
+               else "oracle/_ref build missing")
+        return {"impl": "reference", "unavailable": why, "metric": METRIC, "config": cfg}
     from paper_2405_13364_b200.abi import default_params
 
-    rs = bindings.RefScene.from_arrays(arrays)
-    p = default_params(thread_count=cores)
+    camera_fn = reference_camera_fn(args.workload, lifted)
+    rs = bindings.RefScene.from_arrays(arrays, lifted)
+    p = default_params(thread_count=cores, depth_filter_size=args.df)
+    libs = loaded_native_libs()
+    if any("libveil.so" in x for x in libs):
+        raise RuntimeError(f"reference arm mapped libveil: {libs}")
     for i in range(args.warmup):
         if camera_fn:
             rs.set_camera(*camera_fn(i))
@@ -540,15 +662,19 @@ def run_reference(args):
         frags += rep["fragments"]
     ms = 1e3 * sum(times) / len(times)
     value = frags / sum(times) / 1e9
+    so = "oracle/_ref/libveilref_lifted.so" if lifted else "oracle/_ref/libveilref.so"
     return {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "Gfragments/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64+f32",
-        "data": "synthetic", "config": dict(cfg, parallelism=f"{cores} host threads"),
+        "data": "synthetic", "config": cfg, "parallelism": f"{cores} host threads",
+        "fragments_per_frame": frags // max(1, args.steps),
+        "native_so_loaded": loaded_native_libs(),
         "cpu_baseline": {"value": value, "unit": "Gfragments/s", "cores": cores,
                          "kind": "reference",
                          "sample": f"{args.steps} full frame(s) of {cfg['workload']} through the "
-                                   f"reference's veil_render_scene (oracle/_ref)"},
+                                   f"reference's veil_render_scene ({so}"
+                                   + (", viewport/bin limits lifted" if lifted else "") + ")"},
         "e2e": {"value": value, "unit": "Gfragments/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }

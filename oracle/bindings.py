@@ -24,6 +24,8 @@ from paper_2405_13364_b200.abi import (
 HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "liboracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libveilref.so")
+# limits-lifted build (viewport 4096x4096, 16384 bins; `make -C oracle ref-lifted`)
+REF_LIFTED_SO = os.path.join(HERE, "_ref", "libveilref_lifted.so")
 
 
 class CheckerError(RuntimeError):
@@ -34,7 +36,7 @@ class CheckerError(RuntimeError):
 
 
 _oracle = None
-_ref = None
+_refs = {}
 
 
 def oracle_lib():
@@ -55,14 +57,13 @@ def oracle_lib():
     return _oracle
 
 
-def ref_available():
-    return os.path.exists(REF_SO)
+def ref_available(lifted=False):
+    return os.path.exists(REF_LIFTED_SO if lifted else REF_SO)
 
 
-def ref_lib():
-    global _ref
-    if _ref is None:
-        lib = C.CDLL(REF_SO)
+def ref_lib(lifted=False):
+    if lifted not in _refs:
+        lib = C.CDLL(REF_LIFTED_SO if lifted else REF_SO)
         lib.vref_scene_create.argtypes = [C.POINTER(SceneDesc), C.POINTER(C.c_void_p)]
         lib.vref_scene_create.restype = C.c_int
         lib.vref_scene_describe.argtypes = [C.c_void_p, C.POINTER(SceneDesc)]
@@ -94,8 +95,8 @@ def ref_lib():
         lib.veil_render_height.argtypes = [C.c_void_p]
         lib.veil_render_destroy.argtypes = [C.c_void_p]
         lib.veil_scene_group_quads.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
-        _ref = lib
-    return _ref
+        _refs[lifted] = lib
+    return _refs[lifted]
 
 
 def _collect(getter, handle, names=None):
@@ -134,24 +135,25 @@ def oracle_render(scene: SceneArrays, params=None, extended=False, names=None):
 class RefScene:
     """A scene inside the reference library."""
 
-    def __init__(self, handle):
+    def __init__(self, handle, lifted=False):
         self.h = C.c_void_p(handle)
+        self.lib = ref_lib(lifted)
 
     def __del__(self):
-        if getattr(self, "h", None) and _ref is not None:
-            _ref.vref_scene_forget(self.h)
-            _ref.veil_scene_destroy(self.h)
+        if getattr(self, "h", None) and getattr(self, "lib", None) is not None:
+            self.lib.vref_scene_forget(self.h)
+            self.lib.veil_scene_destroy(self.h)
             self.h = None
 
     @classmethod
-    def from_arrays(cls, scene: SceneArrays):
-        lib = ref_lib()
+    def from_arrays(cls, scene: SceneArrays, lifted=False):
+        lib = ref_lib(lifted)
         desc = scene.desc()
         h = C.c_void_p()
         st = lib.vref_scene_create(C.byref(desc), C.byref(h))
         if st != 0:
             raise CheckerError(st, lib.vref_last_error().decode())
-        return cls(h.value)
+        return cls(h.value, lifted)
 
     @classmethod
     def load(cls, mesh, mtl=None, cam=None):
@@ -172,32 +174,54 @@ class RefScene:
             raise CheckerError(st, lib.veil_last_error().decode())
         return cls(h.value)
 
-    def set_viewport(self, w, h):
-        st = ref_lib().veil_scene_set_viewport(self.h, w, h)
+    @classmethod
+    def synthetic_params(cls, kind, seed, width, height, layers=0, triangles=0, sheets=0):
+        """generate_synthetic_scene with SyntheticParams (acceptance.cpp:80-101)."""
+        lib = ref_lib()
+        lib.vref_scene_synthetic_params.argtypes = [C.c_char_p, C.c_uint64, C.c_int, C.c_int, C.c_int,
+                                                    C.c_int, C.c_int, C.POINTER(C.c_void_p)]
+        h = C.c_void_p()
+        st = lib.vref_scene_synthetic_params(kind.encode(), seed, width, height, layers, triangles,
+                                             sheets, C.byref(h))
         if st != 0:
-            raise CheckerError(st, ref_lib().veil_last_error().decode())
+            raise CheckerError(st, lib.vref_last_error().decode())
+        return cls(h.value)
+
+    def measure_disorder(self, params=None):
+        """RenderConfig::measure_disorder of the reference pipeline."""
+        self.lib.vref_measure_disorder.argtypes = [C.c_void_p, C.POINTER(RenderParams), C.POINTER(C.c_int)]
+        out = C.c_int(0)
+        st = self.lib.vref_measure_disorder(self.h, C.byref(params or default_params()), C.byref(out))
+        if st != 0:
+            raise CheckerError(st, self.lib.vref_last_error().decode())
+        return out.value
+
+    def set_viewport(self, w, h):
+        st = self.lib.veil_scene_set_viewport(self.h, w, h)
+        if st != 0:
+            raise CheckerError(st, self.lib.veil_last_error().decode())
 
     def set_camera(self, matrix, eye=None):
         m = (C.c_double * 16)(*[float(x) for x in np.asarray(matrix).reshape(16)])
         e = None if eye is None else (C.c_double * 3)(*[float(x) for x in eye])
-        st = ref_lib().veil_scene_set_camera(self.h, m, e)
+        st = self.lib.veil_scene_set_camera(self.h, m, e)
         if st != 0:
-            raise CheckerError(st, ref_lib().veil_last_error().decode())
+            raise CheckerError(st, self.lib.veil_last_error().decode())
 
     def group_quads(self):
         d = C.c_double(0)
-        st = ref_lib().veil_scene_group_quads(self.h, C.byref(d))
+        st = self.lib.veil_scene_group_quads(self.h, C.byref(d))
         if st != 0:
-            raise CheckerError(st, ref_lib().veil_last_error().decode())
+            raise CheckerError(st, self.lib.veil_last_error().decode())
         return d.value
 
     def arrays(self) -> SceneArrays:
         d = SceneDesc()
-        ref_lib().vref_scene_describe(self.h, C.byref(d))
+        self.lib.vref_scene_describe(self.h, C.byref(d))
         return SceneArrays.from_desc(d)
 
     def dump(self, params=None, names=None):
-        lib = ref_lib()
+        lib = self.lib
         params = params or default_params()
         h = C.c_void_p()
         st = lib.vref_dump_run(self.h, C.byref(params), C.byref(h))
@@ -211,7 +235,7 @@ class RefScene:
 
     def render(self, params=None):
         """The reference's own C API render (veil_render_scene)."""
-        lib = ref_lib()
+        lib = self.lib
         params = params or default_params()
         r = C.c_void_p()
         st = lib.veil_render_scene(self.h, C.byref(params), C.byref(r))
@@ -227,5 +251,18 @@ class RefScene:
             lib.veil_render_destroy(r)
 
 
-def ref_dump_arrays(scene: SceneArrays, params=None, names=None):
-    return RefScene.from_arrays(scene).dump(params, names)
+def ref_look_at(frm, at, up, fov_deg, near, far, width, height, lifted=False):
+    """The reference's make_look_at_camera (scene.cpp:128-158) -> row-major 4x4."""
+    lib = ref_lib(lifted)
+    arr = lambda v: (C.c_double * 3)(*[float(x) for x in v])
+    out = (C.c_double * 16)()
+    lib.vref_look_at.restype = C.c_int
+    lib.vref_look_at.argtypes = [C.c_double * 3] * 3 + [C.c_double] * 3 + [C.c_int] * 2 + [C.c_double * 16]
+    st = lib.vref_look_at(arr(frm), arr(at), arr(up), fov_deg, near, far, width, height, out)
+    if st != 0:
+        raise CheckerError(st, lib.vref_last_error().decode())
+    return np.array(list(out))
+
+
+def ref_dump_arrays(scene: SceneArrays, params=None, names=None, lifted=False):
+    return RefScene.from_arrays(scene, lifted).dump(params, names)

@@ -22,6 +22,7 @@
 #include "veil/scanline.hpp"
 #include "veil/setup.hpp"
 #include "veil/shading.hpp"
+#include "veil/synthetic.hpp"
 #include "veil/thread_pool.hpp"
 #include "../include/veil_cuda.h"
 
@@ -456,5 +457,51 @@ const void* vref_dump_array(const vref_dump* d, const char* name, uint64_t* coun
 void vref_dump_destroy(vref_dump* d) { delete d; }
 
 void vref_scene_forget(const veil_scene* s) { g_material_views.erase(s); }
+
+// generate_synthetic_scene with explicit SyntheticParams (synthetic.hpp:36-47;
+// the C API's veil_scene_synthetic uses the defaults) -- the scenes of the
+// reference's acceptance criterion 1 (acceptance.cpp:80-101).
+veil_status vref_scene_synthetic_params(const char* kind, uint64_t seed, int width, int height,
+                                        int layers, int triangles, int sheets, veil_scene** out) {
+  if (!kind || !out) return VEIL_ERR_INVALID_ARG;
+  return shim_guard([&] {
+    auto k = veil::parse_synthetic_kind(kind);
+    if (!k) throw veil::Error(veil::ErrorCode::invalid_argument, "unknown synthetic kind");
+    veil::SyntheticParams sp;
+    sp.width = width;
+    sp.height = height;
+    if (layers > 0) sp.layers = layers;
+    if (triangles > 0) sp.triangles = triangles;
+    if (sheets > 0) sp.sheets = sheets;
+    auto s = std::make_unique<veil_scene>();
+    s->scene = veil::generate_synthetic_scene(*k, seed, sp);
+    *out = s.release();
+  });
+}
+
+// The reference pipeline's max per-pixel sort disorder (RenderConfig::
+// measure_disorder, scene.hpp:108; raster.cpp:286-297), which the C API
+// cannot reach; acceptance criterion 1 renders with DF = this value.
+veil_status vref_measure_disorder(const veil_scene* s, const veil_render_params* p, int* out) {
+  if (!s || !p || !out) return VEIL_ERR_INVALID_ARG;
+  return shim_guard([&] {
+    veil::RenderConfig c = config_from(p);
+    c.measure_disorder = true;
+    *out = veil::render_pipeline(s->scene, c).report.max_disorder;
+  });
+}
+
+// The reference's own make_look_at_camera (scene.cpp:128-158), so bench.py's
+// reference arm builds its orbit cameras without libveil.
+veil_status vref_look_at(const double from[3], const double at[3], const double up[3], double fov_deg,
+                         double near_z, double far_z, int width, int height, double out[16]) {
+  if (!from || !at || !up || !out) return VEIL_ERR_INVALID_ARG;
+  return shim_guard([&] {
+    const veil::Camera c = veil::make_look_at_camera({from[0], from[1], from[2]}, {at[0], at[1], at[2]},
+                                                     {up[0], up[1], up[2]}, fov_deg, near_z, far_z,
+                                                     width, height);
+    for (int i = 0; i < 16; ++i) out[i] = c.view_projection.m[i / 4][i % 4];
+  });
+}
 
 }  // extern "C"

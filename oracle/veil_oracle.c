@@ -453,6 +453,7 @@ typedef struct {
   uint8_t* image;
   uint8_t* mask;
   uint64_t* hash;
+  uint64_t* hash_std;
   uint32_t* emit;
   int df;
   int threshold;
@@ -1020,8 +1021,17 @@ static uint64_t sample_key(const ctx_t* c, uint32_t q, uint32_t tri) {
   return ((uint64_t)q << 24) | (tri & 0xffffffu); /* sample_sort_key, raster.hpp:95-97 */
 }
 
+/* The sample key in the reference's 24-bit-triangle format whatever the
+ * mode: (q << 24) | tri24. In extended mode emit_hash_std hashes these, so a
+ * limits-lifted reference build (whose keys are 24-bit) pins the blend order
+ * of frames that need only the lifted viewport / bin limits. */
+static uint64_t std_key(const ctx_t* c, uint64_t k) {
+  if (!c->extended) return k;
+  return ((k >> 32) << 24) | (k & 0xffffffu);
+}
+
 static void write_pixel(ctx_t* c, int px, int py, const float acc[4], int invalid,
-                        uint64_t hash, uint32_t emitted) {
+                        uint64_t hash, uint64_t hash_std, uint32_t emitted) {
   float o[4] = {acc[0], acc[1], acc[2], acc[3]};
   /* blend_front_to_back(acc, background) */
   float t = 1.0f - o[3];
@@ -1031,6 +1041,7 @@ static void write_pixel(ctx_t* c, int px, int py, const float acc[4], int invali
   for (int i = 0; i < 4; ++i) c->image[pix * 4 + i] = quantize_channel(o[i]);
   c->mask[pix] = invalid ? 1 : 0;
   c->hash[pix] = hash;
+  c->hash_std[pix] = hash_std;
   c->emit[pix] = emitted;
 }
 
@@ -1043,14 +1054,14 @@ static void shade_half_block(ctx_t* c, bin_scratch* s, int bin, int hb, bin_stat
   int py0 = byi * BIN + (block / 4) * 8 + half * 4;
   float acc[32][4];
   int invalid[32], saturated[32];
-  uint64_t hh[32];
+  uint64_t hh[32], hs[32];
   uint32_t cnt[32];
   memset(acc, 0, sizeof acc);
   memset(invalid, 0, sizeof invalid);
   memset(saturated, 0, sizeof saturated);
   memset(cnt, 0, sizeof cnt);
   for (int p = 0; p < 32; ++p) {
-    hh[p] = kHashSeed;
+    hh[p] = hs[p] = kHashSeed;
     fl[p].n = 0;
     fl[p].any = 0;
     fl[p].max_key = 0;
@@ -1076,6 +1087,7 @@ static void shade_half_block(ctx_t* c, bin_scratch* s, int bin, int hb, bin_stat
           df_pop(&fl[p], &k2, c2, &ooo);
           blend(acc[p], c2);
           hh[p] = (hh[p] ^ k2) * kHashPrime;
+          hs[p] = (hs[p] ^ std_key(c, k2)) * kHashPrime;
           ++cnt[p];
           ++st->samples;
           if (ooo) invalid[p] = 1;
@@ -1101,6 +1113,7 @@ static void shade_half_block(ctx_t* c, bin_scratch* s, int bin, int hb, bin_stat
         if (done) continue;
         blend(acc[p], c2);
         hh[p] = (hh[p] ^ k2) * kHashPrime;
+        hs[p] = (hs[p] ^ std_key(c, k2)) * kHashPrime;
         ++cnt[p];
         ++st->samples;
         if (ooo) invalid[p] = 1;
@@ -1116,7 +1129,7 @@ static void shade_half_block(ctx_t* c, bin_scratch* s, int bin, int hb, bin_stat
       int px = px0 + lx;
       if (px >= c->cam.w) break;
       int p = ly * 8 + lx;
-      write_pixel(c, px, py, acc[p], invalid[p], hh[p], cnt[p]);
+      write_pixel(c, px, py, acc[p], invalid[p], hh[p], hs[p], cnt[p]);
     }
   }
 }
@@ -1187,13 +1200,14 @@ static void render_abuffer(ctx_t* c, uint64_t* total_samples) {
     for (int px = 0; px < w; ++px) {
       qsort(lists[px], n[px], sizeof(frag_t), cmp_frag);
       float acc[4] = {0, 0, 0, 0};
-      uint64_t hh = kHashSeed;
+      uint64_t hh = kHashSeed, hs = kHashSeed;
       for (uint32_t i = 0; i < n[px]; ++i) {
         blend(acc, lists[px][i].col);
         hh = (hh ^ lists[px][i].key) * kHashPrime;
+        hs = (hs ^ std_key(c, lists[px][i].key)) * kHashPrime;
       }
       *total_samples += n[px];
-      write_pixel(c, px, py, acc, 0, hh, n[px]);
+      write_pixel(c, px, py, acc, 0, hh, hs, n[px]);
     }
   }
   for (int px = 0; px < w; ++px) free(lists[px]);
@@ -1307,15 +1321,16 @@ int vo_render(const veil_scene_desc* sc, const veil_render_params* prm, int exte
   c.image = (uint8_t*)xcalloc(npx * 4, 1);
   c.mask = (uint8_t*)xcalloc(npx, 1);
   c.hash = (uint64_t*)xcalloc(npx, 8);
+  c.hash_std = (uint64_t*)xcalloc(npx, 8);
   c.emit = (uint32_t*)xcalloc(npx, 4);
   for (size_t i = 0; i < npx; ++i) {
-    c.hash[i] = kHashSeed;
+    c.hash[i] = c.hash_std[i] = kHashSeed;
     for (int k = 0; k < 4; ++k) c.image[i * 4 + k] = quantize_channel(c.bg[k]);
   }
 
   st = run_setup(f, &c);
   if (st != VEIL_OK) {
-    free(c.image), free(c.mask), free(c.hash), free(c.emit);
+    free(c.image), free(c.mask), free(c.hash), free(c.hash_std), free(c.emit);
     return st;
   }
   export_setup(f, &c);
@@ -1329,7 +1344,7 @@ int vo_render(const veil_scene_desc* sc, const veil_render_params* prm, int exte
     st = run_binning(f, &c);
     if (st != VEIL_OK) {
       free(counters);
-      free(c.image), free(c.mask), free(c.hash), free(c.emit);
+      free(c.image), free(c.mask), free(c.hash), free(c.hash_std), free(c.emit);
       return st;
     }
     int nb = c.nbins;
@@ -1352,7 +1367,7 @@ int vo_render(const veil_scene_desc* sc, const veil_render_params* prm, int exte
     if (prm->limit_high_thb) high.max_thb = prm->limit_high_thb;
     if (low.max_tbr > high.max_tbr || low.max_thb > high.max_thb) {
       free(counters);
-      free(c.image), free(c.mask), free(c.hash), free(c.emit);
+      free(c.image), free(c.mask), free(c.hash), free(c.hash_std), free(c.emit);
       return fail(f, VEIL_ERR_INVALID_ARG, "low rasterizer limits exceed high limits");
     }
 
@@ -1416,7 +1431,7 @@ int vo_render(const veil_scene_desc* sc, const veil_render_params* prm, int exte
     add_array(f, "thb_prefix", thb_pre.p, thb_pre.n / 4);
     if (st != VEIL_OK) {
       free(counters);
-      free(c.image), free(c.mask), free(c.hash), free(c.emit);
+      free(c.image), free(c.mask), free(c.hash), free(c.hash_std), free(c.emit);
       return st;
     }
     uint64_t inv = 0;
@@ -1442,6 +1457,7 @@ int vo_render(const veil_scene_desc* sc, const veil_render_params* prm, int exte
   add_array(f, "image", c.image, npx * 4);
   add_array(f, "mask", c.mask, npx);
   add_array(f, "emit_hash", c.hash, npx);
+  add_array(f, "emit_hash_std", c.hash_std, npx);
   add_array(f, "emit_count", c.emit, npx);
   add_array(f, "counters", counters, 9);
   free(c.vq);

@@ -142,7 +142,7 @@ DUMP_DTYPES = {
     "bin_dims": np.int32, "bin_quad_counts": np.uint32, "bin_tri_counts": np.uint32,
     "bin_offsets": np.uint32, "bin_categories": np.uint8, "bin_items": np.uint32,
     "bin_path": np.uint8, "thb_offsets": np.uint64, "thb": np.uint64, "thb_tri": np.uint32,
-    "thb_prefix": np.uint32, "emit_hash": np.uint64, "emit_count": np.uint32,
+    "thb_prefix": np.uint32, "emit_hash": np.uint64, "emit_hash_std": np.uint64, "emit_count": np.uint32,
     "image": np.uint8, "mask": np.uint8, "counters": np.uint64,
     "tbr_offsets": np.uint64, "tbr": np.uint64, "reenum_image": np.uint8, "reenum_mask": np.uint8,
 }

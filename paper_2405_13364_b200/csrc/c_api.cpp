@@ -365,6 +365,8 @@ veil_status veil_render_device(const veil_scene* scene, const veil_render_params
   o.host_readback = false;
   if (o.params.flags & VEIL_RENDER_REFERENCE) return bad_arg("device frames use the pipeline");
   if (shard) {
+    if (shard->world_size < 1 || shard->rank < 0 || shard->rank >= shard->world_size)
+      return bad_arg("invalid shard");
     o.rank = shard->rank;
     o.world_size = shard->world_size;
   }

@@ -197,6 +197,11 @@ struct Buffers {
   uint4* seg_queue;  // half-blocks for the segment kernel: (bin * 32 + hb | high pass << 31, off, cnt, frags)
   uint16_t* pool_slot;  // per THB: the triangle's position in the bin list (k_shade staging slot)
   uint2* lpairs;        // (large triangle, bin row) pairs for k_bin_large
+  // depth filters above 8 (HeapFilter): nodes per lane, and the global
+  // scratch ([CTA][warp][node/slot][lane]) when they do not fit shared memory
+  uint8_t* heap_g;
+  uint32_t heap_cap;
+  uint32_t heap_ctas;  // grid cap of the shading kernels when heap_g is used
   Counters* ctr;
 };
 
@@ -1151,6 +1156,115 @@ struct SlotFilter {
   }
 };
 
+// Depth filter for capacities above 8 (DF 9 .. 32768): a binary min-heap per
+// pixel in memory (shared memory when the block's heaps fit next to the
+// staged triangles, else this warp's slice of a global scratch that stays
+// L1/L2-resident). The reference's filter (depth_filter.hpp:31-92) keeps at
+// most k entries and, when an insert overflows it, emits the minimum of
+// (entries + new): with keys unique that is exactly heap replace-top, and its
+// ascending flush is repeated pop-min, so emission order and the out-of-order
+// flag are the reference's for any k. Heap nodes hold (compact key << 15 |
+// colour slot): the colours stay in their slots ([slot][32 lanes], a lane's
+// column) and a sift moves 8 bytes per level. The compact key keeps the
+// (depth, triangle) order in 49 bits: (q << 24 | tri24), or (q << 27 | tri27)
+// with extended limits. A slot is the entry's insertion index: filters are
+// reset per half-block and drained only at its end, so slots are never
+// recycled except by the replace-top, which reuses the emitted entry's slot.
+// Samples per pixel <= THBs per half-block <= the high-path THB limit, so
+// the heap needs min(k, that limit) nodes (host: heap_cap).
+struct HeapFilter {
+  uint64_t* hk;  // this lane's node 0; node i at hk[i * 32]
+  float4* hc;    // this lane's colour slot 0; slot s at hc[s * 32]
+  int n;
+  uint64_t max_key;
+  bool any;
+
+  static constexpr int kSlotBits = 15;
+  static constexpr uint64_t kSlotMask = (1ull << kSlotBits) - 1ull;
+
+  __device__ __forceinline__ void reset(uint64_t* keys, float4* cols) {
+    hk = keys;
+    hc = cols;
+    n = 0;
+    max_key = 0;
+    any = false;
+  }
+  __device__ __forceinline__ static uint64_t pack(uint64_t k) {
+    return c_fc.extended ? (((k >> 32) << 27) | (k & 0x7ffffffull)) : k;
+  }
+  __device__ __forceinline__ static uint64_t unpack(uint64_t ck) {
+    return c_fc.extended ? (((ck >> 27) << 32) | (ck & 0x7ffffffull)) : ck;
+  }
+  __device__ __forceinline__ void note(uint64_t pk, bool* ooo) {
+    *ooo = any && pk < max_key;
+    if (!any || pk > max_key) max_key = pk;
+    any = true;
+  }
+  __device__ __forceinline__ void sift_down(uint64_t e) {
+    int i = 0;
+    for (;;) {
+      int l = 2 * i + 1;
+      if (l >= n) break;
+      uint64_t el = hk[(size_t)l * 32];
+      if (l + 1 < n) {
+        const uint64_t er = hk[(size_t)(l + 1) * 32];
+        if (er < el) el = er, ++l;
+      }
+      if (e < el) break;
+      hk[(size_t)i * 32] = el;
+      i = l;
+    }
+    hk[(size_t)i * 32] = e;
+  }
+  __device__ __forceinline__ bool push(int cap, uint64_t k, float4 c, uint64_t* pk, float4* pc,
+                                       bool* ooo) {
+    if (n < cap) {  // sift the new entry up from the next leaf
+      hc[(size_t)n * 32] = c;
+      const uint64_t e = (pack(k) << kSlotBits) | (uint64_t)n;
+      int i = n++;
+      while (i > 0) {
+        const int par = (i - 1) >> 1;
+        const uint64_t ep = hk[(size_t)par * 32];
+        if (ep < e) break;
+        hk[(size_t)i * 32] = ep;
+        i = par;
+      }
+      hk[(size_t)i * 32] = e;
+      return false;
+    }
+    const uint64_t e0 = hk[0];
+    const uint64_t ck = pack(k);
+    if (ck < (e0 >> kSlotBits)) {  // the new sample is the minimum: it falls straight out
+      *pk = k;
+      *pc = c;
+      note(k, ooo);
+      return true;
+    }
+    const uint32_t s0 = (uint32_t)(e0 & kSlotMask);
+    *pk = unpack(e0 >> kSlotBits);
+    *pc = hc[(size_t)s0 * 32];
+    hc[(size_t)s0 * 32] = c;
+    note(*pk, ooo);
+    sift_down((ck << kSlotBits) | s0);  // replace-top
+    return true;
+  }
+  __device__ __forceinline__ void pop(uint64_t* pk, float4* pc, bool* ooo) {
+    const uint64_t e0 = hk[0];
+    *pk = unpack(e0 >> kSlotBits);
+    *pc = hc[(size_t)(e0 & kSlotMask) * 32];
+    --n;
+    if (n > 0) sift_down(hk[(size_t)n * 32]);
+    note(*pk, ooo);
+  }
+  // Colour push(k) would emit (if any), without modifying the filter.
+  __device__ __forceinline__ bool peek(int cap, uint64_t k, float4 c, float4* pc) const {
+    if (n < cap) return false;
+    const uint64_t e0 = hk[0];
+    *pc = pack(k) < (e0 >> kSlotBits) ? c : hc[(size_t)(e0 & kSlotMask) * 32];
+    return true;
+  }
+};
+
 __device__ __forceinline__ float4 blend(float4 acc, float4 s) {
   float t = __fsub_rn(1.0f, acc.w);
   return make_float4(__fadd_rn(acc.x, __fmul_rn(t, s.x)), __fadd_rn(acc.y, __fmul_rn(t, s.y)),
@@ -1699,15 +1813,13 @@ __device__ __forceinline__ void shade_segments(const FrameConst& fc, const Buffe
 // many pixels (samples/THB high) and, with kThreshold, for the alpha
 // threshold, where the 32nd saturation must be located at its exact stream
 // position.
-template <int KM, bool kThreshold, bool kTex>
+template <int KM, bool kThreshold, bool kTex, typename Filter>
 __device__ __forceinline__ void shade_walk(const FrameConst& fc, const Buffers& B, int px0,
                                            int py0, const uint32_t* tri_l, const uint32_t* mask_l,
                                            uint32_t n, PixelOut& o,
-                                           unsigned long long* enumerated_out) {
+                                           unsigned long long* enumerated_out, Filter& f) {
   const int lane = threadIdx.x & 31;
   const int px = px0 + (lane & 7), py = py0 + (lane >> 3);
-  RegFilter<KM, (KM <= 8)> f;
-  f.reset();
   bool saturated = false, stopped = false;
   unsigned sat_mask = 0;
   unsigned long long enumerated = 0;
@@ -2374,6 +2486,19 @@ __global__ void __launch_bounds__(128, 7) k_extract(Buffers B, int pass,
 // samples composite the background.
 constexpr int kShadeStage = 256;  // THB entries staged per warp; longer lists stream
 
+// This warp's heap filter storage (HeapFilter): after the staged triangles in
+// dynamic shared memory, or its slice of the global scratch.
+template <int kMode>
+__device__ __forceinline__ void heap_reset(const Buffers& B, uint8_t* shade_dyn, HeapFilter& f) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const size_t warp_bytes = (size_t)B.heap_cap * 32u * 24u;
+  uint8_t* base = B.heap_g ? B.heap_g + ((size_t)blockIdx.x * 8u + (size_t)warp) * warp_bytes
+                           : shade_dyn + (kMode == 0 ? (size_t)kStageTris * sizeof(StagedTri) : 0) +
+                                 (size_t)warp * warp_bytes;
+  f.reset(reinterpret_cast<uint64_t*>(base) + lane,
+          reinterpret_cast<float4*>(base + (size_t)B.heap_cap * 32u * 8u) + lane);
+}
+
 // kMode: 0 = broadcast walk for half-blocks with big THBs (also writes every
 // half-block without samples), 1 = segment routing for the rest, 2 = alpha
 // threshold walk for all. Separate instantiations keep each path's register
@@ -2518,11 +2643,19 @@ __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
         pre_l = stage_pre[warp];
         slot_l = stage_slot[warp];
       }
-      if (kMode == 2)
-        shade_walk<KM, true, kTex>(fc, B, hpx0, hpy0, tri_l, mask_l, d.cnt, po, &enumerated);
-      else if (kMode == 0)  // big THBs: wave walk
+      if (kMode == 2) {
+        if constexpr (KM == 0) {
+          HeapFilter f;
+          heap_reset<kMode>(B, shade_dyn, f);
+          shade_walk<KM, true, kTex>(fc, B, hpx0, hpy0, tri_l, mask_l, d.cnt, po, &enumerated, f);
+        } else {
+          RegFilter<KM, true> f;
+          f.reset();
+          shade_walk<KM, true, kTex>(fc, B, hpx0, hpy0, tri_l, mask_l, d.cnt, po, &enumerated, f);
+        }
+      } else if (kMode == 0)  // big THBs: wave walk
       {
-        if constexpr (KM <= 8) {
+        if constexpr (KM != 0) {
           SlotFilter<KM> f;
           f.reset(reinterpret_cast<float4*>(shade_dyn + (size_t)kStageTris * sizeof(StagedTri)) +
                   (size_t)warp * KM * 32 + lane);
@@ -2533,20 +2666,20 @@ __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
             shade_waves<KM, kTex>(fc, B, hpx0, hpy0, tri_l, mask_l, slot_l, staged_ok ? row_tris : nullptr,
                             d.cnt, po, f);
         } else {
-          RegFilter<KM> f;
-          f.reset();
+          HeapFilter f;
+          heap_reset<kMode>(B, shade_dyn, f);
           shade_waves<KM, kTex>(fc, B, hpx0, hpy0, tri_l, mask_l, slot_l, staged_ok ? row_tris : nullptr,
                           d.cnt, po, f);
         }
       }
       else if (d.frags) {  // small THBs: dense segments + routing
-        if constexpr (KM <= 8) {
+        if constexpr (KM != 0) {
           SlotFilter<KM> f;
           f.reset(reinterpret_cast<float4*>(shade_dyn) + (size_t)warp * KM * 32 + lane);
           shade_segments<KM, kTex>(fc, B, hpx0, hpy0, tri_l, mask_l, pre_l, d.cnt, d.frags, route_s[warp], po, f);
         } else {
-          RegFilter<KM> f;
-          f.reset();
+          HeapFilter f;
+          heap_reset<kMode>(B, shade_dyn, f);
           shade_segments<KM, kTex>(fc, B, hpx0, hpy0, tri_l, mask_l, pre_l, d.cnt, d.frags, route_s[warp], po, f);
         }
       }
@@ -2804,13 +2937,15 @@ struct DeviceScene {
   DevBuf zero, vq_uv, vq_src, vq_idx, vq_box, vq_flags, vq_mat, vq_col, vq_nrm, tri, tri_meta, shade,
       tri_y;
   DevBuf off, qcur, tcur, cat, bin_list0, bin_list1, prop_q, bin_cost, bin_order, prop, items, item_rows, slots, spill0, spill1, scratch, fb, mask,
-      hash, emit, tile_ids, hbd, pool_tri, pool_mask, pool_pre, seg_queue, pool_slot, lpairs, lpair_cols;
+      hash, emit, tile_ids, hbd, pool_tri, pool_mask, pool_pre, seg_queue, pool_slot, lpairs, lpair_cols,
+      heap_g;
   uint32_t items_cap = 0;
   uint32_t pool_cap = 0;
   uint32_t lpairs_cap = 0;
   dev::FrameConst* fc_host = nullptr;  // pinned staging of c_fc (graph memcpy source)
   void* peer_fb = nullptr;    // imported root framebuffer (cudaIpcOpenMemHandle)
   void* peer_mask = nullptr;
+  int peer_w = 0, peer_h = 0;  // the imported framebuffer's viewport
   dev::Counters* ctr_host = nullptr;   // pinned counters readback
   // Cached CUDA graph of one whole frame (c_fc upload .. counters readback),
   // valid while the launch-shaping inputs in graph_key are unchanged.
@@ -3072,23 +3207,39 @@ void launch_extract(DeviceScene* d, const dev::FrameConst& fc, const dev::Buffer
   *launches += 2;
 }
 
+// Heap filters (KM == 0, depth_filter_size > 8) live in dynamic shared memory
+// when a block's eight warps' heaps fit next to the staged triangles, else in
+// a global scratch (VEIL_HEAP_GLOBAL=1 forces the latter for A/B tests).
+constexpr size_t kHeapBytesPerNode = 32 * (8 + 16);  // one node per lane: key + colour slot
+constexpr size_t kHeapSmemBudget = 190 * 1024;
+
 template <int KM, int kMode, bool kTex>
 void launch_shade_mode(DeviceScene* d, const dev::FrameConst& fc, const dev::Buffers& B,
                        int* launches) {
-  const size_t dyn = (kMode == 0 ? size_t(dev::kStageTris) * sizeof(dev::StagedTri) : 0) +
-                     (kMode != 2 && KM <= 8 ? size_t(8) * KM * 32 * sizeof(float4) : 0);
-  static bool configured = false;  // per instantiation
-  if (!configured && dyn) {
+  size_t dyn = (kMode == 0 ? size_t(dev::kStageTris) * sizeof(dev::StagedTri) : 0);
+  if (KM != 0)
+    dyn += (kMode != 2 ? size_t(8) * KM * 32 * sizeof(float4) : 0);
+  else if (!B.heap_g)
+    dyn += size_t(8) * B.heap_cap * kHeapBytesPerNode;
+  static size_t configured = 0;  // per instantiation: the largest dynamic size set so far
+  if (dyn > configured) {
     ck(cudaFuncSetAttribute(dev::k_shade<KM, kMode, kTex>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             int(dyn)),
        "cudaFuncSetAttribute");
-    configured = true;
+    configured = dyn;
   }
-  static int per_sm = -1;  // per instantiation (same on every B200)
-  if (per_sm < 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_shade<KM, kMode, kTex>, 256, dyn);
+  static std::map<size_t, int> per_sm_by_dyn;  // per instantiation (same on every B200)
+  auto it = per_sm_by_dyn.find(dyn);
+  if (it == per_sm_by_dyn.end()) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_shade<KM, kMode, kTex>, 256, dyn);
+    it = per_sm_by_dyn.emplace(dyn, per_sm).first;
+  }
+  const int per_sm = it->second;
   const long long items = kMode == 1 ? ((long long)fc.nbins * 32 + 7) / 8 : (long long)fc.nbins;
-  const int grid = int(std::max<long long>(1, std::min<long long>((long long)std::max(1, per_sm) * d->sm_count,
-                                                                   items)));
+  long long cap = (long long)std::max(1, per_sm) * d->sm_count;
+  if (KM == 0 && B.heap_g) cap = std::min<long long>(cap, B.heap_ctas);  // scratch slices
+  const int grid = int(std::max<long long>(1, std::min<long long>(cap, items)));
   dev::k_shade<KM, kMode, kTex><<<grid, 256, dyn, d->stream>>>(B);
   ck(cudaGetLastError(), "k_shade launch");
   ++*launches;
@@ -3108,7 +3259,8 @@ void launch_shade_km(DeviceScene* d, const dev::FrameConst& fc, const dev::Buffe
 template <bool kTex>
 void launch_shade_tex(DeviceScene* d, const dev::FrameConst& fc, const dev::Buffers& B, int* launches) {
   const int df = fc.df;
-  // KM == df exactly up to 8 (the filter capacity is then a compile-time constant)
+  // KM == df exactly up to 8 (register filters, the capacity a compile-time
+  // constant); above 8 the heap filter (KM == 0) with any capacity
   if (df == 1) launch_shade_km<1, kTex>(d, fc, B, launches);
   else if (df == 2) launch_shade_km<2, kTex>(d, fc, B, launches);
   else if (df == 3) launch_shade_km<3, kTex>(d, fc, B, launches);
@@ -3117,9 +3269,7 @@ void launch_shade_tex(DeviceScene* d, const dev::FrameConst& fc, const dev::Buff
   else if (df == 6) launch_shade_km<6, kTex>(d, fc, B, launches);
   else if (df == 7) launch_shade_km<7, kTex>(d, fc, B, launches);
   else if (df == 8) launch_shade_km<8, kTex>(d, fc, B, launches);
-  else if (df <= 16) launch_shade_km<16, kTex>(d, fc, B, launches);
-  else if (df <= 32) launch_shade_km<32, kTex>(d, fc, B, launches);
-  else throw Error(VEIL_ERR_INVALID_ARG, "depth_filter_size above 32 is not supported on the device path");
+  else launch_shade_km<0, kTex>(d, fc, B, launches);
 }
 
 // Scenes with textured materials get the shading kernels compiled with the
@@ -3212,6 +3362,12 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   fc.rank = opt.rank;
   fc.world = opt.world_size;
   if (opt.world_size > 1 && opt.rank != 0 && d->peer_fb) {
+    // the root's framebuffer has the stride and size of the viewport it was
+    // exported with: a later viewport change must not write through it
+    if (d->peer_w != cam.width || d->peer_h != cam.height)
+      throw Error(VEIL_ERR_INVALID_ARG,
+                  "the imported peer framebuffer has another viewport (re-import it after "
+                  "veil_scene_set_viewport)");
     fc.peer_fb = static_cast<uint32_t*>(d->peer_fb);
     fc.peer_mask = static_cast<uint8_t*>(d->peer_mask);
   }
@@ -3312,9 +3468,35 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   d->scratch.ensure(per_cta * d->raster_ctas_global);
   d->fb_w = cam.width;
   d->fb_h = cam.height;
+  // Heap depth filters (depth_filter_size > 8): a pixel receives at most one
+  // sample per THB of its half-block, and a half-block holds at most
+  // max(low, high) THB-limit THBs, so min(k, that) nodes per lane suffice.
+  uint32_t heap_cap = 0, heap_ctas = 0;
+  bool heap_global = false;
+  if (fc.df > 8) {
+    heap_cap = std::min<uint32_t>(uint32_t(fc.df), std::max(fc.low.thb, fc.high.thb));
+    if (heap_cap > (1u << dev::HeapFilter::kSlotBits))
+      throw Error(VEIL_ERR_INVALID_ARG,
+                  "depth_filter_size above 32768 with a THB limit above 32768 is not supported");
+    const size_t per_cta = size_t(8) * heap_cap * kHeapBytesPerNode;
+    const char* hg = std::getenv("VEIL_HEAP_GLOBAL");
+    heap_global = (hg && *hg && *hg != '0') ||
+                  size_t(dev::kStageTris) * sizeof(dev::StagedTri) + per_cta > kHeapSmemBudget;
+    if (heap_global) {
+      // up to 4 CTAs per SM (the shading kernels' occupancy), fewer when the
+      // scratch would pass 4 GiB
+      heap_ctas = uint32_t(d->sm_count) * 4u;
+      while (heap_ctas > uint32_t(d->sm_count) && size_t(heap_ctas) * per_cta > (size_t(4) << 30))
+        heap_ctas -= uint32_t(d->sm_count);
+      d->heap_g.ensure(size_t(heap_ctas) * per_cta);
+    }
+  }
 
   dev::Buffers& B = P.B;
   std::memset(&B, 0, sizeof B);
+  B.heap_g = heap_global ? d->heap_g.as<uint8_t>() : nullptr;
+  B.heap_cap = heap_cap;
+  B.heap_ctas = heap_ctas;
   B.pos = d->pos.as<float4>();
   B.vcol = d->vcol.as<uint32_t>();
   B.vnrm = d->vnrm.as<uint32_t>();
@@ -3929,6 +4111,8 @@ void import_peer_framebuffer(const Scene& s, const veil_ipc_framebuffer* fb) {
   ck(cudaIpcOpenMemHandle(&d->peer_fb, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
   std::memcpy(&h, fb->mask, sizeof h);
   ck(cudaIpcOpenMemHandle(&d->peer_mask, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+  d->peer_w = fb->width;
+  d->peer_h = fb->height;
 }
 
 void device_framebuffer(const Scene& s, void** rgba, void** mask) {

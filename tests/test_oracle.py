@@ -58,6 +58,15 @@ def test_restatement_vs_reference_synthetic(kind, flags, df):
 
 
 @needs_ref
+@pytest.mark.parametrize("sheets,df", [(128, 33), (128, 64), (300, 40), (300, 84), (300, 1024)])
+@pytest.mark.parametrize("flags", [0, RENDER_ALPHA_THRESHOLD])
+def test_restatement_vs_reference_large_depth_filter(sheets, df, flags):
+    """DF far above 8 (the reference's filter is unbounded, depth_filter.hpp:31-60)."""
+    arr = bindings.RefScene.synthetic_params("intersecting_shells", 3, 128, 112, sheets=sheets).arrays()
+    _vs_ref(arr, default_params(flags=flags, depth_filter_size=df))
+
+
+@needs_ref
 @pytest.mark.parametrize("limits", [dict(limit_low_tri_blocks=4), dict(limit_low_tbr=16),
                                     dict(limit_low_frags=64), dict(limit_high_thb=8),
                                     dict(limit_low_tbr=1 << 20)])

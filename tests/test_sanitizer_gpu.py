@@ -1,0 +1,45 @@
+"""compute-sanitizer over libveil's kernels.
+
+The shading kernels route samples between lanes through per-warp shared
+memory with __syncwarp ordering (route_mask), k_setup chains block prefixes
+with a volatile-load decoupled look-back, and k_extract shares its item state
+across four warps with block barriers. memcheck, racecheck and synccheck run
+the plain C embedder (tests/c/capi_render.c, no Python/torch in the process)
+on scenes that reach the wave walk, the segment kernel, the alpha-threshold
+walk, the heap depth filter (shared and global) and both extraction passes.
+"""
+import os
+import shutil
+import subprocess
+
+import pytest
+
+from test_capi_c import _build
+
+pytestmark = pytest.mark.gpu
+
+SANITIZER = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+
+CASES = [
+    ("dense_bin", 3, 256, 256, 3),        # low + high bins, wave walk + segments
+    ("random_soup", 4, 160, 128, 8),      # tiny triangles: segment kernel
+    ("layered_quads", 2, 128, 96, 1),     # big quads: staged wave walk
+    ("intersecting_shells", 5, 128, 96, 12),  # heap filter in shared memory
+    ("intersecting_shells", 6, 96, 64, 40),   # heap filter in global scratch
+]
+
+
+@pytest.mark.skipif(not os.path.exists(SANITIZER), reason="compute-sanitizer not installed")
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
+@pytest.mark.parametrize("kind,seed,w,h,df", CASES)
+def test_compute_sanitizer_clean(tmp_path, tool, kind, seed, w, h, df):
+    exe = _build(tmp_path)
+    args = [SANITIZER, "--tool", tool, "--error-exitcode", "9", "--print-limit", "20"]
+    if tool == "racecheck":
+        args += ["--racecheck-report", "hazard"]
+    p = subprocess.run(args + [str(exe), kind, str(seed), str(w), str(h), str(df),
+                               str(tmp_path / "f.png"), str(tmp_path / "f.raw")],
+                       capture_output=True, text=True, timeout=900)
+    out = p.stdout + p.stderr
+    assert p.returncode == 0, out[-4000:]
+    assert "ERROR SUMMARY: 0 errors" in out or "RACECHECK SUMMARY: 0 hazards" in out, out[-4000:]
