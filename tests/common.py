@@ -174,3 +174,48 @@ def fuzz_scene(seed):
             flags |= f
     params = default_params(flags=flags, depth_filter_size=int(rng.choice([1, 2, 3, 5, 8, 16])))
     return arr, params
+
+
+def read_png_rgba(path):
+    """Decodes an 8-bit RGBA, non-interlaced PNG (what veil_render_write_png
+    writes) with zlib: IHDR, IDAT chunks, per-row filters 0-4."""
+    import struct
+    import zlib
+
+    data = open(path, "rb").read()
+    assert data[:8] == b"\x89PNG\r\n\x1a\n"
+    pos, idat, w, h = 8, b"", 0, 0
+    while pos < len(data):
+        n, kind = struct.unpack(">I4s", data[pos:pos + 8])
+        body = data[pos + 8:pos + 8 + n]
+        if kind == b"IHDR":
+            w, h, depth, ctype, _, _, interlace = struct.unpack(">IIBBBBB", body)
+            assert depth == 8 and ctype == 6 and interlace == 0
+        elif kind == b"IDAT":
+            idat += body
+        pos += 12 + n
+    raw = np.frombuffer(zlib.decompress(idat), dtype=np.uint8).reshape(h, 1 + 4 * w)
+    out = np.zeros((h, 4 * w), dtype=np.int32)
+    for y in range(h):
+        f, line = raw[y, 0], raw[y, 1:].astype(np.int32)
+        prev = out[y - 1] if y else np.zeros(4 * w, dtype=np.int32)
+        if f == 0:
+            out[y] = line
+        elif f == 2:
+            out[y] = (line + prev) & 255
+        else:
+            row = np.zeros(4 * w, dtype=np.int32)
+            for i in range(4 * w):
+                a = row[i - 4] if i >= 4 else 0
+                b = prev[i]
+                c = prev[i - 4] if i >= 4 else 0
+                if f == 1:
+                    p = a
+                elif f == 3:
+                    p = (a + b) // 2
+                else:
+                    pa, pb, pc = abs(b - c), abs(a - c), abs(a + b - 2 * c)
+                    p = a if (pa <= pb and pa <= pc) else (b if pb <= pc else c)
+                row[i] = (line[i] + p) & 255
+            out[y] = row
+    return out.astype(np.uint8).reshape(h, w, 4)

@@ -40,5 +40,5 @@ def test_bench_multirank_frame_identical(world, workload, gather):
     assert res["n_gpus"] == world
     assert res["frame_check"]["identical"], res["frame_check"]
     if gather == "peer":  # CUDA IPC between processes on one device works as across NVLink
-        assert "peer-memory" in res["config"]["parallelism"], res["config"]["parallelism"]
+        assert "peer-memory" in res["parallelism"], res["parallelism"]
     assert res["value"] > 0 and res["e2e"]["value"] > 0
