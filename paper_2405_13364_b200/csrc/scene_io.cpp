@@ -11,10 +11,15 @@
 // The BASELINE.json workloads (stack64k, tiny4m, mixed16m) have no reference
 // generator; their recipes are in SURVEY.md 8(d) and DESIGN.md.
 #include <algorithm>
+#include <array>
+#include <cctype>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 #include <fstream>
 #include <map>
+#include <type_traits>
+#include <unordered_map>
 #include <numeric>
 #include <random>
 #include <sstream>
@@ -191,50 +196,142 @@ Texture texture_from_image(const Image8& img) {
   return t;
 }
 
-// ------------------------------------------------------------------- OBJ
+// ------------------------------------------------------------ text ingest
+//
+// OBJ / MTL / camera-config ingest (behaviour of reference scene.cpp:195-454:
+// the same scenes, vertex numbering, materials, camera doubles and error
+// messages). Files are read whole and scanned line by line with a cursor
+// that tokenises on whitespace and reads numbers the way an istream does
+// (strtof for floats, strtod for doubles, failing on an incomplete number);
+// OBJ directives dispatch through a keyword switch, and each distinct
+// (position, uv, normal) corner becomes a vertex, numbered by first use.
 
-struct FaceRef {
-  int v = 0, vt = 0, vn = 0;
-  bool operator<(const FaceRef& o) const {
-    if (v != o.v) return v < o.v;
-    if (vt != o.vt) return vt < o.vt;
-    return vn < o.vn;
-  }
-};
 
 [[noreturn]] void parse_error(const std::string& path, int line, const std::string& what) {
   throw Error(VEIL_ERR_PARSE, path + ":" + std::to_string(line) + ": " + what);
 }
 
-int obj_index(int idx, size_t count, const std::string& path, int line) {
-  int r = idx > 0 ? idx - 1 : int(count) + idx;
-  if (idx == 0 || r < 0 || r >= int(count))
-    parse_error(path, line, "index " + std::to_string(idx) + " out of range");
-  return r;
+std::string slurp(const std::string& path, const char* what) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw Error(VEIL_ERR_IO, std::string("cannot open ") + what + " " + path);
+  std::ostringstream ss;
+  ss << in.rdbuf();
+  return ss.str();
 }
 
-FaceRef face_ref(const std::string& tok, const std::string& path, int line) {
-  FaceRef f;
-  size_t a = tok.find('/');
-  if (a == std::string::npos) {
-    f.v = std::atoi(tok.c_str());
-    return f;
-  }
-  f.v = std::atoi(tok.substr(0, a).c_str());
-  size_t b = tok.find('/', a + 1);
-  if (b == std::string::npos) {
-    f.vt = std::atoi(tok.substr(a + 1).c_str());
-    return f;
-  }
-  if (b > a + 1) f.vt = std::atoi(tok.substr(a + 1, b - a - 1).c_str());
-  if (b + 1 < tok.size()) f.vn = std::atoi(tok.substr(b + 1).c_str());
-  if (f.v == 0) parse_error(path, line, "malformed face vertex '" + tok + "'");
-  return f;
-}
-
-std::string dir_of(const std::string& p) {
-  size_t s = p.find_last_of('/');
+std::string parent_dir(const std::string& p) {
+  const size_t s = p.find_last_of('/');
   return s == std::string::npos ? std::string() : p.substr(0, s);
+}
+
+bool is_space(char c) { return c == ' ' || c == '\t' || c == '\r' || c == '\n' || c == '\v' || c == '\f'; }
+
+// One line of text with a read position.
+class Cursor {
+ public:
+  Cursor(const char* b, const char* e) : p_(b), e_(e) {}
+  void skip_space() {
+    while (p_ < e_ && is_space(*p_)) ++p_;
+  }
+  bool word(std::string* out) {  // next whitespace-delimited token
+    skip_space();
+    const char* b = p_;
+    while (p_ < e_ && !is_space(*p_)) ++p_;
+    if (b == p_) return false;
+    out->assign(b, p_);
+    return true;
+  }
+  template <typename T>
+  bool number(T* out) {  // a decimal number at the cursor; false leaves *out alone
+    skip_space();
+    const char* b = p_;
+    const char* q = p_;
+    while (q < e_ && (std::isdigit((unsigned char)*q) || *q == '+' || *q == '-' || *q == '.' || *q == 'e' ||
+                      *q == 'E'))
+      ++q;
+    if (q == b) return false;
+    const std::string run(b, q);
+    char* end = nullptr;
+    T v;
+    if constexpr (std::is_same_v<T, float>)
+      v = std::strtof(run.c_str(), &end);
+    else
+      v = std::strtod(run.c_str(), &end);
+    if (end != run.c_str() + run.size()) return false;
+    p_ = q;
+    *out = v;
+    return true;
+  }
+
+ private:
+  const char* p_;
+  const char* e_;
+};
+
+// Calls fn(line_number, cursor) for every line of text.
+template <typename Fn>
+void for_each_line(const std::string& text, Fn&& fn) {
+  const char* p = text.data();
+  const char* end = p + text.size();
+  int line_no = 0;
+  while (p < end) {
+    const char* nl = static_cast<const char*>(std::memchr(p, '\n', size_t(end - p)));
+    const char* le = nl ? nl : end;
+    Cursor c(p, le);
+    fn(++line_no, c);
+    p = nl ? nl + 1 : end;
+  }
+}
+
+// atoi of a field: optional sign, then digits; anything else ends it.
+int leading_int(const std::string& s, size_t b, size_t e) {
+  while (b < e && is_space(s[b])) ++b;
+  bool neg = false;
+  if (b < e && (s[b] == '+' || s[b] == '-')) neg = s[b++] == '-';
+  long long v = 0;
+  for (; b < e && std::isdigit((unsigned char)s[b]); ++b) v = v * 10 + (s[b] - '0');
+  return int(neg ? -v : v);
+}
+
+struct Corner {
+  int v = 0, vt = 0, vn = 0;  // 1-based or negative OBJ references, 0 = absent
+  bool operator==(const Corner& o) const { return v == o.v && vt == o.vt && vn == o.vn; }
+};
+struct CornerHash {
+  size_t operator()(const Corner& c) const {
+    uint64_t h = uint64_t(uint32_t(c.v)) * 0x9e3779b97f4a7c15ull;
+    h ^= uint64_t(uint32_t(c.vt)) + 0x7f4a7c159e3779b9ull + (h << 6) + (h >> 2);
+    h ^= uint64_t(uint32_t(c.vn)) + 0x94d049bb133111ebull + (h << 6) + (h >> 2);
+    return size_t(h);
+  }
+};
+
+// "v", "v/vt", "v/vt/vn" or "v//vn"
+Corner parse_corner(const std::string& tok, const std::string& path, int line) {
+  Corner c;
+  const size_t s1 = tok.find('/');
+  if (s1 == std::string::npos) {
+    c.v = leading_int(tok, 0, tok.size());
+    return c;
+  }
+  c.v = leading_int(tok, 0, s1);
+  const size_t s2 = tok.find('/', s1 + 1);
+  if (s2 == std::string::npos) {
+    c.vt = leading_int(tok, s1 + 1, tok.size());
+    return c;
+  }
+  c.vt = leading_int(tok, s1 + 1, s2);
+  c.vn = leading_int(tok, s2 + 1, tok.size());
+  if (c.v == 0) parse_error(path, line, "malformed face vertex '" + tok + "'");
+  return c;
+}
+
+// An OBJ reference into a list of `count` entries -> 0-based index.
+size_t resolve(int ref, size_t count, const std::string& path, int line) {
+  const long long i = ref > 0 ? (long long)ref - 1 : (long long)count + ref;
+  if (ref == 0 || i < 0 || i >= (long long)count)
+    parse_error(path, line, "index " + std::to_string(ref) + " out of range");
+  return size_t(i);
 }
 
 veil_material default_material() {
@@ -246,104 +343,153 @@ veil_material default_material() {
   return m;
 }
 
+// newmtl / Kd / d / map_Kd; anything else is ignored.
 void read_mtl(const std::string& path, Scene* s, std::map<std::string, uint32_t>* names) {
-  std::ifstream in(path);
-  if (!in) throw Error(VEIL_ERR_IO, "cannot open material file " + path);
-  std::string dir = dir_of(path);
-  std::string line;
-  int ln = 0;
-  int cur = -1;
-  while (std::getline(in, line)) {
-    ++ln;
-    std::istringstream ss(line);
-    std::string key;
-    if (!(ss >> key) || key[0] == '#') continue;
+  const std::string text = slurp(path, "material file");
+  const std::string dir = parent_dir(path);
+  veil_material* cur = nullptr;
+  std::string key, arg;
+  for_each_line(text, [&](int line, Cursor& c) {
+    if (!c.word(&key) || key[0] == '#') return;
     if (key == "newmtl") {
-      std::string name;
-      ss >> name;
-      (*names)[name] = uint32_t(s->materials.size());
+      arg.clear();
+      c.word(&arg);
+      (*names)[arg] = uint32_t(s->materials.size());
       s->materials.push_back(default_material());
-      s->material_names.push_back(name);
-      cur = int(s->materials.size()) - 1;
-    } else if (cur >= 0 && key == "Kd") {
-      veil_material& m = s->materials[cur];
-      ss >> m.base_color[0] >> m.base_color[1] >> m.base_color[2];
-    } else if (cur >= 0 && key == "d") {
-      veil_material& m = s->materials[cur];
-      ss >> m.opacity;
-      if (m.opacity < 0.0f || m.opacity > 1.0f) parse_error(path, ln, "dissolve outside [0,1]");
-    } else if (cur >= 0 && key == "map_Kd") {
-      std::string tp;
-      ss >> tp;
-      if (!dir.empty()) tp = dir + "/" + tp;
-      s->textures.push_back(texture_from_image(read_png(tp)));
-      s->materials[cur].texture = int(s->textures.size()) - 1;
-      s->materials[cur].flags |= VEIL_MATERIAL_UVS;
+      s->material_names.push_back(arg);
+      cur = &s->materials.back();
+      return;
     }
+    if (!cur) return;
+    if (key == "Kd") {
+      for (int k = 0; k < 3 && c.number(&cur->base_color[k]); ++k) {
+      }
+    } else if (key == "d") {
+      c.number(&cur->opacity);
+      if (cur->opacity < 0.0f || cur->opacity > 1.0f) parse_error(path, line, "dissolve outside [0,1]");
+    } else if (key == "map_Kd") {
+      arg.clear();
+      c.word(&arg);
+      if (!dir.empty()) arg = dir + "/" + arg;
+      s->textures.push_back(texture_from_image(read_png(arg)));
+      cur->texture = int(s->textures.size()) - 1;
+      cur->flags |= VEIL_MATERIAL_UVS;
+    }
+  });
+}
+
+enum class Directive { kOther, kPosition, kNormal, kTexcoord, kFace, kUseMtl, kMtlLib };
+
+Directive directive(const std::string& k) {
+  switch (k.size()) {
+    case 1:
+      return k[0] == 'v' ? Directive::kPosition : k[0] == 'f' ? Directive::kFace : Directive::kOther;
+    case 2:
+      return k == "vn" ? Directive::kNormal : k == "vt" ? Directive::kTexcoord : Directive::kOther;
+    case 6:
+      return k == "usemtl" ? Directive::kUseMtl : k == "mtllib" ? Directive::kMtlLib : Directive::kOther;
+    default:
+      return Directive::kOther;
   }
+}
+
+// The OBJ attribute pools and the corner -> vertex numbering of one load.
+struct ObjBuilder {
+  Scene* s;
+  const std::string& path;
+  std::vector<std::array<float, 3>> positions, normals;
+  std::vector<std::array<float, 4>> colours;
+  std::vector<std::array<float, 2>> texcoords;
+  std::unordered_map<Corner, uint32_t, CornerHash> numbering;
+
+  uint32_t vertex(const Corner& c, int line) {
+    auto hit = numbering.find(c);
+    if (hit != numbering.end()) return hit->second;
+    veil_vertex v{};
+    const size_t pi = resolve(c.v, positions.size(), path, line);
+    std::copy(positions[pi].begin(), positions[pi].end(), v.position);
+    std::copy(colours[pi].begin(), colours[pi].end(), v.color);
+    if (c.vt) {
+      const auto& t = texcoords[resolve(c.vt, texcoords.size(), path, line)];
+      v.uv[0] = t[0];
+      v.uv[1] = t[1];
+      s->flags |= VEIL_SCENE_HAS_UVS;
+    }
+    if (c.vn) {
+      // unit normal in float (reference math.hpp:80-85 normalize)
+      const auto& n = normals[resolve(c.vn, normals.size(), path, line)];
+      const float len2 = n[0] * n[0] + n[1] * n[1] + n[2] * n[2];
+      const float inv = len2 <= 0.0f ? 0.0f : 1.0f / std::sqrt(len2);
+      for (int k = 0; k < 3; ++k) v.normal[k] = len2 <= 0.0f ? 0.0f : n[k] * inv;
+      s->flags |= VEIL_SCENE_HAS_NORMALS;
+    }
+    const uint32_t id = uint32_t(s->vertices.size());
+    s->vertices.push_back(v);
+    numbering.emplace(c, id);
+    return id;
+  }
+};
+
+void add_default_material(Scene* s) {
+  if (!s->materials.empty()) return;
+  s->materials.push_back(default_material());
+  s->material_names.push_back("default");
 }
 
 }  // namespace
 
 Camera load_camera_file(const std::string& path) {
-  std::ifstream in(path);
-  if (!in) throw Error(VEIL_ERR_IO, "cannot open camera config " + path);
+  const std::string text = slurp(path, "camera config");
   Camera cam;
   bool have_matrix = false, have_look = false;
   double from[3] = {0, 0, 5}, at[3] = {0, 0, 0}, up[3] = {0, 1, 0};
   double fov = 60.0, nz = 0.1, fz = 100.0;
-  std::string line;
-  int ln = 0;
-  while (std::getline(in, line)) {
-    ++ln;
-    size_t eq = line.find('=');
-    if (line.empty() || line[0] == '#' || eq == std::string::npos) continue;
-    std::string key = line.substr(0, eq);
-    key.erase(std::remove_if(key.begin(), key.end(), [](char c) { return c == ' ' || c == '\t'; }),
-              key.end());
-    std::istringstream vs(line.substr(eq + 1));
-    auto want = [&](int n, double* out) {
+  // "key = values" lines: the key loses its blanks; lines without '=' or
+  // starting with '#' are skipped
+  int line_no = 0;
+  size_t pos = 0;
+  while (pos < text.size()) {
+    size_t nl = text.find('\n', pos);
+    if (nl == std::string::npos) nl = text.size();
+    const std::string row = text.substr(pos, nl - pos);
+    pos = nl + 1;
+    ++line_no;
+    const size_t eq = row.find('=');
+    if (row.empty() || row[0] == '#' || eq == std::string::npos) continue;
+    std::string key;
+    for (size_t i = 0; i < eq; ++i)
+      if (row[i] != ' ' && row[i] != '\t') key += row[i];
+    Cursor c(row.data() + eq + 1, row.data() + row.size());
+    auto take = [&](int n, double* out) {
       for (int i = 0; i < n; ++i)
-        if (!(vs >> out[i])) parse_error(path, ln, "expected " + std::to_string(n) + " numbers");
+        if (!c.number(&out[i])) parse_error(path, line_no, "expected " + std::to_string(n) + " numbers");
     };
     double v[16];
     if (key == "view_projection") {
-      want(16, v);
-      for (int i = 0; i < 16; ++i) cam.m[i] = v[i];
+      take(16, v);
+      std::copy(v, v + 16, cam.m);
       have_matrix = true;
-    } else if (key == "width") {
-      want(1, v);
-      cam.width = int(v[0]);
-    } else if (key == "height") {
-      want(1, v);
-      cam.height = int(v[0]);
+    } else if (key == "width" || key == "height") {
+      take(1, v);
+      (key == "width" ? cam.width : cam.height) = int(v[0]);
     } else if (key == "eye") {
-      want(3, v);
+      take(3, cam.eye);
       cam.has_eye = true;
-      for (int i = 0; i < 3; ++i) cam.eye[i] = v[i];
-    } else if (key == "look_from") {
-      want(3, from);
-      have_look = true;
-    } else if (key == "look_at") {
-      want(3, at);
+    } else if (key == "look_from" || key == "look_at") {
+      take(3, key == "look_from" ? from : at);
       have_look = true;
     } else if (key == "up") {
-      want(3, up);
-    } else if (key == "fov_deg") {
-      want(1, &fov);
-    } else if (key == "near") {
-      want(1, &nz);
-    } else if (key == "far") {
-      want(1, &fz);
+      take(3, up);
+    } else if (key == "fov_deg" || key == "near" || key == "far") {
+      take(1, key == "fov_deg" ? &fov : key == "near" ? &nz : &fz);
     } else {
-      parse_error(path, ln, "unknown camera key '" + key + "'");
+      parse_error(path, line_no, "unknown camera key '" + key + "'");
     }
   }
   if (have_look && !have_matrix) {
+    // the friendly form: a look-at camera; an explicit eye still wins
     Camera look = look_at_camera(from, at, up, fov, nz, fz, cam.width, cam.height);
-    if (cam.has_eye) {
-      for (int i = 0; i < 3; ++i) look.eye[i] = cam.eye[i];
-    }
+    if (cam.has_eye) std::copy(cam.eye, cam.eye + 3, look.eye);
     cam = look;
   }
   validate_camera(cam, false);
@@ -352,114 +498,79 @@ Camera load_camera_file(const std::string& path) {
 
 void load_obj_scene(Scene* s, const std::string& mesh, const std::string& mtl,
                     const std::string& cam) {
-  std::ifstream in(mesh);
-  if (!in) throw Error(VEIL_ERR_IO, "cannot open mesh file " + mesh);
-  std::string dir = dir_of(mesh);
+  const std::string text = slurp(mesh, "mesh file");
+  const std::string dir = parent_dir(mesh);
   std::map<std::string, uint32_t> names;
-  std::vector<float> pos, pcol, nrmv, uvs;  // 3, 4, 3, 2 per entry
-  std::map<FaceRef, uint32_t> cache;
-  uint32_t cur_mat = 0;
   if (!mtl.empty()) read_mtl(mtl, s, &names);
-  auto ensure_default = [&] {
-    if (s->materials.empty()) {
-      s->materials.push_back(default_material());
-      s->material_names.push_back("default");
-    }
-  };
-  auto vertex_for = [&](FaceRef r, int ln) -> uint32_t {
-    auto it = cache.find(r);
-    if (it != cache.end()) return it->second;
-    veil_vertex v{};
-    int pi = obj_index(r.v, pos.size() / 3, mesh, ln);
-    for (int k = 0; k < 3; ++k) v.position[k] = pos[pi * 3 + k];
-    for (int k = 0; k < 4; ++k) v.color[k] = pcol[pi * 4 + k];
-    if (r.vt != 0) {
-      int ti = obj_index(r.vt, uvs.size() / 2, mesh, ln);
-      v.uv[0] = uvs[ti * 2];
-      v.uv[1] = uvs[ti * 2 + 1];
-      s->flags |= VEIL_SCENE_HAS_UVS;
-    }
-    if (r.vn != 0) {
-      int ni = obj_index(r.vn, nrmv.size() / 3, mesh, ln);
-      // float normalize, reference math.hpp:80-85
-      float x = nrmv[ni * 3], y = nrmv[ni * 3 + 1], z = nrmv[ni * 3 + 2];
-      float l2 = x * x + y * y + z * z;
-      if (l2 <= 0.0f) {
-        x = y = z = 0.0f;
-      } else {
-        float inv = 1.0f / std::sqrt(l2);
-        x = x * inv;
-        y = y * inv;
-        z = z * inv;
+  ObjBuilder ob{s, mesh, {}, {}, {}, {}, {}};
+  uint32_t material = 0;
+  std::string key, tok;
+  std::vector<Corner> face;
+  for_each_line(text, [&](int line, Cursor& c) {
+    if (!c.word(&key) || key[0] == '#') return;
+    switch (directive(key)) {
+      case Directive::kPosition: {
+        std::array<float, 3> p;
+        if (!(c.number(&p[0]) && c.number(&p[1]) && c.number(&p[2]))) parse_error(mesh, line, "malformed vertex");
+        std::array<float, 4> col = {1.0f, 1.0f, 1.0f, 1.0f};
+        float rgb[3];
+        if (c.number(&rgb[0]) && c.number(&rgb[1]) && c.number(&rgb[2])) {  // optional vertex colour
+          std::copy(rgb, rgb + 3, col.begin());
+          s->flags |= VEIL_SCENE_HAS_COLORS;
+        }
+        ob.positions.push_back(p);
+        ob.colours.push_back(col);
+        break;
       }
-      v.normal[0] = x;
-      v.normal[1] = y;
-      v.normal[2] = z;
-      s->flags |= VEIL_SCENE_HAS_NORMALS;
-    }
-    uint32_t id = uint32_t(s->vertices.size());
-    s->vertices.push_back(v);
-    cache.emplace(r, id);
-    return id;
-  };
-  std::string line;
-  int ln = 0;
-  while (std::getline(in, line)) {
-    ++ln;
-    std::istringstream ss(line);
-    std::string key;
-    if (!(ss >> key) || key[0] == '#') continue;
-    if (key == "v") {
-      float p[3];
-      if (!(ss >> p[0] >> p[1] >> p[2])) parse_error(mesh, ln, "malformed vertex");
-      float c[4] = {1.0f, 1.0f, 1.0f, 1.0f};
-      float r, g, b;
-      if (ss >> r >> g >> b) {
-        c[0] = r;
-        c[1] = g;
-        c[2] = b;
-        s->flags |= VEIL_SCENE_HAS_COLORS;
+      case Directive::kNormal: {
+        std::array<float, 3> n;
+        if (!(c.number(&n[0]) && c.number(&n[1]) && c.number(&n[2]))) parse_error(mesh, line, "malformed normal");
+        ob.normals.push_back(n);
+        break;
       }
-      pos.insert(pos.end(), p, p + 3);
-      pcol.insert(pcol.end(), c, c + 4);
-    } else if (key == "vn") {
-      float n[3];
-      if (!(ss >> n[0] >> n[1] >> n[2])) parse_error(mesh, ln, "malformed normal");
-      nrmv.insert(nrmv.end(), n, n + 3);
-    } else if (key == "vt") {
-      float t[2];
-      if (!(ss >> t[0] >> t[1])) parse_error(mesh, ln, "malformed texcoord");
-      uvs.insert(uvs.end(), t, t + 2);
-    } else if (key == "f") {
-      std::vector<FaceRef> face;
-      std::string tok;
-      while (ss >> tok) face.push_back(face_ref(tok, mesh, ln));
-      if (face.size() < 3 || face.size() > 4)
-        parse_error(mesh, ln, "unsupported face arity " + std::to_string(face.size()));
-      ensure_default();
-      veil_quad q{};
-      q.material = cur_mat;
-      for (size_t i = 0; i < face.size(); ++i) q.v[i] = vertex_for(face[i], ln);
-      if (face.size() == 3) q.v[3] = q.v[2];
-      s->quads.push_back(q);
-    } else if (key == "usemtl") {
-      std::string name;
-      ss >> name;
-      auto it = names.find(name);
-      if (it == names.end()) {
-        ensure_default();
-        cur_mat = 0;
-      } else {
-        cur_mat = it->second;
+      case Directive::kTexcoord: {
+        std::array<float, 2> t;
+        if (!(c.number(&t[0]) && c.number(&t[1]))) parse_error(mesh, line, "malformed texcoord");
+        ob.texcoords.push_back(t);
+        break;
       }
-    } else if (key == "mtllib" && mtl.empty()) {
-      std::string m;
-      ss >> m;
-      if (!dir.empty()) m = dir + "/" + m;
-      read_mtl(m, s, &names);
+      case Directive::kFace: {
+        face.clear();
+        while (c.word(&tok)) face.push_back(parse_corner(tok, mesh, line));
+        if (face.size() != 3 && face.size() != 4)
+          parse_error(mesh, line, "unsupported face arity " + std::to_string(face.size()));
+        add_default_material(s);
+        veil_quad q{};
+        q.material = material;
+        for (size_t i = 0; i < face.size(); ++i) q.v[i] = ob.vertex(face[i], line);
+        if (face.size() == 3) q.v[3] = q.v[2];  // a triangle is a quad with v3 == v2
+        s->quads.push_back(q);
+        break;
+      }
+      case Directive::kUseMtl: {
+        tok.clear();
+        c.word(&tok);
+        const auto it = names.find(tok);
+        if (it != names.end()) {
+          material = it->second;
+        } else {  // unknown names select the default material
+          add_default_material(s);
+          material = 0;
+        }
+        break;
+      }
+      case Directive::kMtlLib:
+        if (mtl.empty()) {
+          tok.clear();
+          c.word(&tok);
+          read_mtl(dir.empty() ? tok : dir + "/" + tok, s, &names);
+        }
+        break;
+      case Directive::kOther:
+        break;
     }
-  }
-  ensure_default();
+  });
+  add_default_material(s);
   if (!cam.empty()) s->camera = load_camera_file(cam);
   validate_scene(*s);
 }
