@@ -44,7 +44,7 @@ def parse():
     ap.add_argument("--workload", default="stack64k",
                     choices=["stack64k", "boxes1080", "tiny4m", "mixed16m"])
     ap.add_argument("--df", type=int, default=3,
-                    help="depth_filter_size (reference default 3; >8 runs the heap filter)")
+                    help="depth_filter_size (reference default 3; >8 runs the ring filter in memory)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="bound on the CPU-baseline sample (rank 0, N=1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -86,6 +86,7 @@ struct FrameConst {
   int sort_bins;  // host-side: canonical bin-list order (k_bin_sort) this frame
   int walk_min;   // experiment override of kWalkMinSamplesPerThb (VEIL_WALK_MIN), 0 = default
   int walk_min_u; // the same for bins whose triangles are not staged (VEIL_WALK_MIN_U)
+  int wave1;      // experiment: one wave per step in the staged wave walk (VEIL_WAVE1=1)
   // zero-copy readback: the frame's pinned host RGBA8 / mask (device-mapped),
   // written by the shading kernels next to the device framebuffer; null when
   // the caller does not want host pixels
@@ -197,11 +198,11 @@ struct Buffers {
   uint4* seg_queue;  // half-blocks for the segment kernel: (bin * 32 + hb | high pass << 31, off, cnt, frags)
   uint16_t* pool_slot;  // per THB: the triangle's position in the bin list (k_shade staging slot)
   uint2* lpairs;        // (large triangle, bin row) pairs for k_bin_large
-  // depth filters above 8 (HeapFilter): nodes per lane, and the global
+  // depth filters above 8 (MemFilter): nodes per lane, and the global
   // scratch ([CTA][warp][node/slot][lane]) when they do not fit shared memory
-  uint8_t* heap_g;
-  uint32_t heap_cap;
-  uint32_t heap_ctas;  // grid cap of the shading kernels when heap_g is used
+  uint8_t* dfm_g;
+  uint32_t dfm_cap;
+  uint32_t dfm_ctas;  // grid cap of the shading kernels when dfm_g is used
   Counters* ctr;
 };
 
@@ -1156,36 +1157,40 @@ struct SlotFilter {
   }
 };
 
-// Depth filter for capacities above 8 (DF 9 .. 32768): a binary min-heap per
-// pixel in memory (shared memory when the block's heaps fit next to the
-// staged triangles, else this warp's slice of a global scratch that stays
-// L1/L2-resident). The reference's filter (depth_filter.hpp:31-92) keeps at
-// most k entries and, when an insert overflows it, emits the minimum of
-// (entries + new): with keys unique that is exactly heap replace-top, and its
-// ascending flush is repeated pop-min, so emission order and the out-of-order
-// flag are the reference's for any k. Heap nodes hold (compact key << 15 |
-// colour slot): the colours stay in their slots ([slot][32 lanes], a lane's
-// column) and a sift moves 8 bytes per level. The compact key keeps the
-// (depth, triangle) order in 49 bits: (q << 24 | tri24), or (q << 27 | tri27)
-// with extended limits. A slot is the entry's insertion index: filters are
-// reset per half-block and drained only at its end, so slots are never
-// recycled except by the replace-top, which reuses the emitted entry's slot.
-// Samples per pixel <= THBs per half-block <= the high-path THB limit, so
-// the heap needs min(k, that limit) nodes (host: heap_cap).
-struct HeapFilter {
-  uint64_t* hk;  // this lane's node 0; node i at hk[i * 32]
-  float4* hc;    // this lane's colour slot 0; slot s at hc[s * 32]
-  int n;
+// Depth filter for capacities above 8 (DF 9 .. 32768): per pixel, a sorted
+// ring of entries in memory (shared memory when the block's rings fit next to
+// the staged triangles, else this warp's slice of a global scratch that stays
+// L1/L2-resident). Same emission as the reference's sorted filter
+// (depth_filter.hpp:31-92): when an insert overflows it, the minimum of
+// (entries + new) leaves; keys are unique, so that is "the new key if it is
+// below the front, else the front", and the flush pops the front in order.
+// Samples arrive almost sorted (tri-blocks are depth-sorted per block), so an
+// insert usually lands at the tail: O(1) per sample in the common case, a
+// shift of the displaced entries otherwise. Ring entries hold (compact key
+// << 15 | colour slot); colours stay in their slots ([slot][32 lanes], a
+// lane's column), so a shift moves 8 bytes per entry. The compact key keeps
+// the (depth, triangle) order in 49 bits: (q << 24 | tri24), or
+// (q << 27 | tri27) with extended limits. Slots are insertion indices while
+// the filter fills; once full it stays full until the half-block's flush and
+// every insert reuses the slot of the entry it pushes out. A pixel receives
+// at most one sample per THB of its half-block, so min(k, max THB limit)
+// entries suffice (host: dfm_cap).
+struct MemFilter {
+  uint64_t* rk;  // this lane's ring entry 0; entry i at rk[i * 32]
+  float4* rc;    // this lane's colour slot 0; slot s at rc[s * 32]
+  int n, head, cap_mem;
   uint64_t max_key;
   bool any;
 
   static constexpr int kSlotBits = 15;
   static constexpr uint64_t kSlotMask = (1ull << kSlotBits) - 1ull;
 
-  __device__ __forceinline__ void reset(uint64_t* keys, float4* cols) {
-    hk = keys;
-    hc = cols;
+  __device__ __forceinline__ void reset(uint64_t* keys, float4* cols, int cap) {
+    rk = keys;
+    rc = cols;
     n = 0;
+    head = 0;
+    cap_mem = cap;
     max_key = 0;
     any = false;
   }
@@ -1195,45 +1200,36 @@ struct HeapFilter {
   __device__ __forceinline__ static uint64_t unpack(uint64_t ck) {
     return c_fc.extended ? (((ck >> 27) << 32) | (ck & 0x7ffffffull)) : ck;
   }
+  __device__ __forceinline__ size_t at(int i) const {  // logical -> ring position (x32 lanes)
+    const int p = head + i;
+    return (size_t)(p >= cap_mem ? p - cap_mem : p) * 32u;
+  }
   __device__ __forceinline__ void note(uint64_t pk, bool* ooo) {
     *ooo = any && pk < max_key;
     if (!any || pk > max_key) max_key = pk;
     any = true;
   }
-  __device__ __forceinline__ void sift_down(uint64_t e) {
-    int i = 0;
-    for (;;) {
-      int l = 2 * i + 1;
-      if (l >= n) break;
-      uint64_t el = hk[(size_t)l * 32];
-      if (l + 1 < n) {
-        const uint64_t er = hk[(size_t)(l + 1) * 32];
-        if (er < el) el = er, ++l;
-      }
-      if (e < el) break;
-      hk[(size_t)i * 32] = el;
-      i = l;
+  // places e at logical position n (the tail), shifting larger entries up
+  __device__ __forceinline__ void insert_tail(uint64_t e) {
+    int i = n;
+    while (i > 0) {
+      const uint64_t prev = rk[at(i - 1)];
+      if (prev < e) break;
+      rk[at(i)] = prev;
+      --i;
     }
-    hk[(size_t)i * 32] = e;
+    rk[at(i)] = e;
+    ++n;
   }
   __device__ __forceinline__ bool push(int cap, uint64_t k, float4 c, uint64_t* pk, float4* pc,
                                        bool* ooo) {
-    if (n < cap) {  // sift the new entry up from the next leaf
-      hc[(size_t)n * 32] = c;
-      const uint64_t e = (pack(k) << kSlotBits) | (uint64_t)n;
-      int i = n++;
-      while (i > 0) {
-        const int par = (i - 1) >> 1;
-        const uint64_t ep = hk[(size_t)par * 32];
-        if (ep < e) break;
-        hk[(size_t)i * 32] = ep;
-        i = par;
-      }
-      hk[(size_t)i * 32] = e;
+    const uint64_t ck = pack(k);
+    if (n < cap) {
+      rc[(size_t)n * 32] = c;
+      insert_tail((ck << kSlotBits) | (uint64_t)n);
       return false;
     }
-    const uint64_t e0 = hk[0];
-    const uint64_t ck = pack(k);
+    const uint64_t e0 = rk[at(0)];
     if (ck < (e0 >> kSlotBits)) {  // the new sample is the minimum: it falls straight out
       *pk = k;
       *pc = c;
@@ -1242,25 +1238,27 @@ struct HeapFilter {
     }
     const uint32_t s0 = (uint32_t)(e0 & kSlotMask);
     *pk = unpack(e0 >> kSlotBits);
-    *pc = hc[(size_t)s0 * 32];
-    hc[(size_t)s0 * 32] = c;
+    *pc = rc[(size_t)s0 * 32];
+    rc[(size_t)s0 * 32] = c;
     note(*pk, ooo);
-    sift_down((ck << kSlotBits) | s0);  // replace-top
+    head = head + 1 == cap_mem ? 0 : head + 1;  // drop the front, then insert in its slot
+    --n;
+    insert_tail((ck << kSlotBits) | s0);
     return true;
   }
   __device__ __forceinline__ void pop(uint64_t* pk, float4* pc, bool* ooo) {
-    const uint64_t e0 = hk[0];
+    const uint64_t e0 = rk[at(0)];
     *pk = unpack(e0 >> kSlotBits);
-    *pc = hc[(size_t)(e0 & kSlotMask) * 32];
+    *pc = rc[(size_t)(e0 & kSlotMask) * 32];
+    head = head + 1 == cap_mem ? 0 : head + 1;
     --n;
-    if (n > 0) sift_down(hk[(size_t)n * 32]);
     note(*pk, ooo);
   }
   // Colour push(k) would emit (if any), without modifying the filter.
   __device__ __forceinline__ bool peek(int cap, uint64_t k, float4 c, float4* pc) const {
     if (n < cap) return false;
-    const uint64_t e0 = hk[0];
-    *pc = pack(k) < (e0 >> kSlotBits) ? c : hc[(size_t)(e0 & kSlotMask) * 32];
+    const uint64_t e0 = rk[at(0)];
+    *pc = pack(k) < (e0 >> kSlotBits) ? c : rc[(size_t)(e0 & kSlotMask) * 32];
     return true;
   }
 };
@@ -1643,6 +1641,48 @@ __device__ __forceinline__ float4 shade_staged(const FrameConst& fc, const Stage
   return premultiply(color, T.mat, light);
 }
 
+// shade_staged without branches (every path computed, the flags select), so
+// that two independent samples per lane can be interleaved by the scheduler
+// (shade_waves_staged2). Bit-identical to shade_staged: each selected value
+// is computed by the same operations on the same inputs.
+__device__ __forceinline__ float4 shade_staged_bf(const FrameConst& fc, const StagedTri& T, int px, int py,
+                                                  uint32_t* qd) {
+  const double x = (double)px + 0.5, y = (double)py + 0.5;
+  const uint32_t fl = T.flags;
+  const Fn3 fz = {T.dz[0], T.dz[1], T.dz[2]};
+  const uint32_t qz = quantize_depth(eval(fz, x, y));
+  *qd = (fl & 16u) ? T.pad : qz;
+  const Fn3 f0 = {T.e[0], T.e[1], T.e[2]}, f1 = {T.e[3], T.e[4], T.e[5]}, f2 = {T.e[6], T.e[7], T.e[8]};
+  const double e0 = eval(f0, x, y), e1 = eval(f1, x, y), e2 = eval(f2, x, y);
+  const double sum = __dadd_rn(__dadd_rn(e0, e1), e2);
+  const double inv = __ddiv_rn(1.0, sum);
+  const float b0 = (float)__dmul_rn(e0, inv), b1 = (float)__dmul_rn(e1, inv),
+              b2 = (float)__dmul_rn(e2, inv);
+  const float4 c0 = T.c[0], c1 = T.c[1], c2 = T.c[2];
+  const bool hc = fl & 1u;
+  float4 color;
+  color.x = hc ? __fadd_rn(__fadd_rn(__fmul_rn(c0.x, b0), __fmul_rn(c1.x, b1)), __fmul_rn(c2.x, b2)) : 1.0f;
+  color.y = hc ? __fadd_rn(__fadd_rn(__fmul_rn(c0.y, b0), __fmul_rn(c1.y, b1)), __fmul_rn(c2.y, b2)) : 1.0f;
+  color.z = hc ? __fadd_rn(__fadd_rn(__fmul_rn(c0.z, b0), __fmul_rn(c1.z, b1)), __fmul_rn(c2.z, b2)) : 1.0f;
+  color.w = hc ? __fadd_rn(__fadd_rn(__fmul_rn(c0.w, b0), __fmul_rn(c1.w, b1)), __fmul_rn(c2.w, b2)) : 1.0f;
+  float n[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+    n[k] = __fadd_rn(__fadd_rn(__fmul_rn(T.n[k], b0), __fmul_rn(T.n[3 + k], b1)), __fmul_rn(T.n[6 + k], b2));
+  const float len2 = __fadd_rn(__fadd_rn(__fmul_rn(n[0], n[0]), __fmul_rn(n[1], n[1])), __fmul_rn(n[2], n[2]));
+  const bool pos = len2 > 0.0f;
+  const float il = __fdiv_rn(1.0f, __fsqrt_rn(pos ? len2 : 1.0f));
+  const float nx = pos ? __fmul_rn(n[0], il) : 0.0f, ny = pos ? __fmul_rn(n[1], il) : 0.0f,
+              nz = pos ? __fmul_rn(n[2], il) : 0.0f;
+  const float d = __fadd_rn(__fadd_rn(__fmul_rn(nx, fc.light[0]), __fmul_rn(ny, fc.light[1])),
+                            __fmul_rn(nz, fc.light[2]));
+  const float lit = sminf(1.0f, __fadd_rn(fc.ambient, smaxf(0.0f, -d)));
+  const float light = (fl & 4u) ? T.light : lit;
+  const float4 shaded = premultiply(color, T.mat, light);
+  const float4 cc = T.c[0];
+  return (fl & 8u) ? cc : shaded;
+}
+
 __device__ __forceinline__ uint64_t sample_key(const FrameConst& fc, uint32_t qd, uint32_t tri) {
   // sample_sort_key, raster.hpp:95-97 (32-bit triangle field when extended)
   return fc.extended ? (((uint64_t)qd << 32) | tri) : (((uint64_t)qd << 24) | (tri & 0xffffffu));
@@ -1925,6 +1965,52 @@ __device__ __forceinline__ void shade_waves(const FrameConst& fc, const Buffers&
       bool ooo;
       if (f.push(fc.df, sample_key(fc, qd, tri), col, &pk, &pc, &ooo)) commit(o, pk, pc, ooo);
     }
+  }
+  while (f.n > 0) {
+    uint64_t pk;
+    float4 pc;
+    bool ooo;
+    f.pop(&pk, &pc, &ooo);
+    commit(o, pk, pc, ooo);
+  }
+}
+
+// Wave walk over staged triangles, two waves per step: both waves' samples
+// are shaded by straight-line code (shade_staged_bf) so the scheduler can
+// overlap the two dependency chains, then pushed in wave order -- each pixel
+// still receives its samples in the reference's sequence.
+template <int KM, typename Filter>
+__device__ __forceinline__ void shade_waves_staged2(const FrameConst& fc, int px0, int py0,
+                                                    const uint32_t* tri_l, const uint32_t* mask_l,
+                                                    const uint16_t* slot_l, const StagedTri* staged,
+                                                    uint32_t n, PixelOut& o, Filter& f) {
+  const int lane = threadIdx.x & 31;
+  const int px = px0 + (lane & 7), py = py0 + (lane >> 3);
+  constexpr uint32_t kNone = 0xffffffffu;
+  auto form = [&](uint32_t* r) {
+    uint32_t acc_mask = 0, my_r = kNone;
+    while (*r < n) {
+      const uint32_t m = mask_l[*r];
+      if (acc_mask & m) break;
+      if ((m >> lane) & 1u) my_r = *r;
+      acc_mask |= m;
+      ++*r;
+    }
+    return my_r;
+  };
+  uint32_t r = 0;
+  while (r < n) {
+    const uint32_t ra = form(&r);
+    const uint32_t rb = form(&r);
+    const uint32_t ia = ra != kNone ? ra : 0u, ib = rb != kNone ? rb : 0u;
+    uint32_t qa, qb;
+    const float4 ca = shade_staged_bf(fc, staged[slot_l[ia]], px, py, &qa);
+    const float4 cb = shade_staged_bf(fc, staged[slot_l[ib]], px, py, &qb);
+    uint64_t pk;
+    float4 pc;
+    bool ooo;
+    if (ra != kNone && f.push(fc.df, sample_key(fc, qa, tri_l[ia]), ca, &pk, &pc, &ooo)) commit(o, pk, pc, ooo);
+    if (rb != kNone && f.push(fc.df, sample_key(fc, qb, tri_l[ib]), cb, &pk, &pc, &ooo)) commit(o, pk, pc, ooo);
   }
   while (f.n > 0) {
     uint64_t pk;
@@ -2486,17 +2572,17 @@ __global__ void __launch_bounds__(128, 7) k_extract(Buffers B, int pass,
 // samples composite the background.
 constexpr int kShadeStage = 256;  // THB entries staged per warp; longer lists stream
 
-// This warp's heap filter storage (HeapFilter): after the staged triangles in
+// This warp's ring filter storage (MemFilter): after the staged triangles in
 // dynamic shared memory, or its slice of the global scratch.
 template <int kMode>
-__device__ __forceinline__ void heap_reset(const Buffers& B, uint8_t* shade_dyn, HeapFilter& f) {
+__device__ __forceinline__ void dfm_reset(const Buffers& B, uint8_t* shade_dyn, MemFilter& f) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const size_t warp_bytes = (size_t)B.heap_cap * 32u * 24u;
-  uint8_t* base = B.heap_g ? B.heap_g + ((size_t)blockIdx.x * 8u + (size_t)warp) * warp_bytes
+  const size_t warp_bytes = (size_t)B.dfm_cap * 32u * 24u;
+  uint8_t* base = B.dfm_g ? B.dfm_g + ((size_t)blockIdx.x * 8u + (size_t)warp) * warp_bytes
                            : shade_dyn + (kMode == 0 ? (size_t)kStageTris * sizeof(StagedTri) : 0) +
                                  (size_t)warp * warp_bytes;
   f.reset(reinterpret_cast<uint64_t*>(base) + lane,
-          reinterpret_cast<float4*>(base + (size_t)B.heap_cap * 32u * 8u) + lane);
+          reinterpret_cast<float4*>(base + (size_t)B.dfm_cap * 32u * 8u) + lane, (int)B.dfm_cap);
 }
 
 // kMode: 0 = broadcast walk for half-blocks with big THBs (also writes every
@@ -2645,8 +2731,8 @@ __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
       }
       if (kMode == 2) {
         if constexpr (KM == 0) {
-          HeapFilter f;
-          heap_reset<kMode>(B, shade_dyn, f);
+          MemFilter f;
+          dfm_reset<kMode>(B, shade_dyn, f);
           shade_walk<KM, true, kTex>(fc, B, hpx0, hpy0, tri_l, mask_l, d.cnt, po, &enumerated, f);
         } else {
           RegFilter<KM, true> f;
@@ -2659,15 +2745,18 @@ __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
           SlotFilter<KM> f;
           f.reset(reinterpret_cast<float4*>(shade_dyn + (size_t)kStageTris * sizeof(StagedTri)) +
                   (size_t)warp * KM * 32 + lane);
-          if (staged_ok && d.cnt <= (uint32_t)kShadeStage)  // all operands in shared memory
+          if (staged_ok && d.cnt <= (uint32_t)kShadeStage && !fc.wave1)  // all operands in shared memory
+            shade_waves_staged2<KM>(fc, hpx0, hpy0, stage_tri[warp], stage_mask[warp], stage_slot[warp],
+                                    row_tris, d.cnt, po, f);
+          else if (staged_ok && d.cnt <= (uint32_t)kShadeStage)
             shade_waves<KM, kTex>(fc, B, hpx0, hpy0, stage_tri[warp], stage_mask[warp], stage_slot[warp],
-                            row_tris, d.cnt, po, f);
+                                  row_tris, d.cnt, po, f);
           else
             shade_waves<KM, kTex>(fc, B, hpx0, hpy0, tri_l, mask_l, slot_l, staged_ok ? row_tris : nullptr,
                             d.cnt, po, f);
         } else {
-          HeapFilter f;
-          heap_reset<kMode>(B, shade_dyn, f);
+          MemFilter f;
+          dfm_reset<kMode>(B, shade_dyn, f);
           shade_waves<KM, kTex>(fc, B, hpx0, hpy0, tri_l, mask_l, slot_l, staged_ok ? row_tris : nullptr,
                           d.cnt, po, f);
         }
@@ -2678,8 +2767,8 @@ __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
           f.reset(reinterpret_cast<float4*>(shade_dyn) + (size_t)warp * KM * 32 + lane);
           shade_segments<KM, kTex>(fc, B, hpx0, hpy0, tri_l, mask_l, pre_l, d.cnt, d.frags, route_s[warp], po, f);
         } else {
-          HeapFilter f;
-          heap_reset<kMode>(B, shade_dyn, f);
+          MemFilter f;
+          dfm_reset<kMode>(B, shade_dyn, f);
           shade_segments<KM, kTex>(fc, B, hpx0, hpy0, tri_l, mask_l, pre_l, d.cnt, d.frags, route_s[warp], po, f);
         }
       }
@@ -2938,7 +3027,7 @@ struct DeviceScene {
       tri_y;
   DevBuf off, qcur, tcur, cat, bin_list0, bin_list1, prop_q, bin_cost, bin_order, prop, items, item_rows, slots, spill0, spill1, scratch, fb, mask,
       hash, emit, tile_ids, hbd, pool_tri, pool_mask, pool_pre, seg_queue, pool_slot, lpairs, lpair_cols,
-      heap_g;
+      dfm_g;
   uint32_t items_cap = 0;
   uint32_t pool_cap = 0;
   uint32_t lpairs_cap = 0;
@@ -3207,11 +3296,11 @@ void launch_extract(DeviceScene* d, const dev::FrameConst& fc, const dev::Buffer
   *launches += 2;
 }
 
-// Heap filters (KM == 0, depth_filter_size > 8) live in dynamic shared memory
-// when a block's eight warps' heaps fit next to the staged triangles, else in
-// a global scratch (VEIL_HEAP_GLOBAL=1 forces the latter for A/B tests).
-constexpr size_t kHeapBytesPerNode = 32 * (8 + 16);  // one node per lane: key + colour slot
-constexpr size_t kHeapSmemBudget = 190 * 1024;
+// Ring filters (KM == 0, depth_filter_size > 8) live in dynamic shared memory
+// when a block's eight warps' rings fit next to the staged triangles, else in
+// a global scratch (VEIL_DFM_GLOBAL=1 forces the latter for A/B tests).
+constexpr size_t kDfmBytesPerEntry = 32 * (8 + 16);  // one node per lane: key + colour slot
+constexpr size_t kDfmSmemBudget = 190 * 1024;
 
 template <int KM, int kMode, bool kTex>
 void launch_shade_mode(DeviceScene* d, const dev::FrameConst& fc, const dev::Buffers& B,
@@ -3219,8 +3308,8 @@ void launch_shade_mode(DeviceScene* d, const dev::FrameConst& fc, const dev::Buf
   size_t dyn = (kMode == 0 ? size_t(dev::kStageTris) * sizeof(dev::StagedTri) : 0);
   if (KM != 0)
     dyn += (kMode != 2 ? size_t(8) * KM * 32 * sizeof(float4) : 0);
-  else if (!B.heap_g)
-    dyn += size_t(8) * B.heap_cap * kHeapBytesPerNode;
+  else if (!B.dfm_g)
+    dyn += size_t(8) * B.dfm_cap * kDfmBytesPerEntry;
   static size_t configured = 0;  // per instantiation: the largest dynamic size set so far
   if (dyn > configured) {
     ck(cudaFuncSetAttribute(dev::k_shade<KM, kMode, kTex>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -3238,7 +3327,7 @@ void launch_shade_mode(DeviceScene* d, const dev::FrameConst& fc, const dev::Buf
   const int per_sm = it->second;
   const long long items = kMode == 1 ? ((long long)fc.nbins * 32 + 7) / 8 : (long long)fc.nbins;
   long long cap = (long long)std::max(1, per_sm) * d->sm_count;
-  if (KM == 0 && B.heap_g) cap = std::min<long long>(cap, B.heap_ctas);  // scratch slices
+  if (KM == 0 && B.dfm_g) cap = std::min<long long>(cap, B.dfm_ctas);  // scratch slices
   const int grid = int(std::max<long long>(1, std::min<long long>(cap, items)));
   dev::k_shade<KM, kMode, kTex><<<grid, 256, dyn, d->stream>>>(B);
   ck(cudaGetLastError(), "k_shade launch");
@@ -3260,7 +3349,7 @@ template <bool kTex>
 void launch_shade_tex(DeviceScene* d, const dev::FrameConst& fc, const dev::Buffers& B, int* launches) {
   const int df = fc.df;
   // KM == df exactly up to 8 (register filters, the capacity a compile-time
-  // constant); above 8 the heap filter (KM == 0) with any capacity
+  // constant); above 8 the sorted ring filter in memory (KM == 0), any capacity
   if (df == 1) launch_shade_km<1, kTex>(d, fc, B, launches);
   else if (df == 2) launch_shade_km<2, kTex>(d, fc, B, launches);
   else if (df == 3) launch_shade_km<3, kTex>(d, fc, B, launches);
@@ -3380,6 +3469,7 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   if (const char* bs = std::getenv("VEIL_BIN_SORT")) fc.sort_bins = std::atoi(bs) ? 1 : 0;
   if (const char* wm = std::getenv("VEIL_WALK_MIN")) fc.walk_min = std::atoi(wm);
   if (const char* wm = std::getenv("VEIL_WALK_MIN_U")) fc.walk_min_u = std::atoi(wm);
+  if (const char* w1 = std::getenv("VEIL_WAVE1")) fc.wave1 = std::atoi(w1);
 
   const uint32_t Q = d->nquads;
   const size_t nb = size_t(fc.nbins);
@@ -3468,35 +3558,35 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   d->scratch.ensure(per_cta * d->raster_ctas_global);
   d->fb_w = cam.width;
   d->fb_h = cam.height;
-  // Heap depth filters (depth_filter_size > 8): a pixel receives at most one
+  // Ring depth filters (depth_filter_size > 8): a pixel receives at most one
   // sample per THB of its half-block, and a half-block holds at most
   // max(low, high) THB-limit THBs, so min(k, that) nodes per lane suffice.
-  uint32_t heap_cap = 0, heap_ctas = 0;
-  bool heap_global = false;
+  uint32_t dfm_cap = 0, dfm_ctas = 0;
+  bool dfm_global = false;
   if (fc.df > 8) {
-    heap_cap = std::min<uint32_t>(uint32_t(fc.df), std::max(fc.low.thb, fc.high.thb));
-    if (heap_cap > (1u << dev::HeapFilter::kSlotBits))
+    dfm_cap = std::min<uint32_t>(uint32_t(fc.df), std::max(fc.low.thb, fc.high.thb));
+    if (dfm_cap > (1u << dev::MemFilter::kSlotBits))
       throw Error(VEIL_ERR_INVALID_ARG,
                   "depth_filter_size above 32768 with a THB limit above 32768 is not supported");
-    const size_t per_cta = size_t(8) * heap_cap * kHeapBytesPerNode;
-    const char* hg = std::getenv("VEIL_HEAP_GLOBAL");
-    heap_global = (hg && *hg && *hg != '0') ||
-                  size_t(dev::kStageTris) * sizeof(dev::StagedTri) + per_cta > kHeapSmemBudget;
-    if (heap_global) {
+    const size_t per_cta = size_t(8) * dfm_cap * kDfmBytesPerEntry;
+    const char* hg = std::getenv("VEIL_DFM_GLOBAL");
+    dfm_global = (hg && *hg && *hg != '0') ||
+                  size_t(dev::kStageTris) * sizeof(dev::StagedTri) + per_cta > kDfmSmemBudget;
+    if (dfm_global) {
       // up to 4 CTAs per SM (the shading kernels' occupancy), fewer when the
       // scratch would pass 4 GiB
-      heap_ctas = uint32_t(d->sm_count) * 4u;
-      while (heap_ctas > uint32_t(d->sm_count) && size_t(heap_ctas) * per_cta > (size_t(4) << 30))
-        heap_ctas -= uint32_t(d->sm_count);
-      d->heap_g.ensure(size_t(heap_ctas) * per_cta);
+      dfm_ctas = uint32_t(d->sm_count) * 4u;
+      while (dfm_ctas > uint32_t(d->sm_count) && size_t(dfm_ctas) * per_cta > (size_t(4) << 30))
+        dfm_ctas -= uint32_t(d->sm_count);
+      d->dfm_g.ensure(size_t(dfm_ctas) * per_cta);
     }
   }
 
   dev::Buffers& B = P.B;
   std::memset(&B, 0, sizeof B);
-  B.heap_g = heap_global ? d->heap_g.as<uint8_t>() : nullptr;
-  B.heap_cap = heap_cap;
-  B.heap_ctas = heap_ctas;
+  B.dfm_g = dfm_global ? d->dfm_g.as<uint8_t>() : nullptr;
+  B.dfm_cap = dfm_cap;
+  B.dfm_ctas = dfm_ctas;
   B.pos = d->pos.as<float4>();
   B.vcol = d->vcol.as<uint32_t>();
   B.vnrm = d->vnrm.as<uint32_t>();

@@ -1,9 +1,9 @@
-"""Depth-filter sizes above 8 on the device (heap filter), bit-exact.
+"""Depth-filter sizes above 8 on the device (ring filter), bit-exact.
 
 The reference's DepthFilter has no capacity bound (depth_filter.hpp:31-60);
 render_pipeline only requires DF >= 1 (renderer.cpp:70-72) and its CLI
 allows 1..1024 (veil_cli.cpp:81-82). libveil runs DF <= 8 in register
-filters and every larger DF in a per-pixel min-heap (shared memory when it
+filters and every larger DF in a per-pixel sorted ring (shared memory when it
 fits beside the staged triangles, global scratch otherwise). Scenes:
 intersecting_shells with 128 / 300 sheets (reference synthetic.cpp, via the
 shim's generate_synthetic_scene with SyntheticParams), whose measured
@@ -55,19 +55,19 @@ def test_large_depth_filter_300_sheets(df):
     assert not bad, bad
 
 
-@pytest.mark.parametrize("df", [12, 16])
-def test_heap_in_global_memory_equals_shared(df, monkeypatch):
-    """The global-scratch heap (VEIL_HEAP_GLOBAL=1) is bit-identical."""
+@pytest.mark.parametrize("df", [12, 16, 17])
+def test_ring_in_global_memory_equals_shared(df, monkeypatch):
+    """The global-scratch ring (VEIL_DFM_GLOBAL=1) is bit-identical."""
     arr = shells(128)
     p = default_params(depth_filter_size=df)
-    monkeypatch.setenv("VEIL_HEAP_GLOBAL", "1")
+    monkeypatch.setenv("VEIL_DFM_GLOBAL", "1")
     got = gpu_dump(arr, p)
     bad = compare(got, bindings.oracle_render(arr, p), PARITY_ARRAYS)
     assert not bad, bad
 
 
 def test_large_depth_filter_segment_kernel():
-    """Tiny triangles (segment routing, k_shade mode 1) with a heap filter."""
+    """Tiny triangles (segment routing, k_shade mode 1) with a ring filter."""
     arr = bindings.RefScene.synthetic_params("random_soup", 5, 192, 160, triangles=20000).arrays()
     for df in (9, 40):
         p = default_params(depth_filter_size=df)

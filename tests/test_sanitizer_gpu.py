@@ -6,7 +6,7 @@ with a volatile-load decoupled look-back, and k_extract shares its item state
 across four warps with block barriers. memcheck, racecheck and synccheck run
 the plain C embedder (tests/c/capi_render.c, no Python/torch in the process)
 on scenes that reach the wave walk, the segment kernel, the alpha-threshold
-walk, the heap depth filter (shared and global) and both extraction passes.
+walk, the ring depth filter (shared and global) and both extraction passes.
 """
 import os
 import shutil
@@ -24,8 +24,8 @@ CASES = [
     ("dense_bin", 3, 256, 256, 3),        # low + high bins, wave walk + segments
     ("random_soup", 4, 160, 128, 8),      # tiny triangles: segment kernel
     ("layered_quads", 2, 128, 96, 1),     # big quads: staged wave walk
-    ("intersecting_shells", 5, 128, 96, 12),  # heap filter in shared memory
-    ("intersecting_shells", 6, 96, 64, 40),   # heap filter in global scratch
+    ("intersecting_shells", 5, 128, 96, 12),  # ring filter in shared memory
+    ("intersecting_shells", 6, 96, 64, 40),   # ring filter in global scratch
 ]
 
 
