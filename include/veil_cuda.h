@@ -147,6 +147,20 @@ typedef struct veil_ipc_framebuffer {
 veil_status veil_export_framebuffer(const veil_scene* scene, veil_ipc_framebuffer* out);
 veil_status veil_import_peer_framebuffer(const veil_scene* scene, const veil_ipc_framebuffer* fb);
 
+/* Multi-GPU frame in one process (no IPC, no collective): the frame's bins are
+ * interleaved over device_count shards exactly as in veil_render_scene_shard
+ * (shard i = rank i, on devices[i]; setup replicated per device). Every shard
+ * renders concurrently in its own workspace and host thread, and its shading
+ * kernels write their finished pixels straight into devices[0]'s framebuffer
+ * (peer memory over NVLink; the same buffer when a device appears twice), so
+ * the gather overlaps the shading and the frame is read back once. The
+ * render's pixels, mask, report and stats describe the whole frame; stage
+ * times in veil_render_stats are the maximum over shards. Requires peer
+ * access from every device to devices[0]. Output is identical for any
+ * device list. */
+veil_status veil_render_scene_multi(const veil_scene* scene, const veil_render_params* params,
+                                    const int* devices, int device_count, veil_render** out_render);
+
 /* ---- device-resident frame loop ------------------------------------------- */
 
 /* Renders into device memory only (no host copies); for benchmarks that time

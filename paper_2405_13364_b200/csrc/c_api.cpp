@@ -376,6 +376,20 @@ veil_status veil_render_device(const veil_scene* scene, const veil_render_params
   });
 }
 
+veil_status veil_render_scene_multi(const veil_scene* scene, const veil_render_params* params,
+                                    const int* devices, int device_count, veil_render** out) {
+  if (!scene || !devices || !out) return bad_arg("scene, devices and out_render are required");
+  if (device_count < 1 || device_count > 64) return bad_arg("device_count must be in 1..64");
+  veil::RenderOptions o = options_from(params);
+  if (o.params.flags & VEIL_RENDER_REFERENCE) return bad_arg("the a-buffer renderer does not shard");
+  return guard([&] {
+    auto r = std::make_unique<veil_render>();
+    veil::render_frame_multi(scene->s, o, devices, device_count, &r->out);
+    finish_render(scene, o, r.get());
+    *out = r.release();
+  });
+}
+
 veil_status veil_shard_pack_tiles_device(const veil_scene* scene, const veil_shard* shard,
                                          void* dev_tiles, uint64_t bytes) {
   if (!scene || !shard || !dev_tiles) return bad_arg("scene, shard and dev_tiles are required");

@@ -34,6 +34,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <exception>
 #include <thread>
 #include <vector>
 
@@ -44,6 +45,21 @@ namespace veil {
 
 // ============================================================ device side
 namespace dev {
+
+// Device-side invariant checks of the bounds-checked build (make CHECKS=1 ->
+// build_checked/libveil.so, run by tests/test_checked_build_gpu.py; the
+// pool's compute-sanitizer is unavailable): a violated index bound traps the
+// kernel, which fails the frame. Compiled out of the product build.
+#ifdef VEIL_DEVICE_CHECKS
+#define VEIL_CHECK(cond) \
+  do {                   \
+    if (!(cond)) __trap(); \
+  } while (0)
+#else
+#define VEIL_CHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
 
 constexpr int kSetupBlock = 256;
 constexpr uint64_t kHashSeed = 0xcbf29ce484222325ull;
@@ -87,6 +103,16 @@ struct FrameConst {
   int walk_min;   // experiment override of kWalkMinSamplesPerThb (VEIL_WALK_MIN), 0 = default
   int walk_min_u; // the same for bins whose triangles are not staged (VEIL_WALK_MIN_U)
   int wave1;      // experiment: one wave per step in the staged wave walk (VEIL_WAVE1=1)
+  // Fused raster for tiny-triangle frames (not decoded): k_extract recomputes
+  // small quads' triangle setups from the positions instead of reading 128-B
+  // records, and shades its half-blocks right after extracting them (no
+  // k_shade); write_tri: k_setup_tris still stores every record (parity dumps,
+  // the non-fused path; large quads' records are always stored, k_bin_large
+  // reads them).
+  int fused;
+  int write_tri;
+  int fused_read;  // experiment: the fused raster reads stored records (VEIL_FUSED_READ=1)
+  int bulk_stage;  // k_shade stages THB lists with cp.async.bulk (VEIL_BULK_STAGE=0/1)
   // zero-copy readback: the frame's pinned host RGBA8 / mask (device-mapped),
   // written by the shading kernels next to the device framebuffer; null when
   // the caller does not want host pixels
@@ -202,6 +228,14 @@ struct Buffers {
   // scratch ([CTA][warp][node/slot][lane]) when they do not fit shared memory
   uint8_t* dfm_g;
   uint32_t dfm_cap;
+  // fused raster scratch per k_extract CTA: candidate triangle setups (for
+  // row spans spread over the warp) and the item's TBR planes (phase B
+  // centroid depths and the shading), L2-resident while the item runs
+  TriRec* cscratch;
+  struct TriPlanes* tplanes;
+  uint64_t cs_per_cta, tp_per_cta;        // k_extract<false> CTAs (shared-memory items)
+  uint64_t cs_per_cta_g, tp_per_cta_g;    // k_extract<true> CTAs (global-scratch items)
+  uint64_t cs_off_g, tp_off_g;            // where the latter's slices start
   uint32_t dfm_ctas;  // grid cap of the shading kernels when dfm_g is used
   Counters* ctr;
 };
@@ -235,6 +269,11 @@ __device__ __forceinline__ float slut_n(uint32_t w, int shift) {
 }
 
 // ------------------------------------------------------------ setup
+
+__device__ __forceinline__ uint32_t checked_index(uint32_t i, uint32_t n) {
+  VEIL_CHECK(i < n);
+  return i;
+}
 
 __device__ __forceinline__ void load_quad(const Buffers& B, uint32_t q, uint4* idx,
                                           float4 p[4]) {
@@ -436,6 +475,30 @@ __device__ __forceinline__ uint32_t flat_normal(const float4& a, const float4& b
   return encode_normal((float)n[0], (float)n[1], (float)n[2]);
 }
 
+// A triangle's edge and depth planes (the shading inputs of a TriRec).
+struct TriPlanes {
+  Fn3 e[3];
+  Fn3 dz;
+};
+static_assert(sizeof(TriPlanes) == 96, "TriPlanes layout");
+
+// Fused raster: the setup of visible triangle ti recomputed from the scene
+// positions exactly as k_setup_tris computes it (same expressions and
+// roundings, so the same doubles); only called for triangles whose y range
+// in tri_y is non-empty, i.e. valid ones.
+__device__ __forceinline__ void recompute_setup(const FrameConst& fc, const Buffers& B, uint32_t ti,
+                                                TriRec* out) {
+  const uint4 idx = __ldg(&B.vq_idx[ti >> 1]);
+  const uint32_t i1 = (ti & 1u) == 0 ? idx.y : idx.z, i2 = (ti & 1u) == 0 ? idx.z : idx.w;
+  const float4 p0 = __ldg(&B.pos[idx.x]), p1 = __ldg(&B.pos[i1]), p2 = __ldg(&B.pos[i2]);
+  double c0[4], c1[4], c2[4];
+  to_clip(fc.m, p0.x, p0.y, p0.z, c0);
+  to_clip(fc.m, p1.x, p1.y, p1.z, c1);
+  to_clip(fc.m, p2.x, p2.y, p2.z, c2);
+  bool valid;
+  triangle_setup(fc, c0, c1, c2, out, &valid);
+}
+
 // Phase 1 of setup in one pass (setup.cpp:252-302): cull every quad, then
 // compact the visible ones in ascending input order. Blocks take tickets in
 // launch order and chain their visible counts with a decoupled look-back
@@ -555,16 +618,9 @@ __global__ void __launch_bounds__(kSetupBlock, 4) k_setup(Buffers B, uint32_t nb
   B.vq_flags[slot] = (o.large ? 1u : 0u) | (has_c ? 2u : 0u) | (has_n ? 4u : 0u) | (has_uv ? 8u : 0u) |
                      (o.flags << 4);
   B.vq_mat[slot] = mat;
-  if (has_uv) {  // setup.cpp:326-328
-    const float2 u0 = B.vuv[idx.x], u1 = B.vuv[idx.y], u2 = B.vuv[idx.z], u3 = B.vuv[idx.w];
-    B.vq_uv[2 * (size_t)slot] = make_float4(u0.x, u0.y, u1.x, u1.y);
-    B.vq_uv[2 * (size_t)slot + 1] = make_float4(u2.x, u2.y, u3.x, u3.y);
-  }
-  uint4 col = make_uint4(0, 0, 0, 0), nrm = make_uint4(0, 0, 0, 0);
-  if (has_c) col = make_uint4(B.vcol[idx.x], B.vcol[idx.y], B.vcol[idx.z], B.vcol[idx.w]);
-  if (has_n) nrm = make_uint4(B.vnrm[idx.x], B.vnrm[idx.y], B.vnrm[idx.z], B.vnrm[idx.w]);
-  B.vq_col[slot] = col;
-  B.vq_nrm[slot] = nrm;
+  // (the corner colours / normals / UVs are gathered by k_setup_tris, which a
+  // sharded rank runs for its own bins' quads only: this cull + compaction is
+  // the part every rank replicates)
 }
 
 // Triangle setups (setup.cpp:305-349, compute_triangle_setup 209-239): one
@@ -605,12 +661,29 @@ __global__ void __launch_bounds__(kTriBlock, 7) k_setup_tris(Buffers B) {
         needed = any;
       }
     }
+    uint4 qcol = make_uint4(0, 0, 0, 0), qnrm = make_uint4(0, 0, 0, 0);
     if (needed) {
       slot = ti >> 1;
       t = ti & 1u;
       vf = B.vq_flags[slot];
       const uint4 idx = B.vq_idx[slot];
       mat = B.vq_mat[slot];
+      // the visible quad's corner attributes (setup.cpp:326-333), stored once
+      // (by triangle 0) for the shading and gathered by both triangles when
+      // they write decoded records
+      if (t == 0 || fc.decoded) {
+        if (vf & 2u) qcol = make_uint4(B.vcol[idx.x], B.vcol[idx.y], B.vcol[idx.z], B.vcol[idx.w]);
+        if (vf & 4u) qnrm = make_uint4(B.vnrm[idx.x], B.vnrm[idx.y], B.vnrm[idx.z], B.vnrm[idx.w]);
+      }
+      if (t == 0) {
+        B.vq_col[slot] = qcol;
+        B.vq_nrm[slot] = qnrm;
+        if (vf & 8u) {
+          const float2 u0 = B.vuv[idx.x], u1 = B.vuv[idx.y], u2 = B.vuv[idx.z], u3 = B.vuv[idx.w];
+          B.vq_uv[2 * (size_t)slot] = make_float4(u0.x, u0.y, u1.x, u1.y);
+          B.vq_uv[2 * (size_t)slot + 1] = make_float4(u2.x, u2.y, u3.x, u3.y);
+        }
+      }
       if (!((vf >> 4) & (1u << t))) {  // not individually culled
         const uint32_t i1 = t == 0 ? idx.y : idx.z, i2 = t == 0 ? idx.z : idx.w;
         const float4 p0 = __ldg(&B.pos[idx.x]), p1 = __ldg(&B.pos[i1]), p2 = __ldg(&B.pos[i2]);
@@ -626,7 +699,11 @@ __global__ void __launch_bounds__(kTriBlock, 7) k_setup_tris(Buffers B) {
       }
     }
     stage[threadIdx.x] = rec;
-    const unsigned needm = kShard ? __ballot_sync(0xffffffffu, needed) : 0xffffffffu;
+    // the 128-byte record is stored when some consumer reads it: always for
+    // large quads (k_bin_large), for small ones unless the fused raster
+    // recomputes them (fc.write_tri == 0)
+    const bool store = (!kShard || needed) && (fc.write_tri || (vf & 1u));
+    const unsigned needm = __ballot_sync(0xffffffffu, store);
     __syncwarp();
     {  // coalesced copy-out of this warp's 32 records (4 KB)
       const uint32_t wbase = base + (uint32_t)warp * 32u;
@@ -636,7 +713,7 @@ __global__ void __launch_bounds__(kTriBlock, 7) k_setup_tris(Buffers B) {
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const uint32_t e = (uint32_t)k * 32u + lane;  // 16-byte chunk index within the warp
-        if (e < nrec * 8u && (!kShard || ((needm >> (e >> 3)) & 1u))) dst[e] = src[e];
+        if (e < nrec * 8u && ((needm >> (e >> 3)) & 1u)) dst[e] = src[e];
       }
     }
     __syncwarp();
@@ -649,7 +726,7 @@ __global__ void __launch_bounds__(kTriBlock, 7) k_setup_tris(Buffers B) {
         // corner slots (0,1,2) / (0,2,3), shading.cpp:41-44
         const MatDev md = B.mats[mat];
         const bool has_c = vf & 2u, has_n = vf & 4u;
-        const uint4 col = B.vq_col[slot], nrm = B.vq_nrm[slot];
+        const uint4 col = qcol, nrm = qnrm;
         const uint32_t cw[3] = {col.x, t == 0 ? col.y : col.z, t == 0 ? col.z : col.w};
         const uint32_t nw[3] = {nrm.x, t == 0 ? nrm.y : nrm.z, t == 0 ? nrm.z : nrm.w};
         ShadeRec sr;
@@ -783,6 +860,7 @@ __global__ void __launch_bounds__(256) k_bin_pass(Buffers B) {
           uint32_t slot = 0;
           warp_agg_add(B.qcur, bin, act, &slot);
           if (act && slot < fc.items_cap) {
+            VEIL_CHECK(bin < (uint32_t)fc.nbins);
             B.items[slot] = q;
             const uint2 ty = *reinterpret_cast<const uint2*>(&B.tri_y[2 * q]);
             B.item_rows[slot] = (uint8_t)(block_rows_mask(ty.x, (int)by, fc.height) |
@@ -848,6 +926,7 @@ __global__ void __launch_bounds__(256) k_bin_large(Buffers B) {
         if (kWrite) {
           const uint32_t slot = atomicAdd(&B.tcur[bin], 1u);
           if (slot < fc.items_cap) {
+            VEIL_CHECK(bin < fc.nbins);
             B.items[slot] = ti;
             B.item_rows[slot] = (uint8_t)block_rows_mask(B.tri_y[ti], R, fc.height);
           }
@@ -1211,6 +1290,7 @@ struct MemFilter {
   }
   // places e at logical position n (the tail), shifting larger entries up
   __device__ __forceinline__ void insert_tail(uint64_t e) {
+    VEIL_CHECK(n < cap_mem && (uint32_t)(e & kSlotMask) < (uint32_t)cap_mem);
     int i = n;
     while (i > 0) {
       const uint64_t prev = rk[at(i - 1)];
@@ -1374,7 +1454,7 @@ __device__ __forceinline__ float4 premultiply_tex(float4 color, float4 mat, floa
 // instantiations of the shading kernels). UVs by
 // the quotient rule with analytic gradients (shading.cpp:55-74), in double;
 // zero when the quad carries no UVs (SampleContext defaults).
-__device__ __forceinline__ float4 texture_factor(const Buffers& B, const TriRec& t, uint32_t q, int ltri,
+__device__ __forceinline__ float4 texture_factor(const Buffers& B, const Fn3* te, uint32_t q, int ltri,
                                               bool has_uv, int texi, double e0, double e1, double e2,
                                               double sum, double inv) {
   float2 uv = make_float2(0.f, 0.f), duv_dx = uv, duv_dy = uv;
@@ -1387,12 +1467,12 @@ __device__ __forceinline__ float4 texture_factor(const Buffers& B, const TriRec&
       return __dadd_rn(__dadd_rn(__dmul_rn(a0, b0), __dmul_rn(a1, b1)), __dmul_rn(a2, b2));
     };
     const double nu = dot3d(c0.x, c1.x, c2.x, e0, e1, e2), nv = dot3d(c0.y, c1.y, c2.y, e0, e1, e2);
-    const double nu_dx = dot3d(c0.x, c1.x, c2.x, t.e[0].a, t.e[1].a, t.e[2].a);
-    const double nv_dx = dot3d(c0.y, c1.y, c2.y, t.e[0].a, t.e[1].a, t.e[2].a);
-    const double nu_dy = dot3d(c0.x, c1.x, c2.x, t.e[0].b, t.e[1].b, t.e[2].b);
-    const double nv_dy = dot3d(c0.y, c1.y, c2.y, t.e[0].b, t.e[1].b, t.e[2].b);
-    const double d_dx = __dadd_rn(__dadd_rn(t.e[0].a, t.e[1].a), t.e[2].a);
-    const double d_dy = __dadd_rn(__dadd_rn(t.e[0].b, t.e[1].b), t.e[2].b);
+    const double nu_dx = dot3d(c0.x, c1.x, c2.x, te[0].a, te[1].a, te[2].a);
+    const double nv_dx = dot3d(c0.y, c1.y, c2.y, te[0].a, te[1].a, te[2].a);
+    const double nu_dy = dot3d(c0.x, c1.x, c2.x, te[0].b, te[1].b, te[2].b);
+    const double nv_dy = dot3d(c0.y, c1.y, c2.y, te[0].b, te[1].b, te[2].b);
+    const double d_dx = __dadd_rn(__dadd_rn(te[0].a, te[1].a), te[2].a);
+    const double d_dy = __dadd_rn(__dadd_rn(te[0].b, te[1].b), te[2].b);
     const double inv2 = __dmul_rn(inv, inv);
     uv = make_float2((float)__dmul_rn(nu, inv), (float)__dmul_rn(nv, inv));
     duv_dx = make_float2((float)__dmul_rn(__dsub_rn(__dmul_rn(nu_dx, sum), __dmul_rn(nu, d_dx)), inv2),
@@ -1407,16 +1487,19 @@ __device__ __forceinline__ float4 texture_factor(const Buffers& B, const TriRec&
 // textures. Returns the premultiplied colour and the sample depth.
 template <bool kTex>
 __device__ __forceinline__ float4 shade_sample(const FrameConst& fc, const Buffers& B,
-                                               uint32_t tri, int px, int py, double* depth) {
-  const TriRec& t = B.tri[tri];
+                                               uint32_t tri, int px, int py, double* depth,
+                                               const TriPlanes* P = nullptr) {
+  // planes: the fused raster's per-TBR copy, else the triangle's record
+  const Fn3* te = P ? P->e : B.tri[tri].e;
+  const Fn3* tz = P ? &P->dz : &B.tri[tri].dz;
   const uint4 meta = __ldg(&B.tri_meta[tri]);
   const double x = (double)px + 0.5, y = (double)py + 0.5;
-  const double e0 = eval(t.e[0], x, y), e1 = eval(t.e[1], x, y), e2 = eval(t.e[2], x, y);
+  const double e0 = eval(te[0], x, y), e1 = eval(te[1], x, y), e2 = eval(te[2], x, y);
   const double sum = __dadd_rn(__dadd_rn(e0, e1), e2);
   const double inv = __ddiv_rn(1.0, sum);
   const float b0 = (float)__dmul_rn(e0, inv), b1 = (float)__dmul_rn(e1, inv),
               b2 = (float)__dmul_rn(e2, inv);
-  *depth = eval(t.dz, x, y);
+  *depth = eval(*tz, x, y);
   if (fc.decoded) {
     const ShadeRec& sr = B.shade[tri];
     const uint32_t fl = sr.flags;
@@ -1474,7 +1557,7 @@ __device__ __forceinline__ float4 shade_sample(const FrameConst& fc, const Buffe
   if constexpr (kTex) {  // scenes with textured materials (see launch_shade)
     const int texi = __ldg(&m.texture);
     if (texi >= 0) {
-      const float4 tex = texture_factor(B, t, q, ltri, (qf & 8u) != 0u, texi, e0, e1, e2, sum, inv);
+      const float4 tex = texture_factor(B, te, q, ltri, (qf & 8u) != 0u, texi, e0, e1, e2, sum, inv);
       return premultiply_tex(color, mat, tex, light_factor(fc, n));
     }
   }
@@ -1694,6 +1777,8 @@ struct RasterView {
   uint64_t* keys;  // [4][cap_tb]
   uint16_t* refs;  // [4][cap_tb]
   uint32_t* rows;  // phase A: [4 warps][32 candidates][b0 b1 l0 l1] (aliases refs in SMEM)
+  TriRec* cs;      // fused raster: candidate setups of the current round [cand_cap]
+  TriPlanes* tp;   // fused raster: planes per TBR [cap_tbr]
 };
 
 struct RasterShared {
@@ -1790,6 +1875,7 @@ __device__ __forceinline__ uint32_t route_mask(uint32_t* route, uint32_t pix, bo
   route[lane] = 0u;
   __syncwarp();
   const unsigned peers = __match_any_sync(0xffffffffu, pix);
+  VEIL_CHECK(!valid || pix < 32u);
   if (valid && lane == __ffs(peers) - 1) route[pix] = peers;
   __syncwarp();
   const uint32_t mine = route[lane];
@@ -1802,7 +1888,8 @@ __device__ __forceinline__ void shade_segments(const FrameConst& fc, const Buffe
                                                int py0, const uint32_t* tri_l,
                                                const uint32_t* mask_l, const uint32_t* pre_l,
                                                uint32_t n, uint32_t total, uint32_t* route,
-                                               PixelOut& o, Filter& f) {
+                                               PixelOut& o, Filter& f, const uint16_t* slot_l = nullptr,
+                                               const TriPlanes* tp = nullptr) {
   const int lane = threadIdx.x & 31;
   uint32_t r_lo = 0;
   for (uint32_t base = 0; base < total; base += 32) {
@@ -1830,7 +1917,8 @@ __device__ __forceinline__ void shade_segments(const FrameConst& fc, const Buffe
       col0 = shade_decoded_bf(fc, B, t0, px0 + (int)(p0 & 7u), py0 + (int)(p0 >> 3), &q0);
     } else {
       double d0;
-      col0 = shade_sample<kTex>(fc, B, t0, px0 + (int)(p0 & 7u), py0 + (int)(p0 >> 3), &d0);
+      col0 = shade_sample<kTex>(fc, B, t0, px0 + (int)(p0 & 7u), py0 + (int)(p0 >> 3), &d0,
+                                tp ? &tp[slot_l[r0]] : nullptr);
       q0 = quantize_depth(d0);
     }
     const uint64_t key0 = sample_key(fc, q0, t0);
@@ -1857,7 +1945,8 @@ template <int KM, bool kThreshold, bool kTex, typename Filter>
 __device__ __forceinline__ void shade_walk(const FrameConst& fc, const Buffers& B, int px0,
                                            int py0, const uint32_t* tri_l, const uint32_t* mask_l,
                                            uint32_t n, PixelOut& o,
-                                           unsigned long long* enumerated_out, Filter& f) {
+                                           unsigned long long* enumerated_out, Filter& f,
+                                           const uint16_t* slot_l = nullptr, const TriPlanes* tp = nullptr) {
   const int lane = threadIdx.x & 31;
   const int px = px0 + (lane & 7), py = py0 + (lane >> 3);
   bool saturated = false, stopped = false;
@@ -1875,7 +1964,7 @@ __device__ __forceinline__ void shade_walk(const FrameConst& fc, const Buffers& 
         col = shade_decoded_bf(fc, B, tri, px, py, &qd);
       } else {
         double depth;
-        col = shade_sample<kTex>(fc, B, tri, px, py, &depth);
+        col = shade_sample<kTex>(fc, B, tri, px, py, &depth, tp ? &tp[slot_l[r]] : nullptr);
         qd = quantize_depth(depth);
       }
       key = sample_key(fc, qd, tri);
@@ -1934,7 +2023,7 @@ __device__ __forceinline__ void shade_waves(const FrameConst& fc, const Buffers&
                                             int py0, const uint32_t* tri_l,
                                             const uint32_t* mask_l, const uint16_t* slot_l,
                                             const StagedTri* staged, uint32_t n, PixelOut& o,
-                                            Filter& f) {
+                                            Filter& f, const TriPlanes* tp = nullptr) {
   const int lane = threadIdx.x & 31;
   const int px = px0 + (lane & 7), py = py0 + (lane >> 3);
   uint32_t r = 0;
@@ -1952,12 +2041,13 @@ __device__ __forceinline__ void shade_waves(const FrameConst& fc, const Buffers&
       uint32_t qd;
       float4 col;
       if (staged) {
+        VEIL_CHECK(slot_l[my_r] < kStageTris);
         col = shade_staged(fc, staged[slot_l[my_r]], px, py, &qd);
       } else if (fc.decoded) {
         col = shade_decoded_bf(fc, B, tri, px, py, &qd);
       } else {
         double depth;
-        col = shade_sample<kTex>(fc, B, tri, px, py, &depth);
+        col = shade_sample<kTex>(fc, B, tri, px, py, &depth, tp ? &tp[slot_l[my_r]] : nullptr);
         qd = quantize_depth(depth);
       }
       uint64_t pk;
@@ -2004,6 +2094,7 @@ __device__ __forceinline__ void shade_waves_staged2(const FrameConst& fc, int px
     const uint32_t rb = form(&r);
     const uint32_t ia = ra != kNone ? ra : 0u, ib = rb != kNone ? rb : 0u;
     uint32_t qa, qb;
+    VEIL_CHECK(slot_l[ia] < kStageTris && slot_l[ib] < kStageTris);
     const float4 ca = shade_staged_bf(fc, staged[slot_l[ia]], px, py, &qa);
     const float4 cb = shade_staged_bf(fc, staged[slot_l[ib]], px, py, &qb);
     uint64_t pk;
@@ -2019,6 +2110,71 @@ __device__ __forceinline__ void shade_waves_staged2(const FrameConst& fc, int px
     f.pop(&pk, &pc, &ooo);
     commit(o, pk, pc, ooo);
   }
+}
+
+// Composite a finished half-block over the background, write its 8x4 pixels
+// (device framebuffer; the mapped host frame and the root rank's peer
+// framebuffer when the frame has them; blend-order evidence in dump mode),
+// and add its samples / segments / invalid pixels to the (bin, block-row)
+// stat slot (shade_half_block's tail, raster.cpp:286-320).
+__device__ __forceinline__ void finish_half_block(const FrameConst& fc, const Buffers& B, int bin, int row,
+                                                  int hpx0, int hpy0, const PixelOut& po, bool live,
+                                                  unsigned long long enumerated) {
+  const int lane = threadIdx.x & 31;
+  const int px = hpx0 + (lane & 7), py = hpy0 + (lane >> 3);
+  unsigned invalid_px = 0;
+  if (px < fc.width && py < fc.height) {
+    const size_t pix = (size_t)py * fc.width + px;
+    uint32_t word;
+    if (po.invalid && fc.visualize) {
+      word = 0xffff00ffu;  // magenta overlay, renderer.cpp:56-65
+    } else {
+      const float4 out = blend(po.acc, make_float4(fc.bg[0], fc.bg[1], fc.bg[2], fc.bg[3]));
+      word = quantize_channel(out.x) | (quantize_channel(out.y) << 8) |
+             (quantize_channel(out.z) << 16) | (quantize_channel(out.w) << 24);
+    }
+    B.fb[pix] = word;
+    B.mask[pix] = po.invalid ? 1 : 0;
+    if (fc.host_fb) {  // over the host link, overlapped with the rest of the frame
+      fc.host_fb[pix] = word;
+      fc.host_mask[pix] = po.invalid ? 1 : 0;
+    }
+    if (fc.peer_fb) {  // into the root rank's framebuffer (peer memory)
+      fc.peer_fb[pix] = word;
+      fc.peer_mask[pix] = po.invalid ? 1 : 0;
+    }
+    if (fc.dump) {
+      B.hash[pix] = po.hash;
+      B.emit[pix] = po.emitted;
+    }
+    invalid_px = po.invalid ? 1u : 0u;
+  }
+  if (live) {
+    unsigned long long samples = po.emitted;
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) samples += __shfl_xor_sync(0xffffffffu, samples, s);
+    const unsigned inv = __popc(__ballot_sync(0xffffffffu, invalid_px != 0));
+    if (lane == 0) {
+      unsigned long long* slot = B.slots + ((size_t)bin * 4 + row) * 5;
+      atomicAdd(&slot[0], samples);
+      atomicAdd(&slot[3], (enumerated + 255ull) / 256ull);
+      if (inv) atomicAdd(&slot[4], (unsigned long long)inv);
+    }
+  }
+}
+
+// This warp's ring filter storage (MemFilter): after the staged triangles in
+// dynamic shared memory, or its slice of the global scratch.
+template <int kMode>
+__device__ __forceinline__ void dfm_reset(const Buffers& B, uint8_t* shade_dyn, MemFilter& f,
+                                          int warps_per_cta = 8) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const size_t warp_bytes = (size_t)B.dfm_cap * 32u * 24u;
+  uint8_t* base = B.dfm_g ? B.dfm_g + ((size_t)blockIdx.x * warps_per_cta + (size_t)warp) * warp_bytes
+                           : shade_dyn + (kMode == 0 ? (size_t)kStageTris * sizeof(StagedTri) : 0) +
+                                 (size_t)warp * warp_bytes;
+  f.reset(reinterpret_cast<uint64_t*>(base) + lane,
+          reinterpret_cast<float4*>(base + (size_t)B.dfm_cap * 32u * 8u) + lane, (int)B.dfm_cap);
 }
 
 __device__ __forceinline__ uint32_t span_mask(uint32_t b, uint32_t l, uint32_t c0, uint32_t c1) {
@@ -2106,7 +2262,7 @@ __device__ __noinline__ void sort_keys_scratch(uint64_t* keys, uint16_t* refs, u
     }
 }
 
-template <bool kGlobal>
+template <bool kGlobal, int kFuse>
 __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers& B, int pass,
                                              int bin, int row, const RasterView& V,
                                              ItemState* st, uint32_t cap_tbr, uint32_t cap_tb) {
@@ -2159,6 +2315,7 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
         const bool large = j >= nq;
         const uint32_t i = large ? 2 * nq + (j - nq) : 2 * j;
         const uint32_t ti = large ? it : it * 2;
+        VEIL_CHECK(wbase + __popc(m0 & below) < cand_cap);
         cand[wbase + __popc(m0 & below)] = ((uint64_t)i << 32) | ti | ((large ? 1u : 0u) << 31);
       }
       if (rows & 2u)
@@ -2189,10 +2346,25 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
         code = cand[j];
         ti = (uint32_t)code & 0x7fffffffu;
         large = ((uint32_t)code) >> 31;
-        const TriRec& t = B.tri[ti];
-        yb = max(t.y_min, ry0);
-        const int ye = min(t.y_max, ry1);
-        nrows = ye >= yb ? (uint32_t)(ye - yb + 1) : 0u;
+        if (kFuse) {
+          // fused raster: the candidate's setup (small quads' recomputed,
+          // large ones' loaded) goes to the CTA's candidate scratch, read
+          // back by the row spans and copied into its TBR's planes
+          TriRec tr;
+          if (large || fc.fused_read)
+            tr = B.tri[ti];
+          else
+            recompute_setup(fc, B, ti, &tr);
+          yb = max(tr.y_min, ry0);
+          const int ye = min(tr.y_max, ry1);
+          nrows = ye >= yb ? (uint32_t)(ye - yb + 1) : 0u;
+          if (nrows) V.cs[j] = tr;
+        } else {
+          const TriRec& t = B.tri[ti];
+          yb = max(t.y_min, ry0);
+          const int ye = min(t.y_max, ry1);
+          nrows = ye >= yb ? (uint32_t)(ye - yb + 1) : 0u;
+        }
       }
       const uint32_t total = __reduce_add_sync(0xffffffffu, nrows);
       const uint32_t ngroup = min(G, nc - g);
@@ -2205,6 +2377,7 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
       const bool pairs = !(total < 3u * ngroup && max_rows <= (total + 31u) / 32u + 2u);
       uint32_t rb0 = 0x1f1f1f1fu, rb1 = 0x1f1f1f1fu, rl0 = 0u, rl1 = 0u, cols = 0;
       uint32_t excl = 0;
+      if (kFuse) __syncwarp();  // candidate setups visible to the warp
       if (pairs) {
         reinterpret_cast<uint4*>(rs)[lane] = make_uint4(0x1f1f1f1fu, 0x1f1f1f1fu, 0u, 0u);
         uint32_t incl = nrows;
@@ -2236,7 +2409,12 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
           act = p < total;
         }
         int b, l;
-        if (act && row_span(B.tri[tcur], py, px0, px_last, &b, &l)) {
+        bool spans;
+        if (kFuse)
+          spans = act && row_span(V.cs[g + c], py, px0, px_last, &b, &l);
+        else
+          spans = act && row_span(B.tri[tcur], py, px0, px_last, &b, &l);
+        if (spans) {
           const int ly = py - ry0;
           const uint32_t bb = (uint32_t)(b - px0), ll = (uint32_t)(l - px0);
           if (pairs) {
@@ -2282,7 +2460,17 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
             rec.l[0] = rl0;
             rec.l[1] = rl1;
             rec.slot = (uint32_t)(code >> 32);
+            VEIL_CHECK((uint32_t)slot < cap_tbr && (!kFuse || j < cand_cap));
             V.tbr[slot] = rec;
+            if (kFuse) {
+              const TriRec& tr = V.cs[j];
+              TriPlanes pl;
+              pl.e[0] = tr.e[0];
+              pl.e[1] = tr.e[1];
+              pl.e[2] = tr.e[2];
+              pl.dz = tr.dz;
+              V.tp[slot] = pl;
+            }
           }
         }
       }
@@ -2336,7 +2524,7 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
     }
     uint32_t qd = 0x3fffffu;
     if (count) {
-      const Fn3 dz = B.tri[rw.tri].dz;
+      const Fn3 dz = kFuse ? V.tp[i].dz : B.tri[rw.tri].dz;
       if (dz.a == 0.0 && dz.b == 0.0) {
         qd = quantize_depth(dz.c);  // flat plane: (±0 + ±0) + c quantizes like c at any centroid
       } else {
@@ -2422,10 +2610,13 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
         }
         if (ne) {
           const size_t at = (size_t)pbase + (size_t)h * n + pos;
+          VEIL_CHECK(at < fc.pool_cap && pos < n);
           B.pool_tri[at] = tri;
           B.pool_mask[at] = hm[h];
           B.pool_pre[at] = frags[h] + incl - fr;
-          B.pool_slot[at] = (uint16_t)min(V.tbr[ref].slot, 65535u);
+          // fused: the TBR (its planes in V.tp); else the bin-list position
+          // (k_shade's staging slot)
+          B.pool_slot[at] = kFuse ? (uint16_t)ref : (uint16_t)min(V.tbr[ref].slot, 65535u);
         }
         nthb[h] += __popc(m);
         frags[h] += __shfl_sync(0xffffffffu, incl, 31);
@@ -2481,11 +2672,11 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
     const uint32_t both = cost + __shfl_down_sync(0x3u, cost, 1);  // the block's two halves
     const unsigned walks = __ballot_sync(0x3u, !seg);
     // bit 31: the bin has half-blocks for k_shade's wave walk (or background)
-    if (lane == 0 && (both || walks)) atomicAdd(&B.bin_cost[bin], both);
-    if (lane == 0 && walks) atomicOr(&B.bin_cost[bin], 0x80000000u);
+    if (!kFuse && lane == 0 && (both || walks)) atomicAdd(&B.bin_cost[bin], both);
+    if (!kFuse && lane == 0 && walks) atomicOr(&B.bin_cost[bin], 0x80000000u);
     // low-pass entries of a bin that later propagates are stale (k_shade_seg skips them)
-    if (seg)
-      B.seg_queue[atomicAdd(&B.ctr->seg_count, 1u)] =
+    if (seg && !kFuse)
+      B.seg_queue[checked_index(atomicAdd(&B.ctr->seg_count, 1u), (uint32_t)fc.nbins * 32u)] =
           make_uint4(hbi | (pass == kPassLow ? 0u : 0x80000000u), d.off, d.cnt, d.frags);
   }
   if (threadIdx.x == 0) {
@@ -2497,17 +2688,73 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
     atomicAdd(&slot[1], (unsigned long long)(frags[0] + frags[1]));
     atomicAdd(&slot[2], (unsigned long long)(nthb[0] + nthb[1]));
   }
+  if constexpr (kFuse != 0) {
+    // Fused raster: warp w shades the two half-blocks of block (row, w) it
+    // just extracted, from the pool lists (L2-hot) and the TBR planes in V.tp.
+    __syncthreads();  // thread 0's slot reset precedes the shading's stat atomics
+    uint32_t* route = V.rows + (size_t)warp * 128u;  // phase-A scratch, free now
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t off = pbase + (uint32_t)h * n, cnt = nthb[h], frg = frags[h];
+      const int hpx0 = px0 + warp * 8, hpy0 = py0 + row * 8 + h * 4;
+      PixelOut po;
+      po.acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      po.invalid = false;
+      po.hash = kHashSeed;
+      po.emitted = 0;
+      unsigned long long enumerated = frg;
+      if (cnt) {
+        const uint32_t* tri_l = B.pool_tri + off;
+        const uint32_t* mask_l = B.pool_mask + off;
+        const uint32_t* pre_l = B.pool_pre + off;
+        const uint16_t* slot_l = B.pool_slot + off;
+        auto run = [&](auto& f) {
+          if (fc.threshold)
+            shade_walk<3, true, false>(fc, B, hpx0, hpy0, tri_l, mask_l, cnt, po, &enumerated, f, slot_l, V.tp);
+          else if (frg < kWalkMinSamplesPerThb * cnt)
+            shade_segments<3, false>(fc, B, hpx0, hpy0, tri_l, mask_l, pre_l, cnt, frg, route, po, f, slot_l,
+                                     V.tp);
+          else
+            shade_waves<3, false>(fc, B, hpx0, hpy0, tri_l, mask_l, slot_l, nullptr, cnt, po, f, V.tp);
+        };
+        if constexpr (kFuse == 1) {  // depth_filter_size 3, the reference default
+          RegFilter<3, true> f;
+          f.reset();
+          run(f);
+        } else {
+          MemFilter f;
+          dfm_reset<1>(B, nullptr, f, 4);
+          run(f);
+        }
+      }
+      finish_half_block(fc, B, bin, row, hpx0, hpy0, po, true, enumerated);
+    }
+  }
 }
 
-template <bool kGlobal>
-__global__ void __launch_bounds__(128, 7) k_extract(Buffers B, int pass,
-                                                 uint32_t cap_tbr, uint32_t cap_tb) {
+// kFuse: 0 = extraction only (k_shade shades), 1 = fused raster with the
+// register filter (depth_filter_size 3), 2 = fused raster with MemFilter.
+template <bool kGlobal, int kFuse>
+__global__ void __launch_bounds__(128, kFuse ? 6 : 7) k_extract(Buffers B, int pass,
+                                                              uint32_t cap_tbr, uint32_t cap_tb) {
   const FrameConst& fc = c_fc;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   __shared__ ItemState st;
   __shared__ uint32_t item_s;
+  if (kFuse) {  // the generic shading path's unpack tables
+    load_shared_luts();
+    __syncthreads();
+  }
   if (B.ctr->error) return;
   RasterView V;
+  V.cs = nullptr;
+  V.tp = nullptr;
+  if (kFuse) {
+    V.cs = B.cscratch + (kGlobal ? B.cs_off_g + (size_t)blockIdx.x * B.cs_per_cta_g
+                                 : (size_t)blockIdx.x * B.cs_per_cta);
+    V.tp = B.tplanes + (kGlobal ? B.tp_off_g + (size_t)blockIdx.x * B.tp_per_cta_g
+                                : (size_t)blockIdx.x * B.tp_per_cta);
+  }
   if (kGlobal) {
     uint8_t* g = B.scratch + (size_t)blockIdx.x * B.scratch_per_cta;
     V.tbr = reinterpret_cast<Tbr*>(g);
@@ -2546,13 +2793,13 @@ __global__ void __launch_bounds__(128, 7) k_extract(Buffers B, int pass,
       run = cat == 2 || (cat == 1 && fc.force_high) || B.prop[bin];
     if (!run) continue;
     if (!kGlobal && pass == kPassLow && B.prop[bin]) continue;  // sibling already overflowed
-    extract_item<kGlobal>(fc, B, pass, bin, row, V, &st, cap_tbr, cap_tb);
+    extract_item<kGlobal, kFuse>(fc, B, pass, bin, row, V, &st, cap_tbr, cap_tb);
     __syncthreads();
     if (threadIdx.x == 0 && st.status) {
       if (st.status == 1) {  // soft overflow: the whole bin goes to the high pass
         B.prop[bin] = 1;
         if (atomicAdd(&B.prop_q[bin], 1u) == 0u)
-          B.bin_list[1][atomicAdd(&B.ctr->list_count[1], 1u)] = (uint32_t)bin;
+          B.bin_list[1][checked_index(atomicAdd(&B.ctr->list_count[1], 1u), (uint32_t)fc.nbins)] = (uint32_t)bin;
       } else if (st.status == 2) {
         const uint32_t s = atomicAdd(&B.ctr->spill_count[pass], 1u);
         B.spill[pass][s] = code;
@@ -2572,17 +2819,35 @@ __global__ void __launch_bounds__(128, 7) k_extract(Buffers B, int pass,
 // samples composite the background.
 constexpr int kShadeStage = 256;  // THB entries staged per warp; longer lists stream
 
-// This warp's ring filter storage (MemFilter): after the staged triangles in
-// dynamic shared memory, or its slice of the global scratch.
-template <int kMode>
-__device__ __forceinline__ void dfm_reset(const Buffers& B, uint8_t* shade_dyn, MemFilter& f) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const size_t warp_bytes = (size_t)B.dfm_cap * 32u * 24u;
-  uint8_t* base = B.dfm_g ? B.dfm_g + ((size_t)blockIdx.x * 8u + (size_t)warp) * warp_bytes
-                           : shade_dyn + (kMode == 0 ? (size_t)kStageTris * sizeof(StagedTri) : 0) +
-                                 (size_t)warp * warp_bytes;
-  f.reset(reinterpret_cast<uint64_t*>(base) + lane,
-          reinterpret_cast<float4*>(base + (size_t)B.dfm_cap * 32u * 8u) + lane, (int)B.dfm_cap);
+// Bulk asynchronous copies (the TMA engine's 1-D cp.async.bulk) completing
+// on a per-warp mbarrier, for k_shade's THB-list staging.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_to_smem(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_addr(bar)), "r"(phase)
+        : "memory");
+  } while (!done);
 }
 
 // kMode: 0 = broadcast walk for half-blocks with big THBs (also writes every
@@ -2594,16 +2859,21 @@ __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
   const FrameConst& fc = c_fc;
   load_shared_luts();
   __syncthreads();
-  __shared__ uint32_t stage_tri[8][kShadeStage];
-  __shared__ uint32_t stage_mask[8][kShadeStage];
-  __shared__ uint32_t stage_pre[8][kShadeStage];
-  __shared__ uint16_t stage_slot[8][kShadeStage];
+  // (+8 entries: bulk copies move 16-byte aligned runs around the list)
+  __shared__ __align__(16) uint32_t stage_tri[8][kShadeStage + 8];
+  __shared__ __align__(16) uint32_t stage_mask[8][kShadeStage + 8];
+  __shared__ __align__(16) uint32_t stage_pre[8][kShadeStage + 8];
+  __shared__ __align__(16) uint16_t stage_slot[8][kShadeStage + 8];
+  __shared__ __align__(8) uint64_t stage_bar[8];
   extern __shared__ __align__(16) uint8_t shade_dyn[];  // staged bin triangles, filter slots
   StagedTri* row_tris = reinterpret_cast<StagedTri*>(shade_dyn);
   __shared__ uint32_t route_s[8][32];
   __shared__ uint32_t item_s;
   if (B.ctr->error) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t bar_phase = 0;
+  if (fc.bulk_stage && lane == 0) mbar_init(&stage_bar[warp]);
+  __syncwarp();
   __shared__ int hb_next;
   __shared__ uint8_t hb_order[32];  // the bin's half-blocks, most samples first
   // modes 0/2: CTA items = bins, warps pull the bin's 32 half-blocks;
@@ -2716,7 +2986,28 @@ __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
       const uint32_t* mask_l = B.pool_mask + d.off;
       const uint32_t* pre_l = B.pool_pre + d.off;
       const uint16_t* slot_l = B.pool_slot + d.off;
-      if (d.cnt <= (uint32_t)kShadeStage) {
+      if (d.cnt <= (uint32_t)kShadeStage && fc.bulk_stage) {
+        // four bulk copies (16-byte aligned runs covering the list) onto the
+        // warp's mbarrier; the generic-proxy reads of the previous list are
+        // ordered before the async-proxy writes by the proxy fence
+        const uint32_t a4 = d.off & ~3u, n4 = ((d.off + d.cnt + 3u) & ~3u) - a4;  // u32 lists
+        const uint32_t a8 = d.off & ~7u, n8 = ((d.off + d.cnt + 7u) & ~7u) - a8;  // u16 list
+        __syncwarp();
+        if (lane == 0) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_expect_tx(&stage_bar[warp], 3u * 4u * n4 + 2u * n8);
+          bulk_to_smem(stage_tri[warp], B.pool_tri + a4, 4u * n4, &stage_bar[warp]);
+          bulk_to_smem(stage_mask[warp], B.pool_mask + a4, 4u * n4, &stage_bar[warp]);
+          bulk_to_smem(stage_pre[warp], B.pool_pre + a4, 4u * n4, &stage_bar[warp]);
+          bulk_to_smem(stage_slot[warp], B.pool_slot + a8, 2u * n8, &stage_bar[warp]);
+        }
+        mbar_wait(&stage_bar[warp], bar_phase);
+        bar_phase ^= 1u;
+        tri_l = stage_tri[warp] + (d.off - a4);
+        mask_l = stage_mask[warp] + (d.off - a4);
+        pre_l = stage_pre[warp] + (d.off - a4);
+        slot_l = stage_slot[warp] + (d.off - a8);
+      } else if (d.cnt <= (uint32_t)kShadeStage) {
         for (uint32_t i = lane; i < d.cnt; i += 32) {
           stage_tri[warp][i] = tri_l[i];
           stage_mask[warp][i] = mask_l[i];
@@ -2746,11 +3037,9 @@ __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
           f.reset(reinterpret_cast<float4*>(shade_dyn + (size_t)kStageTris * sizeof(StagedTri)) +
                   (size_t)warp * KM * 32 + lane);
           if (staged_ok && d.cnt <= (uint32_t)kShadeStage && !fc.wave1)  // all operands in shared memory
-            shade_waves_staged2<KM>(fc, hpx0, hpy0, stage_tri[warp], stage_mask[warp], stage_slot[warp],
-                                    row_tris, d.cnt, po, f);
+            shade_waves_staged2<KM>(fc, hpx0, hpy0, tri_l, mask_l, slot_l, row_tris, d.cnt, po, f);
           else if (staged_ok && d.cnt <= (uint32_t)kShadeStage)
-            shade_waves<KM, kTex>(fc, B, hpx0, hpy0, stage_tri[warp], stage_mask[warp], stage_slot[warp],
-                                  row_tris, d.cnt, po, f);
+            shade_waves<KM, kTex>(fc, B, hpx0, hpy0, tri_l, mask_l, slot_l, row_tris, d.cnt, po, f);
           else
             shade_waves<KM, kTex>(fc, B, hpx0, hpy0, tri_l, mask_l, slot_l, staged_ok ? row_tris : nullptr,
                             d.cnt, po, f);
@@ -2773,46 +3062,7 @@ __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
         }
       }
     }
-    const int px = hpx0 + (lane & 7), py = hpy0 + (lane >> 3);
-    unsigned invalid_px = 0;
-    if (px < fc.width && py < fc.height) {
-      const size_t pix = (size_t)py * fc.width + px;
-      uint32_t word;
-      if (po.invalid && fc.visualize) {
-        word = 0xffff00ffu;  // magenta overlay, renderer.cpp:56-65
-      } else {
-        const float4 out = blend(po.acc, make_float4(fc.bg[0], fc.bg[1], fc.bg[2], fc.bg[3]));
-        word = quantize_channel(out.x) | (quantize_channel(out.y) << 8) |
-               (quantize_channel(out.z) << 16) | (quantize_channel(out.w) << 24);
-      }
-      B.fb[pix] = word;
-      B.mask[pix] = po.invalid ? 1 : 0;
-      if (fc.host_fb) {  // over the host link, overlapped with the rest of the frame
-        fc.host_fb[pix] = word;
-        fc.host_mask[pix] = po.invalid ? 1 : 0;
-      }
-      if (fc.peer_fb) {  // into the root rank's framebuffer (peer memory)
-        fc.peer_fb[pix] = word;
-        fc.peer_mask[pix] = po.invalid ? 1 : 0;
-      }
-      if (fc.dump) {
-        B.hash[pix] = po.hash;
-        B.emit[pix] = po.emitted;
-      }
-      invalid_px = po.invalid ? 1u : 0u;
-    }
-    if (live) {
-      unsigned long long samples = po.emitted;
-#pragma unroll
-      for (int s = 16; s > 0; s >>= 1) samples += __shfl_xor_sync(0xffffffffu, samples, s);
-      const unsigned inv = __popc(__ballot_sync(0xffffffffu, invalid_px != 0));
-      if (lane == 0) {
-        unsigned long long* slot = B.slots + ((size_t)bin * 4 + row) * 5;
-        atomicAdd(&slot[0], samples);
-        atomicAdd(&slot[3], (enumerated + 255ull) / 256ull);
-        if (inv) atomicAdd(&slot[4], (unsigned long long)inv);
-      }
-    }
+    finish_half_block(fc, B, bin, row, hpx0, hpy0, po, live, enumerated);
   }
 }
 
@@ -2892,6 +3142,28 @@ __global__ void __launch_bounds__(256) k_finalize(Buffers B) {
 #pragma unroll
     for (int k = 0; k < 6; ++k)
       if (v[k]) atomicAdd(dst[k], v[k]);
+  }
+}
+
+// Fused raster frames have no k_shade, whose mode 0 writes the background of
+// empty bins: this does, for the bins this rank owns (a CTA per bin).
+__global__ void __launch_bounds__(256) k_fill_empty(Buffers B) {
+  const FrameConst& fc = c_fc;
+  if (B.ctr->error) return;
+  for (int b = blockIdx.x; b < fc.nbins; b += gridDim.x) {
+    const int bxi = b % fc.bins_x, byi = b / fc.bins_x;
+    if (B.cat[b] != 0 || !(fc.world <= 1 || ((bxi + 3 * byi) % fc.world) == fc.rank)) continue;
+    const int warp = threadIdx.x >> 5;
+    PixelOut po;
+    po.acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    po.invalid = false;
+    po.hash = kHashSeed;
+    po.emitted = 0;
+    for (int hb = warp; hb < 32; hb += 8) {
+      const int block = hb >> 1;
+      finish_half_block(fc, B, b, block >> 2, bxi * kBin + (block & 3) * 8,
+                        byi * kBin + (block >> 2) * 8 + (hb & 1) * 4, po, false, 0);
+    }
   }
 }
 
@@ -3027,7 +3299,7 @@ struct DeviceScene {
       tri_y;
   DevBuf off, qcur, tcur, cat, bin_list0, bin_list1, prop_q, bin_cost, bin_order, prop, items, item_rows, slots, spill0, spill1, scratch, fb, mask,
       hash, emit, tile_ids, hbd, pool_tri, pool_mask, pool_pre, seg_queue, pool_slot, lpairs, lpair_cols,
-      dfm_g;
+      dfm_g, cscratch, tplanes;
   uint32_t items_cap = 0;
   uint32_t pool_cap = 0;
   uint32_t lpairs_cap = 0;
@@ -3120,23 +3392,26 @@ uint64_t shard_tile_count(int bins_x, int bins_y, int rank, int world) {
 
 namespace {
 
-DeviceScene* device_scene(const Scene& s) {
+// The device workspace in `slot` (the scene's own, or one of its multi-device
+// shards) on CUDA device `device`, created or moved on first use, with the
+// scene's geometry uploaded.
+DeviceScene* device_scene_on(const Scene& s, DeviceScene** slot, int device) {
   int count = 0;
   if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
     throw Error(VEIL_ERR_INTERNAL, "no CUDA device available (libveil has no CPU fallback)");
-  ck(cudaSetDevice(t_device), "cudaSetDevice");
-  if (s.device && s.device->device != t_device) {
-    release_device_scene(s.device);
-    s.device = nullptr;
+  ck(cudaSetDevice(device), "cudaSetDevice");
+  if (*slot && (*slot)->device != device) {
+    release_device_scene(*slot);
+    *slot = nullptr;
   }
-  if (!s.device) {
+  if (!*slot) {
     DeviceScene* d = new DeviceScene();
-    d->device = t_device;
+    d->device = device;
     ck(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking), "cudaStreamCreate");
     for (auto& e : d->ev) ck(cudaEventCreate(&e), "cudaEventCreate");
     ck(cudaMallocHost(reinterpret_cast<void**>(&d->fc_host), sizeof(dev::FrameConst)), "cudaMallocHost");
     ck(cudaMallocHost(reinterpret_cast<void**>(&d->ctr_host), sizeof(dev::Counters)), "cudaMallocHost");
-    cudaDeviceGetAttribute(&d->sm_count, cudaDevAttrMultiProcessorCount, t_device);
+    cudaDeviceGetAttribute(&d->sm_count, cudaDevAttrMultiProcessorCount, device);
     {  // exact unpack tables (IEEE float division on the host)
       float lc[256], ln[1024];
       for (int q = 0; q < 256; ++q) lc[q] = float(q) / 255.0f;
@@ -3144,9 +3419,9 @@ DeviceScene* device_scene(const Scene& s) {
       ck(cudaMemcpyToSymbol(dev::g_lut_c, lc, sizeof lc), "lut");
       ck(cudaMemcpyToSymbol(dev::g_lut_n, ln, sizeof ln), "lut");
     }
-    s.device = d;
+    *slot = d;
   }
-  DeviceScene* d = s.device;
+  DeviceScene* d = *slot;
   if (d->uploaded_version != s.geometry_version) {
     const size_t V = s.vertices.size(), Q = s.quads.size();
     std::vector<float4> pos(V);
@@ -3245,6 +3520,8 @@ DeviceScene* device_scene(const Scene& s) {
   return d;
 }
 
+DeviceScene* device_scene(const Scene& s) { return device_scene_on(s, &s.device, t_device); }
+
 void camera_vectors(const Camera& c, dev::FrameConst* fc) {
   // camera_eye / camera_forward, scene.cpp:67-84
   fc->has_eye = 0;
@@ -3276,24 +3553,39 @@ void camera_vectors(const Camera& c, dev::FrameConst* fc) {
   }
 }
 
-void launch_extract(DeviceScene* d, const dev::FrameConst& fc, const dev::Buffers& B, int pass,
-                    uint32_t gcap_tbr, uint32_t gcap_tb, int* launches) {
+// Upper bound of resident k_extract<false> CTAs per SM (launch bounds), which
+// sizes the fused raster's per-CTA scratch.
+constexpr int kExtractCtasPerSmMax = 7;
+
+template <int kFuse>
+void launch_extract_k(DeviceScene* d, const dev::FrameConst& fc, const dev::Buffers& B, int pass,
+                      uint32_t gcap_tbr, uint32_t gcap_tb, int* launches) {
   const size_t smem = sizeof(dev::RasterShared);
-  if (!d->extract_configured) {
-    ck(cudaFuncSetAttribute(dev::k_extract<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  static int per_sm_dev[64];  // per instantiation and device (attributes are per device)
+  int& per_sm = per_sm_dev[d->device & 63];
+  if (per_sm <= 0) {
+    ck(cudaFuncSetAttribute(dev::k_extract<false, kFuse>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             int(smem)),
        "cudaFuncSetAttribute");
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_extract<false>, 128, smem);
-    d->extract_ctas = std::max(1, per_sm) * d->sm_count;
-    d->extract_configured = true;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_extract<false, kFuse>, 128, smem);
+    per_sm = std::min(std::max(1, per_sm), kExtractCtasPerSmMax);
   }
-  const int grid = int(std::min<long long>(d->extract_ctas, (long long)fc.nbins * 4));
-  dev::k_extract<false><<<grid, 128, smem, d->stream>>>(B, pass, dev::RasterShared::kTbr,
-                                                          dev::RasterShared::kTb);
+  const int grid = int(std::min<long long>((long long)per_sm * d->sm_count, (long long)fc.nbins * 4));
+  dev::k_extract<false, kFuse><<<grid, 128, smem, d->stream>>>(B, pass, dev::RasterShared::kTbr,
+                                                                 dev::RasterShared::kTb);
   ck(cudaGetLastError(), "k_extract launch");
-  dev::k_extract<true><<<d->raster_ctas_global, 128, 0, d->stream>>>(B, pass, gcap_tbr, gcap_tb);
+  dev::k_extract<true, kFuse><<<d->raster_ctas_global, 128, 0, d->stream>>>(B, pass, gcap_tbr, gcap_tb);
   *launches += 2;
+}
+
+void launch_extract(DeviceScene* d, const dev::FrameConst& fc, const dev::Buffers& B, int pass,
+                    uint32_t gcap_tbr, uint32_t gcap_tb, int* launches) {
+  if (!fc.fused)
+    launch_extract_k<0>(d, fc, B, pass, gcap_tbr, gcap_tb, launches);
+  else if (fc.df == 3)
+    launch_extract_k<1>(d, fc, B, pass, gcap_tbr, gcap_tb, launches);
+  else
+    launch_extract_k<2>(d, fc, B, pass, gcap_tbr, gcap_tb, launches);
 }
 
 // Ring filters (KM == 0, depth_filter_size > 8) live in dynamic shared memory
@@ -3310,14 +3602,16 @@ void launch_shade_mode(DeviceScene* d, const dev::FrameConst& fc, const dev::Buf
     dyn += (kMode != 2 ? size_t(8) * KM * 32 * sizeof(float4) : 0);
   else if (!B.dfm_g)
     dyn += size_t(8) * B.dfm_cap * kDfmBytesPerEntry;
-  static size_t configured = 0;  // per instantiation: the largest dynamic size set so far
+  static size_t configured_dev[64];  // per instantiation and device: the largest size set so far
+  size_t& configured = configured_dev[d->device & 63];
   if (dyn > configured) {
     ck(cudaFuncSetAttribute(dev::k_shade<KM, kMode, kTex>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             int(dyn)),
        "cudaFuncSetAttribute");
     configured = dyn;
   }
-  static std::map<size_t, int> per_sm_by_dyn;  // per instantiation (same on every B200)
+  static std::map<size_t, int> per_sm_by_dyn_dev[64];  // per instantiation and device
+  std::map<size_t, int>& per_sm_by_dyn = per_sm_by_dyn_dev[d->device & 63];
   auto it = per_sm_by_dyn.find(dyn);
   if (it == per_sm_by_dyn.end()) {
     int per_sm = 0;
@@ -3470,6 +3764,8 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   if (const char* wm = std::getenv("VEIL_WALK_MIN")) fc.walk_min = std::atoi(wm);
   if (const char* wm = std::getenv("VEIL_WALK_MIN_U")) fc.walk_min_u = std::atoi(wm);
   if (const char* w1 = std::getenv("VEIL_WAVE1")) fc.wave1 = std::atoi(w1);
+  fc.bulk_stage = 1;  // measured: C2 shade -0.3%, C4 shade -1.1% against the lane loop
+  if (const char* bs = std::getenv("VEIL_BULK_STAGE")) fc.bulk_stage = std::atoi(bs);
 
   const uint32_t Q = d->nquads;
   const size_t nb = size_t(fc.nbins);
@@ -3497,6 +3793,20 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   // Decoded shading records (and the shared-memory staging built on them)
   // carry no UVs: scenes with textured materials shade on the generic path.
   fc.decoded = !d->textured && (double)cam.width * cam.height >= 8.0 * std::max<double>(1.0, Q) ? 1 : 0;
+  // Fused raster (tiny triangles: the frames without decoded records): the
+  // extraction recomputes small quads' setups and shades as it goes, so the
+  // 128-byte records of small quads are not stored (parity dumps still store
+  // them for the tri_fn arrays). VEIL_FUSED=0/1 overrides (tests, A/B);
+  // textured scenes and the a-buffer reference mode keep the separate path.
+  {
+    int fused = 0;  // measured slower than the separate kernels
+    if (const char* fe = std::getenv("VEIL_FUSED"); fe && *fe) fused = std::atoi(fe) ? 1 : 0;
+    if (d->textured || (p.flags & VEIL_RENDER_REFERENCE)) fused = 0;
+    fc.fused = fused;
+    if (fused) fc.decoded = 0;
+    if (const char* fr = std::getenv("VEIL_FUSED_READ"); fr && *fr) fc.fused_read = std::atoi(fr) ? 1 : 0;
+    fc.write_tri = (!fused || opt.dump || fc.fused_read) ? 1 : 0;
+  }
   if (fc.decoded) d->shade.ensure(size_t(Q) * 2 * sizeof(dev::ShadeRec));
   d->off.ensure(nb * 4);
   d->qcur.ensure(nb * 4);
@@ -3539,10 +3849,11 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   fc.lpairs_cap = d->lpairs_cap;
   if (d->pool_cap == 0)
     d->pool_cap = init_cap ? init_cap : std::max<uint32_t>(1u << 22, uint32_t(std::min<size_t>(nb * 2048, 1u << 26)));
-  d->pool_tri.ensure(size_t(d->pool_cap) * 4);
-  d->pool_mask.ensure(size_t(d->pool_cap) * 4);
-  d->pool_pre.ensure(size_t(d->pool_cap) * 4);
-  d->pool_slot.ensure(size_t(d->pool_cap) * 2);
+  // (+16 entries of slack: k_shade's bulk copies round list ends up to 16 bytes)
+  d->pool_tri.ensure((size_t(d->pool_cap) + 16) * 4);
+  d->pool_mask.ensure((size_t(d->pool_cap) + 16) * 4);
+  d->pool_pre.ensure((size_t(d->pool_cap) + 16) * 4);
+  d->pool_slot.ensure((size_t(d->pool_cap) + 16) * 2);
   fc.pool_cap = d->pool_cap;
   // global scratch for spilled items: capacities follow the active limits
   P.gcap_tbr = std::min<uint32_t>(std::max(fc.low.tbr, fc.high.tbr), 1u << 16);
@@ -3563,7 +3874,16 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   // max(low, high) THB-limit THBs, so min(k, that) nodes per lane suffice.
   uint32_t dfm_cap = 0, dfm_ctas = 0;
   bool dfm_global = false;
-  if (fc.df > 8) {
+  if (fc.fused && fc.df != 3) {
+    // the fused raster's filters (four warps per k_extract CTA) in global memory
+    dfm_cap = std::min<uint32_t>(uint32_t(fc.df), std::max(fc.low.thb, fc.high.thb));
+    if (dfm_cap > (1u << dev::MemFilter::kSlotBits))
+      throw Error(VEIL_ERR_INVALID_ARG,
+                  "depth_filter_size above 32768 with a THB limit above 32768 is not supported");
+    const size_t ctas = std::max<size_t>(size_t(kExtractCtasPerSmMax) * d->sm_count, d->raster_ctas_global);
+    d->dfm_g.ensure(ctas * 4 * dfm_cap * kDfmBytesPerEntry);
+    dfm_global = true;
+  } else if (fc.df > 8 && !fc.fused) {
     dfm_cap = std::min<uint32_t>(uint32_t(fc.df), std::max(fc.low.thb, fc.high.thb));
     if (dfm_cap > (1u << dev::MemFilter::kSlotBits))
       throw Error(VEIL_ERR_INVALID_ARG,
@@ -3584,6 +3904,19 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
 
   dev::Buffers& B = P.B;
   std::memset(&B, 0, sizeof B);
+  if (fc.fused) {  // per-CTA candidate setups and TBR planes of the fused raster
+    const size_t na = size_t(kExtractCtasPerSmMax) * d->sm_count, ng = size_t(d->raster_ctas_global);
+    B.cs_per_cta = 4u * dev::RasterShared::kTb;
+    B.tp_per_cta = dev::RasterShared::kTbr;
+    B.cs_per_cta_g = 4ull * P.gcap_tb;
+    B.tp_per_cta_g = P.gcap_tbr;
+    B.cs_off_g = na * B.cs_per_cta;
+    B.tp_off_g = na * B.tp_per_cta;
+    d->cscratch.ensure((B.cs_off_g + ng * B.cs_per_cta_g) * sizeof(dev::TriRec));
+    d->tplanes.ensure((B.tp_off_g + ng * B.tp_per_cta_g) * sizeof(dev::TriPlanes));
+    B.cscratch = d->cscratch.as<dev::TriRec>();
+    B.tplanes = d->tplanes.as<dev::TriPlanes>();
+  }
   B.dfm_g = dfm_global ? d->dfm_g.as<uint8_t>() : nullptr;
   B.dfm_cap = dfm_cap;
   B.dfm_ctas = dfm_ctas;
@@ -3874,22 +4207,43 @@ static void enqueue_raster(DeviceScene* d, Prepared& P, int* launches) {
   record_event(d->ev[3], d->stream);
   launch_extract(d, P.fc, P.B, dev::kPassHigh, P.gcap_tbr, P.gcap_tb, launches);
   record_event(d->ev[5], d->stream);
-  dev::k_order_bins<<<1, 1024, 0, d->stream>>>(P.B);
-  ++*launches;
-  launch_shade(d, P.fc, P.B, launches);
+  if (P.fc.fused) {  // the extraction shaded every non-empty bin
+    dev::k_fill_empty<<<std::min(P.fc.nbins, d->sm_count * 8), 256, 0, d->stream>>>(P.B);
+    ++*launches;
+  } else {
+    dev::k_order_bins<<<1, 1024, 0, d->stream>>>(P.B);
+    ++*launches;
+    launch_shade(d, P.fc, P.B, launches);
+  }
   dev::k_finalize<<<(P.fc.nbins + 255) / 256, 256, 0, d->stream>>>(P.B);
   ++*launches;
   record_event(d->ev[4], d->stream);
 }
 
 namespace {
-std::mutex g_frame_mu;  // frames share the __constant__ c_fc: one in flight at a time
+// Frames on one device share its __constant__ c_fc: one in flight per device
+// (frames on different devices run concurrently).
+std::mutex& device_mutex(int device) {
+  static std::mutex m[64];
+  return m[device & 63];
 }
+}  // namespace
+
+// One frame on workspace d (the caller holds d's device lock and validated
+// the frame). peer_fb / peer_mask: the root's device framebuffer, written by
+// this (non-root) shard's shading kernels next to its own (multi-device).
+static void render_frame_on(DeviceScene* d, const Scene& s, const RenderOptions& opt, RenderOutput* out,
+                            void* peer_fb, void* peer_mask);
 
 void render_frame(const Scene& s, const RenderOptions& opt, RenderOutput* out) {
-  std::lock_guard<std::mutex> frame_lock(g_frame_mu);
+  std::lock_guard<std::mutex> frame_lock(device_mutex(t_device));
   validate_frame(s, opt);
   DeviceScene* d = device_scene(s);
+  render_frame_on(d, s, opt, out, nullptr, nullptr);
+}
+
+static void render_frame_on(DeviceScene* d, const Scene& s, const RenderOptions& opt, RenderOutput* out,
+                            void* peer_fb, void* peer_mask) {
   static const bool graphs_enabled = [] {
     const char* e = std::getenv("VEIL_NO_GRAPH");
     return !(e && *e && *e != '0');
@@ -3924,6 +4278,10 @@ void render_frame(const Scene& s, const RenderOptions& opt, RenderOutput* out) {
     if (zc_dev) {
       P.fc.host_fb = reinterpret_cast<uint32_t*>(zc_dev);
       P.fc.host_mask = zc_dev + npx_frame * 4;
+    }
+    if (peer_fb) {
+      P.fc.peer_fb = static_cast<uint32_t*>(peer_fb);
+      P.fc.peer_mask = static_cast<uint8_t*>(peer_mask);
     }
     int launches = 0;
     if (graphs_enabled && !opt.dump) {
@@ -4093,7 +4451,7 @@ void render_frame(const Scene& s, const RenderOptions& opt, RenderOutput* out) {
 }
 
 void render_reference_frame(const Scene& s, const RenderOptions& opt, RenderOutput* out) {
-  std::lock_guard<std::mutex> frame_lock(g_frame_mu);
+  std::lock_guard<std::mutex> frame_lock(device_mutex(t_device));
   validate_scene(s);
   DeviceScene* d = device_scene(s);
   Prepared P = prepare(d, s, opt);
@@ -4141,6 +4499,102 @@ void render_reference_frame(const Scene& s, const RenderOptions& opt, RenderOutp
     return;
   }
   throw Error(VEIL_ERR_INTERNAL, "frame buffers could not be sized after 8 attempts");
+}
+
+// One frame over several devices in this process (veil_render_scene_multi):
+// shard i renders the bins owned by rank i of n (the same bin interleave as the
+// one-process-per-GPU path) on devices[i], each shard in its own workspace and
+// host thread, with its shading kernels writing finished pixels straight into
+// shard 0's device framebuffer (peer memory over NVLink, or the same buffer
+// when two shards share a device). Shard 0's framebuffer then holds the whole
+// frame; it is read back once. Counters of owned bins are summed, replicated
+// setup counters taken once, stage times are the maximum over shards.
+void render_frame_multi(const Scene& s, const RenderOptions& opt, const int* devices, int n,
+                        RenderOutput* out) {
+  validate_frame(s, opt);
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+    throw Error(VEIL_ERR_INTERNAL, "no CUDA device available (libveil has no CPU fallback)");
+  for (int i = 0; i < n; ++i)
+    if (devices[i] < 0 || devices[i] >= count) throw Error(VEIL_ERR_INVALID_ARG, "no such CUDA device");
+  if (s.shards.size() < size_t(n)) s.shards.resize(size_t(n), nullptr);
+  const size_t npx = size_t(s.camera.width) * s.camera.height;
+  DeviceScene* root = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(device_mutex(devices[0]));
+    root = device_scene_on(s, &s.shards[0], devices[0]);
+    root->fb.ensure(npx * 4);
+    root->mask.ensure(npx);
+  }
+  for (int i = 1; i < n; ++i) {
+    if (devices[i] == devices[0]) continue;
+    int ok = 0;
+    ck(cudaDeviceCanAccessPeer(&ok, devices[i], devices[0]), "cudaDeviceCanAccessPeer");
+    if (!ok) throw Error(VEIL_ERR_INTERNAL, "device " + std::to_string(devices[i]) +
+                                               " cannot write device " + std::to_string(devices[0]) +
+                                               "'s memory (no peer access)");
+    ck(cudaSetDevice(devices[i]), "cudaSetDevice");
+    const cudaError_t e = cudaDeviceEnablePeerAccess(devices[0], 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled)
+      cudaGetLastError();
+    else
+      ck(e, "cudaDeviceEnablePeerAccess");
+  }
+  std::vector<RenderOutput> outs(static_cast<size_t>(n));
+  std::vector<std::exception_ptr> errs(static_cast<size_t>(n));
+  std::vector<std::thread> threads;
+  for (int i = 0; i < n; ++i)
+    threads.emplace_back([&, i] {
+      try {
+        std::lock_guard<std::mutex> lk(device_mutex(devices[i]));
+        t_device = devices[i];
+        DeviceScene* d = i == 0 ? root : device_scene_on(s, &s.shards[size_t(i)], devices[i]);
+        RenderOptions o = opt;
+        o.rank = i;
+        o.world_size = n;
+        o.host_readback = false;
+        o.dump = false;
+        render_frame_on(d, s, o, &outs[size_t(i)], i ? root->fb.p : nullptr, i ? root->mask.p : nullptr);
+      } catch (...) {
+        errs[size_t(i)] = std::current_exception();
+      }
+    });
+  for (auto& t : threads) t.join();
+  for (auto& e : errs)
+    if (e) std::rethrow_exception(e);
+  ck(cudaSetDevice(devices[0]), "cudaSetDevice");
+  out->width = s.camera.width;
+  out->height = s.camera.height;
+  out->host = acquire_host_frame(npx * 5);
+  ck(cudaMemcpy(out->rgba(), root->fb.p, npx * 4, cudaMemcpyDeviceToHost), "readback");
+  ck(cudaMemcpy(out->mask(), root->mask.p, npx, cudaMemcpyDeviceToHost), "readback");
+  veil_frame_stats& st = out->stats;
+  st = outs[0].stats;  // replicated cull counters
+  st.samples = st.fragments = st.tri_half_blocks = st.segments = st.invalid_pixels = 0;
+  st.bins_propagated = st.bin_pairs = st.kernel_launches = 0;
+  st.bins_low = st.bins_high = 0;  // a shard categorises its own bins (the others read as empty)
+  const uint64_t nbins = uint64_t((s.camera.width + kBinSize - 1) / kBinSize) *
+                         uint64_t((s.camera.height + kBinSize - 1) / kBinSize);
+  for (const RenderOutput& o : outs) {
+    const veil_frame_stats& x = o.stats;
+    st.bins_low += x.bins_low;
+    st.bins_high += x.bins_high;
+    st.samples += x.samples;
+    st.fragments += x.fragments;
+    st.tri_half_blocks += x.tri_half_blocks;
+    st.segments += x.segments;
+    st.invalid_pixels += x.invalid_pixels;
+    st.bins_propagated += x.bins_propagated;
+    st.bin_pairs += x.bin_pairs;
+    st.kernel_launches += x.kernel_launches;
+    st.setup_ms = std::max(st.setup_ms, x.setup_ms);
+    st.binning_ms = std::max(st.binning_ms, x.binning_ms);
+    st.low_raster_ms = std::max(st.low_raster_ms, x.low_raster_ms);
+    st.hi_raster_ms = std::max(st.hi_raster_ms, x.hi_raster_ms);
+    st.shade_ms = std::max(st.shade_ms, x.shade_ms);
+    st.total_ms = std::max(st.total_ms, x.total_ms);
+  }
+  st.bins_empty = nbins - st.bins_low - st.bins_high;
 }
 
 void shard_tiles_device(const Scene& s, int rank, int world, void* tiles, uint64_t bytes,

@@ -32,6 +32,8 @@ Scene::Scene() {}
 
 Scene::~Scene() {
   if (device) release_device_scene(device);
+  for (DeviceScene* d : shards)
+    if (d) release_device_scene(d);
 }
 
 double Scene::degenerate_quad_percent() const {

@@ -73,6 +73,7 @@ struct Scene {
 
   double degenerate_quad_percent() const;
   mutable DeviceScene* device = nullptr;  // owned; see pipeline.cu
+  mutable std::vector<DeviceScene*> shards;  // owned: veil_render_scene_multi workspaces
 };
 
 // --- scene ingest (scene_io.cpp) -------------------------------------------
@@ -126,6 +127,8 @@ struct RenderOutput {
 // Runs one frame on the current CUDA device (pipeline.cu).
 void render_frame(const Scene& scene, const RenderOptions& opt, RenderOutput* out);
 void render_reference_frame(const Scene& scene, const RenderOptions& opt, RenderOutput* out);
+void render_frame_multi(const Scene& scene, const RenderOptions& opt, const int* devices, int n,
+                        RenderOutput* out);
 void release_device_scene(DeviceScene* d);
 void device_framebuffer(const Scene& scene, void** rgba, void** mask);
 void export_framebuffer(const Scene& scene, veil_ipc_framebuffer* out);

@@ -84,6 +84,7 @@ def lib():
         "veil_scene_set_viewport_ext": ([_P, C.c_int, C.c_int], C.c_int),
         "veil_cuda_set_device": ([C.c_int], C.c_int),
         "veil_render_scene_shard": ([_P, C.POINTER(RenderParams), C.POINTER(Shard), _PP], C.c_int),
+        "veil_render_scene_multi": ([_P, C.POINTER(RenderParams), C.POINTER(C.c_int), C.c_int, _PP], C.c_int),
         "veil_shard_tile_count": ([C.c_int, C.c_int, C.POINTER(Shard)], C.c_uint64),
         "veil_shard_pack_tiles": ([_P, C.POINTER(Shard), _P, C.c_uint64], C.c_int),
         "veil_shard_unpack_tiles": ([_P, C.POINTER(Shard), _P, C.c_uint64], C.c_int),
@@ -280,6 +281,16 @@ def render(scene: Scene, params=None, shard=None) -> Render:
     else:
         sh = Shard(*shard)
         _check(lib().veil_render_scene_shard(scene.h, C.byref(params), C.byref(sh), C.byref(r)))
+    return Render(r.value)
+
+
+def render_multi(scene: Scene, devices, params=None) -> Render:
+    """veil_render_scene_multi: one frame over several devices in this process
+    (bins interleaved over len(devices) shards, peer-memory gather)."""
+    params = params or default_params()
+    devs = (C.c_int * len(devices))(*[int(x) for x in devices])
+    r = C.c_void_p()
+    _check(lib().veil_render_scene_multi(scene.h, C.byref(params), devs, len(devices), C.byref(r)))
     return Render(r.value)
 
 

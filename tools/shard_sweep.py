@@ -24,8 +24,12 @@ for name in sys.argv[1:] or ["stack64k", "tiny4m", "mixed16m"]:
         for r in range(g):  # every rank's share, so the slowest rank is visible
             for _ in range(3):
                 veil.render_device(sc, None, (r, g))
-            ms.append(statistics.median(veil.render_device(sc, None, (r, g)).total_ms for _ in range(10)))
-        worst = max(ms)
+            sts = [veil.render_device(sc, None, (r, g)) for _ in range(10)]
+            ms.append((statistics.median(s.total_ms for s in sts),
+                       {k: statistics.median(getattr(s, k) for s in sts)
+                        for k in ("setup_ms", "binning_ms", "low_raster_ms", "hi_raster_ms", "shade_ms")}))
+        worst, stages = max(ms, key=lambda x: x[0])
         base = base or worst
-        print(f"{name:9s} G={g}: slowest rank {worst:.3f} ms/frame (ranks {min(ms):.3f}..{worst:.3f}), "
-              f"speed-up bound {base / worst:.2f}x", flush=True)
+        print(f"{name:9s} G={g}: slowest rank {worst:.3f} ms/frame (ranks {min(m[0] for m in ms):.3f}..{worst:.3f}), "
+              f"speed-up bound {base / worst:.2f}x  stages " +
+              " ".join(f"{k[:-3]} {v:.3f}" for k, v in stages.items()), flush=True)
