@@ -618,9 +618,19 @@ __global__ void __launch_bounds__(kSetupBlock, 4) k_setup(Buffers B, uint32_t nb
   B.vq_flags[slot] = (o.large ? 1u : 0u) | (has_c ? 2u : 0u) | (has_n ? 4u : 0u) | (has_uv ? 8u : 0u) |
                      (o.flags << 4);
   B.vq_mat[slot] = mat;
-  // (the corner colours / normals / UVs are gathered by k_setup_tris, which a
-  // sharded rank runs for its own bins' quads only: this cull + compaction is
-  // the part every rank replicates)
+  if (has_uv) {  // setup.cpp:326-328
+    const float2 u0 = B.vuv[idx.x], u1 = B.vuv[idx.y], u2 = B.vuv[idx.z], u3 = B.vuv[idx.w];
+    B.vq_uv[2 * (size_t)slot] = make_float4(u0.x, u0.y, u1.x, u1.y);
+    B.vq_uv[2 * (size_t)slot + 1] = make_float4(u2.x, u2.y, u3.x, u3.y);
+  }
+  // corner colours / normals (setup.cpp:329-333), one quad per lane (moving
+  // these gathers into the sharded k_setup_tris measured slower: C4 setup
+  // +0.1 ms at one GPU, the same at eight)
+  uint4 col = make_uint4(0, 0, 0, 0), nrm = make_uint4(0, 0, 0, 0);
+  if (has_c) col = make_uint4(B.vcol[idx.x], B.vcol[idx.y], B.vcol[idx.z], B.vcol[idx.w]);
+  if (has_n) nrm = make_uint4(B.vnrm[idx.x], B.vnrm[idx.y], B.vnrm[idx.z], B.vnrm[idx.w]);
+  B.vq_col[slot] = col;
+  B.vq_nrm[slot] = nrm;
 }
 
 // Triangle setups (setup.cpp:305-349, compute_triangle_setup 209-239): one
@@ -661,29 +671,13 @@ __global__ void __launch_bounds__(kTriBlock, 7) k_setup_tris(Buffers B) {
         needed = any;
       }
     }
-    uint4 qcol = make_uint4(0, 0, 0, 0), qnrm = make_uint4(0, 0, 0, 0);
     if (needed) {
       slot = ti >> 1;
       t = ti & 1u;
       vf = B.vq_flags[slot];
       const uint4 idx = B.vq_idx[slot];
       mat = B.vq_mat[slot];
-      // the visible quad's corner attributes (setup.cpp:326-333), stored once
-      // (by triangle 0) for the shading and gathered by both triangles when
-      // they write decoded records
-      if (t == 0 || fc.decoded) {
-        if (vf & 2u) qcol = make_uint4(B.vcol[idx.x], B.vcol[idx.y], B.vcol[idx.z], B.vcol[idx.w]);
-        if (vf & 4u) qnrm = make_uint4(B.vnrm[idx.x], B.vnrm[idx.y], B.vnrm[idx.z], B.vnrm[idx.w]);
-      }
-      if (t == 0) {
-        B.vq_col[slot] = qcol;
-        B.vq_nrm[slot] = qnrm;
-        if (vf & 8u) {
-          const float2 u0 = B.vuv[idx.x], u1 = B.vuv[idx.y], u2 = B.vuv[idx.z], u3 = B.vuv[idx.w];
-          B.vq_uv[2 * (size_t)slot] = make_float4(u0.x, u0.y, u1.x, u1.y);
-          B.vq_uv[2 * (size_t)slot + 1] = make_float4(u2.x, u2.y, u3.x, u3.y);
-        }
-      }
+
       if (!((vf >> 4) & (1u << t))) {  // not individually culled
         const uint32_t i1 = t == 0 ? idx.y : idx.z, i2 = t == 0 ? idx.z : idx.w;
         const float4 p0 = __ldg(&B.pos[idx.x]), p1 = __ldg(&B.pos[i1]), p2 = __ldg(&B.pos[i2]);
@@ -726,7 +720,7 @@ __global__ void __launch_bounds__(kTriBlock, 7) k_setup_tris(Buffers B) {
         // corner slots (0,1,2) / (0,2,3), shading.cpp:41-44
         const MatDev md = B.mats[mat];
         const bool has_c = vf & 2u, has_n = vf & 4u;
-        const uint4 col = qcol, nrm = qnrm;
+        const uint4 col = B.vq_col[slot], nrm = B.vq_nrm[slot];
         const uint32_t cw[3] = {col.x, t == 0 ? col.y : col.z, t == 0 ? col.z : col.w};
         const uint32_t nw[3] = {nrm.x, t == 0 ? nrm.y : nrm.z, t == 0 ? nrm.z : nrm.w};
         ShadeRec sr;
@@ -1732,9 +1726,12 @@ __device__ __forceinline__ float4 shade_staged_bf(const FrameConst& fc, const St
                                                   uint32_t* qd) {
   const double x = (double)px + 0.5, y = (double)py + 0.5;
   const uint32_t fl = T.flags;
-  const Fn3 fz = {T.dz[0], T.dz[1], T.dz[2]};
-  const uint32_t qz = quantize_depth(eval(fz, x, y));
-  *qd = (fl & 16u) ? T.pad : qz;
+  if (fl & 16u) {  // flat depth plane (stage_triangle); the one branch kept: every C2 quad
+    *qd = T.pad;
+  } else {
+    const Fn3 fz = {T.dz[0], T.dz[1], T.dz[2]};
+    *qd = quantize_depth(eval(fz, x, y));
+  }
   const Fn3 f0 = {T.e[0], T.e[1], T.e[2]}, f1 = {T.e[3], T.e[4], T.e[5]}, f2 = {T.e[6], T.e[7], T.e[8]};
   const double e0 = eval(f0, x, y), e1 = eval(f1, x, y), e2 = eval(f2, x, y);
   const double sum = __dadd_rn(__dadd_rn(e0, e1), e2);

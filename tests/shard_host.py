@@ -1,4 +1,7 @@
-"""Screen-space sharding across GPUs.
+"""Host twins of the screen-space sharding layout. TEST HELPER.
+
+tests/test_dist_cpu.py uses these to check, with gloo processes on CPU, the
+tile layout and the gather that bench.py's NCCL path performs on the GPU.
 
 Bins are interleaved over ranks with owner(bx, by) = (bx + 3*by) mod world
 (the same rule libveil's kernels apply, include/veil_cuda.h). Every rank

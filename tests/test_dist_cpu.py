@@ -9,7 +9,7 @@ import pytest
 import torch.multiprocessing as mp
 
 import bindings
-from paper_2405_13364_b200 import dist as vdist
+import shard_host as vdist
 from paper_2405_13364_b200 import veil
 from paper_2405_13364_b200.abi import default_params
 
