@@ -1,0 +1,2 @@
+mkdir -p gpurun_out
+AB_WORKLOADS=stack64k python tools/ab_time.py build_ab/libveil_prev.so build_ab/libveil_C.so > gpurun_out/ab5.log 2>&1; cat gpurun_out/ab5.log
