@@ -648,7 +648,10 @@ constexpr int kTriBlock = 128;
 // triangle and skip the others: C4 at 8 ranks 0.35 ms for 1/8 of the work).
 __global__ void __launch_bounds__(256) k_shard_tris(Buffers B) {
   const FrameConst& fc = c_fc;
+  __shared__ unsigned int n_small;  // per-block count, one global atomic
   if (B.ctr->error & 1u) return;
+  if (threadIdx.x == 0) n_small = 0;
+  __syncthreads();
   const uint32_t nq = B.ctr->nvis;
   const int lane = threadIdx.x & 31;
   for (uint32_t base = blockIdx.x * blockDim.x; base < nq; base += gridDim.x * blockDim.x) {
@@ -665,6 +668,10 @@ __global__ void __launch_bounds__(256) k_shard_tris(Buffers B) {
       }
     }
     const unsigned m = __ballot_sync(0xffffffffu, need);
+    // (the frame's visible small-quad count, which k_bin_pass takes when
+    // it walks every quad)
+    const unsigned sm = __ballot_sync(0xffffffffu, q < nq && !(B.vq_flags[q] & 1u));
+    if (lane == 0 && sm) atomicAdd(&n_small, (unsigned)__popc(sm));
     uint32_t at = 0;
     if (lane == 0 && m) at = atomicAdd(&B.ctr->shard_tri_count, 2u * (uint32_t)__popc(m));
     at = __shfl_sync(0xffffffffu, at, 0);
@@ -674,6 +681,8 @@ __global__ void __launch_bounds__(256) k_shard_tris(Buffers B) {
       B.shard_tris[pos + 1] = 2u * q + 1u;
     }
   }
+  __syncthreads();
+  if (threadIdx.x == 0 && n_small) atomicAdd(&B.ctr->small_quads, (unsigned long long)n_small);
 }
 
 template <bool kShard>
@@ -837,17 +846,22 @@ __global__ void __launch_bounds__(256) k_bin_pass(Buffers B) {
   if (B.ctr->error) return;
   if (threadIdx.x == 0) n_small = n_large = 0;
   __syncthreads();
-  const uint32_t nvis = B.ctr->nvis;
+  // sharded frames walk k_shard_tris's list (its even entries are 2q): the
+  // other quads cannot reach an owned bin; their small-quad count was taken
+  // there
+  const bool listed = fc.world > 1;
+  const uint32_t nvis = listed ? B.ctr->shard_tri_count / 2u : B.ctr->nvis;
   for (uint32_t base = blockIdx.x * 256; base < nvis; base += gridDim.x * 256) {
-    uint32_t q = base + threadIdx.x;
-    bool in = q < nvis;
+    const uint32_t i = base + threadIdx.x;
+    bool in = i < nvis;
+    const uint32_t q = listed ? (in ? B.shard_tris[2u * i] >> 1 : 0u) : i;
     uint32_t flags = in ? B.vq_flags[q] : 0u;
     bool small = in && !(flags & 1u);
     uint2 box = in ? B.vq_box[q] : make_uint2(0, 0);
     uint32_t x0 = box.x & 0xffffu, x1 = box.x >> 16, y0 = box.y & 0xffffu, y1 = box.y >> 16;
     // small quads: every bin of the AABB (binning.hpp:76-81), 1..4 bins
     uint32_t nb = small ? (x1 - x0 + 1) * (y1 - y0 + 1) : 0u;
-    if (!kWrite) {
+    if (!kWrite && !listed) {
       unsigned sm = __ballot_sync(0xffffffffu, small);
       if ((threadIdx.x & 31) == 0 && sm) atomicAdd(&n_small, (unsigned)__popc(sm));
     }
