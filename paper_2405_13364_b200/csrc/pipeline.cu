@@ -528,6 +528,17 @@ __global__ void __launch_bounds__(kSetupBlock, 4) k_setup(Buffers B, uint32_t nb
     load_quad(B, q, &idx, p);
     cull_quad(fc, idx, p, clip, &o);
   }
+  // the visible quad's material and corner attributes (setup.cpp:320-333)
+  // are gathered before the block's compaction barriers, so their latency
+  // overlaps warp 0's look-back instead of following it
+  uint32_t mat = 0, mflags = 0;
+  uint4 col = make_uint4(0, 0, 0, 0), nrm = make_uint4(0, 0, 0, 0);
+  if (o.reason == 0) {
+    mat = B.qmat[q];
+    mflags = B.mats[mat].flags;
+    if (mflags & 1u) col = make_uint4(B.vcol[idx.x], B.vcol[idx.y], B.vcol[idx.z], B.vcol[idx.w]);
+    if (mflags & 2u) nrm = make_uint4(B.vnrm[idx.x], B.vnrm[idx.y], B.vnrm[idx.z], B.vnrm[idx.w]);
+  }
   // visible-rank scan and the four cull-reason counts in two barriers: each
   // warp posts its visible count and reason ballots, warp 0 scans and sums
   constexpr int kWarps = kSetupBlock / 32;
@@ -609,14 +620,12 @@ __global__ void __launch_bounds__(kSetupBlock, 4) k_setup(Buffers B, uint32_t nb
   __syncthreads();
   if (o.reason != 0) return;
   const uint32_t slot = s_excl + rank;
-  uint32_t mat = B.qmat[q];
-  MatDev md = B.mats[mat];
-  bool has_c = md.flags & 1u, has_n = md.flags & 2u;
+  const bool has_c = mflags & 1u, has_n = mflags & 2u;
   B.vq_src[slot] = q;
   B.vq_idx[slot] = idx;
   B.vq_box[slot] = make_uint2((uint32_t)o.x0 | ((uint32_t)o.x1 << 16),
                               (uint32_t)o.y0 | ((uint32_t)o.y1 << 16));
-  const bool has_uv = md.flags & 4u;
+  const bool has_uv = mflags & 4u;
   B.vq_flags[slot] = (o.large ? 1u : 0u) | (has_c ? 2u : 0u) | (has_n ? 4u : 0u) | (has_uv ? 8u : 0u) |
                      (o.flags << 4);
   B.vq_mat[slot] = mat;
@@ -625,12 +634,9 @@ __global__ void __launch_bounds__(kSetupBlock, 4) k_setup(Buffers B, uint32_t nb
     B.vq_uv[2 * (size_t)slot] = make_float4(u0.x, u0.y, u1.x, u1.y);
     B.vq_uv[2 * (size_t)slot + 1] = make_float4(u2.x, u2.y, u3.x, u3.y);
   }
-  // corner colours / normals (setup.cpp:329-333), one quad per lane (moving
-  // these gathers into the sharded k_setup_tris measured slower: C4 setup
-  // +0.1 ms at one GPU, the same at eight)
-  uint4 col = make_uint4(0, 0, 0, 0), nrm = make_uint4(0, 0, 0, 0);
-  if (has_c) col = make_uint4(B.vcol[idx.x], B.vcol[idx.y], B.vcol[idx.z], B.vcol[idx.w]);
-  if (has_n) nrm = make_uint4(B.vnrm[idx.x], B.vnrm[idx.y], B.vnrm[idx.z], B.vnrm[idx.w]);
+  // (corner colours / normals gathered above, one quad per lane; moving these
+  // gathers into the sharded k_setup_tris measured slower: C4 setup +0.1 ms at
+  // one GPU, the same at eight)
   B.vq_col[slot] = col;
   B.vq_nrm[slot] = nrm;
 }
@@ -839,7 +845,7 @@ __device__ __forceinline__ uint32_t block_rows_mask(uint32_t yy, int by, int hei
   return m;
 }
 
-template <bool kWrite>
+template <bool kWrite, bool kList>
 __global__ void __launch_bounds__(256) k_bin_pass(Buffers B) {
   const FrameConst& fc = c_fc;
   __shared__ unsigned int n_small, n_large;  // per-block counts, one global atomic each
@@ -849,7 +855,7 @@ __global__ void __launch_bounds__(256) k_bin_pass(Buffers B) {
   // sharded frames walk k_shard_tris's list (its even entries are 2q): the
   // other quads cannot reach an owned bin; their small-quad count was taken
   // there
-  const bool listed = fc.world > 1;
+  constexpr bool listed = kList;  // (a template parameter: the runtime test cost one GPU 15 us)
   const uint32_t nvis = listed ? B.ctr->shard_tri_count / 2u : B.ctr->nvis;
   for (uint32_t base = blockIdx.x * 256; base < nvis; base += gridDim.x * 256) {
     const uint32_t i = base + threadIdx.x;
@@ -4070,10 +4076,16 @@ int enqueue_front(DeviceScene* d, Prepared& P) {
   }
   record_event(d->ev[1], st);
   int grid = std::max(1, std::min<int>(d->sm_count * 8, int((fc.nquads + 255) / 256)));
-  dev::k_bin_pass<false><<<grid, 256, 0, st>>>(B);
+  if (fc.world > 1)
+    dev::k_bin_pass<false, true><<<grid, 256, 0, st>>>(B);
+  else
+    dev::k_bin_pass<false, false><<<grid, 256, 0, st>>>(B);
   dev::k_bin_large<false><<<d->sm_count * 8, 256, 0, st>>>(B);
   dev::k_bin_scan<<<1, 1024, 0, st>>>(B);
-  dev::k_bin_pass<true><<<grid, 256, 0, st>>>(B);
+  if (fc.world > 1)
+    dev::k_bin_pass<true, true><<<grid, 256, 0, st>>>(B);
+  else
+    dev::k_bin_pass<true, false><<<grid, 256, 0, st>>>(B);
   dev::k_bin_large<true><<<d->sm_count * 8, 256, 0, st>>>(B);
   launches += 5;
   if (fc.sort_bins) {
