@@ -161,6 +161,15 @@ veil_status veil_import_peer_framebuffer(const veil_scene* scene, const veil_ipc
 veil_status veil_render_scene_multi(const veil_scene* scene, const veil_render_params* params,
                                     const int* devices, int device_count, veil_render** out_render);
 
+/* The pipeline's maximum per-pixel sort disorder for these parameters
+ * (reference RenderConfig::measure_disorder, raster.cpp:286-297: over every
+ * pixel, the largest i - position-in-sorted-order of its i-th arriving sample),
+ * which the reference reports as "max_disorder" but its C ABI cannot request.
+ * A depth filter of at least this size renders every pixel in exact order
+ * (acceptance.cpp:115-126). One device frame plus an O(n^2)-per-pixel pass. */
+veil_status veil_measure_disorder(const veil_scene* scene, const veil_render_params* params,
+                                  int* max_disorder);
+
 /* ---- device-resident frame loop ------------------------------------------- */
 
 /* Renders into device memory only (no host copies); for benchmarks that time

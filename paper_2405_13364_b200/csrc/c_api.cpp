@@ -376,6 +376,14 @@ veil_status veil_render_device(const veil_scene* scene, const veil_render_params
   });
 }
 
+veil_status veil_measure_disorder(const veil_scene* scene, const veil_render_params* params,
+                                  int* max_disorder) {
+  if (!scene || !max_disorder) return bad_arg("scene and max_disorder are required");
+  veil::RenderOptions o = options_from(params);
+  if (o.params.flags & VEIL_RENDER_REFERENCE) return bad_arg("disorder is a property of the pipeline");
+  return guard([&] { *max_disorder = veil::measure_disorder(scene->s, o); });
+}
+
 veil_status veil_render_scene_multi(const veil_scene* scene, const veil_render_params* params,
                                     const int* devices, int device_count, veil_render** out) {
   if (!scene || !devices || !out) return bad_arg("scene, devices and out_render are required");

@@ -3222,6 +3222,52 @@ __global__ void __launch_bounds__(256) k_fill_empty(Buffers B) {
   }
 }
 
+// RenderConfig::measure_disorder (raster.cpp:286-297) on the frame just
+// rendered: a warp per (bin, half-block), lane = pixel. The pixel's samples
+// arrive in the canonical enumeration order (THBs in sorted order); sample i's
+// disorder is i minus the number of the pixel's samples with a smaller key
+// (its position in the sorted sequence; keys are unique). The frame's maximum
+// goes to *out. O(n^2) per pixel over the THB list: a measurement, not a
+// frame path.
+__global__ void __launch_bounds__(256) k_disorder(Buffers B, int* out) {
+  const FrameConst& fc = c_fc;
+  if (B.ctr->error) return;
+  const int lane = threadIdx.x & 31;
+  const uint32_t nhb = (uint32_t)fc.nbins * 32u;
+  const uint32_t gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  int best = 0;
+  for (uint32_t item = gwarp; item < nhb; item += nwarps) {
+    const int bin = (int)(item >> 5), hb = (int)(item & 31u);
+    const int bxi = bin % fc.bins_x, byi = bin / fc.bins_x;
+    if (B.cat[bin] == 0 || !(fc.world <= 1 || ((bxi + 3 * byi) % fc.world) == fc.rank)) continue;
+    const HbDesc d = B.hbd[item];
+    const int block = hb >> 1;
+    const int px = bxi * kBin + (block & 3) * 8 + (lane & 7);
+    const int py = byi * kBin + (block >> 2) * 8 + (hb & 1) * 4 + (lane >> 3);
+    const double x = (double)px + 0.5, y = (double)py + 0.5;
+    const uint32_t* tri_l = B.pool_tri + d.off;
+    const uint32_t* mask_l = B.pool_mask + d.off;
+    auto key_of = [&](uint32_t r) {
+      const uint32_t tri = tri_l[r];
+      return sample_key(fc, quantize_depth(eval(B.tri[tri].dz, x, y)), tri);
+    };
+    int i = 0;
+    for (uint32_t r = 0; r < d.cnt; ++r) {
+      if (!((mask_l[r] >> lane) & 1u)) continue;
+      const uint64_t k = key_of(r);
+      int smaller = 0;
+      for (uint32_t s = 0; s < d.cnt; ++s)
+        if (((mask_l[s] >> lane) & 1u) && key_of(s) < k) ++smaller;
+      best = max(best, i - smaller);
+      ++i;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if (lane == 0 && best > 0) atomicMax(out, best);
+}
+
 // a-buffer reference renderer (oracle.cpp:28-117) on the bin lists: every
 // triangle covering a pixel is in that pixel's bin list. Fragments are
 // blended in exact key order by repeated selection of the next key, so no
@@ -3860,7 +3906,7 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
     fc.fused = fused;
     if (fused) fc.decoded = 0;
     if (const char* fr = std::getenv("VEIL_FUSED_READ"); fr && *fr) fc.fused_read = std::atoi(fr) ? 1 : 0;
-    fc.write_tri = (!fused || opt.dump || fc.fused_read) ? 1 : 0;
+    fc.write_tri = (!fused || opt.dump || opt.keep_records || fc.fused_read) ? 1 : 0;
   }
   if (fc.decoded) d->shade.ensure(size_t(Q) * 2 * sizeof(dev::ShadeRec));
   d->off.ensure(nb * 4);
@@ -4724,6 +4770,30 @@ void import_peer_framebuffer(const Scene& s, const veil_ipc_framebuffer* fb) {
   ck(cudaIpcOpenMemHandle(&d->peer_mask, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
   d->peer_w = fb->width;
   d->peer_h = fb->height;
+}
+
+// The reference pipeline's maximum per-pixel sort disorder for these
+// parameters (RenderConfig::measure_disorder): one device frame, then
+// k_disorder over its THB lists.
+int measure_disorder(const Scene& s, const RenderOptions& opt) {
+  RenderOptions o = opt;
+  o.host_readback = false;
+  o.keep_records = true;  // k_disorder reads every triangle's depth plane
+  std::lock_guard<std::mutex> frame_lock(device_mutex(t_device));
+  validate_frame(s, o);
+  DeviceScene* d = device_scene(s);
+  RenderOutput out;
+  render_frame_on(d, s, o, &out, nullptr, nullptr);
+  Prepared P = prepare(d, s, o);  // the same buffers (no growth after a completed frame)
+  DevBuf& res = d->tile_ids;      // (reused as a 4-byte result cell)
+  res.ensure(256);
+  ck(cudaMemsetAsync(res.p, 0, 4, d->stream), "memset");
+  dev::k_disorder<<<d->sm_count * 8, 256, 0, d->stream>>>(P.B, res.as<int>());
+  ck(cudaGetLastError(), "k_disorder");
+  int v = 0;
+  ck(cudaMemcpyAsync(&v, res.p, 4, cudaMemcpyDeviceToHost, d->stream), "disorder");
+  ck(cudaStreamSynchronize(d->stream), "disorder");
+  return v;
 }
 
 void device_framebuffer(const Scene& s, void** rgba, void** mask) {

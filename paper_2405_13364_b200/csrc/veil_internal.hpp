@@ -103,6 +103,7 @@ struct RenderOptions {
   int rank = 0, world_size = 1;
   bool dump = false;          // capture parity arrays
   bool host_readback = true;  // copy framebuffer + mask to the host
+  bool keep_records = false;  // store every triangle record even in the fused raster
 };
 
 struct DumpArray {
@@ -129,6 +130,7 @@ void render_frame(const Scene& scene, const RenderOptions& opt, RenderOutput* ou
 void render_reference_frame(const Scene& scene, const RenderOptions& opt, RenderOutput* out);
 void render_frame_multi(const Scene& scene, const RenderOptions& opt, const int* devices, int n,
                         RenderOutput* out);
+int measure_disorder(const Scene& scene, const RenderOptions& opt);
 void release_device_scene(DeviceScene* d);
 void device_framebuffer(const Scene& scene, void** rgba, void** mask);
 void export_framebuffer(const Scene& scene, veil_ipc_framebuffer* out);

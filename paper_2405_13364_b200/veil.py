@@ -85,6 +85,7 @@ def lib():
         "veil_cuda_set_device": ([C.c_int], C.c_int),
         "veil_render_scene_shard": ([_P, C.POINTER(RenderParams), C.POINTER(Shard), _PP], C.c_int),
         "veil_render_scene_multi": ([_P, C.POINTER(RenderParams), C.POINTER(C.c_int), C.c_int, _PP], C.c_int),
+        "veil_measure_disorder": ([_P, C.POINTER(RenderParams), C.POINTER(C.c_int)], C.c_int),
         "veil_shard_tile_count": ([C.c_int, C.c_int, C.POINTER(Shard)], C.c_uint64),
         "veil_shard_pack_tiles": ([_P, C.POINTER(Shard), _P, C.c_uint64], C.c_int),
         "veil_shard_unpack_tiles": ([_P, C.POINTER(Shard), _P, C.c_uint64], C.c_int),
@@ -292,6 +293,14 @@ def render_multi(scene: Scene, devices, params=None) -> Render:
     r = C.c_void_p()
     _check(lib().veil_render_scene_multi(scene.h, C.byref(params), devs, len(devices), C.byref(r)))
     return Render(r.value)
+
+
+def measure_disorder(scene: Scene, params=None) -> int:
+    """veil_measure_disorder: the pipeline's maximum per-pixel sort disorder."""
+    params = params or default_params()
+    out = C.c_int(0)
+    _check(lib().veil_measure_disorder(scene.h, C.byref(params), C.byref(out)))
+    return out.value
 
 
 def render_dump(scene: Scene, params=None, names=None):

@@ -100,14 +100,29 @@ def test_acceptance_oracle_exactness(kind, seed, kw):
     rs = bindings.RefScene.synthetic_params(kind, seed, 512, 512, **kw)
     arr = rs.arrays()
     disorder = max(0, rs.measure_disorder(default_params()))
+    sc = veil.Scene.from_arrays(arr)
+    assert veil.measure_disorder(sc, default_params()) == disorder  # libveil measures the same
     df = max(1, disorder)
     if disorder <= 3:
         df = 3  # the measuring render already repaired it (acceptance.cpp:118-124)
     img_ref, _, rep_ref = rs.render(default_params(flags=RENDER_REFERENCE))
-    sc = veil.Scene.from_arrays(arr)
     r = veil.render(sc, default_params(depth_filter_size=df))
     assert np.array_equal(r.pixels(), img_ref), (kind, seed, kw, df)
     assert int(r.stats().fragments) == int(rep_ref["samples"])
     assert int(r.stats().invalid_pixels) == 0
     g = veil.render(sc, default_params(flags=RENDER_REFERENCE))
     assert np.array_equal(g.pixels(), img_ref)
+
+
+@pytest.mark.parametrize("kind,seed,kw", [
+    ("intersecting_shells", 3, dict(sheets=128)), ("intersecting_shells", 3, dict(sheets=300)),
+    ("intersecting_shells", 1, dict(sheets=64)), ("random_soup", 1, dict(triangles=10000)),
+    ("random_soup", 2, dict(triangles=1000)), ("layered_quads", 1, dict(layers=48)),
+    ("dense_bin", 4, {})])
+@pytest.mark.parametrize("flags", [0, RENDER_FORCE_HIGH_PATH])
+def test_measure_disorder_equals_reference(kind, seed, kw, flags):
+    """veil_measure_disorder == the reference pipeline's max_disorder
+    (RenderConfig::measure_disorder, raster.cpp:286-297, through the shim)."""
+    rs = bindings.RefScene.synthetic_params(kind, seed, 256, 256, **kw)
+    p = default_params(flags=flags)
+    assert veil.measure_disorder(veil.Scene.from_arrays(rs.arrays()), p) == max(0, rs.measure_disorder(p))
