@@ -202,13 +202,13 @@ struct Buffers {
   uint8_t* cat;
   uint8_t* prop;
   uint32_t* items;
-  uint8_t* item_rows;
+  uint8_t* item_rows;     // per item: which of its bin's block-rows each of its triangles meets
   uint32_t* bin_list[2];  // owned bins per extraction pass (high: + propagated ones)
   uint32_t* lpair_cols;   // per large pair: covered bin-column words from the count pass
   uint32_t lpair_cols_cap;  // words
   uint32_t* prop_q;       // per bin: already appended to the high-pass list
   uint32_t* bin_cost;     // per bin: wave-walk shading cost (samples + 4 per THB)
-  uint32_t* bin_order;    // bins in descending cost, k_shade's bin order  // per item: block-rows (of its bin) each triangle's y range meets
+  uint32_t* bin_order;    // bins in descending cost: k_shade's bin order
   // raster
   unsigned long long* slots;  // per (bin, row): samples, frags, thb, segments, invalid
   uint32_t* spill[2];
@@ -3328,7 +3328,7 @@ __global__ void __launch_bounds__(128) k_abuffer(Buffers B) {
 
 // Owned 32x32 tiles <-> dense tile buffer (RGBA8 4096 B, then mask 1024 B per
 // tile), tile i of a rank = its i-th owned bin in row-major bin order. One
-// CTA per tile; 16-byte loads/stores along tile rows.
+// CTA per tile; a thread per pixel (4-byte RGBA word and 1-byte mask).
 __global__ void __launch_bounds__(256) k_tile_copy(FrameConst fc, uint32_t* fb, uint8_t* mask,
                                                    uint8_t* tiles, const uint32_t* bins,
                                                    uint32_t ntiles, int unpack) {

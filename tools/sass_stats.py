@@ -17,6 +17,8 @@ for line in out.splitlines():
         if op.startswith("D") and op in ("DADD", "DMUL", "DFMA", "DSETP", "DMNMX"): stats[cur]["fp64"] += 1
         if op in ("LDS", "STS"): stats[cur]["smem"] += 1
         if op in ("LDG", "STG"): stats[cur]["gmem"] += 1
+        if op in ("UBLKCP", "UTMALDG", "SYNCS"): stats[cur]["bulk"] += 1
 for k, v in stats.items():
     if flt in k:
-        print(f"{v['inst']:6d} inst {v['local']:4d} local {v['fp64']:5d} fp64 {v['smem']:4d} smem {v['gmem']:4d} gmem  {k[:90]}")
+        print(f"{v['inst']:6d} inst {v['local']:4d} local {v['fp64']:5d} fp64 {v['smem']:4d} smem {v['gmem']:4d} gmem "
+              f"{v['bulk']:3d} bulk/mbar  {k[:90]}")
