@@ -3400,7 +3400,7 @@ struct DeviceScene {
       tri_y;
   DevBuf off, qcur, tcur, cat, bin_list0, bin_list1, prop_q, bin_cost, bin_order, prop, items, item_rows, slots, spill0, spill1, scratch, fb, mask,
       hash, emit, tile_ids, hbd, pool_tri, pool_mask, pool_pre, seg_queue, pool_slot, lpairs, lpair_cols,
-      dfm_g, cscratch, tplanes, shard_tris;
+      dfm_g, cscratch, tplanes, shard_tris, disorder;
   uint32_t items_cap = 0;
   uint32_t pool_cap = 0;
   uint32_t lpairs_cap = 0;
@@ -4785,7 +4785,7 @@ int measure_disorder(const Scene& s, const RenderOptions& opt) {
   RenderOutput out;
   render_frame_on(d, s, o, &out, nullptr, nullptr);
   Prepared P = prepare(d, s, o);  // the same buffers (no growth after a completed frame)
-  DevBuf& res = d->tile_ids;      // (reused as a 4-byte result cell)
+  DevBuf& res = d->disorder;
   res.ensure(256);
   ck(cudaMemsetAsync(res.p, 0, 4, d->stream), "memset");
   dev::k_disorder<<<d->sm_count * 8, 256, 0, d->stream>>>(P.B, res.as<int>());
