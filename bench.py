@@ -323,6 +323,9 @@ def run_ours(args):
     cdev = "cpu" if gloo else "cuda"  # where collective tensors live
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        # NCCL's init log (stderr) shows the communicator's ranks and transports
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         if gloo:
             dist.init_process_group("gloo")
         else:
