@@ -1664,7 +1664,8 @@ struct __align__(16) StagedTri {
   float4 c[3];
   float4 mat;
   float n[9];
-  uint32_t flags;  // 1 colours, 2 normals, 4 constant light, 8 constant colour, 16 flat depth
+  uint32_t flags;  // 1 colours, 2 normals, 4 constant light, 8 constant colour, 16 flat depth,
+                   // 32 one axis-aligned vertex normal (light from s_axis_light, axis in `light`)
   float light;
   uint32_t pad;  // quantized depth when flag 16
 };
@@ -1712,6 +1713,23 @@ __device__ __forceinline__ void stage_triangle(const FrameConst& fc, const Buffe
     // triangle's (bit-identical to evaluating it per sample)
     dst->pad = quantize_depth(t.dz.c);
     fl |= 16u;
+  }
+  if (fl & 2u) {
+    // the three corners carry the same axis-aligned unit normal (components
+    // 0 and +-1, e.g. every C2 quad): the interpolated normal is then exactly
+    // that axis times s = (b0 + b1) + b2 (products by 0 / +-1 are exact and
+    // rounding is sign-symmetric), so the light factor is a function of s
+    // alone, tabulated per frame (axis_light_table)
+    const float4 a = sr.n[0], b = sr.n[1], c = sr.n[2];
+    if (a.x == b.x && a.x == c.x && a.y == b.y && a.y == c.y && a.z == b.z && a.z == c.z) {
+      const int nz = (a.x != 0.0f) + (a.y != 0.0f) + (a.z != 0.0f);
+      const float v = a.x != 0.0f ? a.x : (a.y != 0.0f ? a.y : a.z);
+      if (nz == 1 && (v == 1.0f || v == -1.0f)) {
+        const uint32_t axis = (a.x != 0.0f ? 0u : (a.y != 0.0f ? 1u : 2u)) * 2u + (v < 0.0f ? 1u : 0u);
+        dst->light = __uint_as_float(axis);
+        fl |= 32u;
+      }
+    }
   }
   if (!(fl & 2u)) {
     const float4 n0 = sr.n[0];
@@ -1766,6 +1784,35 @@ __device__ __forceinline__ float4 shade_staged(const FrameConst& fc, const Stage
   return premultiply(color, T.mat, light);
 }
 
+// Light factors of the six axis-aligned unit normals interpolated to
+// s * axis, for the 17 floats s around 1.0f (bit offsets -8..8) that
+// (b0 + b1) + b2 takes in practice; filled per CTA from the frame constants
+// with shade_staged_bf's exact operations.
+constexpr int kAxisLightSpan = 8;
+__shared__ float s_axis_light[6][2 * kAxisLightSpan + 1];
+
+__device__ __forceinline__ float light_of_normal(const FrameConst& fc, float n0, float n1, float n2) {
+  const float len2 = __fadd_rn(__fadd_rn(__fmul_rn(n0, n0), __fmul_rn(n1, n1)), __fmul_rn(n2, n2));
+  const bool pos = len2 > 0.0f;
+  const float il = __fdiv_rn(1.0f, __fsqrt_rn(pos ? len2 : 1.0f));
+  const float nx = pos ? __fmul_rn(n0, il) : 0.0f, ny = pos ? __fmul_rn(n1, il) : 0.0f,
+              nz = pos ? __fmul_rn(n2, il) : 0.0f;
+  const float d = __fadd_rn(__fadd_rn(__fmul_rn(nx, fc.light[0]), __fmul_rn(ny, fc.light[1])),
+                            __fmul_rn(nz, fc.light[2]));
+  return sminf(1.0f, __fadd_rn(fc.ambient, smaxf(0.0f, -d)));
+}
+
+__device__ __forceinline__ void fill_axis_light(const FrameConst& fc) {
+  for (int i = threadIdx.x; i < 6 * (2 * kAxisLightSpan + 1); i += blockDim.x) {
+    const int axis = i / (2 * kAxisLightSpan + 1), o = i % (2 * kAxisLightSpan + 1) - kAxisLightSpan;
+    const float s = __uint_as_float((uint32_t)((int)0x3f800000 + o));
+    const float v = (axis & 1) ? -s : s;
+    const int k = axis >> 1;
+    s_axis_light[axis][o + kAxisLightSpan] = light_of_normal(fc, k == 0 ? v : 0.0f, k == 1 ? v : 0.0f,
+                                                             k == 2 ? v : 0.0f);
+  }
+}
+
 // shade_staged without branches (every path computed, the flags select), so
 // that two independent samples per lane can be interleaved by the scheduler
 // (shade_waves_staged2). Bit-identical to shade_staged: each selected value
@@ -1793,19 +1840,19 @@ __device__ __forceinline__ float4 shade_staged_bf(const FrameConst& fc, const St
   color.y = hc ? __fadd_rn(__fadd_rn(__fmul_rn(c0.y, b0), __fmul_rn(c1.y, b1)), __fmul_rn(c2.y, b2)) : 1.0f;
   color.z = hc ? __fadd_rn(__fadd_rn(__fmul_rn(c0.z, b0), __fmul_rn(c1.z, b1)), __fmul_rn(c2.z, b2)) : 1.0f;
   color.w = hc ? __fadd_rn(__fadd_rn(__fmul_rn(c0.w, b0), __fmul_rn(c1.w, b1)), __fmul_rn(c2.w, b2)) : 1.0f;
-  float n[3];
+  float light;
+  const float s = __fadd_rn(__fadd_rn(b0, b1), b2);
+  const int so = (int)__float_as_uint(s) - (int)0x3f800000;
+  if ((fl & 32u) && so >= -kAxisLightSpan && so <= kAxisLightSpan) {
+    light = s_axis_light[__float_as_uint(T.light)][so + kAxisLightSpan];  // axis-aligned normal
+  } else {
+    float n[3];
 #pragma unroll
-  for (int k = 0; k < 3; ++k)
-    n[k] = __fadd_rn(__fadd_rn(__fmul_rn(T.n[k], b0), __fmul_rn(T.n[3 + k], b1)), __fmul_rn(T.n[6 + k], b2));
-  const float len2 = __fadd_rn(__fadd_rn(__fmul_rn(n[0], n[0]), __fmul_rn(n[1], n[1])), __fmul_rn(n[2], n[2]));
-  const bool pos = len2 > 0.0f;
-  const float il = __fdiv_rn(1.0f, __fsqrt_rn(pos ? len2 : 1.0f));
-  const float nx = pos ? __fmul_rn(n[0], il) : 0.0f, ny = pos ? __fmul_rn(n[1], il) : 0.0f,
-              nz = pos ? __fmul_rn(n[2], il) : 0.0f;
-  const float d = __fadd_rn(__fadd_rn(__fmul_rn(nx, fc.light[0]), __fmul_rn(ny, fc.light[1])),
-                            __fmul_rn(nz, fc.light[2]));
-  const float lit = sminf(1.0f, __fadd_rn(fc.ambient, smaxf(0.0f, -d)));
-  const float light = (fl & 4u) ? T.light : lit;
+    for (int k = 0; k < 3; ++k)
+      n[k] = __fadd_rn(__fadd_rn(__fmul_rn(T.n[k], b0), __fmul_rn(T.n[3 + k], b1)), __fmul_rn(T.n[6 + k], b2));
+    const float lit = light_of_normal(fc, n[0], n[1], n[2]);
+    light = (fl & 4u) ? T.light : lit;
+  }
   // (constant-colour triangles select their staged colour: an early return
   // for them measured C2 shade +3% -- it splits the two interleaved waves --
   // though C3's constant-colour boxes gain 6%)
@@ -2913,6 +2960,7 @@ template <int KM, int kMode, bool kTex>
 __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
   const FrameConst& fc = c_fc;
   load_shared_luts();
+  if (kMode == 0) fill_axis_light(fc);
   __syncthreads();
   // (+8 entries: bulk copies move 16-byte aligned runs around the list)
   __shared__ __align__(16) uint32_t stage_tri[8][kShadeStage + 8];
