@@ -158,7 +158,7 @@ struct __align__(16) ShadeRec {
   float4 c[3];    // corner colours (valid when flags & 1)
   float4 n[3];    // corner normals (flags & 2) or n[0] = flat normal
   float4 mat;     // base rgb, opacity
-  uint32_t flags;
+  uint32_t flags;  // 1 colours, 2 normals, 4 the corners share an axis normal (axis in pad[0])
   uint32_t pad[3];
 };
 static_assert(sizeof(ShadeRec) == 128, "ShadeRec is one cache line");
@@ -268,6 +268,21 @@ __device__ __forceinline__ float slut_c(uint32_t w, int shift) { return s_lut_c[
 __device__ __forceinline__ float slut_n(uint32_t w, int shift) {
   const int32_t q = (int32_t)(((w >> shift) & 0x3ffu) << 22) >> 22;
   return s_lut_n[q + 512];
+}
+
+// Axis index (component * 2 + negative) of a packed X10Y10Z10 normal word
+// that encodes one of the six axis-aligned unit normals (decode_normal gives
+// exactly 0 and +-1 for them), else -1.
+__device__ __forceinline__ int axis_of_word(uint32_t w) {
+  switch (w) {
+    case 0x1ffu: return 0;
+    case 0x201u: return 1;
+    case 0x1ffu << 10: return 2;
+    case 0x201u << 10: return 3;
+    case 0x1ffu << 20: return 4;
+    case 0x201u << 20: return 5;
+    default: return -1;
+  }
 }
 
 // ------------------------------------------------------------ setup
@@ -776,6 +791,10 @@ __global__ void __launch_bounds__(kTriBlock, 7) k_setup_tris(Buffers B) {
         sr.mat = make_float4(md.base[0], md.base[1], md.base[2], md.opacity);
         sr.flags = (has_c ? 1u : 0u) | (has_n ? 2u : 0u);
         sr.pad[0] = sr.pad[1] = sr.pad[2] = 0;
+        if (has_n && nw[0] == nw[1] && nw[1] == nw[2] && axis_of_word(nw[0]) >= 0) {
+          sr.flags |= 4u;  // one axis-aligned vertex normal: light from s_axis_light
+          sr.pad[0] = (uint32_t)axis_of_word(nw[0]);
+        }
         B.shade[ti] = sr;
       }
     }
@@ -1525,6 +1544,47 @@ __device__ __forceinline__ float4 texture_factor(const Buffers& B, const Fn3* te
   return sample_texture(B, texi, uv, duv_dx, duv_dy);
 }
 
+// Light factors of the six axis-aligned unit normals interpolated to
+// s * axis, for the 17 floats s around 1.0f (bit offsets -8..8) that
+// (b0 + b1) + b2 takes in practice; filled per CTA from the frame constants
+// with shade_staged_bf's exact operations.
+constexpr int kAxisLightSpan = 8;
+__shared__ float s_axis_light[6][2 * kAxisLightSpan + 1];
+
+__device__ __forceinline__ float light_of_normal(const FrameConst& fc, float n0, float n1, float n2) {
+  const float len2 = __fadd_rn(__fadd_rn(__fmul_rn(n0, n0), __fmul_rn(n1, n1)), __fmul_rn(n2, n2));
+  const bool pos = len2 > 0.0f;
+  const float il = __fdiv_rn(1.0f, __fsqrt_rn(pos ? len2 : 1.0f));
+  const float nx = pos ? __fmul_rn(n0, il) : 0.0f, ny = pos ? __fmul_rn(n1, il) : 0.0f,
+              nz = pos ? __fmul_rn(n2, il) : 0.0f;
+  const float d = __fadd_rn(__fadd_rn(__fmul_rn(nx, fc.light[0]), __fmul_rn(ny, fc.light[1])),
+                            __fmul_rn(nz, fc.light[2]));
+  return sminf(1.0f, __fadd_rn(fc.ambient, smaxf(0.0f, -d)));
+}
+
+__device__ __forceinline__ void fill_axis_light(const FrameConst& fc) {
+  for (int i = threadIdx.x; i < 6 * (2 * kAxisLightSpan + 1); i += blockDim.x) {
+    const int axis = i / (2 * kAxisLightSpan + 1), o = i % (2 * kAxisLightSpan + 1) - kAxisLightSpan;
+    const float s = __uint_as_float((uint32_t)((int)0x3f800000 + o));
+    const float v = (axis & 1) ? -s : s;
+    const int k = axis >> 1;
+    s_axis_light[axis][o + kAxisLightSpan] = light_of_normal(fc, k == 0 ? v : 0.0f, k == 1 ? v : 0.0f,
+                                                             k == 2 ? v : 0.0f);
+  }
+}
+
+// The light factor of a triangle whose corners share axis normal `axis`
+// (-1: none) from the table, when s = (b0 + b1) + b2 is tabulated; false
+// when the caller must compute it.
+__device__ __forceinline__ bool axis_light(int axis, float b0, float b1, float b2, float* light) {
+  if (axis < 0) return false;
+  const float s = __fadd_rn(__fadd_rn(b0, b1), b2);
+  const int so = (int)__float_as_uint(s) - (int)0x3f800000;
+  if (so < -kAxisLightSpan || so > kAxisLightSpan) return false;
+  *light = s_axis_light[axis][so + kAxisLightSpan];
+  return true;
+}
+
 // make_sample_context (shading.cpp:24-77) + shade_sample (123-139), no
 // textures. Returns the premultiplied colour and the sample depth.
 template <bool kTex>
@@ -1553,17 +1613,21 @@ __device__ __forceinline__ float4 shade_sample(const FrameConst& fc, const Buffe
       color.z = __fadd_rn(__fadd_rn(__fmul_rn(c0.z, b0), __fmul_rn(c1.z, b1)), __fmul_rn(c2.z, b2));
       color.w = __fadd_rn(__fadd_rn(__fmul_rn(c0.w, b0), __fmul_rn(c1.w, b1)), __fmul_rn(c2.w, b2));
     }
-    float n[3];
-    const float4 n0 = sr.n[0];
-    if (fl & 2u) {
-      const float4 n1 = sr.n[1], n2 = sr.n[2];
-      n[0] = __fadd_rn(__fadd_rn(__fmul_rn(n0.x, b0), __fmul_rn(n1.x, b1)), __fmul_rn(n2.x, b2));
-      n[1] = __fadd_rn(__fadd_rn(__fmul_rn(n0.y, b0), __fmul_rn(n1.y, b1)), __fmul_rn(n2.y, b2));
-      n[2] = __fadd_rn(__fadd_rn(__fmul_rn(n0.z, b0), __fmul_rn(n1.z, b1)), __fmul_rn(n2.z, b2));
-    } else {
-      n[0] = n0.x, n[1] = n0.y, n[2] = n0.z;
+    float light;
+    if (!axis_light((fl & 4u) ? (int)sr.pad[0] : -1, b0, b1, b2, &light)) {
+      float n[3];
+      const float4 n0 = sr.n[0];
+      if (fl & 2u) {
+        const float4 n1 = sr.n[1], n2 = sr.n[2];
+        n[0] = __fadd_rn(__fadd_rn(__fmul_rn(n0.x, b0), __fmul_rn(n1.x, b1)), __fmul_rn(n2.x, b2));
+        n[1] = __fadd_rn(__fadd_rn(__fmul_rn(n0.y, b0), __fmul_rn(n1.y, b1)), __fmul_rn(n2.y, b2));
+        n[2] = __fadd_rn(__fadd_rn(__fmul_rn(n0.z, b0), __fmul_rn(n1.z, b1)), __fmul_rn(n2.z, b2));
+      } else {
+        n[0] = n0.x, n[1] = n0.y, n[2] = n0.z;
+      }
+      light = light_factor(fc, n);
     }
-    return light_and_premultiply(fc, n, color, sr.mat);
+    return premultiply(color, sr.mat, light);
   }
   const uint32_t q = tri >> 1;
   const uint32_t qf = __ldg(&B.vq_flags[q]);
@@ -1582,17 +1646,25 @@ __device__ __forceinline__ float4 shade_sample(const FrameConst& fc, const Buffe
                        __fmul_rn(slut_c(w2, 8 * k), b2));
     color = make_float4(r[0], r[1], r[2], r[3]);
   }
-  float n[3];
-  if (qf & 4u) {
+  float light;
+  {
+    // corners sharing one axis-aligned normal take the light from the table
     const uint4 c = qnrm;
     const uint32_t w0 = c.x, w1 = ltri == 0 ? c.y : c.z, w2 = ltri == 0 ? c.z : c.w;
+    const int axis = (qf & 4u) && w0 == w1 && w1 == w2 ? axis_of_word(w0) : -1;
+    if (!axis_light(axis, b0, b1, b2, &light)) {
+      float n[3];
+      if (qf & 4u) {
 #pragma unroll
-    for (int k = 0; k < 3; ++k)
-      n[k] = __fadd_rn(__fadd_rn(__fmul_rn(slut_n(w0, 10 * k), b0), __fmul_rn(slut_n(w1, 10 * k), b1)),
-                       __fmul_rn(slut_n(w2, 10 * k), b2));
-  } else {
+        for (int k = 0; k < 3; ++k)
+          n[k] = __fadd_rn(__fadd_rn(__fmul_rn(slut_n(w0, 10 * k), b0), __fmul_rn(slut_n(w1, 10 * k), b1)),
+                           __fmul_rn(slut_n(w2, 10 * k), b2));
+      } else {
 #pragma unroll
-    for (int k = 0; k < 3; ++k) n[k] = slut_n(meta.x, 10 * k);
+        for (int k = 0; k < 3; ++k) n[k] = slut_n(meta.x, 10 * k);
+      }
+      light = light_factor(fc, n);
+    }
   }
   const MatDev& m = B.mats[meta.y];
   const float4 mat = make_float4(__ldg(&m.base[0]), __ldg(&m.base[1]), __ldg(&m.base[2]), __ldg(&m.opacity));
@@ -1600,10 +1672,10 @@ __device__ __forceinline__ float4 shade_sample(const FrameConst& fc, const Buffe
     const int texi = __ldg(&m.texture);
     if (texi >= 0) {
       const float4 tex = texture_factor(B, te, q, ltri, (qf & 8u) != 0u, texi, e0, e1, e2, sum, inv);
-      return premultiply_tex(color, mat, tex, light_factor(fc, n));
+      return premultiply_tex(color, mat, tex, light);
     }
   }
-  return light_and_premultiply(fc, n, color, mat);
+  return premultiply(color, mat, light);
 }
 
 // Branch-free variant of shade_sample for the decoded-record path (selects
@@ -1629,21 +1701,15 @@ __device__ __forceinline__ float4 shade_decoded_bf(const FrameConst& fc, const B
   color.y = hc ? __fadd_rn(__fadd_rn(__fmul_rn(c0.y, b0), __fmul_rn(c1.y, b1)), __fmul_rn(c2.y, b2)) : 1.0f;
   color.z = hc ? __fadd_rn(__fadd_rn(__fmul_rn(c0.z, b0), __fmul_rn(c1.z, b1)), __fmul_rn(c2.z, b2)) : 1.0f;
   color.w = hc ? __fadd_rn(__fadd_rn(__fmul_rn(c0.w, b0), __fmul_rn(c1.w, b1)), __fmul_rn(c2.w, b2)) : 1.0f;
-  float n[3];
-  n[0] = hn ? __fadd_rn(__fadd_rn(__fmul_rn(n0.x, b0), __fmul_rn(n1.x, b1)), __fmul_rn(n2.x, b2)) : n0.x;
-  n[1] = hn ? __fadd_rn(__fadd_rn(__fmul_rn(n0.y, b0), __fmul_rn(n1.y, b1)), __fmul_rn(n2.y, b2)) : n0.y;
-  n[2] = hn ? __fadd_rn(__fadd_rn(__fmul_rn(n0.z, b0), __fmul_rn(n1.z, b1)), __fmul_rn(n2.z, b2)) : n0.z;
-  float len2 = __fadd_rn(__fadd_rn(__fmul_rn(n[0], n[0]), __fmul_rn(n[1], n[1])), __fmul_rn(n[2], n[2]));
-  const bool pos = len2 > 0.0f;
-  const float il = __fdiv_rn(1.0f, __fsqrt_rn(pos ? len2 : 1.0f));
-  n[0] = pos ? __fmul_rn(n[0], il) : 0.0f;
-  n[1] = pos ? __fmul_rn(n[1], il) : 0.0f;
-  n[2] = pos ? __fmul_rn(n[2], il) : 0.0f;
   const float4 mat = sr.mat;
-  float d = __fadd_rn(__fadd_rn(__fmul_rn(n[0], fc.light[0]), __fmul_rn(n[1], fc.light[1])),
-                      __fmul_rn(n[2], fc.light[2]));
-  float lam = smaxf(0.0f, -d);
-  float light = sminf(1.0f, __fadd_rn(fc.ambient, lam));
+  float light;
+  if (!axis_light((fl & 4u) ? (int)sr.pad[0] : -1, b0, b1, b2, &light)) {
+    float n[3];
+    n[0] = hn ? __fadd_rn(__fadd_rn(__fmul_rn(n0.x, b0), __fmul_rn(n1.x, b1)), __fmul_rn(n2.x, b2)) : n0.x;
+    n[1] = hn ? __fadd_rn(__fadd_rn(__fmul_rn(n0.y, b0), __fmul_rn(n1.y, b1)), __fmul_rn(n2.y, b2)) : n0.y;
+    n[2] = hn ? __fadd_rn(__fadd_rn(__fmul_rn(n0.z, b0), __fmul_rn(n1.z, b1)), __fmul_rn(n2.z, b2)) : n0.z;
+    light = light_of_normal(fc, n[0], n[1], n[2]);
+  }
   float r = __fmul_rn(__fmul_rn(__fmul_rn(mat.x, color.x), 1.0f), light);
   float g = __fmul_rn(__fmul_rn(__fmul_rn(mat.y, color.y), 1.0f), light);
   float b = __fmul_rn(__fmul_rn(__fmul_rn(mat.z, color.z), 1.0f), light);
@@ -1705,7 +1771,7 @@ __device__ __forceinline__ void stage_triangle(const FrameConst& fc, const Buffe
     dst->n[3 * k + 1] = nn.y;
     dst->n[3 * k + 2] = nn.z;
   }
-  uint32_t fl = sr.flags;
+  uint32_t fl = sr.flags & 3u;  // colours / normals (the record's axis bit is re-derived below)
   dst->pad = 0;
   if (t.dz.a == 0.0 && t.dz.b == 0.0) {
     // flat depth plane: (0*x + 0*y) + c is c (or a zero, which quantizes
@@ -1782,35 +1848,6 @@ __device__ __forceinline__ float4 shade_staged(const FrameConst& fc, const Stage
     light = light_factor(fc, n);
   }
   return premultiply(color, T.mat, light);
-}
-
-// Light factors of the six axis-aligned unit normals interpolated to
-// s * axis, for the 17 floats s around 1.0f (bit offsets -8..8) that
-// (b0 + b1) + b2 takes in practice; filled per CTA from the frame constants
-// with shade_staged_bf's exact operations.
-constexpr int kAxisLightSpan = 8;
-__shared__ float s_axis_light[6][2 * kAxisLightSpan + 1];
-
-__device__ __forceinline__ float light_of_normal(const FrameConst& fc, float n0, float n1, float n2) {
-  const float len2 = __fadd_rn(__fadd_rn(__fmul_rn(n0, n0), __fmul_rn(n1, n1)), __fmul_rn(n2, n2));
-  const bool pos = len2 > 0.0f;
-  const float il = __fdiv_rn(1.0f, __fsqrt_rn(pos ? len2 : 1.0f));
-  const float nx = pos ? __fmul_rn(n0, il) : 0.0f, ny = pos ? __fmul_rn(n1, il) : 0.0f,
-              nz = pos ? __fmul_rn(n2, il) : 0.0f;
-  const float d = __fadd_rn(__fadd_rn(__fmul_rn(nx, fc.light[0]), __fmul_rn(ny, fc.light[1])),
-                            __fmul_rn(nz, fc.light[2]));
-  return sminf(1.0f, __fadd_rn(fc.ambient, smaxf(0.0f, -d)));
-}
-
-__device__ __forceinline__ void fill_axis_light(const FrameConst& fc) {
-  for (int i = threadIdx.x; i < 6 * (2 * kAxisLightSpan + 1); i += blockDim.x) {
-    const int axis = i / (2 * kAxisLightSpan + 1), o = i % (2 * kAxisLightSpan + 1) - kAxisLightSpan;
-    const float s = __uint_as_float((uint32_t)((int)0x3f800000 + o));
-    const float v = (axis & 1) ? -s : s;
-    const int k = axis >> 1;
-    s_axis_light[axis][o + kAxisLightSpan] = light_of_normal(fc, k == 0 ? v : 0.0f, k == 1 ? v : 0.0f,
-                                                             k == 2 ? v : 0.0f);
-  }
 }
 
 // shade_staged without branches (every path computed, the flags select), so
@@ -2843,8 +2880,9 @@ __global__ void __launch_bounds__(128, kFuse ? 6 : 7) k_extract(Buffers B, int p
   extern __shared__ __align__(16) uint8_t smem_raw[];
   __shared__ ItemState st;
   __shared__ uint32_t item_s;
-  if (kFuse) {  // the generic shading path's unpack tables
+  if (kFuse) {  // the generic shading path's unpack and axis-light tables
     load_shared_luts();
+    fill_axis_light(fc);
     __syncthreads();
   }
   if (B.ctr->error) return;
@@ -2960,7 +2998,7 @@ template <int KM, int kMode, bool kTex>
 __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
   const FrameConst& fc = c_fc;
   load_shared_luts();
-  if (kMode == 0) fill_axis_light(fc);
+  fill_axis_light(fc);
   __syncthreads();
   // (+8 entries: bulk copies move 16-byte aligned runs around the list)
   __shared__ __align__(16) uint32_t stage_tri[8][kShadeStage + 8];
@@ -3323,6 +3361,7 @@ __global__ void __launch_bounds__(256) k_disorder(Buffers B, int* out) {
 __global__ void __launch_bounds__(128) k_abuffer(Buffers B) {
   const FrameConst& fc = c_fc;
   load_shared_luts();
+  fill_axis_light(fc);
   __syncthreads();
   if (B.ctr->error) return;
   const int px = blockIdx.x * 16 + (threadIdx.x & 15);
