@@ -1431,10 +1431,12 @@ __device__ __forceinline__ float light_factor(const FrameConst& fc, float n[3]) 
 // base * colour * texture(1) * light, premultiplied (shading.cpp:137-139);
 // mat = (base rgb, opacity).
 __device__ __forceinline__ float4 premultiply(float4 color, float4 mat, float light) {
-  float r = __fmul_rn(__fmul_rn(__fmul_rn(mat.x, color.x), 1.0f), light);
-  float g = __fmul_rn(__fmul_rn(__fmul_rn(mat.y, color.y), 1.0f), light);
-  float b = __fmul_rn(__fmul_rn(__fmul_rn(mat.z, color.z), 1.0f), light);
-  float a = __fmul_rn(__fmul_rn(mat.w, color.w), 1.0f);
+  // (the reference's texture factor is 1 here: x * 1.0f == x exactly, so the
+  // product is left out)
+  float r = __fmul_rn(__fmul_rn(mat.x, color.x), light);
+  float g = __fmul_rn(__fmul_rn(mat.y, color.y), light);
+  float b = __fmul_rn(__fmul_rn(mat.z, color.z), light);
+  float a = __fmul_rn(mat.w, color.w);
   return make_float4(__fmul_rn(r, a), __fmul_rn(g, a), __fmul_rn(b, a), a);
 }
 
@@ -1710,10 +1712,12 @@ __device__ __forceinline__ float4 shade_decoded_bf(const FrameConst& fc, const B
     n[2] = hn ? __fadd_rn(__fadd_rn(__fmul_rn(n0.z, b0), __fmul_rn(n1.z, b1)), __fmul_rn(n2.z, b2)) : n0.z;
     light = light_of_normal(fc, n[0], n[1], n[2]);
   }
-  float r = __fmul_rn(__fmul_rn(__fmul_rn(mat.x, color.x), 1.0f), light);
-  float g = __fmul_rn(__fmul_rn(__fmul_rn(mat.y, color.y), 1.0f), light);
-  float b = __fmul_rn(__fmul_rn(__fmul_rn(mat.z, color.z), 1.0f), light);
-  float a = __fmul_rn(__fmul_rn(mat.w, color.w), 1.0f);
+  // (the reference's texture factor is 1 here: x * 1.0f == x exactly, so the
+  // product is left out)
+  float r = __fmul_rn(__fmul_rn(mat.x, color.x), light);
+  float g = __fmul_rn(__fmul_rn(mat.y, color.y), light);
+  float b = __fmul_rn(__fmul_rn(mat.z, color.z), light);
+  float a = __fmul_rn(mat.w, color.w);
   return make_float4(__fmul_rn(r, a), __fmul_rn(g, a), __fmul_rn(b, a), a);
 }
 
