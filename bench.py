@@ -370,8 +370,17 @@ def run_ours(args):
             m, eye = camera_fn(i)
             scene.set_camera(m, eye)
         if timed_events:
-            timed_events[0].record(stream)
-        veil.render_device(scene, params, shard, stats=False)
+            # libveil records the start event right before the frame's graph
+            # launch and (one GPU) the end event right after it, on the same
+            # stream: the region is the frame's device work, without the
+            # host's launch preparation or its wake-up after the frame's wait
+            hs = timed_events[0].cuda_event
+            he = timed_events[1].cuda_event if world == 1 else None
+            veil.render_device(scene, params, shard, stats=False, events=(hs, he))
+            if world == 1:
+                return scene.last_stats()
+        else:
+            veil.render_device(scene, params, shard, stats=False)
         if peer:
             # every rank's pixels are in rank 0's framebuffer once all ranks'
             # frames completed (render_device synchronises its stream)
@@ -402,6 +411,9 @@ def run_ours(args):
 
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
+    for a, b in evs:  # torch creates its events at their first record
+        a.record(stream)
+        b.record(stream)
     stats = []
     if world > 1:
         dist.barrier()
@@ -580,6 +592,11 @@ def run_ours(args):
                            + (", peer-memory framebuffer gather" if peer else
                               (f", {args.dist_backend} tile gather" if world > 1 else "")),
             "fragments_per_frame": int(fragments_per_frame),
+            "timed_region": ("CUDA events on the renderer's stream, recorded by libveil "
+                             "(veil_render_device_timed) right before the frame's graph launch and "
+                             + ("right after it" if world == 1 else
+                                "by bench.py after the gather (max over ranks)")
+                             + "; one frame = c_fc upload, counter reset, every kernel, counter read-back"),
             "parity": parity,
             "e2e": e2e,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

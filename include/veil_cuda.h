@@ -176,6 +176,15 @@ veil_status veil_measure_disorder(const veil_scene* scene, const veil_render_par
  * the device path. Output stays on the scene's device workspace. */
 veil_status veil_render_device(const veil_scene* scene, const veil_render_params* params,
                                const veil_shard* shard);
+/* veil_render_device that also records two caller-owned CUDA events
+ * (cudaEvent_t as void*, either may be NULL) on the scene's stream: `start`
+ * immediately before the frame's work (its graph launch) and `end` right after
+ * it, before the call waits for the frame. cudaEventElapsedTime(start, end) is
+ * then the device time of exactly the frame, without the host's launch
+ * preparation or its wake-up after the wait. A frame that re-runs to grow a
+ * buffer records them around its last attempt. */
+veil_status veil_render_device_timed(const veil_scene* scene, const veil_render_params* params,
+                                     const veil_shard* shard, void* start_event, void* end_event);
 /* Device pointers of the last veil_render_device() output. */
 veil_status veil_device_framebuffer(const veil_scene* scene, void** rgba, void** mask);
 /* CUDA stream the scene's kernels run on (cudaStream_t as void*). */

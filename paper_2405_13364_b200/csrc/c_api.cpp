@@ -360,8 +360,15 @@ veil_status veil_shard_unpack_tiles(veil_render* r, const veil_shard* shard, con
 
 veil_status veil_render_device(const veil_scene* scene, const veil_render_params* params,
                                const veil_shard* shard) {
+  return veil_render_device_timed(scene, params, shard, nullptr, nullptr);
+}
+
+veil_status veil_render_device_timed(const veil_scene* scene, const veil_render_params* params,
+                                     const veil_shard* shard, void* start_event, void* end_event) {
   if (!scene) return bad_arg("scene is required");
   veil::RenderOptions o = options_from(params);
+  o.ev_start = start_event;
+  o.ev_end = end_event;
   o.host_readback = false;
   if (o.params.flags & VEIL_RENDER_REFERENCE) return bad_arg("device frames use the pipeline");
   if (shard) {

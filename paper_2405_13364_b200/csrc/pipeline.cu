@@ -2884,12 +2884,16 @@ __global__ void __launch_bounds__(128, kFuse ? 6 : 7) k_extract(Buffers B, int p
   extern __shared__ __align__(16) uint8_t smem_raw[];
   __shared__ ItemState st;
   __shared__ uint32_t item_s;
+  if (B.ctr->error) return;
+  const uint32_t nitems = kGlobal ? B.ctr->spill_count[pass] : B.ctr->list_count[pass] * 4u;
+  // (the global-scratch and high passes are usually empty: leave before the
+  // work counter, whose atomics every CTA would otherwise serialize on)
+  if (nitems == 0) return;
   if (kFuse) {  // the generic shading path's unpack and axis-light tables
     load_shared_luts();
     fill_axis_light(fc);
     __syncthreads();
   }
-  if (B.ctr->error) return;
   RasterView V;
   V.cs = nullptr;
   V.tp = nullptr;
@@ -2916,7 +2920,6 @@ __global__ void __launch_bounds__(128, kFuse ? 6 : 7) k_extract(Buffers B, int p
     V.refs = sh->refs;
     V.rows = reinterpret_cast<uint32_t*>(sh->refs);  // refs are unused until phase B
   }
-  const uint32_t nitems = kGlobal ? B.ctr->spill_count[pass] : B.ctr->list_count[pass] * 4u;
   unsigned int* counter = &B.ctr->work_next[pass * 2 + (kGlobal ? 1 : 0)];
   for (;;) {
     if (threadIdx.x == 0) item_s = atomicAdd(counter, 1u);
@@ -3001,6 +3004,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 template <int KM, int kMode, bool kTex>
 __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
   const FrameConst& fc = c_fc;
+  // (an empty segment queue: nothing to shade, skip the table set-up)
+  if (kMode == 1 && (B.ctr->error || B.ctr->seg_count == 0)) return;
   load_shared_luts();
   fill_axis_light(fc);
   __syncthreads();
@@ -4535,15 +4540,18 @@ static void render_frame_on(DeviceScene* d, const Scene& s, const RenderOptions&
         d->graph_launches = n;
       }
       *d->fc_host = P.fc;
+      if (opt.ev_start) ck(cudaEventRecord(static_cast<cudaEvent_t>(opt.ev_start), d->stream), "event");
       ck(cudaGraphLaunch(d->graph_exec, d->stream), "cudaGraphLaunch");
       launches = d->graph_launches;
     } else {
+      if (opt.ev_start) ck(cudaEventRecord(static_cast<cudaEvent_t>(opt.ev_start), d->stream), "event");
       launches = enqueue_front(d, P);
       enqueue_raster(d, P, &launches);
       ck(cudaMemcpyAsync(d->ctr_host, P.B.ctr, sizeof(dev::Counters), cudaMemcpyDeviceToHost,
                          d->stream),
          "counters");
     }
+    if (opt.ev_end) ck(cudaEventRecord(static_cast<cudaEvent_t>(opt.ev_end), d->stream), "event");
     ck(cudaStreamSynchronize(d->stream), "frame");
     const dev::Counters c = *d->ctr_host;
     // Grow-on-demand buffers (first frames of a scene only): the device

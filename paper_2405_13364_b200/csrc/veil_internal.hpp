@@ -104,6 +104,8 @@ struct RenderOptions {
   bool dump = false;          // capture parity arrays
   bool host_readback = true;  // copy framebuffer + mask to the host
   bool keep_records = false;  // store every triangle record even in the fused raster
+  void* ev_start = nullptr;   // caller's cudaEvent_t pair around the frame's device work
+  void* ev_end = nullptr;
 };
 
 struct DumpArray {

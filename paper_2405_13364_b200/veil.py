@@ -92,6 +92,7 @@ def lib():
         "veil_shard_pack_tiles_device": ([_P, C.POINTER(Shard), _P, C.c_uint64], C.c_int),
         "veil_shard_unpack_tiles_device": ([_P, C.POINTER(Shard), _P, C.c_uint64], C.c_int),
         "veil_render_device": ([_P, C.POINTER(RenderParams), C.POINTER(Shard)], C.c_int),
+        "veil_render_device_timed": ([_P, C.POINTER(RenderParams), C.POINTER(Shard), _P, _P], C.c_int),
         "veil_device_framebuffer": ([_P, _PP, _PP], C.c_int),
         "veil_export_framebuffer": ([_P, C.POINTER(IpcFramebuffer)], C.c_int),
         "veil_import_peer_framebuffer": ([_P, C.POINTER(IpcFramebuffer)], C.c_int),
@@ -311,13 +312,18 @@ def render_dump(scene: Scene, params=None, names=None):
     return Render(r.value).dumps(names)
 
 
-def render_device(scene: Scene, params=None, shard=None, stats=True):
+def render_device(scene: Scene, params=None, shard=None, stats=True, events=None):
     """One frame into device memory only (bench path); returns FrameStats
     (or None with stats=False, so a caller can close its timed region first
-    and read scene.last_stats() afterwards)."""
+    and read scene.last_stats() afterwards). events = (start, end) raw
+    cudaEvent_t handles (int or None) the library records on the scene's
+    stream right before and after the frame's device work."""
     params = params or default_params()
     sh = None if shard is None else C.byref(Shard(*shard))
-    _check(lib().veil_render_device(scene.h, C.byref(params), sh))
+    if events is None:
+        _check(lib().veil_render_device(scene.h, C.byref(params), sh))
+    else:
+        _check(lib().veil_render_device_timed(scene.h, C.byref(params), sh, events[0], events[1]))
     return scene.last_stats() if stats else None
 
 

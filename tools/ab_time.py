@@ -9,8 +9,12 @@ sys.path.insert(0, os.environ["ROOT"])
 from paper_2405_13364_b200 import veil
 out = {}
 for name in os.environ.get("AB_WORKLOADS", "stack64k,tiny4m").split(","):
-    seed = {"stack64k": 2, "tiny4m": 4, "mixed16m": 5}[name]
-    sc = veil.Scene.workload(name, seed)
+    if name == "boxes1080":  # C3's scene (one orbit camera: the arrays' own)
+        sys.path.insert(0, os.path.join(os.environ["ROOT"], "tests"))
+        from common import boxes_arrays
+        sc = veil.Scene.from_arrays(boxes_arrays(1920, 1080))
+    else:
+        sc = veil.Scene.workload(name, {"stack64k": 2, "tiny4m": 4, "mixed16m": 5}[name])
     for i in range(5): veil.render_device(sc)
     st = [veil.render_device(sc) for i in range(20)]
     med = lambda f: statistics.median(f(s) for s in st)
