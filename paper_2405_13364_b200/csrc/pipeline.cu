@@ -113,6 +113,7 @@ struct FrameConst {
   int write_tri;
   int fused_read;  // experiment: the fused raster reads stored records (VEIL_FUSED_READ=1)
   int bulk_stage;  // k_shade stages THB lists with cp.async.bulk (VEIL_BULK_STAGE=0/1)
+  int fill_split;  // empty bins painted by k_fill_empty, not k_shade (VEIL_FILL_SPLIT=0/1)
   // zero-copy readback: the frame's pinned host RGBA8 / mask (device-mapped),
   // written by the shading kernels next to the device framebuffer; null when
   // the caller does not want host pixels
@@ -3237,11 +3238,11 @@ __global__ void __launch_bounds__(1024) k_order_bins(Buffers B) {
   };
   // bins with no wave-walk work (every half-block queued for the segment
   // kernel) and bins another rank owns are left out; empty bins stay (their
-  // half-blocks get the background)
+  // half-blocks get the background) unless k_fill_empty paints them
   auto wanted = [&](int b) {
     const int bxi = b % fc.bins_x, byi = b / fc.bins_x;
     if (fc.world > 1 && ((bxi + 3 * byi) % fc.world) != fc.rank) return false;
-    return B.cat[b] == 0 || (B.bin_cost[b] & 0x80000000u) != 0u;
+    return (B.cat[b] == 0 && !fc.fill_split) || (B.bin_cost[b] & 0x80000000u) != 0u;
   };
   for (int b = threadIdx.x; b < fc.nbins; b += blockDim.x)
     if (wanted(b)) atomicAdd(&hist[bucket(B.bin_cost[b] & 0x7fffffffu)], 1u);
@@ -3295,8 +3296,10 @@ __global__ void __launch_bounds__(256) k_finalize(Buffers B) {
   }
 }
 
-// Fused raster frames have no k_shade, whose mode 0 writes the background of
-// empty bins: this does, for the bins this rank owns (a CTA per bin).
+// The background of the empty bins this rank owns (a CTA per bin): for fused
+// raster frames (no k_shade) and, by default, for all frames -- eight 256-thread
+// CTAs per SM paint them faster than k_shade's bin loop (two CTAs per SM,
+// three block barriers per bin).
 __global__ void __launch_bounds__(256) k_fill_empty(Buffers B) {
   const FrameConst& fc = c_fc;
   if (B.ctr->error) return;
@@ -3963,6 +3966,8 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   if (const char* w1 = std::getenv("VEIL_WAVE1")) fc.wave1 = std::atoi(w1);
   fc.bulk_stage = 1;  // measured: C2 shade -0.3%, C4 shade -1.1% against the lane loop
   if (const char* bs = std::getenv("VEIL_BULK_STAGE")) fc.bulk_stage = std::atoi(bs);
+  fc.fill_split = 1;
+  if (const char* fs = std::getenv("VEIL_FILL_SPLIT")) fc.fill_split = std::atoi(fs);
 
   const uint32_t Q = d->nquads;
   const size_t nb = size_t(fc.nbins);
@@ -4420,6 +4425,10 @@ static void enqueue_raster(DeviceScene* d, Prepared& P, int* launches) {
     dev::k_fill_empty<<<std::min(P.fc.nbins, d->sm_count * 8), 256, 0, d->stream>>>(P.B);
     ++*launches;
   } else {
+    if (P.fc.fill_split) {
+      dev::k_fill_empty<<<std::min(P.fc.nbins, d->sm_count * 8), 256, 0, d->stream>>>(P.B);
+      ++*launches;
+    }
     dev::k_order_bins<<<1, 1024, 0, d->stream>>>(P.B);
     ++*launches;
     launch_shade(d, P.fc, P.B, launches);
