@@ -1958,10 +1958,14 @@ struct PixelOut {
 };
 
 // Blend one popped sample into the pixel state (shade_half_block,
-// raster.cpp:248-255).
+// raster.cpp:248-255). kDump: 0 = test c_fc.dump, 1 = no dump, 2 = dump frame
+// (the compiler turns the run-time test into a select, so hot callers that
+// know the frame kind drop the hash's instructions entirely).
+template <int kDump = 0>
 __device__ __forceinline__ void commit(PixelOut& o, uint64_t pk, float4 pc, bool ooo) {
   o.acc = blend(o.acc, pc);
-  if (c_fc.dump) o.hash = (o.hash ^ pk) * kHashPrime;  // blend-order evidence (parity dumps)
+  if (kDump == 2 || (kDump == 0 && c_fc.dump))
+    o.hash = (o.hash ^ pk) * kHashPrime;  // blend-order evidence (parity dumps)
   ++o.emitted;
   if (ooo) o.invalid = true;
 }
@@ -2206,7 +2210,7 @@ __device__ __forceinline__ void shade_waves(const FrameConst& fc, const Buffers&
 // are shaded by straight-line code (shade_staged_bf) so the scheduler can
 // overlap the two dependency chains, then pushed in wave order -- each pixel
 // still receives its samples in the reference's sequence.
-template <int KM, typename Filter>
+template <int KM, int kDump, typename Filter>
 __device__ __forceinline__ void shade_waves_staged2(const FrameConst& fc, int px0, int py0,
                                                     const uint32_t* tri_l, const uint32_t* mask_l,
                                                     const uint16_t* slot_l, const StagedTri* staged,
@@ -2244,15 +2248,17 @@ __device__ __forceinline__ void shade_waves_staged2(const FrameConst& fc, int px
     uint64_t pk;
     float4 pc;
     bool ooo;
-    if (ra != kNone && f.push(fc.df, sample_key(fc, qa, tri_l[ia]), ca, &pk, &pc, &ooo)) commit(o, pk, pc, ooo);
-    if (rb != kNone && f.push(fc.df, sample_key(fc, qb, tri_l[ib]), cb, &pk, &pc, &ooo)) commit(o, pk, pc, ooo);
+    if (ra != kNone && f.push(fc.df, sample_key(fc, qa, tri_l[ia]), ca, &pk, &pc, &ooo))
+      commit<kDump>(o, pk, pc, ooo);
+    if (rb != kNone && f.push(fc.df, sample_key(fc, qb, tri_l[ib]), cb, &pk, &pc, &ooo))
+      commit<kDump>(o, pk, pc, ooo);
   }
   while (f.n > 0) {
     uint64_t pk;
     float4 pc;
     bool ooo;
     f.pop(&pk, &pc, &ooo);
-    commit(o, pk, pc, ooo);
+    commit<kDump>(o, pk, pc, ooo);
   }
 }
 
@@ -3187,8 +3193,12 @@ __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
           SlotFilter<KM> f;
           f.reset(reinterpret_cast<float4*>(shade_dyn + (size_t)kStageTris * sizeof(StagedTri)) +
                   (size_t)warp * KM * 32 + lane);
-          if (staged_ok && d.cnt <= (uint32_t)kShadeStage && !fc.wave1)  // all operands in shared memory
-            shade_waves_staged2<KM>(fc, hpx0, hpy0, tri_l, mask_l, slot_l, row_tris, d.cnt, po, f);
+          if (staged_ok && d.cnt <= (uint32_t)kShadeStage && !fc.wave1) {  // all operands in shared memory
+            if (fc.dump)
+              shade_waves_staged2<KM, 2>(fc, hpx0, hpy0, tri_l, mask_l, slot_l, row_tris, d.cnt, po, f);
+            else
+              shade_waves_staged2<KM, 1>(fc, hpx0, hpy0, tri_l, mask_l, slot_l, row_tris, d.cnt, po, f);
+          }
           else if (staged_ok && d.cnt <= (uint32_t)kShadeStage)
             shade_waves<KM, kTex>(fc, B, hpx0, hpy0, tri_l, mask_l, slot_l, row_tris, d.cnt, po, f);
           else
