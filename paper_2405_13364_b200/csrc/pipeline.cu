@@ -1939,9 +1939,20 @@ struct ItemState {
   uint32_t warp_n[4];
   uint32_t pool_base;
   int alloc_ok;
-  uint32_t ncand;
-  uint32_t gnext;  // next candidate group of the row-span pass
+  // candidate count / next row-span group, per phase-A round parity: round
+  // r + 1's pair is reset during round r (no barrier of its own)
+  uint32_t ncand[2];
+  uint32_t gnext[2];
 };
+
+// ItemState before an item (k_extract's thread 0, ahead of the barrier that
+// publishes the item).
+__device__ __forceinline__ void reset_item_state(ItemState* st) {
+  st->ntbr = 0;
+  st->status = 0;
+  st->err_code = 0x7fffffff;
+  st->ncand[0] = st->gnext[0] = 0;
+}
 
 enum { kPassLow = 0, kPassHigh = 1 };
 
@@ -2423,13 +2434,7 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
   const int px_last = min(px0 + kBin - 1, fc.width - 1);
   const int py_last = min(py0 + kBin - 1, fc.height - 1);
   const int ry0 = py0 + row * 8, ry1 = min(ry0 + 7, py_last);
-
-  if (threadIdx.x == 0) {
-    st->ntbr = 0;
-    st->status = 0;
-    st->err_code = 0x7fffffff;
-  }
-  __syncthreads();
+  // (st was reset by k_extract before the barrier that published the item)
 
   // ---- phase A: tri-block-rows of this block-row (raster.cpp:41-98).
   // Candidates (valid triangles whose y range meets the block-row) are first
@@ -2441,10 +2446,9 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
   // rounds over bin items (a small quad's item holds its 2 triangles), sized
   // so that a round's candidates fit the candidate buffer
   const uint32_t nitem = nq + nt, round_items = cand_cap / 2u;
-  for (uint32_t round = 0; round < nitem; round += round_items) {
+  uint32_t par = 0;  // round parity: this round's ncand / gnext
+  for (uint32_t round = 0; round < nitem; round += round_items, par ^= 1u) {
     const uint32_t end = min(nitem, round + round_items);
-    if (threadIdx.x == 0) st->ncand = 0, st->gnext = 0;
-    __syncthreads();
     for (uint32_t j0 = round; j0 < end; j0 += blockDim.x) {
       const uint32_t j = j0 + threadIdx.x;
       uint32_t rows = 0, it = 0;
@@ -2458,7 +2462,7 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
       const unsigned m0 = __ballot_sync(0xffffffffu, rows & 1u);
       const unsigned m1 = __ballot_sync(0xffffffffu, (rows >> 1) & 1u);
       uint32_t wbase = 0;
-      if (lane == 0 && (m0 | m1)) wbase = atomicAdd(&st->ncand, (uint32_t)(__popc(m0) + __popc(m1)));
+      if (lane == 0 && (m0 | m1)) wbase = atomicAdd(&st->ncand[par], (uint32_t)(__popc(m0) + __popc(m1)));
       wbase = __shfl_sync(0xffffffffu, wbase, 0);
       const unsigned below = (1u << lane) - 1u;
       if (rows & 1u) {
@@ -2472,7 +2476,9 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
         cand[wbase + __popc(m0) + __popc(m1 & below)] = ((uint64_t)(2 * j + 1) << 32) | (it * 2 + 1);
     }
     __syncthreads();
-    const uint32_t nc = st->ncand;
+    const uint32_t nc = st->ncand[par];
+    // every thread is past the previous round (which used the other pair)
+    if (threadIdx.x == 0) st->ncand[par ^ 1u] = st->gnext[par ^ 1u] = 0;
     // Row spans, load-balanced per warp: a warp takes 32 candidates, scans
     // their row counts and spreads the (candidate, row) pairs over its lanes,
     // so tall and short triangles keep all lanes busy; each candidate's lane
@@ -2485,7 +2491,7 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
     const uint32_t G = nc < 32u ? max(8u, ((nc + 3u) / 4u + 7u) & ~7u) : 32u;
     for (;;) {
       uint32_t g = 0;
-      if (lane == 0) g = atomicAdd(&st->gnext, G);
+      if (lane == 0) g = atomicAdd(&st->gnext[par], G);
       g = __shfl_sync(0xffffffffu, g, 0);
       if (g >= nc) break;
       const uint32_t j = g + lane;
@@ -2890,8 +2896,8 @@ __global__ void __launch_bounds__(128, kFuse ? 6 : 7) k_extract(Buffers B, int p
   const FrameConst& fc = c_fc;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   __shared__ ItemState st;
-  __shared__ uint32_t item_s;
   if (B.ctr->error) return;
+  __shared__ uint32_t item_next[2];  // by iteration parity (one barrier per item fetch)
   const uint32_t nitems = kGlobal ? B.ctr->spill_count[pass] : B.ctr->list_count[pass] * 4u;
   // (the global-scratch and high passes are usually empty: leave before the
   // work counter, whose atomics every CTA would otherwise serialize on)
@@ -2928,40 +2934,61 @@ __global__ void __launch_bounds__(128, kFuse ? 6 : 7) k_extract(Buffers B, int p
     V.rows = reinterpret_cast<uint32_t*>(sh->refs);  // refs are unused until phase B
   }
   unsigned int* counter = &B.ctr->work_next[pass * 2 + (kGlobal ? 1 : 0)];
-  for (;;) {
-    if (threadIdx.x == 0) item_s = atomicAdd(counter, 1u);
-    __syncthreads();
-    const uint32_t item = item_s;
-    __syncthreads();
-    if (item >= nitems) break;
-    const uint32_t code = kGlobal ? B.spill[pass][item] : (B.bin_list[pass][item >> 2] << 2) | (item & 3u);
-    const int bin = (int)(code >> 2), row = (int)(code & 3u);
-    const int bxi = bin % fc.bins_x, byi = bin / fc.bins_x;
-    const uint8_t cat = B.cat[bin];
-    const bool owned = fc.world <= 1 || ((bxi + 3 * byi) % fc.world) == fc.rank;
-    if (!owned || cat == 0) continue;
-    bool run;
-    if (pass == kPassLow)
-      run = cat == 1 && !fc.force_high;
-    else
-      run = cat == 2 || (cat == 1 && fc.force_high) || B.prop[bin];
-    if (!run) continue;
-    if (!kGlobal && pass == kPassLow && B.prop[bin]) continue;  // sibling already overflowed
-    extract_item<kGlobal, kFuse>(fc, B, pass, bin, row, V, &st, cap_tbr, cap_tb);
-    __syncthreads();
-    if (threadIdx.x == 0 && st.status) {
-      if (st.status == 1) {  // soft overflow: the whole bin goes to the high pass
-        B.prop[bin] = 1;
-        if (atomicAdd(&B.prop_q[bin], 1u) == 0u)
-          B.bin_list[1][checked_index(atomicAdd(&B.ctr->list_count[1], 1u), (uint32_t)fc.nbins)] = (uint32_t)bin;
-      } else if (st.status == 2) {
-        const uint32_t s = atomicAdd(&B.ctr->spill_count[pass], 1u);
-        B.spill[pass][s] = code;
-      } else {
-        atomicMax(&B.ctr->bin_error, ~((unsigned long long)bin * 64ull +
-                                         (unsigned long long)min(st.err_code, 63)));
+  // Thread 0 takes the next item, decides whether this pass extracts it and
+  // resets the item state, all before the one barrier that publishes them
+  // (so the decision is uniform even while a sibling block-row of the same
+  // bin flips B.prop). The published words are double-buffered by iteration
+  // parity: the write for iteration k+1 cannot race the reads of k.
+  auto fetch = [&](uint32_t slot) {
+    const uint32_t item = atomicAdd(counter, 1u);
+    uint32_t code = 0xffffffffu;
+    if (item < nitems) {
+      const uint32_t c = kGlobal ? B.spill[pass][item] : (B.bin_list[pass][item >> 2] << 2) | (item & 3u);
+      const int bin = (int)(c >> 2);
+      const int bxi = bin % fc.bins_x, byi = bin / fc.bins_x;
+      const uint8_t cat = B.cat[bin];
+      const bool owned = fc.world <= 1 || ((bxi + 3 * byi) % fc.world) == fc.rank;
+      bool run = owned && cat != 0;
+      if (run) {
+        if (pass == kPassLow)
+          run = cat == 1 && !fc.force_high && !(!kGlobal && B.prop[bin]);  // sibling already overflowed
+        else
+          run = cat == 2 || (cat == 1 && fc.force_high) || B.prop[bin];
       }
+      code = run ? c : 0xfffffffeu;  // 0xfffffffe: skip this item
     }
+    item_next[slot] = code;
+    reset_item_state(&st);
+  };
+  if (threadIdx.x == 0) fetch(0);
+  __syncthreads();
+  for (uint32_t k = 0;; k ^= 1u) {
+    const uint32_t code = item_next[k];
+    if (code == 0xffffffffu) break;
+    const bool run = code != 0xfffffffeu;
+    const int bin = (int)(code >> 2), row = (int)(code & 3u);
+    if (run) {
+      extract_item<kGlobal, kFuse>(fc, B, pass, bin, row, V, &st, cap_tbr, cap_tb);
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      if (run && st.status) {
+        if (st.status == 1) {  // soft overflow: the whole bin goes to the high pass
+          B.prop[bin] = 1;
+          if (atomicAdd(&B.prop_q[bin], 1u) == 0u)
+            B.bin_list[1][checked_index(atomicAdd(&B.ctr->list_count[1], 1u), (uint32_t)fc.nbins)] =
+                (uint32_t)bin;
+        } else if (st.status == 2) {
+          const uint32_t sl = atomicAdd(&B.ctr->spill_count[pass], 1u);
+          B.spill[pass][sl] = code;
+        } else {
+          atomicMax(&B.ctr->bin_error, ~((unsigned long long)bin * 64ull +
+                                           (unsigned long long)min(st.err_code, 63)));
+        }
+      }
+      fetch(k ^ 1u);
+    }
+    __syncthreads();
   }
 }
 
