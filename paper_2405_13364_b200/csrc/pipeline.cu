@@ -2684,8 +2684,14 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
       if (dz.a == 0.0 && dz.b == 0.0) {
         qd = quantize_depth(dz.c);  // flat plane: (±0 + ±0) + c quantizes like c at any centroid
       } else {
-        const double cx = __dadd_rn(__dadd_rn(bpx0, __ddiv_rn((double)sx, (double)count)), 0.5);
-        const double cy = __dadd_rn(__dadd_rn(bpy0, __ddiv_rn((double)sy, (double)count)), 0.5);
+        // (a zero sum -- the TBR's pixels all in the block's first column /
+        // row, common for tiny triangles -- divides to +0 exactly; testing it
+        // keeps those lanes off the division's out-of-line slow path, which a
+        // zero dividend takes)
+        const double mx = sx ? __ddiv_rn((double)sx, (double)count) : 0.0;
+        const double my = sy ? __ddiv_rn((double)sy, (double)count) : 0.0;
+        const double cx = __dadd_rn(__dadd_rn(bpx0, mx), 0.5);
+        const double cy = __dadd_rn(__dadd_rn(bpy0, my), 0.5);
         qd = quantize_depth(eval(dz, cx, cy));
       }
     }
