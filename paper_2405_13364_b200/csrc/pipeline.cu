@@ -143,12 +143,13 @@ struct Counters {
   unsigned long long samples, fragments, thb, segments, invalid;
   unsigned long long bins_empty, bins_low, bins_high, bins_propagated;
   unsigned long long pool_pair;  // THB pool entries allocated
+  unsigned long long walk_cost;  // sum of the bins' wave-walk costs (k_order_bins' split share)
   unsigned int shade_next[2];
   unsigned int seg_count;  // half-blocks queued for the segment-routing kernel
   unsigned int large_pairs;  // (large triangle, bin row) work pairs
   unsigned int setup_ticket;  // k_setup: block order for the decoupled look-back
   unsigned int list_count[2];  // owned bins to extract in the low / high pass
-  unsigned int order_count;    // bins in k_shade's (mode 0/2) order list
+  unsigned int order_count;    // (bin, part) entries in k_shade's (mode 0/2) order list
   unsigned int shard_tri_count;  // sharded frames: triangles this rank sets up (k_shard_tris)
 };
 
@@ -209,7 +210,7 @@ struct Buffers {
   uint32_t lpair_cols_cap;  // words
   uint32_t* prop_q;       // per bin: already appended to the high-pass list
   uint32_t* bin_cost;     // per bin: wave-walk shading cost (samples + 4 per THB)
-  uint32_t* bin_order;    // bins in descending cost: k_shade's bin order
+  uint32_t* bin_order;    // (bin | part << 24 | log2(parts) << 28) in descending cost: k_shade's order
   // raster
   unsigned long long* slots;  // per (bin, row): samples, frags, thb, segments, invalid
   uint32_t* spill[2];
@@ -2834,7 +2835,10 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
     const uint32_t both = cost + __shfl_down_sync(0x3u, cost, 1);  // the block's two halves
     const unsigned walks = __ballot_sync(0x3u, !seg);
     // bit 31: the bin has half-blocks for k_shade's wave walk (or background)
-    if (!kFuse && lane == 0 && (both || walks)) atomicAdd(&B.bin_cost[bin], both);
+    if (!kFuse && lane == 0 && (both || walks)) {
+      atomicAdd(&B.bin_cost[bin], both);
+      if (both) atomicAdd(&B.ctr->walk_cost, (unsigned long long)both);
+    }
     if (!kFuse && lane == 0 && walks) atomicOr(&B.bin_cost[bin], 0x80000000u);
     // low-pass entries of a bin that later propagates are stale (k_shade_seg skips them)
     if (seg && !kFuse)
@@ -3064,9 +3068,10 @@ __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
   uint32_t bar_phase = 0;
   if (fc.bulk_stage && lane == 0) mbar_init(&stage_bar[warp]);
   __syncwarp();
-  __shared__ int hb_next;
-  __shared__ uint8_t hb_order[32];  // the bin's half-blocks, most samples first
-  // modes 0/2: CTA items = bins, warps pull the bin's 32 half-blocks;
+  __shared__ int hb_next, hb_count;
+  __shared__ uint8_t hb_order[32];  // the item's half-blocks, most samples first
+  // modes 0/2: CTA items = (bin, part) from k_order_bins, warps pull the
+  // part's half-blocks (every parts-th of the bin's longest-first order);
   // mode 1: warp items from the queue mode 0 filled
   const uint32_t nitems = kMode == 1 ? B.ctr->seg_count : B.ctr->order_count;
   uint32_t cta_bin = 0xffffffffu;
@@ -3092,6 +3097,7 @@ __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
       if (cta_bin != 0xffffffffu) {
         if (lane == 0) hbi = atomicAdd(&hb_next, 1);
         hbi = __shfl_sync(0xffffffffu, hbi, 0);
+        if (hbi >= hb_count) hbi = 32;
       }
       if (hbi >= 32) {
         __syncthreads();  // everyone is done with the staged bin
@@ -3100,8 +3106,9 @@ __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
           hb_next = 0;
         }
         __syncthreads();
-        cta_bin = item_s < nitems ? B.bin_order[item_s] : 0xffffffffu;
-        if (cta_bin == 0xffffffffu) break;
+        const uint32_t entry = item_s < nitems ? B.bin_order[item_s] : 0xffffffffu;
+        if (entry == 0xffffffffu) break;
+        cta_bin = entry & 0xffffffu;
         const int bxi = (int)cta_bin % fc.bins_x, byi = (int)cta_bin / fc.bins_x;
         const bool owned = fc.world <= 1 || ((bxi + 3 * byi) % fc.world) == fc.rank;
         staged_ok = false;
@@ -3134,7 +3141,11 @@ __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
               const uint32_t hi = max(key, other), lo = min(key, other);
               key = (desc == lower) ? hi : lo;
             }
-          hb_order[lane] = (uint8_t)(31u - (key & 31u));
+          // this part's share: every parts-th entry of the order (the
+          // whole order when the bin is one item)
+          const uint32_t lp = entry >> 28, part = (entry >> 24) & 7u;
+          if ((lane & ((1 << lp) - 1)) == (int)part) hb_order[lane >> lp] = (uint8_t)(31u - (key & 31u));
+          if (lane == 0) hb_count = 32 >> lp;
         }
         __syncthreads();
         if (!owned) {
@@ -3143,7 +3154,7 @@ __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
         }
         if (lane == 0) hbi = atomicAdd(&hb_next, 1);
         hbi = __shfl_sync(0xffffffffu, hbi, 0);
-        if (hbi >= 32) continue;
+        if (hbi >= hb_count) continue;
       }
       item = cta_bin * 32u + (uint32_t)hb_order[hbi];
     }
@@ -3266,7 +3277,7 @@ __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
 // Longest-first bin order for k_shade (bins with the most wave-walk work
 // first, so the kernel's tail is made of short bins): a 256-bucket
 // log-scale counting sort of the per-bin costs k_extract accumulated.
-__global__ void __launch_bounds__(1024) k_order_bins(Buffers B) {
+__global__ void __launch_bounds__(1024) k_order_bins(Buffers B, uint32_t shade_ctas) {
   const FrameConst& fc = c_fc;
   __shared__ uint32_t hist[256];
   __shared__ uint32_t base[256];
@@ -3287,8 +3298,21 @@ __global__ void __launch_bounds__(1024) k_order_bins(Buffers B) {
     if (fc.world > 1 && ((bxi + 3 * byi) % fc.world) != fc.rank) return false;
     return (B.cat[b] == 0 && !fc.fill_split) || (B.bin_cost[b] & 0x80000000u) != 0u;
   };
+  // A bin costing more than the frame's fair share per shading CTA (a
+  // sharded rank has few bins: its heaviest ones would bound k_shade) is
+  // split into 2..8 parts, each a CTA item taking every parts-th half-block.
+  // (The frame's total is the sum k_extract accumulated next to the bin costs.)
+  const unsigned long long share = max(1ull, B.ctr->walk_cost / max(1u, shade_ctas));
+  auto log_parts = [&](uint32_t c) -> uint32_t {
+    uint32_t lp = 0;
+    while (lp < 3u && (unsigned long long)c > (share << lp)) ++lp;
+    return lp;
+  };
   for (int b = threadIdx.x; b < fc.nbins; b += blockDim.x)
-    if (wanted(b)) atomicAdd(&hist[bucket(B.bin_cost[b] & 0x7fffffffu)], 1u);
+    if (wanted(b)) {
+      const uint32_t c = B.bin_cost[b] & 0x7fffffffu, lp = log_parts(c);
+      atomicAdd(&hist[bucket(c >> lp)], 1u << lp);
+    }
   __syncthreads();
   if (threadIdx.x < 32) {  // exclusive scan of 256 buckets by one warp
     uint32_t run = 0;
@@ -3307,7 +3331,11 @@ __global__ void __launch_bounds__(1024) k_order_bins(Buffers B) {
   }
   __syncthreads();
   for (int b = threadIdx.x; b < fc.nbins; b += blockDim.x)
-    if (wanted(b)) B.bin_order[atomicAdd(&base[bucket(B.bin_cost[b] & 0x7fffffffu)], 1u)] = (uint32_t)b;
+    if (wanted(b)) {
+      const uint32_t c = B.bin_cost[b] & 0x7fffffffu, lp = log_parts(c);
+      const uint32_t at = atomicAdd(&base[bucket(c >> lp)], 1u << lp);
+      for (uint32_t p = 0; p < (1u << lp); ++p) B.bin_order[at + p] = (uint32_t)b | (p << 24) | (lp << 28);
+    }
 }
 
 __global__ void __launch_bounds__(256) k_finalize(Buffers B) {
@@ -4061,7 +4089,7 @@ Prepared prepare(DeviceScene* d, const Scene& s, const RenderOptions& opt) {
   d->bin_list1.ensure(nb * 4);
   d->prop_q.ensure(nb * 4);
   d->bin_cost.ensure(nb * 4);
-  d->bin_order.ensure(nb * 4);
+  d->bin_order.ensure(nb * 4 * 8);  // up to 8 parts per bin
   d->prop.ensure(nb);
   d->slots.ensure(nb * 4 * 5 * 8);
   d->spill0.ensure(nb * 4 * 4);
@@ -4472,7 +4500,8 @@ static void enqueue_raster(DeviceScene* d, Prepared& P, int* launches) {
       dev::k_fill_empty<<<std::min(P.fc.nbins, d->sm_count * 8), 256, 0, d->stream>>>(P.B);
       ++*launches;
     }
-    dev::k_order_bins<<<1, 1024, 0, d->stream>>>(P.B);
+    // (the split threshold uses mode 0's usual 2 CTAs per SM)
+    dev::k_order_bins<<<1, 1024, 0, d->stream>>>(P.B, uint32_t(2 * d->sm_count));
     ++*launches;
     launch_shade(d, P.fc, P.B, launches);
   }
