@@ -903,12 +903,30 @@ __global__ void __launch_bounds__(256) k_bin_pass(Buffers B) {
         atomicAdd(&n_large, 1u);
         if (y_lo > y_hi) continue;
         const uint32_t r0 = (uint32_t)y_lo / kBin, nr = (uint32_t)y_hi / kBin - r0 + 1u;
-        const uint32_t at = atomicAdd(&B.ctr->large_pairs, nr);
-        if ((unsigned long long)at + nr > fc.lpairs_cap) {
+        // a sharded rank keeps the bin rows where the quad's bin columns meet
+        // an owned bin (owner (bx + 3 by) mod G: the first owned column of
+        // row R is x0 + ((rank - 3R - x0) mod G))
+        uint32_t rows_mask = 0xffffffffu;  // (bit r: row r0 + r kept; rows >= 32 always kept)
+        uint32_t nkeep = nr;
+        if (fc.world > 1 && box.x >> 16 < (box.x & 0xffffu) + (uint32_t)fc.world - 1u) {
+          const int G = fc.world, bx0 = (int)(box.x & 0xffffu), bx1 = (int)(box.x >> 16);
+          nkeep = 0;
+          for (uint32_t r = 0; r < nr; ++r) {
+            const int R = (int)(r0 + r);
+            const int first = bx0 + ((((fc.rank - 3 * R - bx0) % G) + G) % G);
+            const bool keep = r >= 32u || first <= bx1;
+            if (r < 32u && !keep) rows_mask &= ~(1u << r);
+            nkeep += keep ? 1u : 0u;
+          }
+        }
+        if (!nkeep) continue;
+        const uint32_t at = atomicAdd(&B.ctr->large_pairs, nkeep);
+        if ((unsigned long long)at + nkeep > fc.lpairs_cap) {
           atomicOr(&B.ctr->error, 16u);  // pair list capacity: grow and re-run
           continue;
         }
-        for (uint32_t r = 0; r < nr; ++r) B.lpairs[at + r] = make_uint2(ti, r0 + r);
+        for (uint32_t r = 0, k = 0; r < nr; ++r)
+          if (r >= 32u || ((rows_mask >> r) & 1u)) B.lpairs[at + k++] = make_uint2(ti, r0 + r);
       }
     }
     for (uint32_t k = 0; k < 4; ++k) {
