@@ -1424,10 +1424,25 @@ struct MemFilter {
   }
 };
 
+// Paired FP32 multiplies (sm_100's FMUL2: two IEEE round-to-nearest products
+// per instruction, each exactly __fmul_rn), so the colour channels' products
+// cost half the issue slots with bit-identical results. The sums stay scalar
+// __fadd_rn: a paired add (the __fadd2_rn intrinsic, or add.rn.f32x2 in inline
+// PTX) was contracted with its product into FFMA2 -- one rounding instead of
+// two -- which moved pixels by one step.
+__device__ __forceinline__ float2 lo2(float4 v) { return make_float2(v.x, v.y); }
+__device__ __forceinline__ float2 hi2(float4 v) { return make_float2(v.z, v.w); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  return make_float2(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y));
+}
+__device__ __forceinline__ float4 cat4(float2 a, float2 b) { return make_float4(a.x, a.y, b.x, b.y); }
+
 __device__ __forceinline__ float4 blend(float4 acc, float4 s) {
-  float t = __fsub_rn(1.0f, acc.w);
-  return make_float4(__fadd_rn(acc.x, __fmul_rn(t, s.x)), __fadd_rn(acc.y, __fmul_rn(t, s.y)),
-                     __fadd_rn(acc.z, __fmul_rn(t, s.z)), __fadd_rn(acc.w, __fmul_rn(t, s.w)));
+  // acc + (1 - acc.w) * s per channel (shade_half_block's blend)
+  const float t = __fsub_rn(1.0f, acc.w);
+  const float2 tt = make_float2(t, t);
+  return cat4(add2(lo2(acc), mul2(tt, lo2(s))), add2(hi2(acc), mul2(tt, hi2(s))));
 }
 
 // normalize + Lambert (shade_sample, shading.cpp:123-136): the light factor.
@@ -1453,11 +1468,12 @@ __device__ __forceinline__ float light_factor(const FrameConst& fc, float n[3]) 
 __device__ __forceinline__ float4 premultiply(float4 color, float4 mat, float light) {
   // (the reference's texture factor is 1 here: x * 1.0f == x exactly, so the
   // product is left out)
-  float r = __fmul_rn(__fmul_rn(mat.x, color.x), light);
-  float g = __fmul_rn(__fmul_rn(mat.y, color.y), light);
-  float b = __fmul_rn(__fmul_rn(mat.z, color.z), light);
-  float a = __fmul_rn(mat.w, color.w);
-  return make_float4(__fmul_rn(r, a), __fmul_rn(g, a), __fmul_rn(b, a), a);
+  // r, g = (base * colour) * light; (b, a) = (base.z * colour.z, opacity * colour.w)
+  const float2 rg = mul2(mul2(lo2(mat), lo2(color)), make_float2(light, light));
+  const float2 ba = mul2(hi2(mat), hi2(color));
+  const float b = __fmul_rn(ba.x, light), a = ba.y;
+  const float2 rga = mul2(rg, make_float2(a, a));
+  return make_float4(rga.x, rga.y, __fmul_rn(b, a), a);
 }
 
 __device__ __forceinline__ float4 light_and_premultiply(const FrameConst& fc, float n[3],
@@ -1734,11 +1750,12 @@ __device__ __forceinline__ float4 shade_decoded_bf(const FrameConst& fc, const B
   }
   // (the reference's texture factor is 1 here: x * 1.0f == x exactly, so the
   // product is left out)
-  float r = __fmul_rn(__fmul_rn(mat.x, color.x), light);
-  float g = __fmul_rn(__fmul_rn(mat.y, color.y), light);
-  float b = __fmul_rn(__fmul_rn(mat.z, color.z), light);
-  float a = __fmul_rn(mat.w, color.w);
-  return make_float4(__fmul_rn(r, a), __fmul_rn(g, a), __fmul_rn(b, a), a);
+  // r, g = (base * colour) * light; (b, a) = (base.z * colour.z, opacity * colour.w)
+  const float2 rg = mul2(mul2(lo2(mat), lo2(color)), make_float2(light, light));
+  const float2 ba = mul2(hi2(mat), hi2(color));
+  const float b = __fmul_rn(ba.x, light), a = ba.y;
+  const float2 rga = mul2(rg, make_float2(a, a));
+  return make_float4(rga.x, rga.y, __fmul_rn(b, a), a);
 }
 
 // A bin-row's triangle, staged in shared memory by k_shade: edge and depth
@@ -1896,11 +1913,15 @@ __device__ __forceinline__ float4 shade_staged_bf(const FrameConst& fc, const St
               b2 = (float)__dmul_rn(e2, inv);
   const float4 c0 = T.c[0], c1 = T.c[1], c2 = T.c[2];
   const bool hc = fl & 1u;
+  // ((c0 * b0) + (c1 * b1)) + (c2 * b2) per channel, two channels per instruction
+  const float2 bb0 = make_float2(b0, b0), bb1 = make_float2(b1, b1), bb2 = make_float2(b2, b2);
+  const float2 clo = add2(add2(mul2(lo2(c0), bb0), mul2(lo2(c1), bb1)), mul2(lo2(c2), bb2));
+  const float2 chi = add2(add2(mul2(hi2(c0), bb0), mul2(hi2(c1), bb1)), mul2(hi2(c2), bb2));
   float4 color;
-  color.x = hc ? __fadd_rn(__fadd_rn(__fmul_rn(c0.x, b0), __fmul_rn(c1.x, b1)), __fmul_rn(c2.x, b2)) : 1.0f;
-  color.y = hc ? __fadd_rn(__fadd_rn(__fmul_rn(c0.y, b0), __fmul_rn(c1.y, b1)), __fmul_rn(c2.y, b2)) : 1.0f;
-  color.z = hc ? __fadd_rn(__fadd_rn(__fmul_rn(c0.z, b0), __fmul_rn(c1.z, b1)), __fmul_rn(c2.z, b2)) : 1.0f;
-  color.w = hc ? __fadd_rn(__fadd_rn(__fmul_rn(c0.w, b0), __fmul_rn(c1.w, b1)), __fmul_rn(c2.w, b2)) : 1.0f;
+  color.x = hc ? clo.x : 1.0f;
+  color.y = hc ? clo.y : 1.0f;
+  color.z = hc ? chi.x : 1.0f;
+  color.w = hc ? chi.y : 1.0f;
   float light;
   const float s = __fadd_rn(__fadd_rn(b0, b1), b2);
   const int so = (int)__float_as_uint(s) - (int)0x3f800000;
