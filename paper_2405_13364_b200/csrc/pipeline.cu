@@ -1438,6 +1438,14 @@ __device__ __forceinline__ float2 add2(float2 a, float2 b) {
 }
 __device__ __forceinline__ float4 cat4(float2 a, float2 b) { return make_float4(a.x, a.y, b.x, b.y); }
 
+// ((c0 * b0) + (c1 * b1)) + (c2 * b2) per channel (the barycentric attribute
+// interpolation, shading.cpp:55-62), products two channels at a time.
+__device__ __forceinline__ float4 interp4(float4 c0, float4 c1, float4 c2, float b0, float b1, float b2) {
+  const float2 bb0 = make_float2(b0, b0), bb1 = make_float2(b1, b1), bb2 = make_float2(b2, b2);
+  return cat4(add2(add2(mul2(lo2(c0), bb0), mul2(lo2(c1), bb1)), mul2(lo2(c2), bb2)),
+              add2(add2(mul2(hi2(c0), bb0), mul2(hi2(c1), bb1)), mul2(hi2(c2), bb2)));
+}
+
 __device__ __forceinline__ float4 blend(float4 acc, float4 s) {
   // acc + (1 - acc.w) * s per channel (shade_half_block's blend)
   const float t = __fsub_rn(1.0f, acc.w);
@@ -1645,11 +1653,7 @@ __device__ __forceinline__ float4 shade_sample(const FrameConst& fc, const Buffe
     const uint32_t fl = sr.flags;
     float4 color = make_float4(1.0f, 1.0f, 1.0f, 1.0f);
     if (fl & 1u) {
-      const float4 c0 = sr.c[0], c1 = sr.c[1], c2 = sr.c[2];
-      color.x = __fadd_rn(__fadd_rn(__fmul_rn(c0.x, b0), __fmul_rn(c1.x, b1)), __fmul_rn(c2.x, b2));
-      color.y = __fadd_rn(__fadd_rn(__fmul_rn(c0.y, b0), __fmul_rn(c1.y, b1)), __fmul_rn(c2.y, b2));
-      color.z = __fadd_rn(__fadd_rn(__fmul_rn(c0.z, b0), __fmul_rn(c1.z, b1)), __fmul_rn(c2.z, b2));
-      color.w = __fadd_rn(__fadd_rn(__fmul_rn(c0.w, b0), __fmul_rn(c1.w, b1)), __fmul_rn(c2.w, b2));
+      color = interp4(sr.c[0], sr.c[1], sr.c[2], b0, b1, b2);
     }
     float light;
     if (!axis_light((fl & 4u) ? (int)sr.pad[0] : -1, b0, b1, b2, &light)) {
@@ -1677,6 +1681,8 @@ __device__ __forceinline__ float4 shade_sample(const FrameConst& fc, const Buffe
   if (qf & 2u) {
     const uint4 c = qcol;
     const uint32_t w0 = c.x, w1 = ltri == 0 ? c.y : c.z, w2 = ltri == 0 ? c.z : c.w;
+    // (scalar here: the paired products measured slower on this gather-bound
+    // path, C4 shade +2%)
     float r[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k)
@@ -1734,11 +1740,12 @@ __device__ __forceinline__ float4 shade_decoded_bf(const FrameConst& fc, const B
   const float4 c0 = sr.c[0], c1 = sr.c[1], c2 = sr.c[2];
   const float4 n0 = sr.n[0], n1 = sr.n[1], n2 = sr.n[2];
   const bool hc = fl & 1u, hn = fl & 2u;
+  const float4 ci = interp4(c0, c1, c2, b0, b1, b2);
   float4 color;
-  color.x = hc ? __fadd_rn(__fadd_rn(__fmul_rn(c0.x, b0), __fmul_rn(c1.x, b1)), __fmul_rn(c2.x, b2)) : 1.0f;
-  color.y = hc ? __fadd_rn(__fadd_rn(__fmul_rn(c0.y, b0), __fmul_rn(c1.y, b1)), __fmul_rn(c2.y, b2)) : 1.0f;
-  color.z = hc ? __fadd_rn(__fadd_rn(__fmul_rn(c0.z, b0), __fmul_rn(c1.z, b1)), __fmul_rn(c2.z, b2)) : 1.0f;
-  color.w = hc ? __fadd_rn(__fadd_rn(__fmul_rn(c0.w, b0), __fmul_rn(c1.w, b1)), __fmul_rn(c2.w, b2)) : 1.0f;
+  color.x = hc ? ci.x : 1.0f;
+  color.y = hc ? ci.y : 1.0f;
+  color.z = hc ? ci.z : 1.0f;
+  color.w = hc ? ci.w : 1.0f;
   const float4 mat = sr.mat;
   float light;
   if (!axis_light((fl & 4u) ? (int)sr.pad[0] : -1, b0, b1, b2, &light)) {
@@ -1872,11 +1879,7 @@ __device__ __forceinline__ float4 shade_staged(const FrameConst& fc, const Stage
               b2 = (float)__dmul_rn(e2, inv);
   float4 color = make_float4(1.0f, 1.0f, 1.0f, 1.0f);
   if (fl & 1u) {
-    const float4 c0 = T.c[0], c1 = T.c[1], c2 = T.c[2];
-    color.x = __fadd_rn(__fadd_rn(__fmul_rn(c0.x, b0), __fmul_rn(c1.x, b1)), __fmul_rn(c2.x, b2));
-    color.y = __fadd_rn(__fadd_rn(__fmul_rn(c0.y, b0), __fmul_rn(c1.y, b1)), __fmul_rn(c2.y, b2));
-    color.z = __fadd_rn(__fadd_rn(__fmul_rn(c0.z, b0), __fmul_rn(c1.z, b1)), __fmul_rn(c2.z, b2));
-    color.w = __fadd_rn(__fadd_rn(__fmul_rn(c0.w, b0), __fmul_rn(c1.w, b1)), __fmul_rn(c2.w, b2));
+    color = interp4(T.c[0], T.c[1], T.c[2], b0, b1, b2);
   }
   float light;
   if (fl & 4u) {
@@ -1913,15 +1916,12 @@ __device__ __forceinline__ float4 shade_staged_bf(const FrameConst& fc, const St
               b2 = (float)__dmul_rn(e2, inv);
   const float4 c0 = T.c[0], c1 = T.c[1], c2 = T.c[2];
   const bool hc = fl & 1u;
-  // ((c0 * b0) + (c1 * b1)) + (c2 * b2) per channel, two channels per instruction
-  const float2 bb0 = make_float2(b0, b0), bb1 = make_float2(b1, b1), bb2 = make_float2(b2, b2);
-  const float2 clo = add2(add2(mul2(lo2(c0), bb0), mul2(lo2(c1), bb1)), mul2(lo2(c2), bb2));
-  const float2 chi = add2(add2(mul2(hi2(c0), bb0), mul2(hi2(c1), bb1)), mul2(hi2(c2), bb2));
+  const float4 ci = interp4(c0, c1, c2, b0, b1, b2);
   float4 color;
-  color.x = hc ? clo.x : 1.0f;
-  color.y = hc ? clo.y : 1.0f;
-  color.z = hc ? chi.x : 1.0f;
-  color.w = hc ? chi.y : 1.0f;
+  color.x = hc ? ci.x : 1.0f;
+  color.y = hc ? ci.y : 1.0f;
+  color.z = hc ? ci.z : 1.0f;
+  color.w = hc ? ci.w : 1.0f;
   float light;
   const float s = __fadd_rn(__fadd_rn(b0, b1), b2);
   const int so = (int)__float_as_uint(s) - (int)0x3f800000;
