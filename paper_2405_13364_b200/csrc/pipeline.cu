@@ -3226,6 +3226,7 @@ __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
       const uint32_t* mask_l = B.pool_mask + d.off;
       const uint32_t* pre_l = B.pool_pre + d.off;
       const uint16_t* slot_l = B.pool_slot + d.off;
+      uint32_t sh4 = 0, sh8 = 0;  // the staged lists' offsets in stage_* (u32 / u16 lists)
       if (d.cnt <= (uint32_t)kShadeStage && fc.bulk_stage) {
         // four bulk copies (16-byte aligned runs covering the list) onto the
         // warp's mbarrier; the generic-proxy reads of the previous list are
@@ -3243,10 +3244,12 @@ __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
         }
         mbar_wait(&stage_bar[warp], bar_phase);
         bar_phase ^= 1u;
-        tri_l = stage_tri[warp] + (d.off - a4);
-        mask_l = stage_mask[warp] + (d.off - a4);
-        pre_l = stage_pre[warp] + (d.off - a4);
-        slot_l = stage_slot[warp] + (d.off - a8);
+        sh4 = d.off - a4;
+        sh8 = d.off - a8;
+        tri_l = stage_tri[warp] + sh4;
+        mask_l = stage_mask[warp] + sh4;
+        pre_l = stage_pre[warp] + sh4;
+        slot_l = stage_slot[warp] + sh8;
       } else if (d.cnt <= (uint32_t)kShadeStage) {
         for (uint32_t i = lane; i < d.cnt; i += 32) {
           stage_tri[warp][i] = tri_l[i];
@@ -3278,9 +3281,13 @@ __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
                   (size_t)warp * KM * 32 + lane);
           if (staged_ok && d.cnt <= (uint32_t)kShadeStage && !fc.wave1) {  // all operands in shared memory
             if (fc.dump)
-              shade_waves_staged2<KM, 2>(fc, hpx0, hpy0, tri_l, mask_l, slot_l, row_tris, d.cnt, po, f);
+              shade_waves_staged2<KM, 2>(fc, hpx0, hpy0, stage_tri[warp] + sh4, stage_mask[warp] + sh4,
+                                         stage_slot[warp] + sh8, row_tris, d.cnt, po, f);
             else
-              shade_waves_staged2<KM, 1>(fc, hpx0, hpy0, tri_l, mask_l, slot_l, row_tris, d.cnt, po, f);
+              // (the lists named through stage_* directly: shared-memory loads
+              // instead of generic ones through the merged list pointers)
+              shade_waves_staged2<KM, 1>(fc, hpx0, hpy0, stage_tri[warp] + sh4, stage_mask[warp] + sh4,
+                                         stage_slot[warp] + sh8, row_tris, d.cnt, po, f);
           }
           else if (staged_ok && d.cnt <= (uint32_t)kShadeStage)
             shade_waves<KM, kTex>(fc, B, hpx0, hpy0, tri_l, mask_l, slot_l, row_tris, d.cnt, po, f);
