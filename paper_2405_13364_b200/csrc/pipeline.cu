@@ -1597,6 +1597,11 @@ __device__ __forceinline__ float4 texture_factor(const Buffers& B, const Fn3* te
 constexpr int kAxisLightSpan = 8;
 __shared__ float s_axis_light[6][2 * kAxisLightSpan + 1];
 
+// 32-bit shared-window address of a shared-memory object (for inline PTX).
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
 __device__ __forceinline__ float light_of_normal(const FrameConst& fc, float n0, float n1, float n2) {
   const float len2 = __fadd_rn(__fadd_rn(__fmul_rn(n0, n0), __fmul_rn(n1, n1)), __fmul_rn(n2, n2));
   const bool pos = len2 > 0.0f;
@@ -1898,8 +1903,11 @@ __device__ __forceinline__ float4 shade_staged(const FrameConst& fc, const Stage
 // that two independent samples per lane can be interleaved by the scheduler
 // (shade_waves_staged2). Bit-identical to shade_staged: each selected value
 // is computed by the same operations on the same inputs.
+// ltab: the 32-bit shared address of s_axis_light, taken once per half-block
+// by the caller (naming the table directly made the compiler rematerialize
+// its cluster-window address -- an S2R and three ALU operations -- per sample).
 __device__ __forceinline__ float4 shade_staged_bf(const FrameConst& fc, const StagedTri& T, int px, int py,
-                                                  uint32_t* qd) {
+                                                  uint32_t* qd, uint32_t ltab) {
   const double x = (double)px + 0.5, y = (double)py + 0.5;
   const uint32_t fl = T.flags;
   if (fl & 16u) {  // flat depth plane (stage_triangle); the one branch kept: every C2 quad
@@ -1926,7 +1934,10 @@ __device__ __forceinline__ float4 shade_staged_bf(const FrameConst& fc, const St
   const float s = __fadd_rn(__fadd_rn(b0, b1), b2);
   const int so = (int)__float_as_uint(s) - (int)0x3f800000;
   if ((fl & 32u) && so >= -kAxisLightSpan && so <= kAxisLightSpan) {
-    light = s_axis_light[__float_as_uint(T.light)][so + kAxisLightSpan];  // axis-aligned normal
+    // s_axis_light[axis][so + span] (axis-aligned normal)
+    const uint32_t at = ltab + 4u * (__float_as_uint(T.light) * (2u * kAxisLightSpan + 1u) +
+                                     (uint32_t)(so + kAxisLightSpan));
+    asm("ld.shared.f32 %0, [%1];" : "=f"(light) : "r"(at));
   } else {
     float n[3];
 #pragma unroll
@@ -2287,6 +2298,11 @@ __device__ __forceinline__ void shade_waves_staged2(const FrameConst& fc, int px
     }
     return my_r;
   };
+  uint32_t ltab, sbase;
+  asm volatile("mov.u32 %0, %1;" : "=r"(ltab) : "r"(smem_addr(&s_axis_light[0][0])));
+  // the staged triangles through an opaque shared address too (same reason)
+  asm volatile("mov.u32 %0, %1;" : "=r"(sbase) : "r"(smem_addr(staged)));
+  const StagedTri* stri = static_cast<const StagedTri*>(__cvta_shared_to_generic(sbase));
   uint32_t r = 0;
   while (r < n) {
     const uint32_t ra = form(&r);
@@ -2294,8 +2310,8 @@ __device__ __forceinline__ void shade_waves_staged2(const FrameConst& fc, int px
     const uint32_t ia = ra != kNone ? ra : 0u, ib = rb != kNone ? rb : 0u;
     uint32_t qa, qb;
     VEIL_CHECK(slot_l[ia] < kStageTris && slot_l[ib] < kStageTris);
-    const float4 ca = shade_staged_bf(fc, staged[slot_l[ia]], px, py, &qa);
-    const float4 cb = shade_staged_bf(fc, staged[slot_l[ib]], px, py, &qb);
+    const float4 ca = shade_staged_bf(fc, stri[slot_l[ia]], px, py, &qa, ltab);
+    const float4 cb = shade_staged_bf(fc, stri[slot_l[ib]], px, py, &qb, ltab);
     uint64_t pk;
     float4 pc;
     bool ooo;
@@ -3051,9 +3067,6 @@ constexpr int kShadeStage = 256;  // THB entries staged per warp; longer lists s
 
 // Bulk asynchronous copies (the TMA engine's 1-D cp.async.bulk) completing
 // on a per-warp mbarrier, for k_shade's THB-list staging.
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
 __device__ __forceinline__ void mbar_init(uint64_t* bar) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)) : "memory");
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
