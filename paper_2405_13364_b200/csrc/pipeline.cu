@@ -529,7 +529,16 @@ __device__ __forceinline__ unsigned long long ld_state(const unsigned long long*
 
 // 4 CTAs/SM (64 registers, small spill) beats 3 at 80 registers: the cull is
 // gather- and FP64-latency bound (C4 setup -6%, measured; 5 or 6 spill more)
+// Programmatic dependent launch: the frame's kernels are launched with
+// programmatic stream serialization, so a kernel's CTAs may become resident
+// while its predecessor drains; each kernel waits here (griddepcontrol.wait:
+// the predecessor grid has completed and its memory is visible) before it
+// touches anything a predecessor wrote. Without the launch attribute it is a
+// no-op.
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __global__ void __launch_bounds__(kSetupBlock, 4) k_setup(Buffers B, uint32_t nblocks) {
+  grid_dep_wait();
   const FrameConst& fc = c_fc;
   __shared__ uint32_t s_bid, s_excl;
   if (threadIdx.x == 0) s_bid = atomicAdd(&B.ctr->setup_ticket, 1u);
@@ -670,6 +679,7 @@ constexpr int kTriBlock = 128;
 // k_setup_tris<true> runs over them only (it used to launch over every
 // triangle and skip the others: C4 at 8 ranks 0.35 ms for 1/8 of the work).
 __global__ void __launch_bounds__(256) k_shard_tris(Buffers B) {
+  grid_dep_wait();
   const FrameConst& fc = c_fc;
   __shared__ unsigned int n_small;  // per-block count, one global atomic
   if (B.ctr->error & 1u) return;
@@ -710,6 +720,7 @@ __global__ void __launch_bounds__(256) k_shard_tris(Buffers B) {
 
 template <bool kShard>
 __global__ void __launch_bounds__(kTriBlock, 7) k_setup_tris(Buffers B) {
+  grid_dep_wait();
   const FrameConst& fc = c_fc;
   __shared__ __align__(16) TriRec stage[kTriBlock];
   if (B.ctr->error & 1u) return;
@@ -868,6 +879,7 @@ __device__ __forceinline__ uint32_t block_rows_mask(uint32_t yy, int by, int hei
 
 template <bool kWrite, bool kList>
 __global__ void __launch_bounds__(256) k_bin_pass(Buffers B) {
+  grid_dep_wait();
   const FrameConst& fc = c_fc;
   __shared__ unsigned int n_small, n_large;  // per-block counts, one global atomic each
   if (B.ctr->error) return;
@@ -968,6 +980,7 @@ __global__ void __launch_bounds__(256) k_bin_pass(Buffers B) {
 // is counted (kWrite = false) or receives the triangle index.
 template <bool kWrite>
 __global__ void __launch_bounds__(256) k_bin_large(Buffers B) {
+  grid_dep_wait();
   const FrameConst& fc = c_fc;
   if (B.ctr->error) return;
   const uint32_t npairs = min(B.ctr->large_pairs, fc.lpairs_cap);
@@ -1021,6 +1034,7 @@ __global__ void __launch_bounds__(256) k_bin_large(Buffers B) {
 
 // offsets (binning.cpp:24-32) + categories (34-37) + write cursors
 __global__ void __launch_bounds__(1024) k_bin_scan(Buffers B) {
+  grid_dep_wait();
   const FrameConst& fc = c_fc;
   if (B.ctr->error) return;
   __shared__ unsigned long long carry;
@@ -1111,6 +1125,7 @@ __device__ void cta_sort_segment(uint32_t* g, uint32_t n, uint32_t* sm, uint32_t
 }
 
 __global__ void __launch_bounds__(256) k_bin_sort(Buffers B) {
+  grid_dep_wait();
   const FrameConst& fc = c_fc;
   if (B.ctr->error) return;
   __shared__ uint32_t sm[4096];
@@ -2958,6 +2973,7 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
 template <bool kGlobal, int kFuse>
 __global__ void __launch_bounds__(128, kFuse ? 6 : 7) k_extract(Buffers B, int pass,
                                                               uint32_t cap_tbr, uint32_t cap_tb) {
+  grid_dep_wait();
   const FrameConst& fc = c_fc;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   __shared__ ItemState st;
@@ -3101,10 +3117,12 @@ template <int KM, int kMode, bool kTex>
 __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
   const FrameConst& fc = c_fc;
   // (an empty segment queue: nothing to shade, skip the table set-up)
+  if (kMode == 1) grid_dep_wait();  // (reads the segment count right away)
   if (kMode == 1 && (B.ctr->error || B.ctr->seg_count == 0)) return;
-  load_shared_luts();
+  load_shared_luts();  // (scene-static tables and the frame constants: ahead of the wait)
   fill_axis_light(fc);
   __syncthreads();
+  grid_dep_wait();
   // (+8 entries: bulk copies move 16-byte aligned runs around the list)
   __shared__ __align__(16) uint32_t stage_tri[8][kShadeStage + 8];
   __shared__ __align__(16) uint32_t stage_mask[8][kShadeStage + 8];
@@ -3337,6 +3355,7 @@ __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
 // first, so the kernel's tail is made of short bins): a 256-bucket
 // log-scale counting sort of the per-bin costs k_extract accumulated.
 __global__ void __launch_bounds__(1024) k_order_bins(Buffers B, uint32_t shade_ctas) {
+  grid_dep_wait();
   const FrameConst& fc = c_fc;
   __shared__ uint32_t hist[256];
   __shared__ uint32_t base[256];
@@ -3398,6 +3417,7 @@ __global__ void __launch_bounds__(1024) k_order_bins(Buffers B, uint32_t shade_c
 }
 
 __global__ void __launch_bounds__(256) k_finalize(Buffers B) {
+  grid_dep_wait();
   const FrameConst& fc = c_fc;
   if (B.ctr->error) return;
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -3431,6 +3451,7 @@ __global__ void __launch_bounds__(256) k_finalize(Buffers B) {
 // CTAs per SM paint them faster than k_shade's bin loop (two CTAs per SM,
 // three block barriers per bin).
 __global__ void __launch_bounds__(256) k_fill_empty(Buffers B) {
+  grid_dep_wait();
   const FrameConst& fc = c_fc;
   if (B.ctr->error) return;
   for (int b = blockIdx.x; b < fc.nbins; b += gridDim.x) {
@@ -3458,6 +3479,7 @@ __global__ void __launch_bounds__(256) k_fill_empty(Buffers B) {
 // goes to *out. O(n^2) per pixel over the THB list: a measurement, not a
 // frame path.
 __global__ void __launch_bounds__(256) k_disorder(Buffers B, int* out) {
+  grid_dep_wait();
   const FrameConst& fc = c_fc;
   if (B.ctr->error) return;
   const int lane = threadIdx.x & 31;
@@ -3501,6 +3523,7 @@ __global__ void __launch_bounds__(256) k_disorder(Buffers B, int* out) {
 // blended in exact key order by repeated selection of the next key, so no
 // per-pixel list storage is needed (an oracle mode, not a fast path).
 __global__ void __launch_bounds__(128) k_abuffer(Buffers B) {
+  grid_dep_wait();
   const FrameConst& fc = c_fc;
   load_shared_luts();
   fill_axis_light(fc);
@@ -3561,6 +3584,7 @@ __global__ void __launch_bounds__(128) k_abuffer(Buffers B) {
 __global__ void __launch_bounds__(256) k_tile_copy(FrameConst fc, uint32_t* fb, uint8_t* mask,
                                                    uint8_t* tiles, const uint32_t* bins,
                                                    uint32_t ntiles, int unpack) {
+  grid_dep_wait();
   for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const int bin = (int)bins[t];
     const int bx = bin % fc.bins_x, by = bin / fc.bins_x;
@@ -3887,6 +3911,28 @@ void camera_vectors(const Camera& c, dev::FrameConst* fc) {
 // sizes the fused raster's per-CTA scratch.
 constexpr int kExtractCtasPerSmMax = 7;
 
+// Frame kernels are launched with programmatic stream serialization (see
+// dev::grid_dep_wait): a kernel's launch and CTA scheduling overlap its
+// predecessor's tail instead of following its completion.
+template <typename... KArgs, typename... Args>
+void pdl_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  static const bool enabled = [] {  // VEIL_NO_PDL=1: plain stream-ordered launches
+    const char* e = std::getenv("VEIL_NO_PDL");
+    return !(e && *e && *e != '0');
+  }();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = enabled ? 1 : 0;
+  ck(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...), "kernel launch");
+}
+
 template <int kFuse>
 void launch_extract_k(DeviceScene* d, const dev::FrameConst& fc, const dev::Buffers& B, int pass,
                       uint32_t gcap_tbr, uint32_t gcap_tb, int* launches) {
@@ -3901,10 +3947,10 @@ void launch_extract_k(DeviceScene* d, const dev::FrameConst& fc, const dev::Buff
     per_sm = std::min(std::max(1, per_sm), kExtractCtasPerSmMax);
   }
   const int grid = int(std::min<long long>((long long)per_sm * d->sm_count, (long long)fc.nbins * 4));
-  dev::k_extract<false, kFuse><<<grid, 128, smem, d->stream>>>(B, pass, dev::RasterShared::kTbr,
-                                                                 dev::RasterShared::kTb);
+  pdl_launch(dev::k_extract<false, kFuse>, grid, 128, smem, d->stream, B, pass,
+             uint32_t(dev::RasterShared::kTbr), uint32_t(dev::RasterShared::kTb));
   ck(cudaGetLastError(), "k_extract launch");
-  dev::k_extract<true, kFuse><<<d->raster_ctas_global, 128, 0, d->stream>>>(B, pass, gcap_tbr, gcap_tb);
+  pdl_launch(dev::k_extract<true, kFuse>, d->raster_ctas_global, 128, 0, d->stream, B, pass, gcap_tbr, gcap_tb);
   *launches += 2;
 }
 
@@ -3953,7 +3999,7 @@ void launch_shade_mode(DeviceScene* d, const dev::FrameConst& fc, const dev::Buf
   long long cap = (long long)std::max(1, per_sm) * d->sm_count;
   if (KM == 0 && B.dfm_g) cap = std::min<long long>(cap, B.dfm_ctas);  // scratch slices
   const int grid = int(std::max<long long>(1, std::min<long long>(cap, items)));
-  dev::k_shade<KM, kMode, kTex><<<grid, 256, dyn, d->stream>>>(B);
+  pdl_launch(dev::k_shade<KM, kMode, kTex>, grid, 256, dyn, d->stream, B);
   ck(cudaGetLastError(), "k_shade launch");
   ++*launches;
 }
@@ -4338,32 +4384,32 @@ int enqueue_front(DeviceScene* d, Prepared& P) {
   ck(cudaMemsetAsync(B.ctr, 0, P.zero_bytes, st), "memset");  // counters, bin counts, look-back
   record_event(d->ev[0], st);
   if (P.nblocks) {
-    dev::k_setup<<<P.nblocks, dev::kSetupBlock, 0, st>>>(B, P.nblocks);
+    pdl_launch(dev::k_setup, P.nblocks, dev::kSetupBlock, 0, st, B, P.nblocks);
     const int tgrid = int(std::min<long long>(((long long)fc.nquads * 2 + dev::kTriBlock - 1) / dev::kTriBlock,
                                               (long long)d->sm_count * 32));
     if (fc.world > 1) {
-      dev::k_shard_tris<<<std::max(1, std::min<int>(d->sm_count * 8, int((fc.nquads + 255) / 256))), 256, 0,
-                          st>>>(B);
-      dev::k_setup_tris<true><<<std::max(1, tgrid), dev::kTriBlock, 0, st>>>(B);
+      pdl_launch(dev::k_shard_tris, std::max(1, std::min<int>(d->sm_count * 8, int((fc.nquads + 255) / 256))), 256, 0,
+                 st, B);
+      pdl_launch(dev::k_setup_tris<true>, std::max(1, tgrid), dev::kTriBlock, 0, st, B);
       ++launches;
     } else {
-      dev::k_setup_tris<false><<<std::max(1, tgrid), dev::kTriBlock, 0, st>>>(B);
+      pdl_launch(dev::k_setup_tris<false>, std::max(1, tgrid), dev::kTriBlock, 0, st, B);
     }
     launches += 2;
   }
   record_event(d->ev[1], st);
   int grid = std::max(1, std::min<int>(d->sm_count * 8, int((fc.nquads + 255) / 256)));
   if (fc.world > 1)
-    dev::k_bin_pass<false, true><<<grid, 256, 0, st>>>(B);
+    pdl_launch(dev::k_bin_pass<false, true>, grid, 256, 0, st, B);
   else
-    dev::k_bin_pass<false, false><<<grid, 256, 0, st>>>(B);
-  dev::k_bin_large<false><<<d->sm_count * 8, 256, 0, st>>>(B);
-  dev::k_bin_scan<<<1, 1024, 0, st>>>(B);
+    pdl_launch(dev::k_bin_pass<false, false>, grid, 256, 0, st, B);
+  pdl_launch(dev::k_bin_large<false>, d->sm_count * 8, 256, 0, st, B);
+  pdl_launch(dev::k_bin_scan, 1, 1024, 0, st, B);
   if (fc.world > 1)
-    dev::k_bin_pass<true, true><<<grid, 256, 0, st>>>(B);
+    pdl_launch(dev::k_bin_pass<true, true>, grid, 256, 0, st, B);
   else
-    dev::k_bin_pass<true, false><<<grid, 256, 0, st>>>(B);
-  dev::k_bin_large<true><<<d->sm_count * 8, 256, 0, st>>>(B);
+    pdl_launch(dev::k_bin_pass<true, false>, grid, 256, 0, st, B);
+  pdl_launch(dev::k_bin_large<true>, d->sm_count * 8, 256, 0, st, B);
   launches += 5;
   if (fc.sort_bins) {
     dev::k_bin_sort<<<std::min(fc.nbins, d->sm_count * 8), 256, 0, st>>>(B);
@@ -4552,19 +4598,19 @@ static void enqueue_raster(DeviceScene* d, Prepared& P, int* launches) {
   launch_extract(d, P.fc, P.B, dev::kPassHigh, P.gcap_tbr, P.gcap_tb, launches);
   record_event(d->ev[5], d->stream);
   if (P.fc.fused) {  // the extraction shaded every non-empty bin
-    dev::k_fill_empty<<<std::min(P.fc.nbins, d->sm_count * 8), 256, 0, d->stream>>>(P.B);
+    pdl_launch(dev::k_fill_empty, std::min(P.fc.nbins, d->sm_count * 8), 256, 0, d->stream, P.B);
     ++*launches;
   } else {
     if (P.fc.fill_split) {
-      dev::k_fill_empty<<<std::min(P.fc.nbins, d->sm_count * 8), 256, 0, d->stream>>>(P.B);
+      pdl_launch(dev::k_fill_empty, std::min(P.fc.nbins, d->sm_count * 8), 256, 0, d->stream, P.B);
       ++*launches;
     }
     // (the split threshold uses mode 0's usual 2 CTAs per SM)
-    dev::k_order_bins<<<1, 1024, 0, d->stream>>>(P.B, uint32_t(2 * d->sm_count));
+    pdl_launch(dev::k_order_bins, 1, 1024, 0, d->stream, P.B, uint32_t(2 * d->sm_count));
     ++*launches;
     launch_shade(d, P.fc, P.B, launches);
   }
-  dev::k_finalize<<<(P.fc.nbins + 255) / 256, 256, 0, d->stream>>>(P.B);
+  pdl_launch(dev::k_finalize, (P.fc.nbins + 255) / 256, 256, 0, d->stream, P.B);
   ++*launches;
   record_event(d->ev[4], d->stream);
 }
