@@ -537,6 +537,11 @@ __device__ __forceinline__ unsigned long long ld_state(const unsigned long long*
 // no-op.
 __device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// 32-bit shared-window address of a shared-memory object (for inline PTX).
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
 __global__ void __launch_bounds__(kSetupBlock, 4) k_setup(Buffers B, uint32_t nblocks) {
   grid_dep_wait();
   const FrameConst& fc = c_fc;
@@ -768,19 +773,36 @@ __global__ void __launch_bounds__(kTriBlock, 7) k_setup_tris(Buffers B) {
     if (kShard) {
       if (store) B.tri[ti] = rec;
     } else {  // coalesced copy-out of this warp's 32 records (4 KB)
+      // the previous run's bulk store has finished reading the stage
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      __syncwarp();
       stage[threadIdx.x] = rec;
       const unsigned needm = __ballot_sync(0xffffffffu, store);
-      __syncwarp();
       const uint32_t wbase = base + (uint32_t)warp * 32u;
-      const uint4* src = reinterpret_cast<const uint4*>(&stage[warp * 32]);
-      uint4* dst = reinterpret_cast<uint4*>(B.tri + wbase);
       const uint32_t nrec = wbase < nt ? min(32u, nt - wbase) : 0u;
+      const unsigned full = nrec >= 32u ? 0xffffffffu : ((1u << nrec) - 1u);
+      if (nrec && (needm & full) == full && fc.bulk_stage) {
+        // every record of the run is stored: one bulk copy (TMA engine)
+        // shared -> global, issued by one lane, the warp moves on
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(B.tri + wbase),
+                       "r"(smem_addr(&stage[warp * 32])), "r"(nrec * (uint32_t)sizeof(TriRec))
+                       : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+      } else {
+        __syncwarp();
+        const uint4* src = reinterpret_cast<const uint4*>(&stage[warp * 32]);
+        uint4* dst = reinterpret_cast<uint4*>(B.tri + wbase);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const uint32_t e = (uint32_t)k * 32u + lane;  // 16-byte chunk index within the warp
-        if (e < nrec * 8u && ((needm >> (e >> 3)) & 1u)) dst[e] = src[e];
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t e = (uint32_t)k * 32u + lane;  // 16-byte chunk index within the warp
+          if (e < nrec * 8u && ((needm >> (e >> 3)) & 1u)) dst[e] = src[e];
+        }
+        __syncwarp();
       }
-      __syncwarp();
     }
     if (needed) {
       B.tri_meta[ti] = meta;
@@ -812,6 +834,8 @@ __global__ void __launch_bounds__(kTriBlock, 7) k_setup_tris(Buffers B) {
       }
     }
   }
+  // outstanding bulk stores complete before the CTA (and its stage) retires
+  if (!kShard && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // ------------------------------------------------------------ binning
@@ -1611,11 +1635,6 @@ __device__ __forceinline__ float4 texture_factor(const Buffers& B, const Fn3* te
 // with shade_staged_bf's exact operations.
 constexpr int kAxisLightSpan = 8;
 __shared__ float s_axis_light[6][2 * kAxisLightSpan + 1];
-
-// 32-bit shared-window address of a shared-memory object (for inline PTX).
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
 
 __device__ __forceinline__ float light_of_normal(const FrameConst& fc, float n0, float n1, float n2) {
   const float len2 = __fadd_rn(__fadd_rn(__fmul_rn(n0, n0), __fmul_rn(n1, n1)), __fmul_rn(n2, n2));
