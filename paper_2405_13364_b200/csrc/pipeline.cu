@@ -2561,9 +2561,12 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
         const uint32_t ti = large ? it : it * 2;
         VEIL_CHECK(wbase + __popc(m0 & below) < cand_cap);
         cand[wbase + __popc(m0 & below)] = ((uint64_t)i << 32) | ti | ((large ? 1u : 0u) << 31);
+        if (!kFuse) asm volatile("prefetch.global.L2 [%0];" ::"l"(B.tri + ti));  // read by the row spans next
       }
-      if (rows & 2u)
+      if (rows & 2u) {
         cand[wbase + __popc(m0) + __popc(m1 & below)] = ((uint64_t)(2 * j + 1) << 32) | (it * 2 + 1);
+        if (!kFuse) asm volatile("prefetch.global.L2 [%0];" ::"l"(B.tri + it * 2 + 1));
+      }
     }
     __syncthreads();
     const uint32_t nc = st->ncand[par];
