@@ -527,8 +527,6 @@ __device__ __forceinline__ unsigned long long ld_state(const unsigned long long*
   return *reinterpret_cast<const volatile unsigned long long*>(p);
 }
 
-// 4 CTAs/SM (64 registers, small spill) beats 3 at 80 registers: the cull is
-// gather- and FP64-latency bound (C4 setup -6%, measured; 5 or 6 spill more)
 // Programmatic dependent launch: the frame's kernels are launched with
 // programmatic stream serialization, so a kernel's CTAs may become resident
 // while its predecessor drains; each kernel waits here (griddepcontrol.wait:
@@ -542,6 +540,8 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
 
+// 4 CTAs/SM (64 registers, small spill) beats 3 at 80 registers: the cull is
+// gather- and FP64-latency bound (C4 setup -6%, measured; 5 or 6 spill more)
 __global__ void __launch_bounds__(kSetupBlock, 4) k_setup(Buffers B, uint32_t nblocks) {
   grid_dep_wait();
   const FrameConst& fc = c_fc;
