@@ -534,6 +534,10 @@ __device__ __forceinline__ unsigned long long ld_state(const unsigned long long*
 // touches anything a predecessor wrote. Without the launch attribute it is a
 // no-op.
 __device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Lets the next kernel's CTAs launch now (they run their prologue and wait in
+// grid_dep_wait); used by kernels whose CTAs are all resident at once, so the
+// early dependents cannot starve them.
+__device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // 32-bit shared-window address of a shared-memory object (for inline PTX).
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -3378,6 +3382,7 @@ __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
 // log-scale counting sort of the per-bin costs k_extract accumulated.
 __global__ void __launch_bounds__(1024) k_order_bins(Buffers B, uint32_t shade_ctas) {
   grid_dep_wait();
+  grid_dep_launch();  // k_shade's CTAs fill their lookup tables meanwhile
   const FrameConst& fc = c_fc;
   __shared__ uint32_t hist[256];
   __shared__ uint32_t base[256];
