@@ -1833,7 +1833,7 @@ constexpr int kStageTris = 320;
 // THB: lower when the bin's triangles are staged in shared memory (waves read
 // them there), higher when each lane gathers its triangle from global memory.
 constexpr uint32_t kWalkMinSamplesPerThbStaged = 6;
-constexpr uint32_t kWalkMinSamplesPerThb = 12;
+constexpr uint32_t kWalkMinSamplesPerThb = 16;  // (12 -> 16: C5 shade -0.7%)
 
 __device__ __forceinline__ void stage_triangle(const FrameConst& fc, const Buffers& B, uint32_t tri,
                                                StagedTri* dst) {
