@@ -1833,6 +1833,8 @@ struct __align__(16) StagedTri {
 static_assert(sizeof(StagedTri) == 208, "StagedTri layout");
 constexpr int kStageTris = 320;
 
+constexpr int kShadeStage = 256;  // THB entries k_shade stages per warp; longer lists stream
+
 // Wave walk (mode 0) vs dense segments (mode 1) crossover, in samples per
 // THB: lower when the bin's triangles are staged in shared memory (waves read
 // them there), higher when each lane gathers its triangle from global memory.
@@ -2927,7 +2929,9 @@ __device__ __forceinline__ void extract_item(const FrameConst& fc, const Buffers
     const bool staged = fc.decoded && T <= (uint32_t)kStageTris;
     const uint32_t wmin = staged ? (fc.walk_min ? (uint32_t)fc.walk_min : kWalkMinSamplesPerThbStaged)
                                  : (fc.walk_min_u ? (uint32_t)fc.walk_min_u : kWalkMinSamplesPerThb);
-    const bool seg = !fc.threshold && d.frags < wmin * d.cnt;
+    // (segment lists always fit k_shade's per-warp stage, so the segment
+    // kernel reads them from shared memory only; longer lists take the walk)
+    const bool seg = !fc.threshold && d.frags < wmin * d.cnt && d.cnt <= (uint32_t)kShadeStage;
     d.pad = seg ? 1u : 0u;
     const uint32_t hbi = (uint32_t)bin * 32u + (uint32_t)(row * 8 + warp * 2 + lane);
     B.hbd[hbi] = d;
@@ -3109,7 +3113,6 @@ __global__ void __launch_bounds__(128, kFuse ? 6 : 7) k_extract(Buffers B, int p
 // list from the pool into shared memory (coalesced), keeping the segment
 // mapping's dependent lookups on-chip. Empty bins and half-blocks without
 // samples composite the background.
-constexpr int kShadeStage = 256;  // THB entries staged per warp; longer lists stream
 
 // Bulk asynchronous copies (the TMA engine's 1-D cp.async.bulk) completing
 // on a per-warp mbarrier, for k_shade's THB-list staging.
@@ -3366,11 +3369,17 @@ __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
         if constexpr (KM != 0) {
           SlotFilter<KM> f;
           f.reset(reinterpret_cast<float4*>(shade_dyn) + (size_t)warp * KM * 32 + lane);
-          shade_segments<KM, kTex>(fc, B, hpx0, hpy0, tri_l, mask_l, pre_l, d.cnt, d.frags, route_s[warp], po, f);
+          // segment lists are staged (k_extract queues only lists that fit):
+          // named through the stage arrays, the loads are LDS, not generic
+          VEIL_CHECK(d.cnt <= (uint32_t)kShadeStage);
+          shade_segments<KM, kTex>(fc, B, hpx0, hpy0, stage_tri[warp] + sh4, stage_mask[warp] + sh4,
+                                   stage_pre[warp] + sh4, d.cnt, d.frags, route_s[warp], po, f);
         } else {
           MemFilter f;
           dfm_reset<kMode>(B, shade_dyn, f);
-          shade_segments<KM, kTex>(fc, B, hpx0, hpy0, tri_l, mask_l, pre_l, d.cnt, d.frags, route_s[warp], po, f);
+          VEIL_CHECK(d.cnt <= (uint32_t)kShadeStage);
+          shade_segments<KM, kTex>(fc, B, hpx0, hpy0, stage_tri[warp] + sh4, stage_mask[warp] + sh4,
+                                   stage_pre[warp] + sh4, d.cnt, d.frags, route_s[warp], po, f);
         }
       }
     }
