@@ -1471,6 +1471,10 @@ struct MemFilter {
   }
 };
 
+// The ring filter's shading paths keep scalar blend products (see blend).
+template <typename F> struct PairBlend { static constexpr bool value = true; };
+template <> struct PairBlend<MemFilter> { static constexpr bool value = false; };
+
 // Paired FP32 multiplies (sm_100's FMUL2: two IEEE round-to-nearest products
 // per instruction, each exactly __fmul_rn), so the colour channels' products
 // cost half the issue slots with bit-identical results. The sums stay scalar
@@ -1493,11 +1497,18 @@ __device__ __forceinline__ float4 interp4(float4 c0, float4 c1, float4 c2, float
               add2(add2(mul2(hi2(c0), bb0), mul2(hi2(c1), bb1)), mul2(hi2(c2), bb2)));
 }
 
+// acc + (1 - acc.w) * s per channel (shade_half_block's blend). kPair: the
+// products two at a time (faster in the register-filter paths; the ring
+// filter's paths measured 6% slower with it, C2 at DF 64).
+template <bool kPair = true>
 __device__ __forceinline__ float4 blend(float4 acc, float4 s) {
-  // acc + (1 - acc.w) * s per channel (shade_half_block's blend)
   const float t = __fsub_rn(1.0f, acc.w);
-  const float2 tt = make_float2(t, t);
-  return cat4(add2(lo2(acc), mul2(tt, lo2(s))), add2(hi2(acc), mul2(tt, hi2(s))));
+  if (kPair) {
+    const float2 tt = make_float2(t, t);
+    return cat4(add2(lo2(acc), mul2(tt, lo2(s))), add2(hi2(acc), mul2(tt, hi2(s))));
+  }
+  return make_float4(__fadd_rn(acc.x, __fmul_rn(t, s.x)), __fadd_rn(acc.y, __fmul_rn(t, s.y)),
+                     __fadd_rn(acc.z, __fmul_rn(t, s.z)), __fadd_rn(acc.w, __fmul_rn(t, s.w)));
 }
 
 // normalize + Lambert (shade_sample, shading.cpp:123-136): the light factor.
@@ -2067,9 +2078,9 @@ struct PixelOut {
 // raster.cpp:248-255). kDump: 0 = test c_fc.dump, 1 = no dump, 2 = dump frame
 // (the compiler turns the run-time test into a select, so hot callers that
 // know the frame kind drop the hash's instructions entirely).
-template <int kDump = 0>
+template <int kDump = 0, bool kPair = true>
 __device__ __forceinline__ void commit(PixelOut& o, uint64_t pk, float4 pc, bool ooo) {
-  o.acc = blend(o.acc, pc);
+  o.acc = blend<kPair>(o.acc, pc);
   if (kDump == 2 || (kDump == 0 && c_fc.dump))
     o.hash = (o.hash ^ pk) * kHashPrime;  // blend-order evidence (parity dumps)
   ++o.emitted;
@@ -2112,7 +2123,7 @@ __device__ __forceinline__ void blend_routed(const FrameConst& fc, Filter& f, Pi
       uint64_t pk;
       float4 pc;
       bool ooo;
-      if (f.push(fc.df, k2, c2, &pk, &pc, &ooo)) commit(o, pk, pc, ooo);
+      if (f.push(fc.df, k2, c2, &pk, &pc, &ooo)) commit<0, PairBlend<Filter>::value>(o, pk, pc, ooo);
     }
   }
 }
@@ -2178,7 +2189,7 @@ __device__ __forceinline__ void shade_segments(const FrameConst& fc, const Buffe
     float4 pc;
     bool ooo;
     f.pop(&pk, &pc, &ooo);
-    commit(o, pk, pc, ooo);
+    commit<0, PairBlend<Filter>::value>(o, pk, pc, ooo);
   }
 }
 
@@ -2235,7 +2246,7 @@ __device__ __forceinline__ void shade_walk(const FrameConst& fc, const Buffers& 
       float4 pc;
       bool ooo;
       if (f.push(fc.df, key, col, &pk, &pc, &ooo)) {
-        commit(o, pk, pc, ooo);
+        commit<0, PairBlend<Filter>::value>(o, pk, pc, ooo);
         if (kThreshold && !saturated && o.acc.w >= kAlphaThreshold) saturated = true;
       }
     }
@@ -2252,7 +2263,7 @@ __device__ __forceinline__ void shade_walk(const FrameConst& fc, const Buffers& 
       bool ooo;
       f.pop(&pk, &pc, &ooo);
       if (done) continue;
-      commit(o, pk, pc, ooo);
+      commit<0, PairBlend<Filter>::value>(o, pk, pc, ooo);
       if (kThreshold && o.acc.w >= kAlphaThreshold) done = true;
     }
   }
@@ -2300,7 +2311,7 @@ __device__ __forceinline__ void shade_waves(const FrameConst& fc, const Buffers&
       uint64_t pk;
       float4 pc;
       bool ooo;
-      if (f.push(fc.df, sample_key(fc, qd, tri), col, &pk, &pc, &ooo)) commit(o, pk, pc, ooo);
+      if (f.push(fc.df, sample_key(fc, qd, tri), col, &pk, &pc, &ooo)) commit<0, PairBlend<Filter>::value>(o, pk, pc, ooo);
     }
   }
   while (f.n > 0) {
@@ -2308,7 +2319,7 @@ __device__ __forceinline__ void shade_waves(const FrameConst& fc, const Buffers&
     float4 pc;
     bool ooo;
     f.pop(&pk, &pc, &ooo);
-    commit(o, pk, pc, ooo);
+    commit<0, PairBlend<Filter>::value>(o, pk, pc, ooo);
   }
 }
 
