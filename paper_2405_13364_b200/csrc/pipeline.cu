@@ -151,6 +151,7 @@ struct Counters {
   unsigned int list_count[2];  // owned bins to extract in the low / high pass
   unsigned int order_count;    // (bin, part) entries in k_shade's (mode 0/2) order list
   unsigned int shard_tri_count;  // sharded frames: triangles this rank sets up (k_shard_tris)
+  unsigned int finalize_done;    // k_finalize CTAs finished (the last one publishes the counters)
 };
 
 // Decoded per-triangle shading inputs (unpack_color / decode_normal of the
@@ -3467,10 +3468,30 @@ __global__ void __launch_bounds__(1024) k_order_bins(Buffers B, uint32_t shade_c
     }
 }
 
-__global__ void __launch_bounds__(256) k_finalize(Buffers B) {
+__device__ __forceinline__ void finalize_sums(const FrameConst& fc, const Buffers& B);
+
+// host_ctr: the scene's pinned counter block (device-mapped); the last CTA
+// copies the frame's final counters there, so no read-back copy follows.
+__global__ void __launch_bounds__(256) k_finalize(Buffers B, Counters* host_ctr) {
   grid_dep_wait();
   const FrameConst& fc = c_fc;
-  if (B.ctr->error) return;
+  __shared__ bool last;
+  if (!B.ctr->error) finalize_sums(fc, B);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(&B.ctr->finalize_done, 1u) == gridDim.x - 1u;
+  }
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    const volatile uint32_t* src = reinterpret_cast<const volatile uint32_t*>(B.ctr);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(host_ctr);
+    for (uint32_t i = threadIdx.x; i < sizeof(Counters) / 4; i += blockDim.x) dst[i] = src[i];
+  }
+}
+
+__device__ __forceinline__ void finalize_sums(const FrameConst& fc, const Buffers& B) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long v[6] = {0, 0, 0, 0, 0, 0};
   if (b < fc.nbins) {
@@ -3712,7 +3733,8 @@ struct DeviceScene {
   void* peer_fb = nullptr;    // imported root framebuffer (cudaIpcOpenMemHandle)
   void* peer_mask = nullptr;
   int peer_w = 0, peer_h = 0;  // the imported framebuffer's viewport
-  dev::Counters* ctr_host = nullptr;   // pinned counters readback
+  dev::Counters* ctr_host = nullptr;   // pinned counters readback (written by k_finalize)
+  dev::Counters* ctr_dev = nullptr;    // ctr_host's device-mapped address
   // Cached CUDA graph of one whole frame (c_fc upload .. counters readback),
   // valid while the launch-shaping inputs in graph_key are unchanged.
   cudaGraphExec_t graph_exec = nullptr;
@@ -3816,6 +3838,7 @@ DeviceScene* device_scene_on(const Scene& s, DeviceScene** slot, int device) {
     for (auto& e : d->ev) ck(cudaEventCreate(&e), "cudaEventCreate");
     ck(cudaMallocHost(reinterpret_cast<void**>(&d->fc_host), sizeof(dev::FrameConst)), "cudaMallocHost");
     ck(cudaMallocHost(reinterpret_cast<void**>(&d->ctr_host), sizeof(dev::Counters)), "cudaMallocHost");
+    ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d->ctr_dev), d->ctr_host, 0), "cudaHostGetDevicePointer");
     cudaDeviceGetAttribute(&d->sm_count, cudaDevAttrMultiProcessorCount, device);
     {  // exact unpack tables (IEEE float division on the host)
       float lc[256], ln[1024];
@@ -4664,7 +4687,7 @@ static void enqueue_raster(DeviceScene* d, Prepared& P, int* launches) {
     ++*launches;
     launch_shade(d, P.fc, P.B, launches);
   }
-  pdl_launch(dev::k_finalize, (P.fc.nbins + 255) / 256, 256, 0, d->stream, P.B);
+  pdl_launch(dev::k_finalize, (P.fc.nbins + 255) / 256, 256, 0, d->stream, P.B, d->ctr_dev);
   ++*launches;
   record_event(d->ev[4], d->stream);
 }
@@ -4764,10 +4787,7 @@ static void render_frame_on(DeviceScene* d, const Scene& s, const RenderOptions&
         int n = 0;
         try {
           n = enqueue_front(d, P);
-          enqueue_raster(d, P, &n);
-          ck(cudaMemcpyAsync(d->ctr_host, P.B.ctr, sizeof(dev::Counters), cudaMemcpyDeviceToHost,
-                             d->stream),
-             "counters");
+          enqueue_raster(d, P, &n);  // (k_finalize publishes the counters to ctr_host)
         } catch (...) {
           if (cudaStreamEndCapture(d->stream, &g) == cudaSuccess && g) cudaGraphDestroy(g);
           throw;
@@ -4787,9 +4807,6 @@ static void render_frame_on(DeviceScene* d, const Scene& s, const RenderOptions&
       if (opt.ev_start) ck(cudaEventRecord(static_cast<cudaEvent_t>(opt.ev_start), d->stream), "event");
       launches = enqueue_front(d, P);
       enqueue_raster(d, P, &launches);
-      ck(cudaMemcpyAsync(d->ctr_host, P.B.ctr, sizeof(dev::Counters), cudaMemcpyDeviceToHost,
-                         d->stream),
-         "counters");
     }
     if (opt.ev_end) ck(cudaEventRecord(static_cast<cudaEvent_t>(opt.ev_end), d->stream), "event");
     ck(cudaStreamSynchronize(d->stream), "frame");
