@@ -596,7 +596,7 @@ def run_ours(args):
                              "(veil_render_device_timed) right before the frame's graph launch and "
                              + ("right after it" if world == 1 else
                                 "by bench.py after the gather (max over ranks)")
-                             + "; one frame = c_fc upload, counter reset, every kernel, counter read-back"),
+                             + "; one frame = c_fc upload, counter reset, every kernel (k_finalize publishes the counters)"),
             "parity": parity,
             "e2e": e2e,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
