@@ -2084,7 +2084,7 @@ __device__ __forceinline__ void commit(PixelOut& o, uint64_t pk, float4 pc, bool
   o.acc = blend<kPair>(o.acc, pc);
   if (kDump == 2 || (kDump == 0 && c_fc.dump))
     o.hash = (o.hash ^ pk) * kHashPrime;  // blend-order evidence (parity dumps)
-  ++o.emitted;
+  if (kDump != 1) ++o.emitted;  // (kDump 1: the caller knows the half-block's sample total)
   if (ooo) o.invalid = true;
 }
 
@@ -3356,14 +3356,19 @@ __global__ void __launch_bounds__(256, kMode == 1 ? 4 : 2) k_shade(Buffers B) {
           f.reset(reinterpret_cast<float4*>(shade_dyn + (size_t)kStageTris * sizeof(StagedTri)) +
                   (size_t)warp * KM * 32 + lane);
           if (staged_ok && d.cnt <= (uint32_t)kShadeStage && !fc.wave1) {  // all operands in shared memory
-            if (fc.dump)
+            // (the lists named through stage_* directly: shared-memory loads
+            // instead of generic ones through the merged list pointers)
+            if (fc.dump) {
               shade_waves_staged2<KM, 2>(fc, hpx0, hpy0, stage_tri[warp] + sh4, stage_mask[warp] + sh4,
                                          stage_slot[warp] + sh8, row_tris, d.cnt, po, f);
-            else
-              // (the lists named through stage_* directly: shared-memory loads
-              // instead of generic ones through the merged list pointers)
+            } else {
               shade_waves_staged2<KM, 1>(fc, hpx0, hpy0, stage_tri[warp] + sh4, stage_mask[warp] + sh4,
                                          stage_slot[warp] + sh8, row_tris, d.cnt, po, f);
+              // every sample pushed is blended exactly once (no threshold), so the
+              // warp's emitted total is the half-block's sample count (stats only;
+              // per-pixel counts exist only in dump frames)
+              po.emitted = lane == 0 ? d.frags : 0u;
+            }
           }
           else if (staged_ok && d.cnt <= (uint32_t)kShadeStage)
             shade_waves<KM, kTex>(fc, B, hpx0, hpy0, tri_l, mask_l, slot_l, row_tris, d.cnt, po, f);
